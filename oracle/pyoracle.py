@@ -1,0 +1,206 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes bindings to the CPU checkers.
+
+  Oracle()     -> oracle/liboracle.so      (plain-C restatement, "port")
+  RefOracle()  -> oracle/_ref/libcyqref.so (the reference built from its own
+                                            sources, "reference")
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU legs may import this
+module; the product path never does. Both libraries are (re)built with
+`make -C oracle` when missing and buildable (the reference only where
+/root/reference exists; its .so travels to the GPU box prebuilt).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SRC = "/root/reference/proj"
+
+i64 = C.c_int64
+dp = C.POINTER(C.c_double)
+
+
+class Dims(C.Structure):
+    _fields_ = [("N", i64), ("nx", i64), ("nu", i64), ("P", i64), ("batch", i64)]
+
+
+class Ocp(C.Structure):
+    _fields_ = [(k, dp) for k in ("A", "B", "R", "S", "Q", "f", "r", "q", "x_init")]
+
+
+class Rhs(C.Structure):
+    _fields_ = [(k, dp) for k in ("ru", "qx", "fd")]
+
+
+class Sol(C.Structure):
+    _fields_ = [(k, dp) for k in ("u", "x", "lam")]
+
+
+class FactorBlocks(C.Structure):
+    _fields_ = [(k, dp) for k in ("LH", "LB", "Acl", "LA", "T", "Mfwd", "Mbwd", "W",
+                                  "schur_diag", "schur_sub")]
+
+
+class Status(C.Structure):
+    _fields_ = [("code", C.c_int32), ("kind", C.c_int32), ("instance", i64),
+                ("column_or_level", i64), ("stage", i64), ("pivot", i64)]
+
+
+def _p(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(dp)
+
+
+def _dims(p, P):
+    return Dims(p.N, p.nx, p.nu, P, p.batch)
+
+
+def _ocp(p):
+    return Ocp(*[_p(a) for a in p.arrays()])
+
+
+def _sol_arrays(p):
+    from paper_2512_09058_b200.ocp import EqSolutionBatch
+    return EqSolutionBatch.empty(p.batch, p.N, p.nx, p.nu)
+
+
+def _load(path, target):
+    if not os.path.exists(path):
+        r = subprocess.run(["make", "-C", HERE, target], capture_output=True, text=True)
+        if r.returncode != 0 or not os.path.exists(path):
+            raise RuntimeError(f"cannot build {path}: {r.stderr[-2000:]}")
+    return C.CDLL(path)
+
+
+def ref_available() -> bool:
+    return os.path.exists(os.path.join(HERE, "_ref", "libcyqref.so")) or os.path.isdir(REF_SRC)
+
+
+class _Base:
+    prefix = ""
+
+    def __init__(self, lib):
+        self.lib = lib
+
+    def fn(self, name):
+        return getattr(self.lib, self.prefix + name)
+
+    def kkt_residual(self, p, rhs, sol):
+        out = np.zeros((p.batch, 4))
+        f = self.fn("kkt_residual")
+        f.restype = None
+        f(C.byref(_dims(p, 1)), C.byref(_ocp(p)), C.byref(Rhs(*[_p(a) for a in rhs.arrays()])),
+          C.byref(Sol(*[_p(a) for a in sol.arrays()])), _p(out))
+        return out
+
+    def fma_counts(self, N, nx, nu, P):
+        out = (C.c_uint64 * 2)()
+        f = self.fn("fma_counts")
+        f.restype = None
+        f(C.byref(Dims(N, nx, nu, P, 1)), out)
+        return int(out[0]), int(out[1])
+
+
+class Oracle(_Base):
+    """The plain-C restatement (oracle/cyq_oracle.c)."""
+
+    prefix = "oc_"
+
+    def __init__(self):
+        super().__init__(_load(os.path.join(HERE, "liboracle.so"), "oracle"))
+        self.lib.oc_bench_solve_problem.restype = C.c_double
+
+    def solve_problem(self, p, P):
+        sol = _sol_arrays(p)
+        st = (Status * p.batch)()
+        rc = self.lib.oc_solve_problem(C.byref(_dims(p, P)), C.byref(_ocp(p)),
+                                       C.byref(Sol(*[_p(a) for a in sol.arrays()])), st)
+        return sol, rc, list(st)
+
+    def solve(self, p, rhs, P):
+        sol = _sol_arrays(p)
+        st = (Status * p.batch)()
+        rc = self.lib.oc_solve(C.byref(_dims(p, P)), C.byref(_ocp(p)),
+                               C.byref(Rhs(*[_p(a) for a in rhs.arrays()])),
+                               C.byref(Sol(*[_p(a) for a in sol.arrays()])), st)
+        return sol, rc, list(st)
+
+    def factor_blocks(self, p, P):
+        return _factor_blocks(self.lib.oc_factor_export, p, P, None)
+
+    def bench(self, p, P, n_solves, threads):
+        sol = _sol_arrays(p)
+        return self.lib.oc_bench_solve_problem(
+            C.byref(_dims(p, P)), C.byref(_ocp(p)), i64(n_solves), C.c_int(threads),
+            C.byref(Sol(*[_p(a) for a in sol.arrays()])))
+
+
+class RefOracle(_Base):
+    """The reference's own sources (oracle/_ref/libcyqref.so)."""
+
+    prefix = "ref_"
+
+    def __init__(self):
+        super().__init__(_load(os.path.join(HERE, "_ref", "libcyqref.so"), "ref"))
+        self.lib.ref_bench_solve_problem.restype = C.c_double
+
+    def solve_problem(self, p, P, vlen=4, threads=1):
+        sol = _sol_arrays(p)
+        res = np.zeros(p.batch)
+        st = (Status * p.batch)()
+        rc = self.lib.ref_solve_problem(C.byref(_dims(p, P)), C.byref(_ocp(p)), i64(vlen),
+                                        C.c_int(threads),
+                                        C.byref(Sol(*[_p(a) for a in sol.arrays()])),
+                                        _p(res), st)
+        return sol, res, rc, list(st)
+
+    def solve(self, p, rhs, P, vlen=4):
+        sol = _sol_arrays(p)
+        st = (Status * p.batch)()
+        rc = self.lib.ref_solve(C.byref(_dims(p, P)), C.byref(_ocp(p)),
+                                C.byref(Rhs(*[_p(a) for a in rhs.arrays()])), i64(vlen),
+                                C.byref(Sol(*[_p(a) for a in sol.arrays()])), st)
+        return sol, rc, list(st)
+
+    def factor_blocks(self, p, P, vlen=4):
+        return _factor_blocks(self.lib.ref_factor_export, p, P, vlen)
+
+    def random_eq_ocp(self, N, nx, nu, seed, conditioning=10.0):
+        from paper_2512_09058_b200.ocp import EqOCPBatch
+        arrs = [np.zeros(s) for s in [(1, N, nx, nx), (1, N, nx, nu), (1, N, nu, nu),
+                                      (1, N, nu, nx), (1, N + 1, nx, nx), (1, N, nx),
+                                      (1, N, nu), (1, N + 1, nx), (1, nx)]]
+        f = self.lib.ref_random_eq_ocp
+        f.restype = None
+        f(i64(N), i64(nx), i64(nu), C.c_uint64(seed), C.c_double(conditioning),
+          *[_p(a) for a in arrs])
+        return EqOCPBatch(*arrs)
+
+    def bench(self, p, P, n_solves, threads, vlen=4):
+        return self.lib.ref_bench_solve_problem(C.byref(_dims(p, P)), C.byref(_ocp(p)),
+                                                i64(vlen), i64(n_solves), C.c_int(threads))
+
+
+def _factor_blocks(fn, p, P, vlen):
+    N, nx, nu = p.N, p.nx, p.nu
+    nux = nx + nu
+    Np = P * ((N + P - 1) // P)
+    n = Np // P
+    out = {
+        "LH": np.zeros((n, P, nux, nux)), "LB": np.zeros((n, P, nx, nu)),
+        "Acl": np.zeros((n, P, nx, nx)), "LA": np.zeros((P, nx, nx)),
+        "T": np.zeros((P, nx, nx)), "Mfwd": np.zeros((P, nx, nx)),
+        "Mbwd": np.zeros((P, nx, nx)), "W": np.zeros((P, nx, nx)),
+        "schur_diag": np.zeros((P, nx, nx)), "schur_sub": np.zeros((P, nx, nx)),
+    }
+    fb = FactorBlocks(*[_p(out[k]) for k, _ in FactorBlocks._fields_])
+    st = Status()
+    args = [C.byref(_dims(p, P)), C.byref(_ocp(p))]
+    if vlen is not None:
+        args.append(i64(vlen))
+    rc = fn(*args, C.byref(fb), C.byref(st))
+    return out, rc, st
