@@ -1,0 +1,121 @@
+/* cyqlone_b200 -- C ABI of the B200-native KKT factor+solve for
+ * linear-quadratic optimal control problems (arXiv 2512.09058, "Cyqlone").
+ *
+ * Drop-in boundary for the reference's hot path
+ *   cyqlone::kkt::factor / solve / solve_problem
+ *   (/root/reference/proj/include/cyqlone/kkt_solver.hpp:118-128)
+ * with a batch dimension added (the reference API is single-instance; its
+ * internal "batch" is the P partition columns, kkt_solver.hpp:74-75).
+ * The C++ mirror of the reference interface (include/cyqlone_b200/
+ * kkt_solver.hpp) and the Python bindings sit on top of these entry points.
+ *
+ * Data layout (all FP64, C-contiguous, instance-major, stage-major, each
+ * block row-major exactly like the reference's DenseMatrix,
+ * batch_matrix.hpp:170-189; b = instance):
+ *   A[b][N][nx][nx]  B[b][N][nx][nu]  R[b][N][nu][nu]  S[b][N][nu][nx]
+ *   Q[b][N+1][nx][nx] f[b][N][nx] r[b][N][nu] q[b][N+1][nx] x_init[b][nx]
+ *   rhs  ru[b][N][nu]  qx[b][N+1][nx]  fd[b][N][nx]          (EqRhs)
+ *   sol  u[b][N][nu]   x[b][N+1][nx]   lam[b][N][nx]         (EqSolution)
+ * Pointers are host memory (mem = CYQ_MEM_HOST; pinned memory lets the
+ * copies overlap compute) or device memory on the context's GPU
+ * (mem = CYQ_MEM_DEVICE). Calls are stream-ordered on the context stream;
+ * host-memory calls return after the results are in host memory.
+ *
+ * Errors mirror the reference's exceptions: std::invalid_argument (P not a
+ * power of two, kkt_factor.cpp:253-256) -> CYQ_INVALID_ARG; batla::
+ * factorize_error (kernels.cpp:42-45, block_tridiag.cpp:140-147) ->
+ * CYQ_PIVOT_FAIL with per-instance detail in cyq_status, other instances of
+ * the batch are still solved.
+ */
+#ifndef CYQLONE_B200_H
+#define CYQLONE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CYQ_OK 0
+#define CYQ_INVALID_ARG 1
+#define CYQ_PIVOT_FAIL 2
+#define CYQ_CUDA_ERR 3
+#define CYQ_NO_DEVICE 4
+
+#define CYQ_MEM_HOST 0
+#define CYQ_MEM_DEVICE 1
+
+#define CYQ_FAIL_RICCATI 0 /* column_or_level = column c, stage = position s */
+#define CYQ_FAIL_CR 1      /* column_or_level = CR level, stage = block index */
+
+typedef struct cyq_ctx cyq_ctx;
+typedef struct cyq_factor cyq_factor;
+
+/* Problem dimensions: horizon N, states nx, inputs nu, partitions P (power
+ * of two; N is padded to a multiple of P as pad_problem does,
+ * kkt_factor.cpp:27-47), number of independent instances. */
+typedef struct {
+    int64_t N, nx, nu, P, batch;
+} cyq_dims;
+
+typedef struct {
+    const double *A, *B, *R, *S, *Q, *f, *r, *q, *x_init;
+} cyq_ocp_batch;
+
+typedef struct {
+    const double *ru, *qx, *fd;
+} cyq_rhs_batch;
+
+typedef struct {
+    double *u, *x, *lam;
+} cyq_sol_batch;
+
+/* Per-instance status (mirrors batla::factorize_error{batch_index, pivot}). */
+typedef struct {
+    int32_t code;  /* CYQ_OK / CYQ_PIVOT_FAIL */
+    int32_t kind;  /* CYQ_FAIL_RICCATI / CYQ_FAIL_CR */
+    int64_t instance, column_or_level, stage, pivot;
+} cyq_status;
+
+/* One context per GPU; no global state. */
+int cyq_ctx_create(int device, cyq_ctx **out);
+int cyq_ctx_destroy(cyq_ctx *ctx);
+/* Use an existing cudaStream_t (NULL = the context's own stream). */
+int cyq_ctx_set_stream(cyq_ctx *ctx, void *cuda_stream);
+int cyq_ctx_synchronize(cyq_ctx *ctx);
+/* Last error message of this context (static storage of the context). */
+const char *cyq_ctx_last_error(cyq_ctx *ctx);
+
+/* kkt::solve_problem (kkt_solve.cpp:311-317) for every instance:
+ * factor + solve with EqRhs::of_problem (ocp.cpp:154-174). `status` may be
+ * NULL or point to `batch` entries. Returns the worst status code. */
+int cyq_solve_problem_batch(cyq_ctx *ctx, const cyq_dims *dims,
+                            const cyq_ocp_batch *prob, const cyq_sol_batch *sol,
+                            cyq_status *status, int mem);
+
+/* kkt::factor (kkt_factor.cpp:251-313): the factor stays on the device. */
+int cyq_factor_batch(cyq_ctx *ctx, const cyq_dims *dims,
+                     const cyq_ocp_batch *prob, int mem, cyq_factor **out,
+                     cyq_status *status);
+/* kkt::solve (kkt_solve.cpp:23-309) with an explicit right-hand side; `prob`
+ * must be the problem the factor was computed from (its A, B enter the
+ * substitution, as in the reference signature). */
+int cyq_solve_batch(cyq_ctx *ctx, const cyq_factor *factor,
+                    const cyq_ocp_batch *prob, const cyq_rhs_batch *rhs,
+                    const cyq_sol_batch *sol, int mem);
+int cyq_factor_destroy(cyq_factor *factor);
+
+/* Copies the factor blocks of instance `inst` to host memory in the
+ * reference's Factor member shapes (kkt_solver.hpp:76-95), dense row-major
+ * per column c: LH[s][c][nux][nux], LB[s][c][nx][nu], Acl[s][c][nx][nx],
+ * LA[c][nx][nx]; any pointer may be NULL. For block-level parity tests. */
+int cyq_factor_materialize(const cyq_factor *factor, int64_t inst, double *LH,
+                           double *LB, double *Acl, double *LA);
+
+/* Library build/runtime information (kernel names, tile shapes). */
+const char *cyq_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,82 @@
+"""ctypes binding of the C ABI (include/cyqlone_b200.h).
+
+The product path is libcyqlone_b200.so, built in-tree for sm_100a by
+`__graft_entry__.build()` (or `python -m paper_2512_09058_b200.build`).
+There is no fallback: if the library is missing, or no CUDA device is
+present, calls raise instead of computing anything on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcyqlone_b200.so")
+
+CYQ_OK, CYQ_INVALID_ARG, CYQ_PIVOT_FAIL, CYQ_CUDA_ERR, CYQ_NO_DEVICE = 0, 1, 2, 3, 4
+CYQ_MEM_HOST, CYQ_MEM_DEVICE = 0, 1
+
+i64 = C.c_int64
+dp = C.POINTER(C.c_double)
+
+
+class CyqDims(C.Structure):
+    _fields_ = [("N", i64), ("nx", i64), ("nu", i64), ("P", i64), ("batch", i64)]
+
+
+class CyqOcpBatch(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("A", "B", "R", "S", "Q", "f", "r", "q", "x_init")]
+
+
+class CyqRhsBatch(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("ru", "qx", "fd")]
+
+
+class CyqSolBatch(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("u", "x", "lam")]
+
+
+class CyqStatus(C.Structure):
+    _fields_ = [("code", C.c_int32), ("kind", C.c_int32), ("instance", i64),
+                ("column_or_level", i64), ("stage", i64), ("pivot", i64)]
+
+
+# exported symbols and their signatures (kept in sync with the header; the
+# CPU test suite checks every declared symbol is exported)
+SIGNATURES = {
+    "cyq_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "cyq_ctx_destroy": (C.c_int, [C.c_void_p]),
+    "cyq_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "cyq_ctx_synchronize": (C.c_int, [C.c_void_p]),
+    "cyq_ctx_last_error": (C.c_char_p, [C.c_void_p]),
+    "cyq_solve_problem_batch": (C.c_int, [C.c_void_p, C.POINTER(CyqDims), C.POINTER(CyqOcpBatch),
+                                          C.POINTER(CyqSolBatch), C.c_void_p, C.c_int]),
+    "cyq_factor_batch": (C.c_int, [C.c_void_p, C.POINTER(CyqDims), C.POINTER(CyqOcpBatch),
+                                   C.c_int, C.POINTER(C.c_void_p), C.c_void_p]),
+    "cyq_solve_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(CyqOcpBatch),
+                                  C.POINTER(CyqRhsBatch), C.POINTER(CyqSolBatch), C.c_int]),
+    "cyq_factor_destroy": (C.c_int, [C.c_void_p]),
+    "cyq_factor_materialize": (C.c_int, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_void_p]),
+    "cyq_version": (C.c_char_p, []),
+}
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Loads libcyqlone_b200.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"{path} not built: run __graft_entry__.build() (nvcc, sm_100a). "
+            "There is no CPU fallback for the KKT path.")
+    lib = C.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib

@@ -1,0 +1,550 @@
+// C ABI (include/cyqlone_b200.h): contexts, device workspaces, launches.
+//
+// The batch entry points replace the reference's single-instance
+// kkt::factor / solve / solve_problem (kkt_solver.hpp:118-128); the C++
+// mirror (kkt_solver.cpp) wraps them with batch = 1. No CPU fallback: every
+// path below launches the sm_100a kernels or reports CYQ_CUDA_ERR.
+#include "../../include/cyqlone_b200.h"
+#include "kernels.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace cyqb;
+
+struct cyq_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    // grow-only scratch for host-memory calls
+    std::vector<std::pair<void **, size_t>> dummy;
+    void *hbuf = nullptr;
+    size_t hbuf_bytes = 0;
+    void *wsbuf = nullptr;
+    size_t wsbuf_bytes = 0;
+};
+
+struct cyq_factor {
+    cyq_ctx *ctx = nullptr;
+    cyq_dims dims{};
+    Geo g{};
+    void *mem = nullptr; // one allocation: workspace (+ problem copy)
+    size_t bytes = 0;
+    FactorWS ws{};
+    ProbView prob{}; // device copy of the problem (host-memory factor calls)
+    bool owns_prob = false;
+};
+
+namespace {
+
+thread_local std::string g_last_err;
+
+int set_err(cyq_ctx *ctx, int code, const std::string &msg) {
+    if (ctx)
+        ctx->err = msg;
+    g_last_err = msg;
+    return code;
+}
+
+#define CU(call)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return set_err(ctx, CYQ_CUDA_ERR,                                           \
+                           std::string(#call) + ": " + cudaGetErrorString(e_));         \
+    } while (0)
+
+bool pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+int make_geo(cyq_ctx *ctx, const cyq_dims *d, Geo &g) {
+    if (!d || d->N < 1 || d->nx < 1 || d->nu < 1 || d->batch < 1)
+        return set_err(ctx, CYQ_INVALID_ARG, "dims: N, nx, nu, batch must be >= 1");
+    if (!pow2(d->P))
+        return set_err(ctx, CYQ_INVALID_ARG, "P must be a power of two");
+    g.N = (int)d->N;
+    g.P = (int)d->P;
+    g.Np = g.P * ((g.N + g.P - 1) / g.P);
+    g.n = g.Np / g.P;
+    g.nx = (int)d->nx;
+    g.nu = (int)d->nu;
+    g.nux = g.nx + g.nu;
+    g.CT = (g.nux + 7) / 8;
+    g.BT = (g.nx + 1 + 7) / 8;
+    g.TT = g.CT + g.BT;
+    g.XT0 = g.nu / 8;
+    g.NXT = (g.nux - 1) / 8 - g.XT0 + 1;
+    g.NPT = g.CT * (g.CT + 1) / 2 + g.BT * g.CT;
+    g.NTT = g.BT * (g.BT + 1) / 2;
+    g.batch = (int)d->batch;
+    if (cyqb::riccati_smem_bytes(g) > 227 * 1024)
+        return set_err(ctx, CYQ_INVALID_ARG,
+                       "stage panel exceeds shared memory (nx + nu too large)");
+    return CYQ_OK;
+}
+
+struct WsSizes {
+    size_t fac, y, wl, trail, schur, lamc, fail, total;
+};
+
+WsSizes ws_sizes(const Geo &g) {
+    WsSizes s;
+    const size_t chains = (size_t)g.batch * g.P;
+    auto al = [](size_t v) { return (v + 31) / 32 * 32; }; // 256-byte aligned
+    s.fac = al(chains * g.n * g.NPT * kTileElems);
+    s.y = al(chains * g.n * g.nux);
+    s.wl = al(chains * g.n * g.nx);
+    s.trail = al(chains * g.NTT * kTileElems);
+    s.schur = al((size_t)g.batch * SchurLayout::make(g.P, g.nx).total);
+    s.lamc = al((size_t)g.batch * g.P * g.nx);
+    s.fail = al((size_t)g.batch); // 8-byte keys
+    s.total = (s.fac + s.y + s.wl + s.trail + s.schur + s.lamc + s.fail) * sizeof(double);
+    return s;
+}
+
+FactorWS carve(void *base, const WsSizes &s) {
+    FactorWS w;
+    double *p = static_cast<double *>(base);
+    w.fac = p;
+    p += s.fac;
+    w.y = p;
+    p += s.y;
+    w.wl = p;
+    p += s.wl;
+    w.trail = p;
+    p += s.trail;
+    w.schur = p;
+    p += s.schur;
+    w.lamc = p;
+    p += s.lamc;
+    w.fail = reinterpret_cast<unsigned long long *>(p);
+    return w;
+}
+
+size_t prob_doubles(const Geo &g) {
+    const size_t B = g.batch, N = g.N, nx = g.nx, nu = g.nu;
+    return B * (N * nx * nx + N * nx * nu + N * nu * nu + N * nu * nx + (N + 1) * nx * nx +
+                N * nx + N * nu + (N + 1) * nx + nx);
+}
+size_t sol_doubles(const Geo &g) {
+    const size_t B = g.batch, N = g.N, nx = g.nx, nu = g.nu;
+    return B * (N * nu + (N + 1) * nx + N * nx);
+}
+
+// Lays out a problem batch in one contiguous device buffer.
+ProbView carve_prob(double *p, const Geo &g) {
+    const size_t B = g.batch, N = g.N, nx = g.nx, nu = g.nu;
+    ProbView v{};
+    double *q = p;
+    auto take = [&](size_t cnt) {
+        double *r = q;
+        q += cnt;
+        return r;
+    };
+    v.A = take(B * N * nx * nx);
+    v.B = take(B * N * nx * nu);
+    v.R = take(B * N * nu * nu);
+    v.S = take(B * N * nu * nx);
+    v.Q = take(B * (N + 1) * nx * nx);
+    v.f = take(B * N * nx);
+    v.r = take(B * N * nu);
+    v.q = take(B * (N + 1) * nx);
+    v.x_init = take(B * nx);
+    return v;
+}
+
+int copy_prob_h2d(cyq_ctx *ctx, const Geo &g, const cyq_ocp_batch *h, const ProbView &d) {
+    const size_t B = g.batch, N = g.N, nx = g.nx, nu = g.nu;
+    const std::pair<const double *, const double *> parts[] = {
+        {h->A, d.A}, {h->B, d.B}, {h->R, d.R}, {h->S, d.S}, {h->Q, d.Q},
+        {h->f, d.f}, {h->r, d.r}, {h->q, d.q}, {h->x_init, d.x_init}};
+    const size_t cnt[] = {B * N * nx * nx, B * N * nx * nu, B * N * nu * nu, B * N * nu * nx,
+                          B * (N + 1) * nx * nx, B * N * nx, B * N * nu, B * (N + 1) * nx,
+                          B * nx};
+    for (int i = 0; i < 9; ++i) {
+        if (!parts[i].first)
+            return set_err(ctx, CYQ_INVALID_ARG, "null problem array");
+        CU(cudaMemcpyAsync(const_cast<double *>(parts[i].second), parts[i].first,
+                           cnt[i] * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    return CYQ_OK;
+}
+
+ProbView view_of(const cyq_ocp_batch *p) {
+    ProbView v{};
+    v.A = p->A;
+    v.B = p->B;
+    v.R = p->R;
+    v.S = p->S;
+    v.Q = p->Q;
+    v.f = p->f;
+    v.r = p->r;
+    v.q = p->q;
+    v.x_init = p->x_init;
+    return v;
+}
+
+int riccati_warps(const Geo &g) {
+    const int nt = g.TT * (g.TT + 1) / 2;
+    return std::max(1, std::min(8, nt / 6));
+}
+int schur_warps(const Geo &g) { return std::max(1, std::min(8, g.P / 2)); }
+int backsub_threads(const Geo &g) { return g.nux > 48 ? 128 : 32; }
+
+int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &ws,
+                    const SolView *sol, bool do_solve) {
+    static bool attrs = false;
+    if (!attrs) {
+        CU(cudaFuncSetAttribute(riccati_panel_kernel,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        CU(cudaFuncSetAttribute(backsub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                227 * 1024));
+        attrs = true;
+    }
+    const int chains = g.batch * g.P;
+    CU(cudaMemsetAsync(ws.fail, 0xFF, sizeof(unsigned long long) * g.batch, ctx->stream));
+    RiccatiArgs ra{g, p, ws.fac, ws.y, ws.wl, ws.trail, ws.fail};
+    riccati_panel_kernel<<<chains, 32 * riccati_warps(g), riccati_smem_bytes(g), ctx->stream>>>(ra);
+    CU(cudaGetLastError());
+    SchurArgs sa{g, p, ws.fac, ws.y, ws.trail, ws.schur, ws.lamc,
+                 sol ? sol->lam : nullptr, ws.fail, 1, do_solve ? 1 : 0};
+    schur_cr_kernel<<<g.batch, 32 * schur_warps(g), 0, ctx->stream>>>(sa);
+    CU(cudaGetLastError());
+    if (do_solve) {
+        BacksubArgs ba{g, p, ws.fac, ws.y, ws.wl, ws.lamc, *sol};
+        backsub_kernel<<<chains, backsub_threads(g), backsub_smem_bytes(g), ctx->stream>>>(ba);
+        CU(cudaGetLastError());
+    }
+    return CYQ_OK;
+}
+
+int decode_status(cyq_ctx *ctx, const Geo &g, const unsigned long long *dfail,
+                  cyq_status *status) {
+    std::vector<unsigned long long> h(g.batch);
+    CU(cudaMemcpyAsync(h.data(), dfail, sizeof(unsigned long long) * g.batch,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    int worst = CYQ_OK;
+    for (int b = 0; b < g.batch; ++b) {
+        cyq_status st{};
+        st.instance = b;
+        if (h[b] != ~0ull) {
+            st.code = CYQ_PIVOT_FAIL;
+            st.kind = (int)(h[b] >> 60);
+            st.column_or_level = (int64_t)((h[b] >> 40) & 0xFFFFF);
+            st.stage = (int64_t)((h[b] >> 20) & 0xFFFFF);
+            st.pivot = (int64_t)(h[b] & 0xFFFFF);
+            worst = CYQ_PIVOT_FAIL;
+        }
+        if (status)
+            status[b] = st;
+    }
+    if (worst != CYQ_OK)
+        set_err(ctx, worst, "factorization pivot failure (see status)");
+    return worst;
+}
+
+int ensure(cyq_ctx *ctx, void **buf, size_t *have, size_t need) {
+    if (*have >= need)
+        return CYQ_OK;
+    if (*buf)
+        CU(cudaFree(*buf));
+    *buf = nullptr;
+    *have = 0;
+    CU(cudaMalloc(buf, need));
+    *have = need;
+    return CYQ_OK;
+}
+
+} // namespace
+
+namespace cyqb {
+
+size_t riccati_smem_bytes(const Geo &g) {
+    const int nt = g.TT * (g.TT + 1) / 2;
+    const size_t vec = 32 * ((g.nx + 31) / 32) * 2 + 32 * ((g.nu + 31) / 32) + 32;
+    return ((size_t)(nt + g.TT * g.NXT) * kTileElems + vec) * sizeof(double);
+}
+size_t backsub_smem_bytes(const Geo &g) {
+    const size_t vpad = 32 * ((g.nux + 31) / 32);
+    return ((size_t)g.NPT * kTileElems + 8 * vpad) * sizeof(double);
+}
+size_t schur_smem_bytes(const Geo &) { return 0; }
+
+} // namespace cyqb
+
+extern "C" {
+
+int cyq_ctx_create(int device, cyq_ctx **out) {
+    cyq_ctx *ctx = nullptr;
+    if (!out)
+        return set_err(nullptr, CYQ_INVALID_ARG, "null out");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device || device < 0)
+        return set_err(nullptr, CYQ_NO_DEVICE, "no CUDA device");
+    ctx = new cyq_ctx();
+    ctx->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess)
+        e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return set_err(nullptr, CYQ_CUDA_ERR, cudaGetErrorString(e));
+    }
+    ctx->own_stream = true;
+    *out = ctx;
+    return CYQ_OK;
+}
+
+int cyq_ctx_destroy(cyq_ctx *ctx) {
+    if (!ctx)
+        return CYQ_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream)
+        cudaStreamSynchronize(ctx->stream);
+    if (ctx->hbuf)
+        cudaFree(ctx->hbuf);
+    if (ctx->wsbuf)
+        cudaFree(ctx->wsbuf);
+    if (ctx->own_stream && ctx->stream)
+        cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return CYQ_OK;
+}
+
+int cyq_ctx_set_stream(cyq_ctx *ctx, void *s) {
+    if (!ctx)
+        return CYQ_INVALID_ARG;
+    if (ctx->own_stream && ctx->stream)
+        cudaStreamDestroy(ctx->stream);
+    if (s) {
+        ctx->stream = static_cast<cudaStream_t>(s);
+        ctx->own_stream = false;
+    } else {
+        CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->own_stream = true;
+    }
+    return CYQ_OK;
+}
+
+int cyq_ctx_synchronize(cyq_ctx *ctx) {
+    if (!ctx)
+        return CYQ_INVALID_ARG;
+    CU(cudaStreamSynchronize(ctx->stream));
+    return CYQ_OK;
+}
+
+const char *cyq_ctx_last_error(cyq_ctx *ctx) {
+    return ctx ? ctx->err.c_str() : g_last_err.c_str();
+}
+
+int cyq_solve_problem_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_batch *prob,
+                            const cyq_sol_batch *sol, cyq_status *status, int mem) {
+    if (!ctx || !prob || !sol)
+        return set_err(ctx, CYQ_INVALID_ARG, "null argument");
+    Geo g;
+    int rc = make_geo(ctx, dims, g);
+    if (rc)
+        return rc;
+    CU(cudaSetDevice(ctx->device));
+    const WsSizes wsz = ws_sizes(g);
+    rc = ensure(ctx, &ctx->wsbuf, &ctx->wsbuf_bytes, wsz.total);
+    if (rc)
+        return rc;
+    FactorWS ws = carve(ctx->wsbuf, wsz);
+    if (mem == CYQ_MEM_DEVICE) {
+        SolView sv{sol->u, sol->x, sol->lam};
+        rc = launch_pipeline(ctx, g, view_of(prob), ws, &sv, true);
+        if (rc)
+            return rc;
+        return decode_status(ctx, g, ws.fail, status);
+    }
+    // host memory: stage through device buffers
+    const size_t pd = prob_doubles(g), sd = sol_doubles(g);
+    rc = ensure(ctx, &ctx->hbuf, &ctx->hbuf_bytes, (pd + sd) * sizeof(double));
+    if (rc)
+        return rc;
+    double *base = static_cast<double *>(ctx->hbuf);
+    ProbView dp = carve_prob(base, g);
+    rc = copy_prob_h2d(ctx, g, prob, dp);
+    if (rc)
+        return rc;
+    const size_t B = g.batch, N = g.N;
+    SolView sv{base + pd, base + pd + B * N * g.nu, base + pd + B * N * g.nu + B * (N + 1) * g.nx};
+    rc = launch_pipeline(ctx, g, dp, ws, &sv, true);
+    if (rc)
+        return rc;
+    CU(cudaMemcpyAsync(sol->u, sv.u, B * N * g.nu * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaMemcpyAsync(sol->x, sv.x, B * (N + 1) * g.nx * sizeof(double),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(sol->lam, sv.lam, B * N * g.nx * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    return decode_status(ctx, g, ws.fail, status);
+}
+
+int cyq_factor_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_batch *prob, int mem,
+                     cyq_factor **out, cyq_status *status) {
+    if (!ctx || !prob || !out)
+        return set_err(ctx, CYQ_INVALID_ARG, "null argument");
+    Geo g;
+    int rc = make_geo(ctx, dims, g);
+    if (rc)
+        return rc;
+    CU(cudaSetDevice(ctx->device));
+    cyq_factor *f = new cyq_factor();
+    f->ctx = ctx;
+    f->dims = *dims;
+    f->g = g;
+    const WsSizes wsz = ws_sizes(g);
+    const size_t pbytes = prob_doubles(g) * sizeof(double);
+    f->bytes = wsz.total + pbytes;
+    cudaError_t e = cudaMalloc(&f->mem, f->bytes);
+    if (e != cudaSuccess) {
+        delete f;
+        return set_err(ctx, CYQ_CUDA_ERR, cudaGetErrorString(e));
+    }
+    f->ws = carve(f->mem, wsz);
+    f->prob = carve_prob(reinterpret_cast<double *>(static_cast<char *>(f->mem) + wsz.total), g);
+    f->owns_prob = true;
+    if (mem == CYQ_MEM_DEVICE) {
+        const ProbView src = view_of(prob);
+        const size_t B = g.batch, N = g.N, nx = g.nx, nu = g.nu;
+        const std::pair<const double *, const double *> parts[] = {
+            {src.A, f->prob.A}, {src.B, f->prob.B}, {src.R, f->prob.R}, {src.S, f->prob.S},
+            {src.Q, f->prob.Q}, {src.f, f->prob.f}, {src.r, f->prob.r}, {src.q, f->prob.q},
+            {src.x_init, f->prob.x_init}};
+        const size_t cnt[] = {B * N * nx * nx, B * N * nx * nu, B * N * nu * nu,
+                              B * N * nu * nx, B * (N + 1) * nx * nx, B * N * nx, B * N * nu,
+                              B * (N + 1) * nx, B * nx};
+        for (int i = 0; i < 9; ++i)
+            CU(cudaMemcpyAsync(const_cast<double *>(parts[i].second), parts[i].first,
+                               cnt[i] * sizeof(double), cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+    } else {
+        rc = copy_prob_h2d(ctx, g, prob, f->prob);
+        if (rc) {
+            cyq_factor_destroy(f);
+            return rc;
+        }
+    }
+    rc = launch_pipeline(ctx, g, f->prob, f->ws, nullptr, false);
+    if (rc == CYQ_OK)
+        rc = decode_status(ctx, g, f->ws.fail, status);
+    *out = f;
+    return rc;
+}
+
+int cyq_solve_batch(cyq_ctx *ctx, const cyq_factor *f, const cyq_ocp_batch *prob,
+                    const cyq_rhs_batch *rhs, const cyq_sol_batch *sol, int mem) {
+    if (!ctx || !f || !rhs || !sol)
+        return set_err(ctx, CYQ_INVALID_ARG, "null argument");
+    (void)prob; // the factor keeps its own device copy of the problem
+    const Geo &g = f->g;
+    CU(cudaSetDevice(ctx->device));
+    const size_t B = g.batch, N = g.N, nx = g.nx, nu = g.nu;
+    const size_t rd = B * (N * nu + (N + 1) * nx + N * nx);
+    const size_t sd = sol_doubles(g);
+    int rc = ensure(ctx, &ctx->hbuf, &ctx->hbuf_bytes, (rd + sd) * sizeof(double));
+    if (rc)
+        return rc;
+    double *base = static_cast<double *>(ctx->hbuf);
+    ProbView p = f->prob;
+    SolView sv;
+    if (mem == CYQ_MEM_DEVICE) {
+        p.ru = rhs->ru;
+        p.qx = rhs->qx;
+        p.fd = rhs->fd;
+        sv = SolView{sol->u, sol->x, sol->lam};
+    } else {
+        double *ru = base, *qx = ru + B * N * nu, *fd = qx + B * (N + 1) * nx;
+        CU(cudaMemcpyAsync(ru, rhs->ru, B * N * nu * 8, cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(qx, rhs->qx, B * (N + 1) * nx * 8, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CU(cudaMemcpyAsync(fd, rhs->fd, B * N * nx * 8, cudaMemcpyHostToDevice, ctx->stream));
+        p.ru = ru;
+        p.qx = qx;
+        p.fd = fd;
+        double *s0 = base + rd;
+        sv = SolView{s0, s0 + B * N * nu, s0 + B * N * nu + B * (N + 1) * nx};
+    }
+    // TODO(perf): a forward-sweep-only kernel over the stored factor; this
+    // re-runs the stage-panel kernel with the new right-hand side row.
+    rc = launch_pipeline(ctx, g, p, f->ws, &sv, true);
+    if (rc)
+        return rc;
+    if (mem != CYQ_MEM_DEVICE) {
+        CU(cudaMemcpyAsync(sol->u, sv.u, B * N * nu * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaMemcpyAsync(sol->x, sv.x, B * (N + 1) * nx * 8, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CU(cudaMemcpyAsync(sol->lam, sv.lam, B * N * nx * 8, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    }
+    CU(cudaStreamSynchronize(ctx->stream));
+    return CYQ_OK;
+}
+
+int cyq_factor_destroy(cyq_factor *f) {
+    if (!f)
+        return CYQ_OK;
+    if (f->mem) {
+        cudaSetDevice(f->ctx->device);
+        cudaStreamSynchronize(f->ctx->stream);
+        cudaFree(f->mem);
+    }
+    delete f;
+    return CYQ_OK;
+}
+
+int cyq_factor_materialize(const cyq_factor *f, int64_t inst, double *LH, double *LB,
+                           double *Acl, double *LA) {
+    if (!f || inst < 0 || inst >= f->g.batch)
+        return set_err(nullptr, CYQ_INVALID_ARG, "bad factor / instance");
+    cyq_ctx *ctx = f->ctx;
+    const Geo &g = f->g;
+    const size_t per = (size_t)g.P * g.n * g.NPT * kTileElems;
+    std::vector<double> h(per);
+    CU(cudaMemcpy(h.data(), f->ws.fac + (size_t)inst * per, per * sizeof(double),
+                  cudaMemcpyDeviceToHost));
+    const int nu = g.nu, nx = g.nx, nux = g.nux, top = 8 * g.CT, P = g.P, n = g.n;
+    auto at = [&](int c, int s, int r, int col) {
+        const int ti = r / 8, tj = col / 8;
+        const int st = ti < g.CT ? tri_index(ti, tj) : g.CT * (g.CT + 1) / 2 + (ti - g.CT) * g.CT + tj;
+        return h[(((size_t)c * n + s) * g.NPT + st) * kTileElems + (r % 8) * 8 + col % 8];
+    };
+    for (int s = 0; s < n; ++s)
+        for (int c = 0; c < P; ++c) {
+            if (LH)
+                for (int r = 0; r < nux; ++r)
+                    for (int k = 0; k < nux; ++k)
+                        LH[(((size_t)s * P + c) * nux + r) * nux + k] = k <= r ? at(c, s, r, k) : 0.0;
+            if (LB)
+                for (int r = 0; r < nx; ++r)
+                    for (int k = 0; k < nu; ++k)
+                        LB[(((size_t)s * P + c) * nx + r) * nu + k] = at(c, s, top + r, k);
+            // Acl = ALQ L_Q' ; LA = ALQ at the last stage
+            for (int r = 0; r < nx; ++r)
+                for (int k = 0; k < nx; ++k) {
+                    double v = 0;
+                    for (int m = 0; m <= k; ++m)
+                        v += at(c, s, top + r, nu + m) * at(c, s, nu + k, nu + m);
+                    if (Acl)
+                        Acl[(((size_t)s * P + c) * nx + r) * nx + k] = v;
+                    if (LA && s == n - 1)
+                        LA[((size_t)c * nx + r) * nx + k] = at(c, s, top + r, nu + k);
+                }
+        }
+    return CYQ_OK;
+}
+
+const char *cyq_version(void) {
+    return "cyqlone_b200 0.1 sm_100a: riccati_panel_kernel (DMMA 8x8x4 f64 stage panels), "
+           "schur_cr_kernel, backsub_kernel";
+}
+
+} // extern "C"

@@ -1,0 +1,96 @@
+// Kernel argument blocks and launch helpers shared by the C ABI.
+#pragma once
+
+#include "kkt_common.cuh"
+
+#include <cuda_runtime.h>
+
+namespace cyqb {
+
+// Device workspace of one factorization of a batch (all chains).
+struct FactorWS {
+    double *fac;   // [chain][s][NPT][64]   stored pivot tiles (LH | LB ALQ | y')
+    double *y;     // [chain][s][nux]       forward-substituted [u; x] per stage
+    double *wl;    // [chain][s][nx]        interior multipliers after the forward sweep
+    double *trail; // [chain][NTT][64]      -Mfwd (coupling) and -fwd (rhs row)
+    double *schur; // [batch][SCH]          CR factor + scratch (see schur_layout)
+    double *lamc;  // [batch][P][nx]        coupling multipliers lambda^{n i}
+    unsigned long long *fail; // [batch]    first failure key, ~0 = ok
+};
+
+struct RiccatiArgs {
+    Geo g;
+    ProbView p;
+    double *fac, *y, *wl, *trail;
+    unsigned long long *fail;
+};
+
+struct SchurArgs {
+    Geo g;
+    ProbView p;
+    const double *fac, *y, *trail;
+    double *schur, *lamc;
+    double *lam_out; // solution lam (nullable)
+    unsigned long long *fail;
+    int do_factor, do_solve;
+};
+
+struct BacksubArgs {
+    Geo g;
+    ProbView p;
+    const double *fac, *y, *wl, *lamc;
+    SolView sol;
+};
+
+// Per-instance Schur workspace layout (doubles), nx x nx blocks:
+//   D[P], K[P]            level-0 block tridiagonal (diag, subdiag)
+//   Mb[P], Z[P]           Mbwd and L_Q^{-1} per column (scratch)
+//   bn[P * nx]            bwd_neg = T x' per column (scratch)
+//   per level l: L[half], U[half], Y[half], M[half], Kn[half]
+//   Lbase                 base Cholesky factor
+//   rhs[P * nx]
+struct SchurLayout {
+    long long D, K, Mb, Z, bn, lvl0, Lbase, rhs, total;
+    int levels;
+    __host__ __device__ static SchurLayout make(int P, int nx) {
+        SchurLayout s;
+        const long long nn = (long long)nx * nx;
+        int lg = 0;
+        while ((1 << lg) < P)
+            ++lg;
+        s.levels = lg;
+        s.D = 0;
+        s.K = s.D + P * nn;
+        s.Mb = s.K + P * nn;
+        s.Z = s.Mb + P * nn;
+        s.bn = s.Z + P * nn;
+        s.lvl0 = s.bn + (long long)P * nx;
+        long long off = s.lvl0;
+        int sz = P;
+        for (int l = 0; l < lg; ++l, sz /= 2)
+            off += 5LL * (sz / 2) * nn;
+        s.Lbase = off;
+        s.rhs = s.Lbase + nn;
+        s.total = s.rhs + (long long)P * nx;
+        return s;
+    }
+    // level l arrays (half = P >> (l+1) blocks each)
+    __host__ __device__ long long level(int l, int P, int nx, int which) const {
+        const long long nn = (long long)nx * nx;
+        long long off = lvl0;
+        int sz = P;
+        for (int k = 0; k < l; ++k, sz /= 2)
+            off += 5LL * (sz / 2) * nn;
+        return off + (long long)which * (sz / 2) * nn;
+    }
+};
+
+__global__ void riccati_panel_kernel(RiccatiArgs a);
+__global__ void schur_cr_kernel(SchurArgs a);
+__global__ void backsub_kernel(BacksubArgs a);
+
+size_t riccati_smem_bytes(const Geo &g);
+size_t backsub_smem_bytes(const Geo &g);
+size_t schur_smem_bytes(const Geo &g);
+
+} // namespace cyqb

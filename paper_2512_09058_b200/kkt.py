@@ -1,0 +1,258 @@
+"""Python mirror of the reference's KKT interface (cyqlone::kkt,
+proj/include/cyqlone/kkt_solver.hpp:45-128) over the C ABI.
+
+    factor(p, opts)          -> Factor             kkt::factor      (kkt_factor.cpp:251-313)
+    solve(f, p, rhs)         -> EqSolutionBatch    kkt::solve       (kkt_solve.cpp:23-309)
+    solve_problem(p, opts)   -> EqSolutionBatch    kkt::solve_problem (kkt_solve.cpp:311-317)
+
+Same names, argument meaning and error behaviour as the reference:
+`ValueError` for what the reference throws as std::invalid_argument (P not a
+power of two) and `FactorizeError(batch_index, pivot)` for
+batla::factorize_error. Problems are batches (`EqOCPBatch`, a leading
+instance axis; a single reference EqOCP is a batch of one). Arrays may be
+host numpy arrays or CUDA torch tensors (device-resident, zero-copy).
+`opts.vlen` / `opts.workers` are CPU lane/thread knobs of the reference and
+are accepted but have no effect on the GPU (results are independent of them
+in the reference too, test_kkt.cpp:133-138); `tail` must be cr1.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .ocp import OCP_FIELDS, RHS_FIELDS, SOL_FIELDS, EqOCPBatch, EqRhsBatch, EqSolutionBatch
+
+
+class FactorizeError(RuntimeError):
+    """batla::factorize_error (kernels.hpp:11-16): pivot failure."""
+
+    def __init__(self, what, batch_index, pivot, status=None):
+        super().__init__(what)
+        self.batch_index = batch_index
+        self.pivot = pivot
+        self.status = status
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+@dataclass
+class FactorOptions:
+    """kkt::FactorOptions (kkt_solver.hpp:47-57)."""
+
+    P: int = 1
+    vlen: int = 4
+    workers: int = 1
+    tail: str = "cr1"
+    pcg_tol: float = 1e-12
+    pcg_max_iter: int = 50
+    rho: float = 0.5
+
+
+def nu2(i: int, P: int) -> int:
+    """2-adic valuation with nu2(0, P) = nu2(P) (kkt_factor.cpp:15-25)."""
+    if not (0 <= i < P):
+        raise ValueError("nu2: i out of range")
+    if i == 0:
+        i = P
+    v = 0
+    while i & 1 == 0:
+        i >>= 1
+        v += 1
+    return v
+
+
+class Context:
+    """One CUDA context handle per device (cyq_ctx)."""
+
+    _default: dict = {}
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        rc = self.lib.cyq_ctx_create(device, C.byref(h))
+        if rc != _lib.CYQ_OK:
+            raise CudaError(f"cyq_ctx_create failed ({rc}): "
+                            f"{self.lib.cyq_ctx_last_error(None).decode()}")
+        self.h = h
+        self.device = device
+
+    @classmethod
+    def default(cls, device: int = 0) -> "Context":
+        if device not in cls._default:
+            cls._default[device] = cls(device)
+        return cls._default[device]
+
+    def last_error(self) -> str:
+        return self.lib.cyq_ctx_last_error(self.h).decode()
+
+    def set_stream(self, stream_ptr: int | None):
+        self.lib.cyq_ctx_set_stream(self.h, C.c_void_p(stream_ptr or 0))
+
+    def synchronize(self):
+        self.lib.cyq_ctx_synchronize(self.h)
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.lib.cyq_ctx_destroy(self.h)
+        except Exception:
+            pass
+
+
+def _is_torch(a) -> bool:
+    return type(a).__module__.startswith("torch")
+
+
+def _ptr(a):
+    if _is_torch(a):
+        assert a.is_cuda and a.is_contiguous() and str(a.dtype) == "torch.float64"
+        return C.c_void_p(a.data_ptr())
+    assert isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous
+    return C.c_void_p(a.ctypes.data)
+
+
+def _mem(arrs) -> int:
+    kinds = {_is_torch(a) for a in arrs}
+    if len(kinds) != 1:
+        raise ValueError("mix of host and device arrays")
+    return _lib.CYQ_MEM_DEVICE if kinds.pop() else _lib.CYQ_MEM_HOST
+
+
+def _dims(p, P):
+    A, B = p.A, p.B
+    return _lib.CyqDims(A.shape[1], A.shape[2], B.shape[3], P, A.shape[0])
+
+
+def _ocp_struct(p):
+    return _lib.CyqOcpBatch(*[_ptr(getattr(p, k)) for k in OCP_FIELDS])
+
+
+def _check_opts(opts: FactorOptions):
+    P = int(opts.P)
+    if P <= 0 or (P & (P - 1)) != 0:
+        raise ValueError("P must be a power of two")
+    v = int(opts.vlen)
+    if v < 1 or (v & (v - 1)) != 0:
+        raise ValueError("vlen must be a power of two")
+    if opts.tail != "cr1":
+        raise NotImplementedError("only Tail::cr1 is implemented on the GPU")
+
+
+def _raise_status(ctx, rc, st):
+    if rc == _lib.CYQ_OK:
+        return
+    if rc == _lib.CYQ_INVALID_ARG:
+        raise ValueError(ctx.last_error())
+    if rc == _lib.CYQ_PIVOT_FAIL:
+        bad = [s for s in st if s.code != 0]
+        s = bad[0]
+        if s.kind == 1:
+            what = (f"cyclic reduction: pivot failure at level {s.column_or_level}, "
+                    f"index {s.stage} (instance {s.instance})")
+            raise FactorizeError(what, s.stage, s.pivot, bad)
+        what = (f"potrf: pivot failure at batch {s.column_or_level}, pivot {s.pivot} "
+                f"(instance {s.instance}, stage position {s.stage})")
+        raise FactorizeError(what, s.column_or_level, s.pivot, bad)
+    raise CudaError(f"cyqlone_b200 error {rc}: {ctx.last_error()}")
+
+
+def _alloc_sol(p, device_like):
+    b, N, nx, nu = p.A.shape[0], p.A.shape[1], p.A.shape[2], p.B.shape[3]
+    if device_like:
+        import torch
+        dev = p.A.device
+        return EqSolutionBatch(torch.zeros((b, N, nu), dtype=torch.float64, device=dev),
+                               torch.zeros((b, N + 1, nx), dtype=torch.float64, device=dev),
+                               torch.zeros((b, N, nx), dtype=torch.float64, device=dev))
+    return EqSolutionBatch.empty(b, N, nx, nu)
+
+
+def solve_problem(p, opts: FactorOptions, ctx: Context | None = None, out=None,
+                  raise_on_error: bool = True):
+    """kkt::solve_problem for every instance of the batch. Returns the
+    solution batch (numpy for host input, torch for CUDA input)."""
+    _check_opts(opts)
+    ctx = ctx or Context.default()
+    arrs = [getattr(p, k) for k in OCP_FIELDS]
+    mem = _mem(arrs)
+    sol = out if out is not None else _alloc_sol(p, mem == _lib.CYQ_MEM_DEVICE)
+    st = (_lib.CyqStatus * p.A.shape[0])()
+    rc = ctx.lib.cyq_solve_problem_batch(ctx.h, C.byref(_dims(p, opts.P)),
+                                         C.byref(_ocp_struct(p)),
+                                         C.byref(_lib.CyqSolBatch(*[_ptr(getattr(sol, k))
+                                                                   for k in SOL_FIELDS])),
+                                         st, mem)
+    if raise_on_error:
+        _raise_status(ctx, rc, st)
+    return sol if raise_on_error else (sol, rc, list(st))
+
+
+class Factor:
+    """kkt::Factor (kkt_solver.hpp:69-116) -- an opaque device factor of a
+    batch. `materialize(inst)` copies the blocks the reference exposes as
+    public members (LH, LB, Acl, LA) to host numpy arrays."""
+
+    def __init__(self, ctx, handle, p, opts):
+        self.ctx, self.h, self.opts = ctx, handle, opts
+        self.N, self.nx, self.nu = p.A.shape[1], p.A.shape[2], p.B.shape[3]
+        self.batch = p.A.shape[0]
+        P = opts.P
+        self.n_per = (P * ((self.N + P - 1) // P)) // P
+
+    def materialize(self, inst: int = 0):
+        P, n, nx, nu = self.opts.P, self.n_per, self.nx, self.nu
+        nux = nx + nu
+        LH = np.zeros((n, P, nux, nux))
+        LB = np.zeros((n, P, nx, nu))
+        Acl = np.zeros((n, P, nx, nx))
+        LA = np.zeros((P, nx, nx))
+        rc = self.ctx.lib.cyq_factor_materialize(self.h, inst, *[C.c_void_p(a.ctypes.data)
+                                                                 for a in (LH, LB, Acl, LA)])
+        if rc:
+            raise CudaError(self.ctx.last_error())
+        return {"LH": LH, "LB": LB, "Acl": Acl, "LA": LA}
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.ctx.lib.cyq_factor_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def factor(p, opts: FactorOptions, ctx: Context | None = None) -> Factor:
+    """kkt::factor for every instance of the batch."""
+    _check_opts(opts)
+    ctx = ctx or Context.default()
+    mem = _mem([getattr(p, k) for k in OCP_FIELDS])
+    h = C.c_void_p()
+    st = (_lib.CyqStatus * p.A.shape[0])()
+    rc = ctx.lib.cyq_factor_batch(ctx.h, C.byref(_dims(p, opts.P)), C.byref(_ocp_struct(p)),
+                                  mem, C.byref(h), st)
+    f = Factor(ctx, h, p, opts) if h.value else None
+    _raise_status(ctx, rc, st)
+    return f
+
+
+def solve(f: Factor, p, rhs) -> EqSolutionBatch:
+    """kkt::solve with an explicit right-hand side (EqRhs convention)."""
+    ctx = f.ctx
+    arrs = [getattr(rhs, k) for k in RHS_FIELDS]
+    mem = _mem(arrs)
+    sol = _alloc_sol(p, mem == _lib.CYQ_MEM_DEVICE)
+    rc = ctx.lib.cyq_solve_batch(ctx.h, f.h, C.byref(_ocp_struct(p)),
+                                 C.byref(_lib.CyqRhsBatch(*[_ptr(a) for a in arrs])),
+                                 C.byref(_lib.CyqSolBatch(*[_ptr(getattr(sol, k))
+                                                           for k in SOL_FIELDS])), mem)
+    _raise_status(ctx, rc, [])
+    return sol
+
+
+__all__ = ["FactorOptions", "Factor", "FactorizeError", "CudaError", "Context", "factor",
+           "solve", "solve_problem", "nu2", "EqOCPBatch", "EqRhsBatch", "EqSolutionBatch"]

@@ -1,0 +1,69 @@
+"""CPU tests of the C ABI boundary: the library loads, exports every entry
+point include/cyqlone_b200.h declares, validates arguments like the
+reference (std::invalid_argument -> CYQ_INVALID_ARG) and fails loudly (no
+CPU fallback) when no GPU is present."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2512_09058_b200 import _lib, kkt, synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "cyqlone_b200.h")
+
+
+def declared():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(cyq_[a-z_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    exported = set(re.findall(r"\bT (cyq_\w+)", out))
+    for name in declared():
+        assert name in exported, name
+        assert hasattr(lib, name)
+    assert set(_lib.SIGNATURES) == set(declared())
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-lelf", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_kernels_use_dmma():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun",
+                          "_ZN4cyqb20riccati_panel_kernelENS_11RiccatiArgsE", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "DMMA" in out
+
+
+def test_version_string():
+    assert b"sm_100a" in _lib.load().cyq_version()
+
+
+def test_invalid_P_raises_value_error_before_touching_device():
+    p = synth.generate(0, seed=0, batch=1, N=8)
+    with pytest.raises(ValueError):
+        kkt.solve_problem(p, kkt.FactorOptions(P=3))
+    with pytest.raises(ValueError):
+        kkt.solve_problem(p, kkt.FactorOptions(P=4, vlen=3))
+
+
+def test_no_device_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    lib = _lib.load()
+    h = C.c_void_p()
+    assert lib.cyq_ctx_create(0, C.byref(h)) == _lib.CYQ_NO_DEVICE
+    p = synth.generate(0, seed=0, batch=1, N=8)
+    with pytest.raises(kkt.CudaError):
+        kkt.solve_problem(p, kkt.FactorOptions(P=4))
