@@ -112,6 +112,14 @@ int cyq_factor_destroy(cyq_factor *factor);
 int cyq_factor_materialize(const cyq_factor *factor, int64_t inst, double *LH,
                            double *LB, double *Acl, double *LA);
 
+/* Per-kernel device timing: when enabled, every launch of the pipeline is
+ * bracketed by CUDA events on the context stream. `read` synchronizes and
+ * returns, per kernel (0 riccati_panel, 1 schur_cr, 2 backsub, 3 forward
+ * sweep), the summed milliseconds and launch counts since the last reset. */
+int cyq_ctx_profile(cyq_ctx *ctx, int enable);
+int cyq_ctx_profile_read(cyq_ctx *ctx, double *ms, int64_t *launches,
+                         int reset);
+
 /* Library build/runtime information (kernel names, tile shapes). */
 const char *cyq_version(void);
 

@@ -58,6 +58,9 @@ SIGNATURES = {
     "cyq_factor_destroy": (C.c_int, [C.c_void_p]),
     "cyq_factor_materialize": (C.c_int, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p,
                                          C.c_void_p]),
+    "cyq_ctx_profile": (C.c_int, [C.c_void_p, C.c_int]),
+    "cyq_ctx_profile_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(i64),
+                                       C.c_int]),
     "cyq_version": (C.c_char_p, []),
 }
 

@@ -28,6 +28,12 @@ struct cyq_ctx {
     size_t hbuf_bytes = 0;
     void *wsbuf = nullptr;
     size_t wsbuf_bytes = 0;
+    // per-kernel timing (cyq_ctx_profile)
+    bool profile = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+    std::vector<cudaEvent_t> pool;
+    double ms[4] = {0, 0, 0, 0};
+    int64_t launches[4] = {0, 0, 0, 0};
 };
 
 struct cyq_factor {
@@ -196,6 +202,37 @@ int riccati_warps(const Geo &g) {
 int schur_warps(const Geo &g) { return std::max(1, std::min(8, g.P / 2)); }
 int backsub_threads(const Geo &g) { return g.nux > 48 ? 128 : 32; }
 
+cudaEvent_t take_event(cyq_ctx *ctx) {
+    if (ctx->pool.empty()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    cudaEvent_t e = ctx->pool.back();
+    ctx->pool.pop_back();
+    return e;
+}
+
+// Brackets one launch with events when profiling is on.
+struct Timed {
+    cyq_ctx *ctx;
+    int kind;
+    cudaEvent_t a = nullptr, b = nullptr;
+    Timed(cyq_ctx *c, int k) : ctx(c), kind(k) {
+        if (ctx->profile) {
+            a = take_event(ctx);
+            b = take_event(ctx);
+            cudaEventRecord(a, ctx->stream);
+        }
+    }
+    ~Timed() {
+        if (ctx->profile) {
+            cudaEventRecord(b, ctx->stream);
+            ctx->ev.push_back({kind, {a, b}});
+        }
+    }
+};
+
 int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &ws,
                     const SolView *sol, bool do_solve) {
     static bool attrs = false;
@@ -209,15 +246,26 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
     const int chains = g.batch * g.P;
     CU(cudaMemsetAsync(ws.fail, 0xFF, sizeof(unsigned long long) * g.batch, ctx->stream));
     RiccatiArgs ra{g, p, ws.fac, ws.y, ws.wl, ws.trail, ws.fail};
-    riccati_panel_kernel<<<chains, 32 * riccati_warps(g), riccati_smem_bytes(g), ctx->stream>>>(ra);
+    {
+        Timed t(ctx, 0);
+        riccati_panel_kernel<<<chains, 32 * riccati_warps(g), riccati_smem_bytes(g),
+                               ctx->stream>>>(ra);
+    }
     CU(cudaGetLastError());
     SchurArgs sa{g, p, ws.fac, ws.y, ws.trail, ws.schur, ws.lamc,
                  sol ? sol->lam : nullptr, ws.fail, 1, do_solve ? 1 : 0};
-    schur_cr_kernel<<<g.batch, 32 * schur_warps(g), 0, ctx->stream>>>(sa);
+    {
+        Timed t(ctx, 1);
+        schur_cr_kernel<<<g.batch, 32 * schur_warps(g), 0, ctx->stream>>>(sa);
+    }
     CU(cudaGetLastError());
     if (do_solve) {
         BacksubArgs ba{g, p, ws.fac, ws.y, ws.wl, ws.lamc, *sol};
-        backsub_kernel<<<chains, backsub_threads(g), backsub_smem_bytes(g), ctx->stream>>>(ba);
+        {
+            Timed t(ctx, 2);
+            backsub_kernel<<<chains, backsub_threads(g), backsub_smem_bytes(g),
+                             ctx->stream>>>(ba);
+        }
         CU(cudaGetLastError());
     }
     return CYQ_OK;
@@ -311,6 +359,12 @@ int cyq_ctx_destroy(cyq_ctx *ctx) {
         cudaFree(ctx->hbuf);
     if (ctx->wsbuf)
         cudaFree(ctx->wsbuf);
+    for (auto &e : ctx->ev) {
+        cudaEventDestroy(e.second.first);
+        cudaEventDestroy(e.second.second);
+    }
+    for (auto e : ctx->pool)
+        cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream)
         cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -539,6 +593,39 @@ int cyq_factor_materialize(const cyq_factor *f, int64_t inst, double *LH, double
                         LA[((size_t)c * nx + r) * nx + k] = at(c, s, top + r, nu + k);
                 }
         }
+    return CYQ_OK;
+}
+
+int cyq_ctx_profile(cyq_ctx *ctx, int enable) {
+    if (!ctx)
+        return CYQ_INVALID_ARG;
+    ctx->profile = enable != 0;
+    return CYQ_OK;
+}
+
+int cyq_ctx_profile_read(cyq_ctx *ctx, double *ms, int64_t *launches, int reset) {
+    if (!ctx)
+        return CYQ_INVALID_ARG;
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (auto &e : ctx->ev) {
+        float t = 0;
+        CU(cudaEventElapsedTime(&t, e.second.first, e.second.second));
+        ctx->ms[e.first] += t;
+        ctx->launches[e.first] += 1;
+        ctx->pool.push_back(e.second.first);
+        ctx->pool.push_back(e.second.second);
+    }
+    ctx->ev.clear();
+    for (int k = 0; k < 4; ++k) {
+        if (ms)
+            ms[k] = ctx->ms[k];
+        if (launches)
+            launches[k] = ctx->launches[k];
+        if (reset) {
+            ctx->ms[k] = 0;
+            ctx->launches[k] = 0;
+        }
+    }
     return CYQ_OK;
 }
 

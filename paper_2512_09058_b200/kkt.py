@@ -96,6 +96,17 @@ class Context:
     def synchronize(self):
         self.lib.cyq_ctx_synchronize(self.h)
 
+    KERNELS = ("riccati_panel", "schur_cr", "backsub", "forward_sweep")
+
+    def profile(self, enable: bool = True):
+        self.lib.cyq_ctx_profile(self.h, int(enable))
+
+    def profile_read(self, reset: bool = True):
+        ms = (C.c_double * 4)()
+        n = (C.c_int64 * 4)()
+        self.lib.cyq_ctx_profile_read(self.h, ms, n, int(reset))
+        return {k: (ms[i], n[i]) for i, k in enumerate(self.KERNELS)}
+
     def __del__(self):
         try:
             if getattr(self, "h", None):
