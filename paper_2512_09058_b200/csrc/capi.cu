@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -195,9 +196,37 @@ ProbView view_of(const cyq_ocp_batch *p) {
     return v;
 }
 
-int riccati_warps(const Geo &g) {
+// Warps per chain CTA and register tiles per warp (MAXT template).
+void riccati_shape(const Geo &g, int &nw, int &maxt) {
     const int nt = g.TT * (g.TT + 1) / 2;
-    return std::max(1, std::min(8, nt / 6));
+    nw = 4;
+    if (const char *e = getenv("CYQ_RICCATI_WARPS"))
+        nw = std::max(1, std::min(4, atoi(e)));
+    while ((nt + nw - 1) / nw > 32 && nw < 4)
+        ++nw;
+    const int per = (nt + nw - 1) / nw;
+    maxt = per <= 4 ? 4 : per <= 8 ? 8 : per <= 16 ? 16 : 32;
+}
+
+template <int M> void launch_riccati_t(const Geo &g, int nw, cudaStream_t st, const RiccatiArgs &ra) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(riccati_panel_kernel_t<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             227 * 1024);
+        attr = true;
+    }
+    riccati_panel_kernel_t<M><<<g.batch * g.P, 32 * nw, riccati_smem_bytes(g), st>>>(ra);
+}
+
+void launch_riccati(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
+    int nw, maxt;
+    riccati_shape(g, nw, maxt);
+    switch (maxt) {
+    case 4: launch_riccati_t<4>(g, nw, st, ra); break;
+    case 8: launch_riccati_t<8>(g, nw, st, ra); break;
+    case 16: launch_riccati_t<16>(g, nw, st, ra); break;
+    default: launch_riccati_t<32>(g, nw, st, ra); break;
+    }
 }
 int schur_warps(const Geo &g) { return std::max(1, std::min(8, g.P / 2)); }
 int backsub_threads(const Geo &g) { return g.nux > 48 ? 128 : 32; }
@@ -237,8 +266,6 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
                     const SolView *sol, bool do_solve) {
     static bool attrs = false;
     if (!attrs) {
-        CU(cudaFuncSetAttribute(riccati_panel_kernel,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         CU(cudaFuncSetAttribute(backsub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 227 * 1024));
         attrs = true;
@@ -248,8 +275,7 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
     RiccatiArgs ra{g, p, ws.fac, ws.y, ws.wl, ws.trail, ws.fail};
     {
         Timed t(ctx, 0);
-        riccati_panel_kernel<<<chains, 32 * riccati_warps(g), riccati_smem_bytes(g),
-                               ctx->stream>>>(ra);
+        launch_riccati(g, ctx->stream, ra);
     }
     CU(cudaGetLastError());
     SchurArgs sa{g, p, ws.fac, ws.y, ws.trail, ws.schur, ws.lamc,
@@ -313,11 +339,6 @@ int ensure(cyq_ctx *ctx, void **buf, size_t *have, size_t need) {
 
 namespace cyqb {
 
-size_t riccati_smem_bytes(const Geo &g) {
-    const int nt = g.TT * (g.TT + 1) / 2;
-    const size_t vec = 32 * ((g.nx + 31) / 32) * 2 + 32 * ((g.nu + 31) / 32) + 32;
-    return ((size_t)(nt + g.TT * g.NXT) * kTileElems + vec) * sizeof(double);
-}
 size_t backsub_smem_bytes(const Geo &g) {
     const size_t vpad = 32 * ((g.nux + 31) / 32);
     return ((size_t)g.NPT * kTileElems + 8 * vpad) * sizeof(double);

@@ -85,7 +85,7 @@ struct SchurLayout {
     }
 };
 
-__global__ void riccati_panel_kernel(RiccatiArgs a);
+template <int MAXT> __global__ void riccati_panel_kernel_t(RiccatiArgs a);
 __global__ void schur_cr_kernel(SchurArgs a);
 __global__ void backsub_kernel(BacksubArgs a);
 

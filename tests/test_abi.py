@@ -39,10 +39,11 @@ def test_library_is_sm100a():
 
 
 def test_kernels_use_dmma():
-    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun",
-                          "_ZN4cyqb20riccati_panel_kernelENS_11RiccatiArgsE", _lib.LIB_PATH],
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _lib.LIB_PATH],
                          capture_output=True, text=True).stdout
-    assert "DMMA" in out
+    funcs = out.split("Function : ")
+    ric = [f for f in funcs if f.startswith("_ZN4cyqb22riccati_panel_kernel_t")]
+    assert ric and all("DMMA" in f for f in ric)
 
 
 def test_version_string():
