@@ -89,9 +89,9 @@ int make_geo(cyq_ctx *ctx, const cyq_dims *d, Geo &g) {
     g.NPT = g.CT * (g.CT + 1) / 2 + g.BT * g.CT;
     g.NTT = g.BT * (g.BT + 1) / 2;
     g.batch = (int)d->batch;
-    if (cyqb::riccati_smem_bytes(g) > 227 * 1024)
+    if (cyqb::riccati_smem_bytes(g) > 227 * 1024 || g.TT * (g.TT + 1) / 2 > 8 * 32)
         return set_err(ctx, CYQ_INVALID_ARG,
-                       "stage panel exceeds shared memory (nx + nu too large)");
+                       "stage panel too large (2 nx + nu > ~160 not supported)");
     return CYQ_OK;
 }
 
@@ -202,9 +202,11 @@ void riccati_shape(const Geo &g, int &nw, int &maxt) {
     nw = 4;
     if (const char *e = getenv("CYQ_RICCATI_WARPS"))
         nw = std::max(1, std::min(4, atoi(e)));
-    while ((nt + nw - 1) / nw > 32 && nw < 4)
-        ++nw;
-    const int per = (nt + nw - 1) / nw;
+    int per = (nt + nw - 1) / nw;
+    if (per > 16) { // large panels: the 256-thread, 32-tile-per-warp variant
+        nw = 8;
+        per = (nt + nw - 1) / nw;
+    }
     maxt = per <= 4 ? 4 : per <= 8 ? 8 : per <= 16 ? 16 : 32;
 }
 

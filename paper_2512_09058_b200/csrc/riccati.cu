@@ -113,7 +113,8 @@ __device__ __forceinline__ double panel_init(const Geo &g, const Bufs &bf, int s
 } // namespace
 
 template <int MAXT>
-__global__ void __launch_bounds__(128, (MAXT <= 8 ? 4 : 2)) riccati_panel_kernel_t(RiccatiArgs a) {
+__global__ void __launch_bounds__(MAXT == 32 ? 256 : 128, (MAXT <= 8 ? 4 : 1))
+riccati_panel_kernel_t(RiccatiArgs a) {
     extern __shared__ __align__(16) double sm[];
     const Geo &g = a.g;
     const int chain = blockIdx.x;
