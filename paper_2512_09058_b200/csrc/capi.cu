@@ -230,7 +230,6 @@ void launch_riccati(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
     default: launch_riccati_t<32>(g, nw, st, ra); break;
     }
 }
-int schur_warps(const Geo &g) { return std::max(1, std::min(8, g.P / 2)); }
 int backsub_threads(const Geo &g) { return g.nux > 48 ? 128 : 32; }
 
 cudaEvent_t take_event(cyq_ctx *ctx) {
@@ -270,6 +269,8 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
     if (!attrs) {
         CU(cudaFuncSetAttribute(backsub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 227 * 1024));
+        CU(cudaFuncSetAttribute(schur_cr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                227 * 1024));
         attrs = true;
     }
     const int chains = g.batch * g.P;
@@ -277,14 +278,15 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
     RiccatiArgs ra{g, p, ws.fac, ws.y, ws.wl, ws.trail, ws.fail};
     {
         Timed t(ctx, 0);
-        launch_riccati(g, ctx->stream, ra);
+        if (!launch_riccati_warp(g, ctx->stream, ra))
+            launch_riccati(g, ctx->stream, ra);
     }
     CU(cudaGetLastError());
     SchurArgs sa{g, p, ws.fac, ws.y, ws.trail, ws.schur, ws.lamc,
                  sol ? sol->lam : nullptr, ws.fail, 1, do_solve ? 1 : 0};
     {
         Timed t(ctx, 1);
-        schur_cr_kernel<<<g.batch, 32 * schur_warps(g), 0, ctx->stream>>>(sa);
+        schur_cr_kernel<<<g.batch, 32 * schur_warps(g), schur_smem_bytes(g), ctx->stream>>>(sa);
     }
     CU(cudaGetLastError());
     if (do_solve) {
@@ -345,7 +347,6 @@ size_t backsub_smem_bytes(const Geo &g) {
     const size_t vpad = 32 * ((g.nux + 31) / 32);
     return ((size_t)g.NPT * kTileElems + 8 * vpad) * sizeof(double);
 }
-size_t schur_smem_bytes(const Geo &) { return 0; }
 
 } // namespace cyqb
 

@@ -1,0 +1,474 @@
+// Warp-per-chain stage-panel Riccati kernel, specialised at compile time on
+// (nu, nx): the fast path for stage blocks up to nux = 32 (BASELINE configs
+// 0, 1, 2, 4). Same algorithm and outputs as riccati.cu (the runtime-shape
+// CTA kernel used for every other shape):
+//   kkt_factor.cpp:125-158  modified Riccati recursion (LH, LB, Acl, LA)
+//   kkt_factor.cpp:163-185  Mfwd = sum LB LB' + LA LA' (trailing block)
+//   kkt_solve.cpp:72-134    forward substitution + coupling rows (rhs row)
+//
+// One warp owns one partition column. The whole extended panel lives in the
+// warp's registers as 8x8 DMMA C-fragments (tile indices are compile-time,
+// so all index arithmetic folds away); the rank-8 block updates are DMMAs
+// whose A/B operands are the register tiles themselves (k permuted, no
+// shuffles). Shared memory holds only what must be re-read in another
+// layout: W = [V; ALQ; -wl] (operands of the next stage's W W' update),
+// L_Q (the transposed B operand of V = BA' L_Q) and the cp.async staging
+// buffers for the next stage's R, S, Q, B, A, r, q, f (issued one stage
+// ahead; full-sector 16-byte copies when aligned).
+#include "kkt_common.cuh"
+#include "kernels.h"
+
+namespace cyqb {
+
+namespace {
+
+template <int NU, int NX> struct Shp {
+    static constexpr int NUX = NU + NX;
+    static constexpr int CT = (NUX + 7) / 8;      // pivot tile columns
+    static constexpr int BT = (NX + 1 + 7) / 8;   // coupling + rhs tile rows
+    static constexpr int TT = CT + BT;
+    static constexpr int NT = TT * (TT + 1) / 2;
+    static constexpr int XT0 = NU / 8, XT1 = (NUX - 1) / 8, NXT = XT1 - XT0 + 1;
+    static constexpr int TOP = 8 * CT, RHS = TOP + NX;
+    static constexpr int NLQ = NXT * (NXT + 1) / 2; // x-x tiles of L_Q
+    static constexpr int NPT = CT * (CT + 1) / 2 + BT * CT;
+    // staging (doubles)
+    static constexpr int HB = NU * NU + NU * NX + NX * NX + NU + NX;
+    static constexpr int BB = NX * NU + NX * NX + NX;
+    static constexpr int HBp = (HB + 1) & ~1, BBp = (BB + 1) & ~1;
+    static constexpr int SMEM_DBL =
+        (TT * NXT + NLQ) * kTileElems + HBp + BBp + 2 * ((NX + 1) & ~1);
+    __host__ __device__ static constexpr int T(int i, int j) { return i * (i + 1) / 2 + j; }
+};
+
+__device__ __forceinline__ void cp8(double *dst, const double *src) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp16(double *dst, const double *src) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int K> __device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory");
+}
+
+// async copy of cnt doubles (16-byte granules when both ends are aligned),
+// or an identity / zero fill when src == nullptr
+template <int CNT, int DIAG>
+__device__ __forceinline__ void wcopy(double *dst, const double *src, int lane) {
+    if (src) {
+        const bool al = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+        if (al) {
+#pragma unroll
+            for (int i = 2 * lane; i < (CNT & ~1); i += 64)
+                cp16(dst + i, src + i);
+            if ((CNT & 1) && lane == 0)
+                cp8(dst + CNT - 1, src + CNT - 1);
+        } else {
+#pragma unroll
+            for (int i = lane; i < CNT; i += 32)
+                cp8(dst + i, src + i);
+        }
+    } else {
+#pragma unroll
+        for (int i = lane; i < CNT; i += 32)
+            dst[i] = (DIAG > 0 && i / (DIAG > 0 ? DIAG : 1) == i % (DIAG > 0 ? DIAG : 1)) ? 1.0 : 0.0;
+    }
+}
+
+template <int NU, int NX> struct Stage {
+    double *R, *S, *Q, *r, *q; // H buffer
+    double *B, *A, *f;         // BA buffer
+};
+
+template <int NU, int NX>
+__device__ __forceinline__ void load_H(const Geo &g, const ProbView &p, int b, int j, int xi,
+                                       const Stage<NU, NX> &st, int lane) {
+    const int N = g.N;
+    const bool in = j < N;
+    wcopy<NU * NU, NU>(st.R, in ? p.R + ((size_t)b * N + j) * NU * NU : nullptr, lane);
+    wcopy<NU * NX, 0>(st.S, in ? p.S + ((size_t)b * N + j) * NU * NX : nullptr, lane);
+    wcopy<NX * NX, NX>(st.Q, xi <= N ? p.Q + ((size_t)b * (N + 1) + xi) * NX * NX : nullptr,
+                       lane);
+    const double *rs = p.ru ? p.ru : p.r;
+    const double *qs = p.qx ? p.qx : p.q;
+    wcopy<NU, 0>(st.r, in ? rs + ((size_t)b * N + j) * NU : nullptr, lane);
+    wcopy<NX, 0>(st.q, xi <= N ? qs + ((size_t)b * (N + 1) + xi) * NX : nullptr, lane);
+}
+
+template <int NU, int NX>
+__device__ __forceinline__ void load_BA(const Geo &g, const ProbView &p, int b, int j,
+                                        const Stage<NU, NX> &st, int lane) {
+    const int N = g.N;
+    const bool in = j < N;
+    wcopy<NX * NU, 0>(st.B, in ? p.B + ((size_t)b * N + j) * NX * NU : nullptr, lane);
+    wcopy<NX * NX, 0>(st.A, (in && j != 0) ? p.A + ((size_t)b * N + j) * NX * NX : nullptr,
+                      lane);
+    const double *fs = p.fd ? p.fd : p.f;
+    wcopy<NX, 0>(st.f, in ? fs + ((size_t)b * N + j) * NX : nullptr, lane);
+}
+
+// initial entry (r, col) of a pivot tile (compile-time tile, runtime lane)
+template <int NU, int NX>
+__device__ __forceinline__ double pinit(const Stage<NU, NX> &st, bool s0, bool j0, double sgn,
+                                        const double *ru0, int r, int col) {
+    using S = Shp<NU, NX>;
+    if (r < S::TOP) {
+        if (r >= S::NUX || col >= S::NUX)
+            return r == col ? 1.0 : 0.0;
+        if (col > r)
+            return 0.0;
+        if (r < NU)
+            return st.R[r * NU + col];
+        if (col < NU)
+            return j0 ? 0.0 : st.S[col * NX + (r - NU)];
+        return st.Q[(r - NU) * NX + (col - NU)];
+    }
+    const int rb = r - S::TOP;
+    if (rb < NX) {
+        if (!s0 || col >= S::NUX)
+            return 0.0;
+        return col < NU ? st.B[rb * NU + col] : st.A[rb * NX + (col - NU)];
+    }
+    if (rb == NX) {
+        if (col < NU)
+            return sgn * st.r[col] - (ru0 ? ru0[col] : 0.0);
+        if (col < S::NUX)
+            return sgn * st.q[col - NU];
+    }
+    return 0.0;
+}
+
+} // namespace
+
+template <int NU, int NX, int WPB>
+__global__ void __launch_bounds__(32 * WPB) riccati_warp_kernel(RiccatiArgs a) {
+    using S = Shp<NU, NX>;
+    extern __shared__ __align__(16) double sm[];
+    const Geo &g = a.g;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int chain = blockIdx.x * WPB + wib;
+    if (chain >= g.batch * g.P)
+        return;
+    const int b = chain / g.P, c = chain % g.P, n = g.n;
+    const int rq = lane >> 2, cq = 2 * (lane & 3);
+
+    double *base = sm + (size_t)wib * S::SMEM_DBL;
+    double *Wsm = base;                                   // TT x NXT tiles
+    double *Lsm = Wsm + S::TT * S::NXT * kTileElems;      // NLQ tiles (x-x block of L)
+    Stage<NU, NX> st;
+    st.R = Lsm + S::NLQ * kTileElems;
+    st.S = st.R + NU * NU;
+    st.Q = st.S + NU * NX;
+    st.r = st.Q + NX * NX;
+    st.q = st.r + NU;
+    st.B = st.R + S::HBp;
+    st.A = st.B + NX * NU;
+    st.f = st.A + NX * NX;
+    double *ru0 = st.B + S::BBp; // NU (S_0 x_init), NX scratch after it
+    const bool implicit_rhs = (a.p.ru == nullptr);
+    const double sgn = implicit_rhs ? -1.0 : 1.0;
+    unsigned long long my_fail = ~0ull;
+
+    // prologue: H_0, BA_0 and the x_init term of ru[0]
+    {
+        const int j0 = g.stage_of(c, 0);
+        load_H<NU, NX>(g, a.p, b, j0, g.x_index_of(c, 0), st, lane);
+        load_BA<NU, NX>(g, a.p, b, j0, st, lane);
+        cp_commit();
+        if (implicit_rhs && c == 0 && lane < NU) {
+            double s0 = 0;
+            for (int k = 0; k < NX; ++k)
+                s0 += __ldg(a.p.S + (size_t)b * g.N * NU * NX + lane * NX + k) *
+                      __ldg(a.p.x_init + (size_t)b * NX + k);
+            ru0[lane] = s0;
+        }
+        cp_wait<0>();
+        __syncwarp();
+    }
+
+    Frag P[S::NT];
+#pragma unroll
+    for (int t = 0; t < S::NT; ++t)
+        P[t] = Frag{0.0, 0.0};
+
+    for (int s = 0; s < n; ++s) {
+        const int j = g.stage_of(c, s);
+        const double *ru0p = (implicit_rhs && j == 0) ? ru0 : nullptr;
+        if (s > 0) {
+            cp_wait<1>(); // H_s has landed (the newest group may still fly)
+            __syncwarp();
+        }
+        // ---- init pivot tiles, += W W' ------------------------------------
+#pragma unroll
+        for (int ti = 0; ti < S::TT; ++ti) {
+#pragma unroll
+            for (int tj = 0; tj <= ti; ++tj) {
+                Frag &f = P[S::T(ti, tj)];
+                if (tj < S::CT) {
+                    const int r = 8 * ti + rq, col = 8 * tj + cq;
+                    f.a = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, r, col);
+                    f.b = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, r, col + 1);
+                }
+                if (s > 0) {
+#pragma unroll
+                    for (int kt = 0; kt < S::NXT; ++kt)
+                        tile_gemm_nt(f, ld_frag(Wsm + (ti * S::NXT + kt) * kTileElems, lane),
+                                     ld_frag(Wsm + (tj * S::NXT + kt) * kTileElems, lane));
+                }
+            }
+        }
+        __syncwarp();
+        // the H buffer is free: prefetch H_{s+1} (and BA_1 at s = 0)
+        if (s + 1 < n) {
+            load_H<NU, NX>(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), st, lane);
+            if (s == 0)
+                load_BA<NU, NX>(g, a.p, b, g.stage_of(c, 1), st, lane);
+        }
+        cp_commit();
+
+        // ---- pivot floor: max |diag| of H_s + V V' (kernels.cpp:21-29) ----
+        double dmax = 0.0;
+#pragma unroll
+        for (int kb = 0; kb < S::CT; ++kb) {
+            const Frag &d = P[S::T(kb, kb)];
+            const double v = (rq & 1) ? d.b : d.a;
+            if ((lane & 3) == rq / 2 && 8 * kb + rq < S::NUX)
+                dmax = fmax(dmax, fabs(v));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        const double dfloor = 1e-14 * dmax;
+
+        // ---- blocked Cholesky of the pivot columns -------------------------
+#pragma unroll
+        for (int kb = 0; kb < S::CT; ++kb) {
+            Frag &dg = P[S::T(kb, kb)];
+            double inv[8], lc0[8], lc1[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const double vk = (k & 1) ? dg.b : dg.a;
+                double pv = __shfl_sync(0xffffffffu, vk, 4 * k + k / 2);
+                const double urk = __shfl_sync(0xffffffffu, vk, 4 * rq + k / 2);
+                const double uc0 = __shfl_sync(0xffffffffu, vk, 4 * cq + k / 2);
+                const double uc1 = __shfl_sync(0xffffffffu, vk, 4 * (cq + 1) + k / 2);
+                if (8 * kb + k < S::NUX && !(pv > dfloor && isfinite(pv))) {
+                    my_fail = min(my_fail, fail_key(kKindRiccati, c, s, 8 * kb + k));
+                    pv = 1.0;
+                }
+                const double iv = rsqrt(pv);
+                inv[k] = iv;
+                lc0[k] = uc0 * iv;
+                lc1[k] = uc1 * iv;
+                const double lrk = urk * iv;
+                if ((lane & 3) == k / 2) {
+                    double &e = (k & 1) ? dg.b : dg.a;
+                    if (rq == k)
+                        e = pv * iv;
+                    else if (rq > k)
+                        e = lrk;
+                }
+                if (cq > k && rq >= cq)
+                    dg.a -= lrk * lc0[k];
+                if (cq + 1 > k && rq >= cq + 1)
+                    dg.b -= lrk * lc1[k];
+            }
+            if (cq > rq) dg.a = 0.0;
+            if (cq + 1 > rq) dg.b = 0.0;
+            // sub-diagonal tiles X <- X L^{-T}, all rows interleaved (ILP)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+#pragma unroll
+                for (int ti = kb + 1; ti < S::TT; ++ti) {
+                    Frag &x = P[S::T(ti, kb)];
+                    const double vq = (q & 1) ? x.b : x.a;
+                    const double xrq = __shfl_sync(0xffffffffu, vq, 4 * rq + q / 2) * inv[q];
+                    if ((lane & 3) == q / 2) {
+                        if (q & 1) x.b = xrq;
+                        else x.a = xrq;
+                    }
+                    if (cq > q) x.a -= xrq * lc0[q];
+                    if (cq + 1 > q) x.b -= xrq * lc1[q];
+                }
+            }
+            // trailing update: C(ti,tj) -= L(ti,kb) L(tj,kb)'
+#pragma unroll
+            for (int tj = kb + 1; tj < S::TT; ++tj)
+#pragma unroll
+                for (int ti = tj; ti < S::TT; ++ti)
+                    tile_gemm_nt_sub(P[S::T(ti, tj)], P[S::T(ti, kb)], P[S::T(tj, kb)]);
+        }
+
+        // ---- store the factor tiles and y_s' ---------------------------------
+        {
+            double *dst = a.fac + ((size_t)chain * n + s) * S::NPT * kTileElems;
+            int o = 0;
+#pragma unroll
+            for (int ti = 0; ti < S::TT; ++ti)
+#pragma unroll
+                for (int tj = 0; tj < S::CT; ++tj)
+                    if (tj <= ti) {
+                        st_frag(dst + o * kTileElems, lane, P[S::T(ti, tj)]);
+                        ++o;
+                    }
+            constexpr int RT = S::RHS / 8, RR = S::RHS % 8;
+            if (rq == RR) {
+                double *yv = a.y + ((size_t)chain * n + s) * S::NUX;
+#pragma unroll
+                for (int tj = 0; tj < S::CT; ++tj) {
+                    const int col = 8 * tj + cq;
+                    if (col < S::NUX) yv[col] = P[S::T(RT, tj)].a;
+                    if (col + 1 < S::NUX) yv[col + 1] = P[S::T(RT, tj)].b;
+                }
+            }
+        }
+
+        if (s + 1 < n) {
+            // ---- W for stage s+1 -------------------------------------------
+            if (s == 0) cp_wait<0>();
+            else cp_wait<1>();   // BA_{s+1} has landed
+            __syncwarp();
+            // -wl_new = L_Q' wl + x'  (kkt_solve.cpp:85-90), column-wise
+            // reduction over the 8 rows of each tile row group
+            double mw[S::NXT][2];
+#pragma unroll
+            for (int kt = 0; kt < S::NXT; ++kt) {
+                const int ct = S::XT0 + kt;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int C = 8 * ct + cq + e;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int ti = ct; ti < S::CT; ++ti) {
+                        const int K = 8 * ti + rq;
+                        const double lv = e ? P[S::T(ti, ct)].b : P[S::T(ti, ct)].a;
+                        if (K >= NU && K < S::NUX && K >= C && C >= NU && C < S::NUX)
+                            acc += lv * (sgn * st.f[K - NU]);
+                    }
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 8);
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+                    constexpr int RT = S::RHS / 8, RR = S::RHS % 8;
+                    const double xr = e ? P[S::T(RT, ct)].b : P[S::T(RT, ct)].a;
+                    const double xp = __shfl_sync(0xffffffffu, xr, 4 * RR + (lane & 3));
+                    mw[kt][e] = (C >= NU && C < S::NUX) ? acc + xp : 0.0;
+                }
+            }
+            if (rq == 0) {
+                double *wl = a.wl + ((size_t)chain * n + s) * NX;
+#pragma unroll
+                for (int kt = 0; kt < S::NXT; ++kt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int C = 8 * (S::XT0 + kt) + cq + e;
+                        if (C >= NU && C < S::NUX)
+                            wl[C - NU] = -mw[kt][e];
+                    }
+            }
+            // W bottom rows: ALQ (x columns of the coupling rows), rhs row -wl
+#pragma unroll
+            for (int ti = S::CT; ti < S::TT; ++ti)
+#pragma unroll
+                for (int kt = 0; kt < S::NXT; ++kt) {
+                    const int ct = S::XT0 + kt;
+                    Frag w = P[S::T(ti, ct)];
+                    const int r = 8 * ti + rq, c0 = 8 * ct + cq;
+                    if (r == S::RHS) {
+                        w.a = mw[kt][0];
+                        w.b = mw[kt][1];
+                    } else if (r > S::RHS) {
+                        w.a = w.b = 0.0;
+                    }
+                    if (c0 < NU || c0 >= S::NUX) w.a = 0.0;
+                    if (c0 + 1 < NU || c0 + 1 >= S::NUX) w.b = 0.0;
+                    st_frag(Wsm + (ti * S::NXT + kt) * kTileElems, lane, w);
+                }
+            // L_Q tiles (x rows/cols, masked) -> Lsm for the transposed access
+#pragma unroll
+            for (int u = 0; u < S::NXT; ++u)
+#pragma unroll
+                for (int v = 0; v <= u; ++v) {
+                    Frag w = P[S::T(S::XT0 + u, S::XT0 + v)];
+                    const int K = 8 * (S::XT0 + u) + rq, C0 = 8 * (S::XT0 + v) + cq;
+                    const bool rin = K >= NU && K < S::NUX;
+                    if (!(rin && C0 >= NU && C0 < S::NUX && C0 <= K)) w.a = 0.0;
+                    if (!(rin && C0 + 1 >= NU && C0 + 1 < S::NUX && C0 + 1 <= K)) w.b = 0.0;
+                    st_frag(Lsm + S::T(u, v) * kTileElems, lane, w);
+                }
+            __syncwarp();
+            // V = BA_{s+1}' L_Q : rows 0..nux-1 of W (DMMA)
+#pragma unroll
+            for (int ti = 0; ti < S::CT; ++ti) {
+#pragma unroll
+                for (int kt = 0; kt < S::NXT; ++kt) {
+                    const int ct = S::XT0 + kt;
+                    Frag f{0.0, 0.0};
+                    const int r = 8 * ti + rq;
+#pragma unroll
+                    for (int ks = 2 * S::XT0; ks < 2 * (S::XT1 + 1); ++ks) {
+                        if (4 * ks + 3 < 8 * ct)
+                            continue; // L_Q upper part is zero
+                        const int K = 4 * ks + (lane & 3);
+                        double av = 0.0;
+                        if (K >= NU && K < S::NUX && r < S::NUX)
+                            av = r < NU ? st.B[(K - NU) * NU + r] : st.A[(K - NU) * NX + (r - NU)];
+                        // B[kk][n] = L[K][8ct + n]: tile (K/8, ct) of Lsm
+                        const int u = ks / 2 - S::XT0, v = kt;
+                        const double bv =
+                            Lsm[S::T(u, v) * kTileElems + (4 * (ks & 1) + (lane & 3)) * 8 + (lane >> 2)];
+                        dmma(f, av, bv);
+                    }
+                    st_frag(Wsm + (ti * S::NXT + kt) * kTileElems, lane, f);
+                }
+            }
+            __syncwarp();
+            if (s + 2 < n)
+                load_BA<NU, NX>(g, a.p, b, g.stage_of(c, s + 2), st, lane);
+            cp_commit();
+        }
+    }
+
+    // trailing tiles (coupling x coupling = -Mfwd, rhs x coupling = -fwd)
+#pragma unroll
+    for (int u = 0; u < S::BT; ++u)
+#pragma unroll
+        for (int v = 0; v <= u; ++v)
+            st_frag(a.trail + ((size_t)chain * g.NTT + S::T(u, v)) * kTileElems, lane,
+                    P[S::T(S::CT + u, S::CT + v)]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        my_fail = min(my_fail, __shfl_xor_sync(0xffffffffu, my_fail, o));
+    if (lane == 0 && my_fail != ~0ull)
+        atomicMin(a.fail + b, my_fail);
+}
+
+// ---- dispatch ----------------------------------------------------------------
+namespace {
+template <int NU, int NX, int WPB> bool launch_w(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
+    if (g.nu != NU || g.nx != NX)
+        return false;
+    using S = Shp<NU, NX>;
+    const size_t smem = (size_t)WPB * S::SMEM_DBL * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(riccati_warp_kernel<NU, NX, WPB>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const int chains = g.batch * g.P;
+    riccati_warp_kernel<NU, NX, WPB><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ra);
+    return true;
+}
+} // namespace
+
+bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
+    if (getenv("CYQ_NO_WARP_KERNEL"))
+        return false;
+    return launch_w<10, 20, 2>(g, st, ra) || launch_w<8, 16, 2>(g, st, ra) ||
+           launch_w<4, 12, 2>(g, st, ra) || launch_w<5, 10, 2>(g, st, ra);
+}
+
+} // namespace cyqb

@@ -2,120 +2,129 @@
 // system, one CTA per OCP instance (warps take independent blocks).
 //
 // Restates:
-//   kkt_factor.cpp:163-178   T = L_Q^{-T}, Mbwd = T T', W = T LA'
-//   kkt_factor.cpp:194-212   assemble_schur (diag, subdiag)
+//   kkt_factor.cpp:163-178    T = L_Q^{-T}, Mbwd = T T', W = T LA'
+//   kkt_factor.cpp:194-212    assemble_schur (diag, subdiag)
 //   block_tridiag.cpp:126-238 cr_level / cr_factor / cr_factor_base (non-circular)
 //   kkt_solve.cpp:137-182     Schur rhs, CRFactor::forward/backward, negate
 //   block_tridiag.cpp:252-333 CRFactor::forward / backward
-// Blocks live in a per-instance global workspace (L2-resident); all block
-// kernels are warp-cooperative and deterministic (fixed reduction order).
+// The level arrays live in a per-instance global workspace (L2-resident);
+// every block operation stages its operands in per-warp shared-memory
+// scratch (row stride nx|1 to avoid bank conflicts) and runs warp-wide.
+// Fixed reduction orders: results are bit-reproducible.
 #include "kernels.h"
+
+#include <algorithm>
 
 namespace cyqb {
 
 namespace {
 
-// ---- warp-level dense kernels on row-major n x n blocks (ld = n) --------
+__device__ __forceinline__ int stride_of(int n) { return n | 1; }
 
-// In-place lower Cholesky; potrf semantics of kernels.cpp:32-58 (relative
+// copy an n x n block global (ld n) -> scratch (ld s); lower only if `lower`
+__device__ void w_load(double *dst, int s, const double *src, int n, bool lower, bool trans,
+                       int lane) {
+    for (int e = lane; e < n * n; e += 32) {
+        const int r = e / n, c = e % n;
+        const double v = trans ? src[c * n + r] : src[e];
+        dst[r * s + c] = (!lower || c <= r) ? v : 0.0;
+    }
+    __syncwarp();
+}
+__device__ void w_store(double *dst, const double *src, int s, int n, double scale, int lane) {
+    __syncwarp();
+    for (int e = lane; e < n * n; e += 32)
+        dst[e] = scale * src[(e / n) * s + e % n];
+}
+
+// In-place lower Cholesky (potrf semantics of kernels.cpp:32-58: relative
 // pivot floor 1e-14 * max|diag| of the input). Returns failing pivot or -1.
-__device__ int w_potrf(double *A, int n, int lane) {
+__device__ int w_potrf(double *A, int s, int n, int lane) {
     double dmax = 0;
     for (int d = 0; d < n; ++d)
-        dmax = fmax(dmax, fabs(A[d * n + d]));
+        dmax = fmax(dmax, fabs(A[d * s + d]));
     int fail = -1;
     for (int k = 0; k < n; ++k) {
         __syncwarp();
-        double pv = A[k * n + k];
+        double pv = A[k * s + k];
         if (!(pv > 1e-14 * dmax && isfinite(pv))) {
             if (fail < 0) fail = k;
             pv = 1.0;
         }
-        const double d = sqrt(pv), inv = 1.0 / d;
+        const double iv = rsqrt(pv);
         __syncwarp();
         if (lane == 0)
-            A[k * n + k] = d;
+            A[k * s + k] = pv * iv;
         for (int i = k + 1 + lane; i < n; i += 32)
-            A[i * n + k] *= inv;
+            A[i * s + k] *= iv;
         __syncwarp();
-        for (int i = k + 1 + lane; i < n; i += 32) {
-            const double lik = A[i * n + k];
-            for (int j = k + 1; j <= i; ++j)
-                A[i * n + j] -= lik * A[j * n + k];
+        for (int e = lane; e < (n - k - 1) * (n - k - 1); e += 32) {
+            const int i = k + 1 + e / (n - k - 1), j = k + 1 + e % (n - k - 1);
+            if (j <= i)
+                A[i * s + j] -= A[i * s + k] * A[j * s + k];
         }
     }
-    __syncwarp();
-    // zero the strict upper triangle: the factor is lower triangular
-    for (int i = lane; i < n; i += 32)
-        for (int j = i + 1; j < n; ++j)
-            A[i * n + j] = 0.0;
     __syncwarp();
     return fail;
 }
 
-// B (m x n) <- B L^{-T}   (TrsmMode::right_lower_trans), rows per lane.
-__device__ void w_trsm_rlt(double *B, int m, int n, const double *L, int lane) {
+// B (m x n) <- B L^{-T}  (TrsmMode::right_lower_trans), a row per lane
+__device__ void w_trsm_rlt(double *B, int sb, int m, int n, const double *L, int sl, int lane) {
     for (int r = lane; r < m; r += 32) {
-        double *br = B + r * n;
+        double *br = B + r * sb;
         for (int c = 0; c < n; ++c) {
             double x = br[c];
             for (int k = 0; k < c; ++k)
-                x -= br[k] * L[c * n + k];
-            br[c] = x / L[c * n + c];
+                x -= br[k] * L[c * sl + k];
+            br[c] = x / L[c * sl + c];
         }
     }
     __syncwarp();
 }
 
-// C (lower) -= A A'
-__device__ void w_syrk_sub(double *C, const double *A, int n, int lane) {
-    for (int i = lane; i < n; i += 32)
-        for (int j = 0; j <= i; ++j) {
-            double s = 0;
-            for (int k = 0; k < n; ++k)
-                s += A[i * n + k] * A[j * n + k];
-            C[i * n + j] -= s;
-        }
-    __syncwarp();
-}
-
-// x <- L^{-1} x (lower, column-oriented); x shared in global/smem
-__device__ void w_trsv_l(const double *L, double *x, int n, int lane) {
-    for (int k = 0; k < n; ++k) {
-        __syncwarp();
-        const double xk = x[k] / L[k * n + k];
-        __syncwarp();
-        if (lane == 0)
-            x[k] = xk;
-        for (int i = k + 1 + lane; i < n; i += 32)
-            x[i] -= L[i * n + k] * xk;
+// C (lower) -= A A'   (all n x n elements spread over lanes)
+__device__ void w_syrk_sub(double *C, int sc, const double *A, int sa, int n, int lane) {
+    for (int e = lane; e < n * n; e += 32) {
+        const int i = e / n, j = e % n;
+        if (j > i)
+            continue;
+        double acc = 0;
+        for (int k = 0; k < n; ++k)
+            acc += A[i * sa + k] * A[j * sa + k];
+        C[i * sc + j] -= acc;
     }
     __syncwarp();
 }
 
-// x <- L^{-T} x
-__device__ void w_trsv_lt(const double *L, double *x, int n, int lane) {
-    for (int k = n - 1; k >= 0; --k) {
+// x <- L^{-1} x / L^{-T} x  (global or shared vectors; column-oriented)
+__device__ void w_trsv(const double *L, int sl, double *x, int n, bool trans, int lane) {
+    for (int kk = 0; kk < n; ++kk) {
+        const int k = trans ? n - 1 - kk : kk;
         __syncwarp();
-        const double xk = x[k] / L[k * n + k];
+        const double xk = x[k] / L[k * sl + k];
         __syncwarp();
         if (lane == 0)
             x[k] = xk;
-        for (int i = lane; i < k; i += 32)
-            x[i] -= L[k * n + i] * xk;
+        if (!trans) {
+            for (int i = k + 1 + lane; i < n; i += 32)
+                x[i] -= L[i * sl + k] * xk;
+        } else {
+            for (int i = lane; i < k; i += 32)
+                x[i] -= L[k * sl + i] * xk;
+        }
     }
     __syncwarp();
 }
 
 // y -= op(A) x
-__device__ void w_gemv_sub(const double *A, bool trans, const double *x,
-                           double *y, int n, int lane) {
+__device__ void w_gemv_sub(const double *A, bool trans, const double *x, double *y, int n,
+                           int lane) {
     __syncwarp();
     for (int i = lane; i < n; i += 32) {
-        double s = 0;
+        double acc = 0;
         for (int k = 0; k < n; ++k)
-            s += (trans ? A[k * n + i] : A[i * n + k]) * x[k];
-        y[i] -= s;
+            acc += (trans ? A[k * n + i] : A[i * n + k]) * x[k];
+        y[i] -= acc;
     }
     __syncwarp();
 }
@@ -123,110 +132,129 @@ __device__ void w_gemv_sub(const double *A, bool trans, const double *x,
 __device__ __forceinline__ int stored_tile(const Geo &g, int ti, int tj) {
     return ti < g.CT ? tri_index(ti, tj) : g.CT * (g.CT + 1) / 2 + (ti - g.CT) * g.CT + tj;
 }
-// entry (r, col) of the stored pivot tiles of one stage
 __device__ __forceinline__ double fac_at(const Geo &g, const double *st, int r, int col) {
     return st[stored_tile(g, r / 8, col / 8) * kTileElems + (r % 8) * 8 + col % 8];
 }
 
 } // namespace
 
+size_t schur_smem_bytes(const Geo &g) {
+    const int s = stride_of(g.nx);
+    return (size_t)schur_warps(g) * 4 * g.nx * s * sizeof(double);
+}
+
+int schur_warps(const Geo &g) {
+    const size_t per = 4 * (size_t)g.nx * stride_of(g.nx) * sizeof(double);
+    int nw = (int)std::min<size_t>(8, (200 * 1024) / per);
+    nw = nw < 1 ? 1 : nw;
+    const int want = g.P / 2 > 1 ? g.P / 2 : 1;
+    return nw < want ? nw : want;
+}
+
 __global__ void __launch_bounds__(256) schur_cr_kernel(SchurArgs a) {
+    extern __shared__ __align__(16) double sm[];
     const Geo &g = a.g;
     const int b = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int NW = blockDim.x >> 5;
     const int P = g.P, nx = g.nx, nu = g.nu, n = g.n;
+    const int ss = stride_of(nx);
     const long long nn = (long long)nx * nx;
     const SchurLayout L = SchurLayout::make(P, nx);
     double *ws = a.schur + (size_t)b * L.total;
-    double *D = ws + L.D, *K = ws + L.K, *Mb = ws + L.Mb, *Z = ws + L.Z;
+    double *D = ws + L.D, *K = ws + L.K, *Mb = ws + L.Mb, *Zg = ws + L.Z;
     double *bn = ws + L.bn, *rhs = ws + L.rhs;
     const int top = 8 * g.CT;
+    double *S0 = sm + (size_t)warp * 4 * nx * ss, *S1 = S0 + nx * ss, *S2 = S1 + nx * ss,
+           *S3 = S2 + nx * ss;
     unsigned long long my_fail = ~0ull;
 
-    if (a.do_factor || a.do_solve) {
-        // ---- phase 1: per-column Schur contributions ----------------------
-        for (int c = warp; c < P; c += NW) {
-            const size_t chain = (size_t)b * P + c;
-            const double *st = a.fac + (chain * n + (n - 1)) * g.NPT * kTileElems;
-            double *Zc = Z + c * nn;
-            // Z = L_Q^{-1} (column per lane), L_Q = LH_{n-1}[nu:, nu:]
+    // ---- phase 1: per-column T-contributions (Z = L_Q^{-1} = T') --------
+    for (int c = warp; c < P; c += NW) {
+        const size_t chain = (size_t)b * P + c;
+        const double *st = a.fac + (chain * n + (n - 1)) * g.NPT * kTileElems;
+        double *Zc = Zg + c * nn;
+        if (a.do_factor) {
+            // L_Q of the last stage position -> S0, LA -> S1
+            for (int e = lane; e < nx * nx; e += 32) {
+                const int r = e / nx, k = e % nx;
+                S0[r * ss + k] = k <= r ? fac_at(g, st, nu + r, nu + k) : 0.0;
+                S1[r * ss + k] = fac_at(g, st, top + r, nu + k);
+            }
+            __syncwarp();
+            // Z = L_Q^{-1}: column per lane (trtri, kernels.cpp:246-271)
             for (int jc = lane; jc < nx; jc += 32) {
                 for (int i = 0; i < jc; ++i)
-                    Zc[i * nx + jc] = 0.0;
-                Zc[jc * nx + jc] = 1.0 / fac_at(g, st, nu + jc, nu + jc);
+                    S2[i * ss + jc] = 0.0;
+                S2[jc * ss + jc] = 1.0 / S0[jc * ss + jc];
                 for (int i = jc + 1; i < nx; ++i) {
-                    double s = 0;
+                    double acc = 0;
                     for (int k = jc; k < i; ++k)
-                        s += fac_at(g, st, nu + i, nu + k) * Zc[k * nx + jc];
-                    Zc[i * nx + jc] = -s / fac_at(g, st, nu + i, nu + i);
+                        acc += S0[i * ss + k] * S2[k * ss + jc];
+                    S2[i * ss + jc] = -acc / S0[i * ss + i];
                 }
             }
             __syncwarp();
-            if (a.do_factor) {
-                // Mbwd = T T' = Z' Z ; K[c-1] = -W' = -(LA Z) ; D[c] = Mfwd_c
-                const double *tr = a.trail + chain * g.NTT * kTileElems;
-                for (int i = lane; i < nx; i += 32) {
-                    for (int jj = 0; jj < nx; ++jj) {
-                        double s = 0;
-                        for (int k = max(i, jj); k < nx; ++k)
-                            s += Zc[k * nx + i] * Zc[k * nx + jj];
-                        Mb[c * nn + i * nx + jj] = s;
-                        // -Mfwd lives in the trailing coupling block (lower)
-                        const int r = max(i, jj), cc = min(i, jj);
-                        const int u = r / 8, v = cc / 8;
-                        D[c * nn + i * nx + jj] =
-                            -tr[tri_index(u, v) * kTileElems + (r % 8) * 8 + cc % 8];
-                        if (c > 0) {
-                            double w = 0;
-                            for (int k = jj; k < nx; ++k)
-                                w += fac_at(g, st, top + i, nu + k) * Zc[k * nx + jj];
-                            K[(c - 1) * nn + i * nx + jj] = -w;
-                        }
-                    }
-                }
-                if (c == P - 1)
-                    for (int i = lane; i < nn; i += 32)
-                        K[(P - 1) * nn + i] = 0.0;
-            }
-            if (a.do_solve) {
-                // bwd_neg_c = T x'_{n-1} = Z' x'
-                const double *yv = a.y + (chain * n + (n - 1)) * g.nux;
-                for (int i = lane; i < nx; i += 32) {
-                    double s = 0;
-                    for (int k = i; k < nx; ++k)
-                        s += Zc[k * nx + i] * yv[nu + k];
-                    bn[c * nx + i] = s;
+            w_store(Zc, S2, ss, nx, 1.0, lane);
+            // Mbwd = Z' Z ; K[c-1] = -(LA Z) ; D[c] = Mfwd_c (from -Mfwd trail)
+            const double *tr = a.trail + chain * g.NTT * kTileElems;
+            for (int e = lane; e < nx * nx; e += 32) {
+                const int i = e / nx, jj = e % nx;
+                double m = 0;
+                for (int k = max(i, jj); k < nx; ++k)
+                    m += S2[k * ss + i] * S2[k * ss + jj];
+                Mb[c * nn + e] = m;
+                const int r = max(i, jj), cc = min(i, jj);
+                D[c * nn + e] = -tr[tri_index(r / 8, cc / 8) * kTileElems + (r % 8) * 8 + cc % 8];
+                if (c > 0) {
+                    double w = 0;
+                    for (int k = jj; k < nx; ++k)
+                        w += S1[i * ss + k] * S2[k * ss + jj];
+                    K[(c - 1) * nn + e] = -w;
                 }
             }
+            if (c == P - 1)
+                for (int e = lane; e < nn; e += 32)
+                    K[(P - 1) * nn + e] = 0.0;
         }
-        __syncthreads();
-        // ---- phase 1b: diag += Mbwd of the next column; Schur rhs --------
-        if (a.do_factor)
-            for (long long e = threadIdx.x; e < (long long)P * nn; e += blockDim.x) {
-                const int c = (int)(e / nn);
-                D[e] += Mb[((c + 1) % P) * nn + (e % nn)];
-            }
         if (a.do_solve) {
-            ProbAcc pa{a.p, g, b};
-            for (int e = threadIdx.x; e < P * nx; e += blockDim.x) {
-                const int i = e / nx, k = e % nx;
-                const int jst = n * i;
-                double v = pa.fd(jst, k);
-                if (jst == 0 && a.p.fd == nullptr) // fd[0] -= A_0 x_init
-                    for (int m = 0; m < nx; ++m)
-                        v -= pa.A(0, k, m) * __ldg(a.p.x_init + (size_t)b * nx + m);
-                const size_t chain = (size_t)b * P + i;
-                const double *tr = a.trail + chain * g.NTT * kTileElems;
-                const int rr = nx; // rhs row inside the trailing block
-                // trailing (rhs, coupling k) = -fwd_i[k]
-                v += tr[tri_index(rr / 8, k / 8) * kTileElems + (rr % 8) * 8 + k % 8];
-                v += bn[((i + 1) % P) * nx + k];
-                rhs[e] = v;
+            // bwd_neg_c = T x'_{n-1} = Z' x'
+            __syncwarp();
+            const double *yv = a.y + (chain * n + (n - 1)) * g.nux;
+            for (int i = lane; i < nx; i += 32) {
+                double acc = 0;
+                for (int k = i; k < nx; ++k)
+                    acc += Zc[k * nx + i] * yv[nu + k];
+                bn[c * nx + i] = acc;
             }
         }
-        __syncthreads();
+        __syncwarp();
     }
+    __syncthreads();
+    // ---- phase 1b: diag += Mbwd of the next column; Schur rhs -----------
+    if (a.do_factor)
+        for (long long e = threadIdx.x; e < (long long)P * nn; e += blockDim.x) {
+            const int c = (int)(e / nn);
+            D[e] += Mb[((c + 1) % P) * nn + (e % nn)];
+        }
+    if (a.do_solve) {
+        ProbAcc pa{a.p, g, b};
+        for (int e = threadIdx.x; e < P * nx; e += blockDim.x) {
+            const int i = e / nx, k = e % nx;
+            const int jst = n * i;
+            double v = pa.fd(jst, k);
+            if (jst == 0 && a.p.fd == nullptr) // fd[0] -= A_0 x_init
+                for (int m = 0; m < nx; ++m)
+                    v -= pa.A(0, k, m) * __ldg(a.p.x_init + (size_t)b * nx + m);
+            const size_t chain = (size_t)b * P + i;
+            const double *tr = a.trail + chain * g.NTT * kTileElems;
+            const int rr = nx; // rhs row inside the trailing block: -fwd_i
+            v += tr[tri_index(rr / 8, k / 8) * kTileElems + (rr % 8) * 8 + k % 8];
+            v += bn[((i + 1) % P) * nx + k];
+            rhs[e] = v;
+        }
+    }
+    __syncthreads();
 
     // ---- phase 2: cyclic reduction factor (block_tridiag.cpp:126-238) ----
     if (a.do_factor) {
@@ -240,52 +268,57 @@ __global__ void __launch_bounds__(256) schur_cr_kernel(SchurArgs a) {
             double *K2 = ws + L.level(l, P, nx, 4);
             for (int mm = warp; mm < half; mm += NW) {
                 const int k = 2 * mm + 1;
-                double *Lm = Ll + mm * nn, *Um = Ul + mm * nn, *Ym = Yl + mm * nn;
-                for (int e = lane; e < nn; e += 32) {
-                    const int r = e / nx, cc = e % nx;
-                    Lm[e] = r >= cc ? Ml[k * nn + e] : 0.0;
-                    Um[e] = Kl[(k - 1) * nn + cc * nx + r];
-                    Ym[e] = k < s - 1 ? Kl[k * nn + e] : 0.0;
-                }
-                __syncwarp();
-                const int pf = w_potrf(Lm, nx, lane);
+                w_load(S0, ss, Ml + k * nn, nx, true, false, lane);
+                w_load(S1, ss, Kl + (k - 1) * nn, nx, false, true, lane); // U = K_{k-1}'
+                const int pf = w_potrf(S0, ss, nx, lane);
                 if (pf >= 0)
                     my_fail = min(my_fail, fail_key(kKindCR, l, k, pf));
-                w_trsm_rlt(Um, nx, nx, Lm, lane);
-                if (k < s - 1)
-                    w_trsm_rlt(Ym, nx, nx, Lm, lane);
+                w_trsm_rlt(S1, ss, nx, nx, S0, ss, lane);
+                w_store(Ll + mm * nn, S0, ss, nx, 1.0, lane);
+                w_store(Ul + mm * nn, S1, ss, nx, 1.0, lane);
+                if (k < s - 1) {
+                    w_load(S2, ss, Kl + k * nn, nx, false, false, lane);
+                    w_trsm_rlt(S2, ss, nx, nx, S0, ss, lane);
+                    w_store(Yl + mm * nn, S2, ss, nx, 1.0, lane);
+                } else {
+                    for (int e = lane; e < nn; e += 32)
+                        Yl[mm * nn + e] = 0.0;
+                }
             }
             __syncthreads();
             for (int mm = warp; mm < half; mm += NW) {
-                double *Md = M2 + mm * nn, *Kd = K2 + mm * nn;
-                for (int e = lane; e < nn; e += 32)
-                    Md[e] = Ml[2 * mm * nn + e];
-                __syncwarp();
-                w_syrk_sub(Md, Ul + mm * nn, nx, lane);
-                if (mm > 0)
-                    w_syrk_sub(Md, Yl + (mm - 1) * nn, nx, lane);
-                for (int e = lane; e < nn; e += 32) {
-                    const int r = e / nx, cc = e % nx;
-                    double v = 0;
-                    if (mm < half - 1)
-                        for (int q = 0; q < nx; ++q)
-                            v -= Yl[mm * nn + r * nx + q] * Ul[mm * nn + cc * nx + q];
-                    Kd[e] = v;
+                w_load(S0, ss, Ml + 2 * mm * nn, nx, true, false, lane);
+                w_load(S1, ss, Ul + mm * nn, nx, false, false, lane);
+                w_syrk_sub(S0, ss, S1, ss, nx, lane);
+                if (mm > 0) {
+                    w_load(S2, ss, Yl + (mm - 1) * nn, nx, false, false, lane);
+                    w_syrk_sub(S0, ss, S2, ss, nx, lane);
                 }
+                w_store(M2 + mm * nn, S0, ss, nx, 1.0, lane);
+                if (mm < half - 1) { // K' = -Y U'
+                    w_load(S3, ss, Yl + mm * nn, nx, false, false, lane);
+                    for (int e = lane; e < nn; e += 32) {
+                        const int r = e / nx, cc = e % nx;
+                        double acc = 0;
+                        for (int q = 0; q < nx; ++q)
+                            acc += S3[r * ss + q] * S1[cc * ss + q];
+                        K2[mm * nn + e] = -acc;
+                    }
+                } else {
+                    for (int e = lane; e < nn; e += 32)
+                        K2[mm * nn + e] = 0.0;
+                }
+                __syncwarp();
             }
             __syncthreads();
         }
         if (warp == 0) {
             const double *Mlast = L.levels == 0 ? D : ws + L.level(L.levels - 1, P, nx, 3);
-            double *Lb = ws + L.Lbase;
-            for (int e = lane; e < nn; e += 32) {
-                const int r = e / nx, cc = e % nx;
-                Lb[e] = r >= cc ? Mlast[e] : 0.0;
-            }
-            __syncwarp();
-            const int pf = w_potrf(Lb, nx, lane);
+            w_load(S0, ss, Mlast, nx, true, false, lane);
+            const int pf = w_potrf(S0, ss, nx, lane);
             if (pf >= 0)
                 my_fail = min(my_fail, fail_key(kKindCR, L.levels, 0, pf));
+            w_store(ws + L.Lbase, S0, ss, nx, 1.0, lane);
         }
         __syncthreads();
     }
@@ -299,7 +332,7 @@ __global__ void __launch_bounds__(256) schur_cr_kernel(SchurArgs a) {
             const double *Ll = ws + L.level(l, P, nx, 0), *Ul = ws + L.level(l, P, nx, 1);
             const double *Yl = ws + L.level(l, P, nx, 2);
             for (int mm = warp; mm < half; mm += NW)
-                w_trsv_l(Ll + mm * nn, x + (2 * mm + 1) * stride * nx, nx, lane);
+                w_trsv(Ll + mm * nn, nx, x + (2 * mm + 1) * stride * nx, nx, false, lane);
             __syncthreads();
             for (int mm = warp; mm < half; mm += NW) {
                 double *ye = x + 2 * mm * stride * nx;
@@ -311,8 +344,8 @@ __global__ void __launch_bounds__(256) schur_cr_kernel(SchurArgs a) {
             __syncthreads();
         }
         if (warp == 0) {
-            w_trsv_l(ws + L.Lbase, x, nx, lane);
-            w_trsv_lt(ws + L.Lbase, x, nx, lane);
+            w_trsv(ws + L.Lbase, nx, x, nx, false, lane);
+            w_trsv(ws + L.Lbase, nx, x, nx, true, lane);
         }
         __syncthreads();
         s = P >> L.levels;
@@ -326,7 +359,7 @@ __global__ void __launch_bounds__(256) schur_cr_kernel(SchurArgs a) {
                 if (2 * mm + 2 < sl)
                     w_gemv_sub(Yl + mm * nn, true, x + ((2 * mm + 2) * stride % P) * nx, xo, nx,
                                lane);
-                w_trsv_lt(Ll + mm * nn, xo, nx, lane);
+                w_trsv(Ll + mm * nn, nx, xo, nx, true, lane);
             }
             __syncthreads();
         }
