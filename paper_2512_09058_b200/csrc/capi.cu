@@ -96,7 +96,7 @@ int make_geo(cyq_ctx *ctx, const cyq_dims *d, Geo &g) {
 }
 
 struct WsSizes {
-    size_t fac, y, wl, trail, schur, lamc, fail, total;
+    size_t fac, y, wl, trail, schur, lamc, fail, consts, total;
 };
 
 WsSizes ws_sizes(const Geo &g) {
@@ -110,7 +110,9 @@ WsSizes ws_sizes(const Geo &g) {
     s.schur = al((size_t)g.batch * SchurLayout::make(g.P, g.nx).total);
     s.lamc = al((size_t)g.batch * g.P * g.nx);
     s.fail = al((size_t)g.batch); // 8-byte keys
-    s.total = (s.fac + s.y + s.wl + s.trail + s.schur + s.lamc + s.fail) * sizeof(double);
+    s.consts = al(riccati_consts_doubles(g));
+    s.total = (s.fac + s.y + s.wl + s.trail + s.schur + s.lamc + s.fail + s.consts) *
+              sizeof(double);
     return s;
 }
 
@@ -130,6 +132,8 @@ FactorWS carve(void *base, const WsSizes &s) {
     w.lamc = p;
     p += s.lamc;
     w.fail = reinterpret_cast<unsigned long long *>(p);
+    p += s.fail;
+    w.consts = p;
     return w;
 }
 
@@ -275,7 +279,17 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
     }
     const int chains = g.batch * g.P;
     CU(cudaMemsetAsync(ws.fail, 0xFF, sizeof(unsigned long long) * g.batch, ctx->stream));
-    RiccatiArgs ra{g, p, ws.fac, ws.y, ws.wl, ws.trail, ws.fail};
+    const bool staged = riccati_staged(g);
+    if (!staged) { // identity / zero constants for the direct-mode kernel
+        std::vector<double> h(riccati_consts_doubles(g), 0.0);
+        for (int i = 0; i < g.nu; ++i)
+            h[(size_t)i * g.nu + i] = 1.0;
+        for (int i = 0; i < g.nx; ++i)
+            h[(size_t)g.nu * g.nu + (size_t)i * g.nx + i] = 1.0;
+        CU(cudaMemcpyAsync(ws.consts, h.data(), h.size() * sizeof(double),
+                           cudaMemcpyHostToDevice, ctx->stream));
+    }
+    RiccatiArgs ra{g, p, ws.fac, ws.y, ws.wl, ws.trail, ws.fail, ws.consts, staged ? 1 : 0};
     {
         Timed t(ctx, 0);
         if (!launch_riccati_warp(g, ctx->stream, ra))

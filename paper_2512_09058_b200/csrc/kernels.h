@@ -16,6 +16,7 @@ struct FactorWS {
     double *schur; // [batch][SCH]          CR factor + scratch (see schur_layout)
     double *lamc;  // [batch][P][nx]        coupling multipliers lambda^{n i}
     unsigned long long *fail; // [batch]    first failure key, ~0 = ok
+    double *consts;           // identity / zero constants (generic kernel)
 };
 
 struct RiccatiArgs {
@@ -23,6 +24,8 @@ struct RiccatiArgs {
     ProbView p;
     double *fac, *y, *wl, *trail;
     unsigned long long *fail;
+    const double *consts; // I_nu | I_nx | zeros (direct-mode generic kernel)
+    int staged;           // generic kernel: stage data staged in smem
 };
 
 struct SchurArgs {
@@ -92,6 +95,8 @@ __global__ void schur_cr_kernel(SchurArgs a);
 __global__ void backsub_kernel(BacksubArgs a);
 
 size_t riccati_smem_bytes(const Geo &g);
+bool riccati_staged(const Geo &g);
+size_t riccati_consts_doubles(const Geo &g);
 size_t backsub_smem_bytes(const Geo &g);
 size_t schur_smem_bytes(const Geo &g);
 int schur_warps(const Geo &g);

@@ -53,9 +53,37 @@ struct Bufs {
     double *B, *A, *f;
 };
 
+// Direct mode (panels too large to also stage the stage data in shared
+// memory): point the buffers at the global matrices instead, with identity /
+// zero constants for padding stages.
+__device__ void point_H(const Geo &g, const ProbView &p, const double *cst, int b, int j, int xi,
+                        Bufs &bf) {
+    const int nu = g.nu, nx = g.nx, N = g.N;
+    const double *eye_nu = cst, *eye_nx = cst + nu * nu, *zero = eye_nx + nx * nx;
+    const bool in = j < N;
+    bf.R = const_cast<double *>(in ? p.R + ((size_t)b * N + j) * nu * nu : eye_nu);
+    bf.S = const_cast<double *>(in ? p.S + ((size_t)b * N + j) * nu * nx : zero);
+    bf.Q = const_cast<double *>(xi <= N ? p.Q + ((size_t)b * (N + 1) + xi) * nx * nx : eye_nx);
+    bf.r = const_cast<double *>(in ? (p.ru ? p.ru : p.r) + ((size_t)b * N + j) * nu : zero);
+    bf.q = const_cast<double *>(xi <= N ? (p.qx ? p.qx : p.q) + ((size_t)b * (N + 1) + xi) * nx : zero);
+}
+__device__ void point_BA(const Geo &g, const ProbView &p, const double *cst, int b, int j,
+                         Bufs &bf) {
+    const int nu = g.nu, nx = g.nx, N = g.N;
+    const double *zero = cst + nu * nu + nx * nx;
+    const bool in = j < N;
+    bf.B = const_cast<double *>(in ? p.B + ((size_t)b * N + j) * nx * nu : zero);
+    bf.A = const_cast<double *>((in && j != 0) ? p.A + ((size_t)b * N + j) * nx * nx : zero);
+    bf.f = const_cast<double *>(in ? (p.fd ? p.fd : p.f) + ((size_t)b * N + j) * nx : zero);
+}
+
 // Issue the (async) loads of H_j (R_j, S_j, Q_xi, r_j, q_xi).
-__device__ void load_H(const Geo &g, const ProbView &p, int b, int j, int xi, const Bufs &bf,
-                       int tid, int nthr) {
+__device__ void load_H(const Geo &g, const ProbView &p, int b, int j, int xi, Bufs &bf,
+                       int tid, int nthr, const double *cst) {
+    if (cst) {
+        point_H(g, p, cst, b, j, xi, bf);
+        return;
+    }
     const int nu = g.nu, nx = g.nx, N = g.N;
     const bool in = j < N;
     stage_copy(bf.R, in ? p.R + ((size_t)b * N + j) * nu * nu : nullptr, nu * nu, nu, tid, nthr);
@@ -69,8 +97,12 @@ __device__ void load_H(const Geo &g, const ProbView &p, int b, int j, int xi, co
 }
 
 // Issue the (async) loads of BA_j = [B_j A_j] and f_j (fd).
-__device__ void load_BA(const Geo &g, const ProbView &p, int b, int j, const Bufs &bf, int tid,
-                        int nthr) {
+__device__ void load_BA(const Geo &g, const ProbView &p, int b, int j, Bufs &bf, int tid,
+                        int nthr, const double *cst) {
+    if (cst) {
+        point_BA(g, p, cst, b, j, bf);
+        return;
+    }
     const int nu = g.nu, nx = g.nx, N = g.N;
     const bool in = j < N;
     stage_copy(bf.B, in ? p.B + ((size_t)b * N + j) * nx * nu : nullptr, nx * nu, 0, tid, nthr);
@@ -130,7 +162,9 @@ riccati_panel_kernel_t(RiccatiArgs a) {
     // ---- shared memory carve-up --------------------------------------
     double *pan = sm;                              // NT tiles
     double *Vs = pan + NT * kTileElems;            // CT x NXT tiles
+    const double *cst = a.staged ? nullptr : a.consts;
     double *hb = Vs + CT * NXT * kTileElems;
+    const int stg = a.staged ? (nu * nu + nu * nx + nx * nx + nu + nx + nx * nu + nx * nx + nx) : 0;
     Bufs bf;
     bf.R = hb;
     bf.S = bf.R + nu * nu;
@@ -140,7 +174,7 @@ riccati_panel_kernel_t(RiccatiArgs a) {
     bf.B = bf.q + nx;
     bf.A = bf.B + nx * nu;
     bf.f = bf.A + nx * nx;
-    double *mwl = bf.f + nx;       // nx: -wl_new (the rhs row of W)
+    double *mwl = hb + stg;        // nx: -wl_new (the rhs row of W)
     double *ru0 = mwl + nx;        // nu: S_0 x_init
     double *red = ru0 + nu;        // 32
     unsigned char *tab = reinterpret_cast<unsigned char *>(red + 32); // 2*NT
@@ -159,8 +193,8 @@ riccati_panel_kernel_t(RiccatiArgs a) {
     // prologue: stage 0 data (H_0, BA_0), S_0 x_init for the ru[0] term
     {
         const int j0 = g.stage_of(c, 0), x0i = g.x_index_of(c, 0);
-        load_H(g, a.p, b, j0, x0i, bf, tid, NTH);
-        load_BA(g, a.p, b, j0, bf, tid, NTH);
+        load_H(g, a.p, b, j0, x0i, bf, tid, NTH, cst);
+        load_BA(g, a.p, b, j0, bf, tid, NTH, cst);
         cp_commit();
         if (implicit_rhs && c == 0) {
             for (int i = tid; i < nu; i += NTH) {
@@ -229,9 +263,9 @@ riccati_panel_kernel_t(RiccatiArgs a) {
         __syncthreads(); // all reads of W / staging done
         // prefetch the next stage's H (H buffer is free now); BA_1 at s = 0
         if (s + 1 < n)
-            load_H(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), bf, tid, NTH);
+            load_H(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), bf, tid, NTH, cst);
         if (s == 0 && n > 1)
-            load_BA(g, a.p, b, g.stage_of(c, 1), bf, tid, NTH);
+            load_BA(g, a.p, b, g.stage_of(c, 1), bf, tid, NTH, cst);
         cp_commit();
         // publish block column 0
 #pragma unroll
@@ -412,7 +446,7 @@ riccati_panel_kernel_t(RiccatiArgs a) {
             }
             __syncthreads();
             if (s + 2 < n) {
-                load_BA(g, a.p, b, g.stage_of(c, s + 2), bf, tid, NTH);
+                load_BA(g, a.p, b, g.stage_of(c, s + 2), bf, tid, NTH, cst);
                 cp_commit();
             }
         }
@@ -442,12 +476,19 @@ template __global__ void riccati_panel_kernel_t<8>(RiccatiArgs);
 template __global__ void riccati_panel_kernel_t<16>(RiccatiArgs);
 template __global__ void riccati_panel_kernel_t<32>(RiccatiArgs);
 
-size_t riccati_smem_bytes(const Geo &g) {
+size_t riccati_smem_bytes(const Geo &g, bool staged) {
     const int nt = g.TT * (g.TT + 1) / 2;
-    const size_t dbl = (size_t)(nt + g.CT * g.NXT) * kTileElems +
-                       (size_t)g.nu * g.nu + g.nu * g.nx + g.nx * g.nx + g.nu + g.nx +
-                       (size_t)g.nx * g.nu + g.nx * g.nx + g.nx + g.nx + g.nu + 32;
+    size_t dbl = (size_t)(nt + g.CT * g.NXT) * kTileElems + g.nx + g.nu + 32;
+    if (staged)
+        dbl += (size_t)g.nu * g.nu + g.nu * g.nx + g.nx * g.nx + g.nu + g.nx +
+               (size_t)g.nx * g.nu + g.nx * g.nx + g.nx;
     return dbl * sizeof(double) + 2 * nt + 64;
+}
+bool riccati_staged(const Geo &g) { return riccati_smem_bytes(g, true) <= 200 * 1024; }
+size_t riccati_smem_bytes(const Geo &g) { return riccati_smem_bytes(g, riccati_staged(g)); }
+size_t riccati_consts_doubles(const Geo &g) {
+    return (size_t)g.nu * g.nu + (size_t)g.nx * g.nx +
+           (size_t)g.nx * (g.nx > g.nu ? g.nx : g.nu) + g.nx + g.nu;
 }
 
 } // namespace cyqb

@@ -19,7 +19,7 @@ namespace cyqb {
 
 namespace {
 
-__device__ __forceinline__ int stride_of(int n) { return n | 1; }
+__host__ __device__ __forceinline__ int stride_of(int n) { return n | 1; }
 
 // copy an n x n block global (ld n) -> scratch (ld s); lower only if `lower`
 __device__ void w_load(double *dst, int s, const double *src, int n, bool lower, bool trans,
