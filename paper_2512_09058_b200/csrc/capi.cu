@@ -234,7 +234,6 @@ void launch_riccati(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
     default: launch_riccati_t<32>(g, nw, st, ra); break;
     }
 }
-int backsub_threads(const Geo &g) { return g.nux > 48 ? 128 : 32; }
 
 cudaEvent_t take_event(cyq_ctx *ctx) {
     if (ctx->pool.empty()) {
@@ -307,8 +306,8 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
         BacksubArgs ba{g, p, ws.fac, ws.y, ws.wl, ws.lamc, *sol};
         {
             Timed t(ctx, 2);
-            backsub_kernel<<<chains, backsub_threads(g), backsub_smem_bytes(g),
-                             ctx->stream>>>(ba);
+            backsub_kernel<<<(chains + BACKSUB_WPB - 1) / BACKSUB_WPB, 32 * BACKSUB_WPB,
+                             backsub_smem_bytes(g), ctx->stream>>>(ba);
         }
         CU(cudaGetLastError());
     }
@@ -357,10 +356,6 @@ int ensure(cyq_ctx *ctx, void **buf, size_t *have, size_t need) {
 
 namespace cyqb {
 
-size_t backsub_smem_bytes(const Geo &g) {
-    const size_t vpad = 32 * ((g.nux + 31) / 32);
-    return ((size_t)g.NPT * kTileElems + 8 * vpad) * sizeof(double);
-}
 
 } // namespace cyqb
 

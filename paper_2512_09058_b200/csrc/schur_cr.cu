@@ -116,14 +116,14 @@ __device__ void w_trsv(const double *L, int sl, double *x, int n, bool trans, in
     __syncwarp();
 }
 
-// y -= op(A) x
-__device__ void w_gemv_sub(const double *A, bool trans, const double *x, double *y, int n,
-                           int lane) {
+// y -= op(A) x   (A in scratch with row stride sa)
+__device__ void w_gemv_sub(const double *A, int sa, bool trans, const double *x, double *y,
+                           int n, int lane) {
     __syncwarp();
     for (int i = lane; i < n; i += 32) {
         double acc = 0;
         for (int k = 0; k < n; ++k)
-            acc += (trans ? A[k * n + i] : A[i * n + k]) * x[k];
+            acc += (trans ? A[k * sa + i] : A[i * sa + k]) * x[k];
         y[i] -= acc;
     }
     __syncwarp();
@@ -140,12 +140,13 @@ __device__ __forceinline__ double fac_at(const Geo &g, const double *st, int r, 
 
 size_t schur_smem_bytes(const Geo &g) {
     const int s = stride_of(g.nx);
-    return (size_t)schur_warps(g) * 4 * g.nx * s * sizeof(double);
+    return ((size_t)schur_warps(g) * 4 * g.nx * s + (size_t)g.P * g.nx) * sizeof(double);
 }
 
 int schur_warps(const Geo &g) {
     const size_t per = 4 * (size_t)g.nx * stride_of(g.nx) * sizeof(double);
-    int nw = (int)std::min<size_t>(8, (200 * 1024) / per);
+    const size_t xbytes = (size_t)g.P * g.nx * sizeof(double);
+    int nw = (int)std::min<size_t>(8, (200 * 1024 - std::min<size_t>(xbytes, 100 * 1024)) / per);
     nw = nw < 1 ? 1 : nw;
     const int want = g.P / 2 > 1 ? g.P / 2 : 1;
     return nw < want ? nw : want;
@@ -167,6 +168,7 @@ __global__ void __launch_bounds__(256) schur_cr_kernel(SchurArgs a) {
     const int top = 8 * g.CT;
     double *S0 = sm + (size_t)warp * 4 * nx * ss, *S1 = S0 + nx * ss, *S2 = S1 + nx * ss,
            *S3 = S2 + nx * ss;
+    double *xs = sm + (size_t)NW * 4 * nx * ss; // P * nx (CR solve vector)
     unsigned long long my_fail = ~0ull;
 
     // ---- phase 1: per-column T-contributions (Z = L_Q^{-1} = T') --------
@@ -219,12 +221,16 @@ __global__ void __launch_bounds__(256) schur_cr_kernel(SchurArgs a) {
         }
         if (a.do_solve) {
             // bwd_neg_c = T x'_{n-1} = Z' x'
-            __syncwarp();
+            if (!a.do_factor)
+                w_load(S2, ss, Zc, nx, false, false, lane);
             const double *yv = a.y + (chain * n + (n - 1)) * g.nux;
+            for (int k = lane; k < nx; k += 32)
+                S3[k] = yv[nu + k];
+            __syncwarp();
             for (int i = lane; i < nx; i += 32) {
                 double acc = 0;
                 for (int k = i; k < nx; ++k)
-                    acc += Zc[k * nx + i] * yv[nu + k];
+                    acc += S2[k * ss + i] * S3[k];
                 bn[c * nx + i] = acc;
             }
         }
@@ -324,28 +330,39 @@ __global__ void __launch_bounds__(256) schur_cr_kernel(SchurArgs a) {
     }
 
     // ---- phase 3: CR solve (block_tridiag.cpp:252-333), negate ----------
+    // x lives in shared memory; every block is staged into the warp's
+    // scratch with coalesced loads before its sequential trsv / gemv.
     if (a.do_solve) {
-        double *x = rhs;
+        double *x = xs;
+        for (int e = threadIdx.x; e < P * nx; e += blockDim.x)
+            x[e] = rhs[e];
+        __syncthreads();
         int s = P;
         for (int l = 0; l < L.levels; ++l, s /= 2) {
             const int half = s / 2, stride = P / s;
             const double *Ll = ws + L.level(l, P, nx, 0), *Ul = ws + L.level(l, P, nx, 1);
             const double *Yl = ws + L.level(l, P, nx, 2);
-            for (int mm = warp; mm < half; mm += NW)
-                w_trsv(Ll + mm * nn, nx, x + (2 * mm + 1) * stride * nx, nx, false, lane);
+            for (int mm = warp; mm < half; mm += NW) {
+                w_load(S0, ss, Ll + mm * nn, nx, false, false, lane);
+                w_trsv(S0, ss, x + (2 * mm + 1) * stride * nx, nx, false, lane);
+            }
             __syncthreads();
             for (int mm = warp; mm < half; mm += NW) {
                 double *ye = x + 2 * mm * stride * nx;
-                w_gemv_sub(Ul + mm * nn, false, x + (2 * mm + 1) * stride * nx, ye, nx, lane);
-                if (mm > 0)
-                    w_gemv_sub(Yl + (mm - 1) * nn, false,
-                               x + ((2 * (mm - 1) + 1) * stride % P) * nx, ye, nx, lane);
+                w_load(S1, ss, Ul + mm * nn, nx, false, false, lane);
+                w_gemv_sub(S1, ss, false, x + (2 * mm + 1) * stride * nx, ye, nx, lane);
+                if (mm > 0) {
+                    w_load(S2, ss, Yl + (mm - 1) * nn, nx, false, false, lane);
+                    w_gemv_sub(S2, ss, false, x + ((2 * (mm - 1) + 1) * stride % P) * nx, ye,
+                               nx, lane);
+                }
             }
             __syncthreads();
         }
         if (warp == 0) {
-            w_trsv(ws + L.Lbase, nx, x, nx, false, lane);
-            w_trsv(ws + L.Lbase, nx, x, nx, true, lane);
+            w_load(S0, ss, ws + L.Lbase, nx, false, false, lane);
+            w_trsv(S0, ss, x, nx, false, lane);
+            w_trsv(S0, ss, x, nx, true, lane);
         }
         __syncthreads();
         s = P >> L.levels;
@@ -355,11 +372,14 @@ __global__ void __launch_bounds__(256) schur_cr_kernel(SchurArgs a) {
             const double *Yl = ws + L.level(l, P, nx, 2);
             for (int mm = warp; mm < half; mm += NW) {
                 double *xo = x + (2 * mm + 1) * stride * nx;
-                w_gemv_sub(Ul + mm * nn, true, x + 2 * mm * stride * nx, xo, nx, lane);
-                if (2 * mm + 2 < sl)
-                    w_gemv_sub(Yl + mm * nn, true, x + ((2 * mm + 2) * stride % P) * nx, xo, nx,
-                               lane);
-                w_trsv(Ll + mm * nn, nx, xo, nx, true, lane);
+                w_load(S1, ss, Ul + mm * nn, nx, false, false, lane);
+                w_gemv_sub(S1, ss, true, x + 2 * mm * stride * nx, xo, nx, lane);
+                if (2 * mm + 2 < sl) {
+                    w_load(S2, ss, Yl + mm * nn, nx, false, false, lane);
+                    w_gemv_sub(S2, ss, true, x + ((2 * mm + 2) * stride % P) * nx, xo, nx, lane);
+                }
+                w_load(S0, ss, Ll + mm * nn, nx, false, false, lane);
+                w_trsv(S0, ss, xo, nx, true, lane);
             }
             __syncthreads();
         }
