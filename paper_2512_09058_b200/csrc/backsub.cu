@@ -95,16 +95,23 @@ __device__ __forceinline__ int bs_stored_tile(const Geo &g, int ti, int tj) {
 __host__ __device__ size_t backsub_smem_per_warp(const Geo &g, int nbuf) {
     return ((size_t)nbuf * bs_buf_doubles(g) + bs_vec_doubles(g)) * sizeof(double);
 }
-__host__ __device__ int backsub_nbuf(const Geo &g) { return backsub_smem_per_warp(g, 2) <= 64 * 1024 ? 2 : 1; }
+// single buffer + high occupancy (many warps alternate load / compute)
+__host__ __device__ int backsub_nbuf(const Geo &) { return 1; }
+int backsub_wpb(const Geo &g) {
+    int w = BACKSUB_WPB;
+    while (w > 1 && (size_t)w * backsub_smem_per_warp(g, backsub_nbuf(g)) > 200 * 1024)
+        w /= 2;
+    return w;
+}
 size_t backsub_smem_bytes(const Geo &g) {
-    return (size_t)BACKSUB_WPB * backsub_smem_per_warp(g, backsub_nbuf(g));
+    return (size_t)backsub_wpb(g) * backsub_smem_per_warp(g, backsub_nbuf(g));
 }
 
-__global__ void __launch_bounds__(32 * BACKSUB_WPB) backsub_kernel(BacksubArgs a) {
+__global__ void __launch_bounds__(32 * BACKSUB_WPB, 4) backsub_kernel(BacksubArgs a) {
     extern __shared__ __align__(16) double sm[];
     const Geo &g = a.g;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const size_t chain = (size_t)blockIdx.x * BACKSUB_WPB + wib;
+    const size_t chain = (size_t)blockIdx.x * (blockDim.x >> 5) + wib;
     if (chain >= (size_t)g.batch * g.P)
         return;
     const int b = (int)(chain / g.P), c = (int)(chain % g.P);

@@ -98,7 +98,8 @@ size_t riccati_smem_bytes(const Geo &g);
 bool riccati_staged(const Geo &g);
 size_t riccati_consts_doubles(const Geo &g);
 size_t backsub_smem_bytes(const Geo &g);
-constexpr int BACKSUB_WPB = 2; // chains (warps) per back-substitution CTA
+constexpr int BACKSUB_WPB = 4; // chains (warps) per back-substitution CTA (max)
+int backsub_wpb(const Geo &g);
 size_t schur_smem_bytes(const Geo &g);
 int schur_warps(const Geo &g);
 
