@@ -18,6 +18,8 @@
 #include "kkt_common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace cyqb {
 
 namespace {
@@ -244,62 +246,64 @@ __global__ void __launch_bounds__(32 * WPB) riccati_warp_kernel(RiccatiArgs a) {
         const double dfloor = 1e-14 * dmax;
 
         // ---- blocked Cholesky of the pivot columns -------------------------
+        // Step k of the diagonal tile and step k of every sub-diagonal tile of
+        // block column kb are interleaved, so the independent sub-diagonal
+        // work fills the latency of the pivot chain (broadcast, rsqrt) and
+        // no per-column arrays stay live. Updates are unconditional FMAs with
+        // zeroed multipliers instead of predicated branches.
+        const int q2 = lane & 3; // this lane holds columns 2*q2, 2*q2 + 1
 #pragma unroll
         for (int kb = 0; kb < S::CT; ++kb) {
             Frag &dg = P[S::T(kb, kb)];
-            double inv[8], lc0[8], lc1[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
+                constexpr unsigned FULL = 0xffffffffu;
+                const int src = k / 2;
                 const double vk = (k & 1) ? dg.b : dg.a;
-                double pv = __shfl_sync(0xffffffffu, vk, 4 * k + k / 2);
-                const double urk = __shfl_sync(0xffffffffu, vk, 4 * rq + k / 2);
-                const double uc0 = __shfl_sync(0xffffffffu, vk, 4 * cq + k / 2);
-                const double uc1 = __shfl_sync(0xffffffffu, vk, 4 * (cq + 1) + k / 2);
-                if (8 * kb + k < S::NUX && !(pv > dfloor && isfinite(pv))) {
-                    my_fail = min(my_fail, fail_key(kKindRiccati, c, s, 8 * kb + k));
-                    pv = 1.0;
+                double pv = __shfl_sync(FULL, vk, 4 * k + src);
+                const double urk = __shfl_sync(FULL, vk, 4 * rq + src);
+                const double uc0 = __shfl_sync(FULL, vk, 4 * cq + src);
+                const double uc1 = __shfl_sync(FULL, vk, 4 * (cq + 1) + src);
+                if (8 * kb + k < S::NUX) {
+                    const bool bad = !(pv > dfloor && isfinite(pv));
+                    my_fail = bad ? min(my_fail, fail_key(kKindRiccati, c, s, 8 * kb + k)) : my_fail;
+                    pv = bad ? 1.0 : pv;
                 }
                 const double iv = rsqrt(pv);
-                inv[k] = iv;
-                lc0[k] = uc0 * iv;
-                lc1[k] = uc1 * iv;
+                const double lc0 = (cq > k) ? uc0 * iv : 0.0;
+                const double lc1 = (cq + 1 > k) ? uc1 * iv : 0.0;
                 const double lrk = urk * iv;
-                if ((lane & 3) == k / 2) {
+                if (q2 == src) {
                     double &e = (k & 1) ? dg.b : dg.a;
-                    if (rq == k)
-                        e = pv * iv;
-                    else if (rq > k)
-                        e = lrk;
+                    e = (rq == k) ? pv * iv : lrk;
                 }
-                if (cq > k && rq >= cq)
-                    dg.a -= lrk * lc0[k];
-                if (cq + 1 > k && rq >= cq + 1)
-                    dg.b -= lrk * lc1[k];
-            }
-            if (cq > rq) dg.a = 0.0;
-            if (cq + 1 > rq) dg.b = 0.0;
-            // sub-diagonal tiles X <- X L^{-T}, all rows interleaved (ILP)
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
+                dg.a -= lrk * lc0;
+                dg.b -= lrk * lc1;
 #pragma unroll
                 for (int ti = kb + 1; ti < S::TT; ++ti) {
                     Frag &x = P[S::T(ti, kb)];
-                    const double vq = (q & 1) ? x.b : x.a;
-                    const double xrq = __shfl_sync(0xffffffffu, vq, 4 * rq + q / 2) * inv[q];
-                    if ((lane & 3) == q / 2) {
-                        if (q & 1) x.b = xrq;
+                    const double vq = (k & 1) ? x.b : x.a;
+                    const double xrq = __shfl_sync(FULL, vq, 4 * rq + src) * iv;
+                    if (q2 == src) {
+                        if (k & 1) x.b = xrq;
                         else x.a = xrq;
                     }
-                    if (cq > q) x.a -= xrq * lc0[q];
-                    if (cq + 1 > q) x.b -= xrq * lc1[q];
+                    x.a -= xrq * lc0;
+                    x.b -= xrq * lc1;
                 }
             }
-            // trailing update: C(ti,tj) -= L(ti,kb) L(tj,kb)'
+            if (cq > rq) dg.a = 0.0;
+            if (cq + 1 > rq) dg.b = 0.0;
+            // trailing update C(ti,tj) -= L(ti,kb) L(tj,kb)': the next diagonal
+            // tile first, so its factorization can start early
+            if (kb + 1 < S::TT)
+                tile_gemm_nt_sub(P[S::T(kb + 1, kb + 1)], P[S::T(kb + 1, kb)], P[S::T(kb + 1, kb)]);
 #pragma unroll
             for (int tj = kb + 1; tj < S::TT; ++tj)
 #pragma unroll
                 for (int ti = tj; ti < S::TT; ++ti)
-                    tile_gemm_nt_sub(P[S::T(ti, tj)], P[S::T(ti, kb)], P[S::T(tj, kb)]);
+                    if (!(ti == kb + 1 && tj == kb + 1))
+                        tile_gemm_nt_sub(P[S::T(ti, tj)], P[S::T(ti, kb)], P[S::T(tj, kb)]);
         }
 
         // ---- store the factor tiles and y_s' ---------------------------------
@@ -467,8 +471,12 @@ template <int NU, int NX, int WPB> bool launch_w(const Geo &g, cudaStream_t st, 
 bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
     if (getenv("CYQ_NO_WARP_KERNEL"))
         return false;
-    return launch_w<10, 20, 2>(g, st, ra) || launch_w<8, 16, 2>(g, st, ra) ||
-           launch_w<4, 12, 2>(g, st, ra) || launch_w<5, 10, 2>(g, st, ra);
+    static const int wpb = getenv("CYQ_RICCATI_WPB") ? atoi(getenv("CYQ_RICCATI_WPB")) : 1;
+    if (wpb == 2)
+        return launch_w<10, 20, 2>(g, st, ra) || launch_w<8, 16, 2>(g, st, ra) ||
+               launch_w<4, 12, 2>(g, st, ra) || launch_w<5, 10, 2>(g, st, ra);
+    return launch_w<10, 20, 1>(g, st, ra) || launch_w<8, 16, 1>(g, st, ra) ||
+           launch_w<4, 12, 1>(g, st, ra) || launch_w<5, 10, 1>(g, st, ra);
 }
 
 } // namespace cyqb
