@@ -38,8 +38,10 @@ template <int NU, int NX> struct Shp {
     static constexpr int HB = NU * NU + NU * NX + NX * NX + NU + NX;
     static constexpr int BB = NX * NU + NX * NX + NX;
     static constexpr int HBp = (HB + 1) & ~1, BBp = (BB + 1) & ~1;
-    static constexpr int SMEM_DBL =
+    static constexpr int SMEM_STAGED =
         (TT * NXT + NLQ) * kTileElems + HBp + BBp + 2 * ((NX + 1) & ~1);
+    // direct mode: stage data read from global (L2-prefetched one stage ahead)
+    static constexpr int SMEM_DIRECT = (TT * NXT + NLQ) * kTileElems + 2 * ((NU + 1) & ~1);
     __host__ __device__ static constexpr int T(int i, int j) { return i * (i + 1) / 2 + j; }
 };
 
@@ -112,6 +114,51 @@ __device__ __forceinline__ void load_BA(const Geo &g, const ProbView &p, int b, 
     wcopy<NX, 0>(st.f, in ? fs + ((size_t)b * N + j) * NX : nullptr, lane);
 }
 
+__device__ __forceinline__ void pf_l2(const double *p, int bytes, int lane) {
+    for (int o = lane * 128; o < bytes; o += 32 * 128)
+        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(reinterpret_cast<const char *>(p) + o));
+}
+
+// Direct mode: point at the global matrices of stage j (identity / zero
+// constants for padding stages) and pull their lines into L2.
+template <int NU, int NX>
+__device__ __forceinline__ void point_H(const Geo &g, const ProbView &p, const double *cst, int b,
+                                        int j, int xi, Stage<NU, NX> &st, int lane) {
+    const int N = g.N;
+    const double *eye_nu = cst, *eye_nx = cst + NU * NU, *zero = eye_nx + NX * NX;
+    const bool in = j < N, qin = xi <= N;
+    st.R = const_cast<double *>(in ? p.R + ((size_t)b * N + j) * NU * NU : eye_nu);
+    st.S = const_cast<double *>(in ? p.S + ((size_t)b * N + j) * NU * NX : zero);
+    st.Q = const_cast<double *>(qin ? p.Q + ((size_t)b * (N + 1) + xi) * NX * NX : eye_nx);
+    st.r = const_cast<double *>(in ? (p.ru ? p.ru : p.r) + ((size_t)b * N + j) * NU : zero);
+    st.q = const_cast<double *>(qin ? (p.qx ? p.qx : p.q) + ((size_t)b * (N + 1) + xi) * NX : zero);
+    if (in) {
+        pf_l2(st.R, NU * NU * 8, lane);
+        pf_l2(st.S, NU * NX * 8, lane);
+        pf_l2(st.r, NU * 8, lane);
+    }
+    if (qin) {
+        pf_l2(st.Q, NX * NX * 8, lane);
+        pf_l2(st.q, NX * 8, lane);
+    }
+}
+template <int NU, int NX>
+__device__ __forceinline__ void point_BA(const Geo &g, const ProbView &p, const double *cst, int b,
+                                         int j, Stage<NU, NX> &st, int lane) {
+    const int N = g.N;
+    const double *zero = cst + NU * NU + NX * NX;
+    const bool in = j < N;
+    st.B = const_cast<double *>(in ? p.B + ((size_t)b * N + j) * NX * NU : zero);
+    st.A = const_cast<double *>((in && j != 0) ? p.A + ((size_t)b * N + j) * NX * NX : zero);
+    st.f = const_cast<double *>(in ? (p.fd ? p.fd : p.f) + ((size_t)b * N + j) * NX : zero);
+    if (in) {
+        pf_l2(st.B, NX * NU * 8, lane);
+        if (j != 0)
+            pf_l2(st.A, NX * NX * 8, lane);
+        pf_l2(st.f, NX * 8, lane);
+    }
+}
+
 // initial entry (r, col) of a pivot tile (compile-time tile, runtime lane)
 template <int NU, int NX>
 __device__ __forceinline__ double pinit(const Stage<NU, NX> &st, bool s0, bool j0, double sgn,
@@ -145,8 +192,8 @@ __device__ __forceinline__ double pinit(const Stage<NU, NX> &st, bool s0, bool j
 
 } // namespace
 
-template <int NU, int NX, int WPB>
-__global__ void __launch_bounds__(32 * WPB) riccati_warp_kernel(RiccatiArgs a) {
+template <int NU, int NX, int WPB, bool DIRECT>
+__global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_kernel(RiccatiArgs a) {
     using S = Shp<NU, NX>;
     extern __shared__ __align__(16) double sm[];
     const Geo &g = a.g;
@@ -157,7 +204,8 @@ __global__ void __launch_bounds__(32 * WPB) riccati_warp_kernel(RiccatiArgs a) {
     const int b = chain / g.P, c = chain % g.P, n = g.n;
     const int rq = lane >> 2, cq = 2 * (lane & 3);
 
-    double *base = sm + (size_t)wib * S::SMEM_DBL;
+    constexpr int SMEM_DBL = DIRECT ? S::SMEM_DIRECT : S::SMEM_STAGED;
+    double *base = sm + (size_t)wib * SMEM_DBL;
     double *Wsm = base;                                   // TT x NXT tiles
     double *Lsm = Wsm + S::TT * S::NXT * kTileElems;      // NLQ tiles (x-x block of L)
     Stage<NU, NX> st;
@@ -169,7 +217,7 @@ __global__ void __launch_bounds__(32 * WPB) riccati_warp_kernel(RiccatiArgs a) {
     st.B = st.R + S::HBp;
     st.A = st.B + NX * NU;
     st.f = st.A + NX * NX;
-    double *ru0 = st.B + S::BBp; // NU (S_0 x_init), NX scratch after it
+    double *ru0 = DIRECT ? st.R : st.B + S::BBp; // NU: S_0 x_init
     const bool implicit_rhs = (a.p.ru == nullptr);
     const double sgn = implicit_rhs ? -1.0 : 1.0;
     unsigned long long my_fail = ~0ull;
@@ -177,8 +225,13 @@ __global__ void __launch_bounds__(32 * WPB) riccati_warp_kernel(RiccatiArgs a) {
     // prologue: H_0, BA_0 and the x_init term of ru[0]
     {
         const int j0 = g.stage_of(c, 0);
-        load_H<NU, NX>(g, a.p, b, j0, g.x_index_of(c, 0), st, lane);
-        load_BA<NU, NX>(g, a.p, b, j0, st, lane);
+        if (DIRECT) {
+            point_H<NU, NX>(g, a.p, a.consts, b, j0, g.x_index_of(c, 0), st, lane);
+            point_BA<NU, NX>(g, a.p, a.consts, b, j0, st, lane);
+        } else {
+            load_H<NU, NX>(g, a.p, b, j0, g.x_index_of(c, 0), st, lane);
+            load_BA<NU, NX>(g, a.p, b, j0, st, lane);
+        }
         cp_commit();
         if (implicit_rhs && c == 0 && lane < NU) {
             double s0 = 0;
@@ -225,9 +278,16 @@ __global__ void __launch_bounds__(32 * WPB) riccati_warp_kernel(RiccatiArgs a) {
         __syncwarp();
         // the H buffer is free: prefetch H_{s+1} (and BA_1 at s = 0)
         if (s + 1 < n) {
-            load_H<NU, NX>(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), st, lane);
-            if (s == 0)
-                load_BA<NU, NX>(g, a.p, b, g.stage_of(c, 1), st, lane);
+            if (DIRECT) {
+                point_H<NU, NX>(g, a.p, a.consts, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1),
+                                st, lane);
+                if (s == 0)
+                    point_BA<NU, NX>(g, a.p, a.consts, b, g.stage_of(c, 1), st, lane);
+            } else {
+                load_H<NU, NX>(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), st, lane);
+                if (s == 0)
+                    load_BA<NU, NX>(g, a.p, b, g.stage_of(c, 1), st, lane);
+            }
         }
         cp_commit();
 
@@ -429,8 +489,12 @@ __global__ void __launch_bounds__(32 * WPB) riccati_warp_kernel(RiccatiArgs a) {
                 }
             }
             __syncwarp();
-            if (s + 2 < n)
-                load_BA<NU, NX>(g, a.p, b, g.stage_of(c, s + 2), st, lane);
+            if (s + 2 < n) {
+                if (DIRECT)
+                    point_BA<NU, NX>(g, a.p, a.consts, b, g.stage_of(c, s + 2), st, lane);
+                else
+                    load_BA<NU, NX>(g, a.p, b, g.stage_of(c, s + 2), st, lane);
+            }
             cp_commit();
         }
     }
@@ -451,20 +515,25 @@ __global__ void __launch_bounds__(32 * WPB) riccati_warp_kernel(RiccatiArgs a) {
 
 // ---- dispatch ----------------------------------------------------------------
 namespace {
-template <int NU, int NX, int WPB> bool launch_w(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
-    if (g.nu != NU || g.nx != NX)
-        return false;
+template <int NU, int NX, int WPB, bool DIRECT>
+bool launch_wd(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
     using S = Shp<NU, NX>;
-    const size_t smem = (size_t)WPB * S::SMEM_DBL * sizeof(double);
+    const size_t smem = (size_t)WPB * (DIRECT ? S::SMEM_DIRECT : S::SMEM_STAGED) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(riccati_warp_kernel<NU, NX, WPB>,
+        cudaFuncSetAttribute(riccati_warp_kernel<NU, NX, WPB, DIRECT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     const int chains = g.batch * g.P;
-    riccati_warp_kernel<NU, NX, WPB><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ra);
+    riccati_warp_kernel<NU, NX, WPB, DIRECT><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ra);
     return true;
+}
+template <int NU, int NX, int WPB> bool launch_w(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
+    if (g.nu != NU || g.nx != NX)
+        return false;
+    static const bool staged = getenv("CYQ_RICCATI_STAGED") != nullptr;
+    return staged ? launch_wd<NU, NX, WPB, false>(g, st, ra) : launch_wd<NU, NX, WPB, true>(g, st, ra);
 }
 } // namespace
 
