@@ -288,7 +288,14 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
         CU(cudaMemcpyAsync(ws.consts, h.data(), h.size() * sizeof(double),
                            cudaMemcpyHostToDevice, ctx->stream));
     }
-    RiccatiArgs ra{g, p, ws.fac, ws.y, ws.wl, ws.trail, ws.fail, ws.consts, staged ? 1 : 0};
+    RiccatiArgs ra{g, p, ws.fac, ws.y, ws.wl, ws.trail, ws.fail, ws.consts, staged ? 1 : 0,
+                   nullptr};
+    static long long *phase_dev = nullptr;
+    if (getenv("CYQ_PHASE_PROF")) {
+        if (!phase_dev)
+            CU(cudaMalloc(&phase_dev, 8 * 4096 * sizeof(long long)));
+        ra.phase = phase_dev;
+    }
     {
         Timed t(ctx, 0);
         if (!launch_riccati_warp(g, ctx->stream, ra))
@@ -302,6 +309,17 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
         schur_cr_kernel<<<g.batch, 32 * schur_warps(g), schur_smem_bytes(g), ctx->stream>>>(sa);
     }
     CU(cudaGetLastError());
+    if (ra.phase) { // dump chain 0's phase clocks (profiling aid)
+        std::vector<long long> h(8 * (g.n + 1));
+        CU(cudaMemcpyAsync(h.data(), ra.phase, h.size() * sizeof(long long),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        for (int s = 0; s < g.n; ++s)
+            fprintf(stderr, "phase s=%d init+WW %lld chol %lld store %lld mw %lld V %lld\n", s,
+                    h[s * 8 + 1] - h[s * 8 + 0], h[s * 8 + 2] - h[s * 8 + 1],
+                    h[s * 8 + 3] - h[s * 8 + 2], h[s * 8 + 4] - h[s * 8 + 3],
+                    (s + 1 < g.n ? h[(s + 1) * 8] : h[g.n * 8]) - h[s * 8 + 4]);
+    }
     if (do_solve) {
         BacksubArgs ba{g, p, ws.fac, ws.y, ws.wl, ws.lamc, *sol};
         {

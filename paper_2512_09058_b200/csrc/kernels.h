@@ -26,6 +26,7 @@ struct RiccatiArgs {
     unsigned long long *fail;
     const double *consts; // I_nu | I_nx | zeros (direct-mode generic kernel)
     int staged;           // generic kernel: stage data staged in smem
+    long long *phase;     // optional per-stage phase clocks of chain 0 (profiling)
 };
 
 struct SchurArgs {

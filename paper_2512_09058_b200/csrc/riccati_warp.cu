@@ -249,7 +249,11 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
     for (int t = 0; t < S::NT; ++t)
         P[t] = Frag{0.0, 0.0};
 
+    // optional phase timing (CYQ_PHASE_PROF): chain 0's lane 0 records
+    // clock64 at the phase boundaries of every stage
+    long long *ph = (a.phase && chain == 0 && lane == 0) ? a.phase : nullptr;
     for (int s = 0; s < n; ++s) {
+        if (ph) ph[s * 8 + 0] = clock64();
         const int j = g.stage_of(c, s);
         const double *ru0p = (implicit_rhs && j == 0) ? ru0 : nullptr;
         if (s > 0) {
@@ -291,6 +295,7 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
         }
         cp_commit();
 
+        if (ph) ph[s * 8 + 1] = clock64();
         // ---- pivot floor: max |diag| of H_s + V V' (kernels.cpp:21-29) ----
         double dmax = 0.0;
 #pragma unroll
@@ -366,6 +371,7 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
                         tile_gemm_nt_sub(P[S::T(ti, tj)], P[S::T(ti, kb)], P[S::T(tj, kb)]);
         }
 
+        if (ph) ph[s * 8 + 2] = clock64();
         // ---- store the factor tiles and y_s' ---------------------------------
         {
             double *dst = a.fac + ((size_t)chain * n + s) * S::NPT * kTileElems;
@@ -391,6 +397,7 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
         }
 
         if (s + 1 < n) {
+            if (ph) ph[s * 8 + 3] = clock64();
             // ---- W for stage s+1 -------------------------------------------
             if (s == 0) cp_wait<0>();
             else cp_wait<1>();   // BA_{s+1} has landed
@@ -463,6 +470,7 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
                     st_frag(Lsm + S::T(u, v) * kTileElems, lane, w);
                 }
             __syncwarp();
+            if (ph) ph[s * 8 + 4] = clock64();
             // V = BA_{s+1}' L_Q : rows 0..nux-1 of W (DMMA)
 #pragma unroll
             for (int ti = 0; ti < S::CT; ++ti) {
@@ -499,6 +507,7 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
         }
     }
 
+    if (ph) ph[n * 8] = clock64();
     // trailing tiles (coupling x coupling = -Mfwd, rhs x coupling = -fwd)
 #pragma unroll
     for (int u = 0; u < S::BT; ++u)
