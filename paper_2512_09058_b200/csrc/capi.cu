@@ -298,7 +298,10 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
     }
     {
         Timed t(ctx, 0);
-        if (!launch_riccati_warp(g, ctx->stream, ra))
+        static const char *sel = getenv("CYQ_RICCATI");
+        const bool want_warp = sel && sel[0] == 'w', want_gen = sel && sel[0] == 'g';
+        if (want_gen || !((want_warp ? false : launch_riccati_cta2(g, ctx->stream, ra)) ||
+                          launch_riccati_warp(g, ctx->stream, ra)))
             launch_riccati(g, ctx->stream, ra);
     }
     CU(cudaGetLastError());

@@ -92,6 +92,7 @@ struct SchurLayout {
 template <int MAXT> __global__ void riccati_panel_kernel_t(RiccatiArgs a);
 // compile-time (nu, nx) warp-per-chain fast path; false if not instantiated
 bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
+bool launch_riccati_cta2(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
 __global__ void schur_cr_kernel(SchurArgs a);
 __global__ void backsub_kernel(BacksubArgs a);
 

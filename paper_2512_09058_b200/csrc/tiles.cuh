@@ -1,0 +1,141 @@
+// Register-resident 8x8 FP64 tile algorithms for one warp (compile-time
+// tile shapes). A "panel" is a lower-trapezoidal set of C-fragment tiles
+// P[T(i, j)], j <= i, rows 0..TT-1; its first CT tile columns are pivots.
+//
+// The blocked Cholesky restates batla::potrf + trsm(right_lower_trans) +
+// syrk (kernels.cpp:32-58, 95-119, 158-168) for a stacked panel: the
+// diagonal 8x8 tiles are factored with warp shuffles (one rsqrt per pivot),
+// the rows below are solved in the same pivot steps, and the trailing
+// updates are DMMA rank-8 products of register tiles.
+#pragma once
+
+#include "kkt_common.cuh"
+
+namespace cyqb {
+namespace tiles {
+
+__host__ __device__ constexpr int T(int i, int j) { return i * (i + 1) / 2 + j; }
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// Blocked Cholesky of the first CT tile columns of a TT-row panel.
+// Pivots with global column index >= npiv are padding (unit, unchecked).
+// On a pivot failure (potrf semantics: !(p > dfloor) or non-finite) the
+// first failing global pivot index is stored in `fail` and the pivot is
+// replaced by 1 so the sweep completes.
+template <int TT, int CT, int NT>
+__device__ __forceinline__ void panel_cholesky(Frag (&P)[NT], int npiv, double dfloor, int lane,
+                                               int &fail) {
+    const int rq = lane >> 2, cq = 2 * (lane & 3), q2 = lane & 3;
+#pragma unroll
+    for (int kb = 0; kb < CT; ++kb) {
+        Frag &dg = P[T(kb, kb)];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int src = k / 2;
+            const double vk = (k & 1) ? dg.b : dg.a;
+            double pv = __shfl_sync(kFull, vk, 4 * k + src);
+            const double urk = __shfl_sync(kFull, vk, 4 * rq + src);
+            const double uc0 = __shfl_sync(kFull, vk, 4 * cq + src);
+            const double uc1 = __shfl_sync(kFull, vk, 4 * (cq + 1) + src);
+            if (8 * kb + k < npiv) {
+                const bool bad = !(pv > dfloor && isfinite(pv));
+                fail = (bad && fail < 0) ? 8 * kb + k : fail;
+                pv = bad ? 1.0 : pv;
+            }
+            const double iv = rsqrt(pv);
+            const double lc0 = (cq > k) ? uc0 * iv : 0.0;
+            const double lc1 = (cq + 1 > k) ? uc1 * iv : 0.0;
+            const double lrk = urk * iv;
+            if (q2 == src) {
+                double &e = (k & 1) ? dg.b : dg.a;
+                e = (rq == k) ? pv * iv : lrk;
+            }
+            dg.a -= lrk * lc0;
+            dg.b -= lrk * lc1;
+#pragma unroll
+            for (int ti = kb + 1; ti < TT; ++ti) {
+                Frag &x = P[T(ti, kb)];
+                const double vq = (k & 1) ? x.b : x.a;
+                const double xrq = __shfl_sync(kFull, vq, 4 * rq + src) * iv;
+                if (q2 == src) {
+                    if (k & 1) x.b = xrq;
+                    else x.a = xrq;
+                }
+                x.a -= xrq * lc0;
+                x.b -= xrq * lc1;
+            }
+        }
+        if (cq > rq) dg.a = 0.0;
+        if (cq + 1 > rq) dg.b = 0.0;
+        if (kb + 1 < TT)
+            tile_gemm_nt_sub(P[T(kb + 1, kb + 1)], P[T(kb + 1, kb)], P[T(kb + 1, kb)]);
+#pragma unroll
+        for (int tj = kb + 1; tj < TT; ++tj)
+#pragma unroll
+            for (int ti = tj; ti < TT; ++ti)
+                if (!(ti == kb + 1 && tj == kb + 1))
+                    tile_gemm_nt_sub(P[T(ti, tj)], P[T(ti, kb)], P[T(tj, kb)]);
+    }
+}
+
+// Rows X (RT x CT tiles, X[i * CT + j]) <- X L^{-T} for a factored lower
+// L (CT x CT tiles, L[T(i, j)]): TrsmMode::right_lower_trans
+// (kernels.cpp:107-119) in the tile layout.
+template <int RT, int CT, int NL>
+__device__ __forceinline__ void trsm_rows(Frag (&X)[RT * CT], const Frag (&L)[NL], int lane) {
+    const int rq = lane >> 2, cq = 2 * (lane & 3), q2 = lane & 3;
+#pragma unroll
+    for (int kb = 0; kb < CT; ++kb) {
+        const Frag &dg = L[T(kb, kb)];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int src = k / 2;
+            const double vk = (k & 1) ? dg.b : dg.a;
+            const double dkk = __shfl_sync(kFull, vk, 4 * k + src);
+            const double uc0 = __shfl_sync(kFull, vk, 4 * cq + src);
+            const double uc1 = __shfl_sync(kFull, vk, 4 * (cq + 1) + src);
+            const double iv = 1.0 / dkk;
+            const double lc0 = (cq > k) ? uc0 : 0.0;
+            const double lc1 = (cq + 1 > k) ? uc1 : 0.0;
+#pragma unroll
+            for (int ti = 0; ti < RT; ++ti) {
+                Frag &x = X[ti * CT + kb];
+                const double vq = (k & 1) ? x.b : x.a;
+                const double xrq = __shfl_sync(kFull, vq, 4 * rq + src) * iv;
+                if (q2 == src) {
+                    if (k & 1) x.b = xrq;
+                    else x.a = xrq;
+                }
+                x.a -= xrq * lc0;
+                x.b -= xrq * lc1;
+            }
+        }
+#pragma unroll
+        for (int tj = kb + 1; tj < CT; ++tj)
+#pragma unroll
+            for (int ti = 0; ti < RT; ++ti)
+                tile_gemm_nt_sub(X[ti * CT + tj], X[ti * CT + kb], L[T(tj, kb)]);
+    }
+}
+
+// max |diag| over the first npiv diagonal entries of the CT diagonal tiles
+template <int CT, int NT>
+__device__ __forceinline__ double diag_absmax(const Frag (&P)[NT], int npiv, int lane) {
+    const int rq = lane >> 2;
+    double m = 0.0;
+#pragma unroll
+    for (int kb = 0; kb < CT; ++kb) {
+        const Frag &d = P[T(kb, kb)];
+        const double v = (rq & 1) ? d.b : d.a;
+        if ((lane & 3) == rq / 2 && 8 * kb + rq < npiv)
+            m = fmax(m, fabs(v));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        m = fmax(m, __shfl_xor_sync(kFull, m, o));
+    return m;
+}
+
+} // namespace tiles
+} // namespace cyqb
