@@ -309,7 +309,16 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
                  sol ? sol->lam : nullptr, ws.fail, 1, do_solve ? 1 : 0};
     {
         Timed t(ctx, 1);
-        schur_cr_kernel<<<g.batch, 32 * schur_warps(g), schur_smem_bytes(g), ctx->stream>>>(sa);
+        if (launch_schur_tiles(g, ctx->stream, sa)) { // DMMA-tile factorization
+            if (do_solve) {
+                SchurArgs sv = sa;
+                sv.do_factor = 0;
+                schur_cr_kernel<<<g.batch, 32 * schur_warps(g), schur_smem_bytes(g),
+                                  ctx->stream>>>(sv);
+            }
+        } else {
+            schur_cr_kernel<<<g.batch, 32 * schur_warps(g), schur_smem_bytes(g), ctx->stream>>>(sa);
+        }
     }
     CU(cudaGetLastError());
     if (ra.phase) { // dump chain 0's phase clocks (profiling aid)
