@@ -98,19 +98,30 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
 #pragma unroll
         for (int ti = 0; ti < S::TT; ++ti) {
 #pragma unroll
-            for (int tj = 0; tj <= ti; ++tj) {
+            for (int tj = 0; tj <= ti && tj < S::CT; ++tj) {
                 Frag &f = P[S::T(ti, tj)];
-                if (tj < S::CT) {
-                    const int r = 8 * ti + rq, col = 8 * tj + cq;
-                    f.a = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, r, col);
-                    f.b = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, r, col + 1);
-                }
-                if (s > 0) {
+                const int r = 8 * ti + rq, col = 8 * tj + cq;
+                f.a = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, r, col);
+                f.b = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, r, col + 1);
+            }
+        }
+        if (s > 0) {
+            // k-slice outer, tiles inner: consecutive DMMAs hit different
+            // accumulators (no dependent-DMMA stalls); each W fragment is
+            // read from shared memory once per slice
 #pragma unroll
-                    for (int kt = 0; kt < S::NXT; ++kt)
-                        tile_gemm_nt(f, ld_frag(Wsm + (ti * S::NXT + kt) * kTileElems, lane),
-                                     ld_frag(Wsm + (tj * S::NXT + kt) * kTileElems, lane));
-                }
+            for (int kt = 0; kt < S::NXT; ++kt) {
+                Frag w[S::TT];
+#pragma unroll
+                for (int i = 0; i < S::TT; ++i)
+                    w[i] = ld_frag(Wsm + (i * S::NXT + kt) * kTileElems, lane);
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int ti = 0; ti < S::TT; ++ti)
+#pragma unroll
+                        for (int tj = 0; tj <= ti; ++tj)
+                            dmma(P[S::T(ti, tj)], h ? w[ti].b : w[ti].a, h ? w[tj].b : w[tj].a);
             }
         }
         __syncwarp();
@@ -194,15 +205,20 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
             if (cq > rq) dg.a = 0.0;
             if (cq + 1 > rq) dg.b = 0.0;
             // trailing update C(ti,tj) -= L(ti,kb) L(tj,kb)': the next diagonal
-            // tile first, so its factorization can start early
+            // tile first (its factorization can start early), then both k
+            // slices over all tiles so consecutive DMMAs are independent
             if (kb + 1 < S::TT)
                 tile_gemm_nt_sub(P[S::T(kb + 1, kb + 1)], P[S::T(kb + 1, kb)], P[S::T(kb + 1, kb)]);
 #pragma unroll
-            for (int tj = kb + 1; tj < S::TT; ++tj)
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int ti = tj; ti < S::TT; ++ti)
-                    if (!(ti == kb + 1 && tj == kb + 1))
-                        tile_gemm_nt_sub(P[S::T(ti, tj)], P[S::T(ti, kb)], P[S::T(tj, kb)]);
+                for (int tj = kb + 1; tj < S::TT; ++tj)
+#pragma unroll
+                    for (int ti = tj; ti < S::TT; ++ti)
+                        if (!(ti == kb + 1 && tj == kb + 1)) {
+                            const Frag &li = P[S::T(ti, kb)], &lj = P[S::T(tj, kb)];
+                            dmma(P[S::T(ti, tj)], h ? -li.b : -li.a, h ? lj.b : lj.a);
+                        }
         }
 
         if (ph) ph[s * 8 + 2] = clock64();
@@ -305,30 +321,42 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
                 }
             __syncwarp();
             if (ph) ph[s * 8 + 4] = clock64();
-            // V = BA_{s+1}' L_Q : rows 0..nux-1 of W (DMMA)
+            // V = BA_{s+1}' L_Q : rows 0..nux-1 of W (DMMA), k-slice outer
+            {
+                Frag vacc[S::CT * S::NXT];
 #pragma unroll
-            for (int ti = 0; ti < S::CT; ++ti) {
+                for (int v = 0; v < S::CT * S::NXT; ++v)
+                    vacc[v] = Frag{0.0, 0.0};
 #pragma unroll
-                for (int kt = 0; kt < S::NXT; ++kt) {
-                    const int ct = S::XT0 + kt;
-                    Frag f{0.0, 0.0};
-                    const int r = 8 * ti + rq;
+                for (int ks = 2 * S::XT0; ks < 2 * (S::XT1 + 1); ++ks) {
+                    const int K = 4 * ks + (lane & 3);
+                    const bool kin = K >= NU && K < S::NUX;
+                    double av[S::CT], bv[S::NXT];
 #pragma unroll
-                    for (int ks = 2 * S::XT0; ks < 2 * (S::XT1 + 1); ++ks) {
-                        if (4 * ks + 3 < 8 * ct)
-                            continue; // L_Q upper part is zero
-                        const int K = 4 * ks + (lane & 3);
-                        double av = 0.0;
-                        if (K >= NU && K < S::NUX && r < S::NUX)
-                            av = r < NU ? st.B[(K - NU) * NU + r] : st.A[(K - NU) * NX + (r - NU)];
-                        // B[kk][n] = L[K][8ct + n]: tile (K/8, ct) of Lsm
-                        const int u = ks / 2 - S::XT0, v = kt;
-                        const double bv =
-                            Lsm[S::T(u, v) * kTileElems + (4 * (ks & 1) + (lane & 3)) * 8 + (lane >> 2)];
-                        dmma(f, av, bv);
+                    for (int ti = 0; ti < S::CT; ++ti) {
+                        const int r = 8 * ti + rq;
+                        av[ti] = (kin && r < S::NUX)
+                                     ? (r < NU ? st.B[(K - NU) * NU + r] : st.A[(K - NU) * NX + (r - NU)])
+                                     : 0.0;
                     }
-                    st_frag(Wsm + (ti * S::NXT + kt) * kTileElems, lane, f);
+#pragma unroll
+                    for (int kt = 0; kt < S::NXT; ++kt) {
+                        // B[kk][n] = L[K][8ct + n]: tile (K/8, ct) of Lsm
+                        const int u = ks / 2 - S::XT0;
+                        bv[kt] = (u >= kt) ? Lsm[S::T(u >= kt ? u : kt, kt) * kTileElems +
+                                                 (4 * (ks & 1) + (lane & 3)) * 8 + (lane >> 2)]
+                                           : 0.0;
+                    }
+#pragma unroll
+                    for (int ti = 0; ti < S::CT; ++ti)
+#pragma unroll
+                        for (int kt = 0; kt < S::NXT; ++kt)
+                            if (4 * ks + 3 >= 8 * (S::XT0 + kt)) // L_Q upper part is zero
+                                dmma(vacc[ti * S::NXT + kt], av[ti], bv[kt]);
                 }
+#pragma unroll
+                for (int v = 0; v < S::CT * S::NXT; ++v)
+                    st_frag(Wsm + v * kTileElems, lane, vacc[v]);
             }
             __syncwarp();
             if (s + 2 < n) {

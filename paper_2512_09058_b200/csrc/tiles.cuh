@@ -71,11 +71,15 @@ __device__ __forceinline__ void panel_cholesky(Frag (&P)[NT], int npiv, double d
         if (kb + 1 < TT)
             tile_gemm_nt_sub(P[T(kb + 1, kb + 1)], P[T(kb + 1, kb)], P[T(kb + 1, kb)]);
 #pragma unroll
-        for (int tj = kb + 1; tj < TT; ++tj)
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int ti = tj; ti < TT; ++ti)
-                if (!(ti == kb + 1 && tj == kb + 1))
-                    tile_gemm_nt_sub(P[T(ti, tj)], P[T(ti, kb)], P[T(tj, kb)]);
+            for (int tj = kb + 1; tj < TT; ++tj)
+#pragma unroll
+                for (int ti = tj; ti < TT; ++ti)
+                    if (!(ti == kb + 1 && tj == kb + 1)) {
+                        const Frag &li = P[T(ti, kb)], &lj = P[T(tj, kb)];
+                        dmma(P[T(ti, tj)], h ? -li.b : -li.a, h ? lj.b : lj.a);
+                    }
     }
 }
 
