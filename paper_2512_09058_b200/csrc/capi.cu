@@ -298,10 +298,17 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
     }
     {
         Timed t(ctx, 0);
+        // kernel choice: compile-time-shape one-warp kernel (default), the
+        // two-warp variant (CYQ_RICCATI=c) or the runtime-shape CTA kernel
+        // (CYQ_RICCATI=g, and every shape without a specialisation)
         static const char *sel = getenv("CYQ_RICCATI");
-        const bool want_warp = sel && sel[0] == 'w', want_gen = sel && sel[0] == 'g';
-        if (want_gen || !((want_warp ? false : launch_riccati_cta2(g, ctx->stream, ra)) ||
-                          launch_riccati_warp(g, ctx->stream, ra)))
+        const bool want_c2 = sel && sel[0] == 'c', want_gen = sel && sel[0] == 'g';
+        bool done = false;
+        if (!want_gen && want_c2)
+            done = launch_riccati_cta2(g, ctx->stream, ra);
+        if (!want_gen && !done)
+            done = launch_riccati_warp(g, ctx->stream, ra);
+        if (!done)
             launch_riccati(g, ctx->stream, ra);
     }
     CU(cudaGetLastError());

@@ -146,35 +146,38 @@ __device__ __forceinline__ void point_BA(const Geo &g, const ProbView &p, const 
     }
 }
 
-// initial entry (r, col) of a pivot tile (compile-time tile, runtime lane)
+// initial entry (r, col) of a pivot tile (compile-time tile, runtime lane).
+// Branch-free: every candidate source is read with a clamped index and the
+// result selected, so the panel initialisation is straight-line code that
+// the scheduler can interleave (the tile row TI is a compile-time constant,
+// so whole cases fold away).
 template <int NU, int NX>
 __device__ __forceinline__ double pinit(const Stage<NU, NX> &st, bool s0, bool j0, double sgn,
-                                        const double *ru0, int r, int col) {
+                                        const double *ru0, int ti, int r, int col) {
     using S = Shp<NU, NX>;
-    if (r < S::TOP) {
-        if (r >= S::NUX || col >= S::NUX)
-            return r == col ? 1.0 : 0.0;
-        if (col > r)
-            return 0.0;
-        if (r < NU)
-            return st.R[r * NU + col];
-        if (col < NU)
-            return j0 ? 0.0 : st.S[col * NX + (r - NU)];
-        return st.Q[(r - NU) * NX + (col - NU)];
+    if (8 * ti < S::TOP) { // top block: H_s (lower), identity padding
+        const bool inb = r < S::NUX && col < S::NUX;
+        const bool low = col <= r;
+        const bool isR = inb && low && r < NU;
+        const bool isS = inb && r >= NU && col < NU;
+        const bool isQ = inb && low && r >= NU && col >= NU;
+        const double vR = st.R[isR ? r * NU + col : 0];
+        const double vS = st.S[isS ? col * NX + (r - NU) : 0];
+        const double vQ = st.Q[isQ ? (r - NU) * NX + (col - NU) : 0];
+        const double pad = (!inb && r == col) ? 1.0 : 0.0;
+        return isR ? vR : isS ? (j0 ? 0.0 : vS) : isQ ? vQ : pad;
+    } else {
+        const int rb = r - S::TOP;
+        const bool cin = col < S::NUX;
+        const bool isB = s0 && rb < NX && col < NU;
+        const bool isA = s0 && rb < NX && cin && col >= NU;
+        const double vB = st.B[isB ? rb * NU + col : 0];
+        const double vA = st.A[isA ? rb * NX + (col - NU) : 0];
+        const bool isr = rb == NX && col < NU, isq = rb == NX && cin && col >= NU;
+        const double vr = sgn * st.r[isr ? col : 0] - ((ru0 && isr) ? ru0[col] : 0.0);
+        const double vq = sgn * st.q[isq ? col - NU : 0];
+        return isB ? vB : isA ? vA : isr ? vr : isq ? vq : 0.0;
     }
-    const int rb = r - S::TOP;
-    if (rb < NX) {
-        if (!s0 || col >= S::NUX)
-            return 0.0;
-        return col < NU ? st.B[rb * NU + col] : st.A[rb * NX + (col - NU)];
-    }
-    if (rb == NX) {
-        if (col < NU)
-            return sgn * st.r[col] - (ru0 ? ru0[col] : 0.0);
-        if (col < S::NUX)
-            return sgn * st.q[col - NU];
-    }
-    return 0.0;
 }
 
 } // namespace ric

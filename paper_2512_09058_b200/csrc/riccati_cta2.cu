@@ -114,8 +114,8 @@ __device__ __forceinline__ void cta2_body(const RiccatiArgs &a, double *sm, int 
                 Frag &f = P[S::T(ti, tj)];
                 if (tj < S::CT) {
                     const int r = 8 * ti + rq, col = 8 * tj + cq;
-                    f.a = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, r, col);
-                    f.b = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, r, col + 1);
+                    f.a = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, ti, r, col);
+                    f.b = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, ti, r, col + 1);
                 }
                 if (s > 0) {
 #pragma unroll

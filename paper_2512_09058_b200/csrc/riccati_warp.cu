@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
     double *ru0 = DIRECT ? st.R : st.B + S::BBp; // NU: S_0 x_init
     const bool implicit_rhs = (a.p.ru == nullptr);
     const double sgn = implicit_rhs ? -1.0 : 1.0;
-    unsigned long long my_fail = ~0ull;
+    int fail_piv = -1, fail_stage = 0;
 
     // prologue: H_0, BA_0 and the x_init term of ru[0]
     {
@@ -101,8 +101,8 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
             for (int tj = 0; tj <= ti && tj < S::CT; ++tj) {
                 Frag &f = P[S::T(ti, tj)];
                 const int r = 8 * ti + rq, col = 8 * tj + cq;
-                f.a = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, r, col);
-                f.b = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, r, col + 1);
+                f.a = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, ti, r, col);
+                f.b = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, ti, r, col + 1);
             }
         }
         if (s > 0) {
@@ -174,19 +174,20 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
                 const double urk = __shfl_sync(FULL, vk, 4 * rq + src);
                 const double uc0 = __shfl_sync(FULL, vk, 4 * cq + src);
                 const double uc1 = __shfl_sync(FULL, vk, 4 * (cq + 1) + src);
-                if (8 * kb + k < S::NUX) {
-                    const bool bad = !(pv > dfloor && isfinite(pv));
-                    my_fail = bad ? min(my_fail, fail_key(kKindRiccati, c, s, 8 * kb + k)) : my_fail;
-                    pv = bad ? 1.0 : pv;
+                if (8 * kb + k < S::NUX) { // potrf pivot check (off the critical path)
+                    const bool first = !(pv > dfloor && isfinite(pv)) && fail_piv < 0;
+                    fail_piv = first ? 8 * kb + k : fail_piv;
+                    fail_stage = first ? s : fail_stage;
                 }
-                const double iv = rsqrt(pv);
+                const double iv = rsqrt_nr(pv);
                 const double lc0 = (cq > k) ? uc0 * iv : 0.0;
                 const double lc1 = (cq + 1 > k) ? uc1 * iv : 0.0;
                 const double lrk = urk * iv;
-                if (q2 == src) {
-                    double &e = (k & 1) ? dg.b : dg.a;
-                    e = (rq == k) ? pv * iv : lrk;
-                }
+                const double nv = (rq == k) ? pv * iv : lrk;
+                if (k & 1)
+                    dg.b = (q2 == src) ? nv : dg.b;
+                else
+                    dg.a = (q2 == src) ? nv : dg.a;
                 dg.a -= lrk * lc0;
                 dg.b -= lrk * lc1;
 #pragma unroll
@@ -194,10 +195,10 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
                     Frag &x = P[S::T(ti, kb)];
                     const double vq = (k & 1) ? x.b : x.a;
                     const double xrq = __shfl_sync(FULL, vq, 4 * rq + src) * iv;
-                    if (q2 == src) {
-                        if (k & 1) x.b = xrq;
-                        else x.a = xrq;
-                    }
+                    if (k & 1)
+                        x.b = (q2 == src) ? xrq : x.b;
+                    else
+                        x.a = (q2 == src) ? xrq : x.a;
                     x.a -= xrq * lc0;
                     x.b -= xrq * lc1;
                 }
@@ -377,6 +378,8 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
         for (int v = 0; v <= u; ++v)
             st_frag(a.trail + ((size_t)chain * g.NTT + S::T(u, v)) * kTileElems, lane,
                     P[S::T(S::CT + u, S::CT + v)]);
+    unsigned long long my_fail =
+        fail_piv >= 0 ? fail_key(kKindRiccati, c, fail_stage, fail_piv) : ~0ull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
         my_fail = min(my_fail, __shfl_xor_sync(0xffffffffu, my_fail, o));
@@ -403,8 +406,8 @@ bool launch_wd(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
 template <int NU, int NX, int WPB> bool launch_w(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
     if (g.nu != NU || g.nx != NX)
         return false;
-    static const bool staged = getenv("CYQ_RICCATI_STAGED") != nullptr;
-    return staged ? launch_wd<NU, NX, WPB, false>(g, st, ra) : launch_wd<NU, NX, WPB, true>(g, st, ra);
+    static const bool direct = getenv("CYQ_RICCATI_DIRECT") != nullptr;
+    return direct ? launch_wd<NU, NX, WPB, true>(g, st, ra) : launch_wd<NU, NX, WPB, false>(g, st, ra);
 }
 } // namespace
 

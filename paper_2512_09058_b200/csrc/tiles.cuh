@@ -41,16 +41,16 @@ __device__ __forceinline__ void panel_cholesky(Frag (&P)[NT], int npiv, double d
             if (8 * kb + k < npiv) {
                 const bool bad = !(pv > dfloor && isfinite(pv));
                 fail = (bad && fail < 0) ? 8 * kb + k : fail;
-                pv = bad ? 1.0 : pv;
             }
-            const double iv = rsqrt(pv);
+            const double iv = rsqrt_nr(pv);
             const double lc0 = (cq > k) ? uc0 * iv : 0.0;
             const double lc1 = (cq + 1 > k) ? uc1 * iv : 0.0;
             const double lrk = urk * iv;
-            if (q2 == src) {
-                double &e = (k & 1) ? dg.b : dg.a;
-                e = (rq == k) ? pv * iv : lrk;
-            }
+            const double nv = (rq == k) ? pv * iv : lrk;
+            if (k & 1)
+                dg.b = (q2 == src) ? nv : dg.b;
+            else
+                dg.a = (q2 == src) ? nv : dg.a;
             dg.a -= lrk * lc0;
             dg.b -= lrk * lc1;
 #pragma unroll
@@ -58,10 +58,10 @@ __device__ __forceinline__ void panel_cholesky(Frag (&P)[NT], int npiv, double d
                 Frag &x = P[T(ti, kb)];
                 const double vq = (k & 1) ? x.b : x.a;
                 const double xrq = __shfl_sync(kFull, vq, 4 * rq + src) * iv;
-                if (q2 == src) {
-                    if (k & 1) x.b = xrq;
-                    else x.a = xrq;
-                }
+                if (k & 1)
+                    x.b = (q2 == src) ? xrq : x.b;
+                else
+                    x.a = (q2 == src) ? xrq : x.a;
                 x.a -= xrq * lc0;
                 x.b -= xrq * lc1;
             }
