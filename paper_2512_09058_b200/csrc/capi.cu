@@ -320,8 +320,8 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
             if (do_solve) {
                 SchurArgs sv = sa;
                 sv.do_factor = 0;
-                schur_cr_kernel<<<g.batch, 32 * schur_warps(g), schur_smem_bytes(g),
-                                  ctx->stream>>>(sv);
+                const int nw = schur_warps_solve(g);
+                schur_cr_kernel<<<g.batch, 32 * nw, schur_smem_for(g, nw), ctx->stream>>>(sv);
             }
         } else {
             schur_cr_kernel<<<g.batch, 32 * schur_warps(g), schur_smem_bytes(g), ctx->stream>>>(sa);

@@ -50,7 +50,7 @@ struct BacksubArgs {
 //   D[P], K[P]            level-0 block tridiagonal (diag, subdiag)
 //   Mb[P], Z[P]           Mbwd and L_Q^{-1} per column (scratch)
 //   bn[P * nx]            bwd_neg = T x' per column (scratch)
-//   per level l: L[half], U[half], Y[half], M[half], Kn[half]
+//   per level l: L[half], U[half], Y[half], M[half], Kn[half], CY[half]
 //   Lbase                 base Cholesky factor
 //   rhs[P * nx]
 struct SchurLayout {
@@ -72,7 +72,7 @@ struct SchurLayout {
         long long off = s.lvl0;
         int sz = P;
         for (int l = 0; l < lg; ++l, sz /= 2)
-            off += 5LL * (sz / 2) * nn;
+            off += 6LL * (sz / 2) * nn;
         s.Lbase = off;
         s.rhs = s.Lbase + nn;
         s.total = s.rhs + (long long)P * nx;
@@ -84,7 +84,7 @@ struct SchurLayout {
         long long off = lvl0;
         int sz = P;
         for (int k = 0; k < l; ++k, sz /= 2)
-            off += 5LL * (sz / 2) * nn;
+            off += 6LL * (sz / 2) * nn;
         return off + (long long)which * (sz / 2) * nn;
     }
 };
@@ -106,5 +106,7 @@ constexpr int BACKSUB_WPB = 4; // chains (warps) per back-substitution CTA (max)
 int backsub_wpb(const Geo &g);
 size_t schur_smem_bytes(const Geo &g);
 int schur_warps(const Geo &g);
+int schur_warps_solve(const Geo &g);
+size_t schur_smem_for(const Geo &g, int nw);
 
 } // namespace cyqb

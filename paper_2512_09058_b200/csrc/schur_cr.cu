@@ -138,9 +138,16 @@ __device__ __forceinline__ double fac_at(const Geo &g, const double *st, int r, 
 
 } // namespace
 
-size_t schur_smem_bytes(const Geo &g) {
+size_t schur_smem_bytes(const Geo &g) { return schur_smem_for(g, schur_warps(g)); }
+size_t schur_smem_for(const Geo &g, int nw) {
     const int s = stride_of(g.nx);
-    return ((size_t)schur_warps(g) * 4 * g.nx * s + (size_t)g.P * g.nx) * sizeof(double);
+    return ((size_t)nw * 4 * g.nx * s + (size_t)g.P * g.nx) * sizeof(double);
+}
+// solve-only launches (factor done by the tile kernels): a few warps per
+// instance, several instances per SM
+int schur_warps_solve(const Geo &g) {
+    const int w = schur_warps(g);
+    return w < 4 ? w : 4;
 }
 
 int schur_warps(const Geo &g) {
