@@ -1,0 +1,207 @@
+// Back substitution, compile-time (nu, nx) warp-per-chain fast path for the
+// BASELINE shapes (nux <= 32, nx <= 32); same algorithm and output as
+// backsub.cu (kkt_solve.cpp:185-307):
+//   y_s   = [u'; x']_s - [LB ALQ]_s' lam_f
+//   s = n-1:  x_s += L_Q^{-1} lam_b                      (T' lam_b)
+//   s < n-1:  w  = -wl_s - ALQ_s' lam_f,  t = w - L_Q' (BA_{s+1} z_{s+1}),
+//             lam^{j(s+1)} = -L_Q t,   x_s -= t
+//   z_s   = LH_s^{-T} y_s
+// Lane k owns vector entry k; the stage's stored pivot tiles, y, wl and
+// BA_{s+1} are staged with cp.async (16-byte granules) one stage ahead into
+// a per-warp double buffer; all tile addressing is compile-time except the
+// lane's own column.
+#include "kernels.h"
+#include "riccati_common.cuh"
+
+#include <cstdlib>
+
+namespace cyqb {
+
+using namespace cyqb::ric;
+
+namespace {
+
+template <int NU, int NX> struct BS {
+    using S = Shp<NU, NX>;
+    static constexpr int TILES = S::NPT * kTileElems;
+    static constexpr int OFF_Y = TILES, OFF_WL = OFF_Y + ((S::NUX + 1) & ~1);
+    static constexpr int OFF_B = OFF_WL + ((NX + 1) & ~1);
+    static constexpr int OFF_A = OFF_B + ((NX * NU + 1) & ~1);
+    static constexpr int BUF = OFF_A + ((NX * NX + 1) & ~1);
+    static constexpr int VEC = 64; // z (nux), lf/lb scratch
+    static constexpr int PER_WARP = 2 * BUF + VEC;
+    // stored-tile offset of panel entry (r, col), r/col compile-time or not
+    __host__ __device__ static constexpr int at(int r, int col) {
+        return ((r / 8) < S::CT ? S::T(r / 8, col / 8)
+                                : S::CT * (S::CT + 1) / 2 + (r / 8 - S::CT) * S::CT + col / 8) *
+                   kTileElems +
+               (r % 8) * 8 + col % 8;
+    }
+};
+
+template <int NU, int NX>
+__device__ __forceinline__ void bs_stage(const BacksubArgs &a, double *buf, size_t chain, int b,
+                                         int c, int s, int lane) {
+    using S = Shp<NU, NX>;
+    using L = BS<NU, NX>;
+    const Geo &g = a.g;
+    const int n = g.n, N = g.N;
+    wcopy<L::TILES, 0>(buf, a.fac + (chain * n + s) * S::NPT * kTileElems, lane);
+    wcopy<S::NUX, 0>(buf + L::OFF_Y, a.y + (chain * n + s) * S::NUX, lane);
+    if (s + 1 < n) {
+        wcopy<NX, 0>(buf + L::OFF_WL, a.wl + (chain * n + s) * NX, lane);
+        const int j1 = g.stage_of(c, s + 1);
+        const bool in = j1 < N;
+        wcopy<NX * NU, 0>(buf + L::OFF_B, in ? a.p.B + ((size_t)b * N + j1) * NX * NU : nullptr,
+                          lane);
+        wcopy<NX * NX, 0>(buf + L::OFF_A,
+                          (in && j1 != 0) ? a.p.A + ((size_t)b * N + j1) * NX * NX : nullptr, lane);
+    }
+    cp_commit();
+}
+
+} // namespace
+
+template <int NU, int NX, int WPB>
+__global__ void __launch_bounds__(32 * WPB) backsub_warp_kernel(BacksubArgs a) {
+    using S = Shp<NU, NX>;
+    using L = BS<NU, NX>;
+    constexpr int NUX = S::NUX, TOP = S::TOP;
+    extern __shared__ __align__(16) double sm[];
+    const Geo &g = a.g;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const size_t chain = (size_t)blockIdx.x * WPB + wib;
+    if (chain >= (size_t)g.batch * g.P)
+        return;
+    const int b = (int)(chain / g.P), c = (int)(chain % g.P), n = g.n;
+    double *base = sm + (size_t)wib * L::PER_WARP;
+    double *bufs[2] = {base, base + L::BUF};
+    double *z = base + 2 * L::BUF; // nux: z_{s+1}
+    double *lf = z + 32;           // nx: lam_f (smem broadcast)
+
+    const double lfk = lane < NX ? a.lamc[((size_t)b * g.P + c) * NX + lane] : 0.0;
+    const double lbk = lane < NX ? a.lamc[((size_t)b * g.P + (c - 1 + g.P) % g.P) * NX + lane] : 0.0;
+    if (lane < NX)
+        lf[lane] = lfk;
+    bs_stage<NU, NX>(a, bufs[0], chain, b, c, n - 1, lane);
+
+    for (int s = n - 1; s >= 0; --s) {
+        const double *buf = bufs[(n - 1 - s) & 1];
+        if (s > 0) {
+            bs_stage<NU, NX>(a, bufs[(n - s) & 1], chain, b, c, s - 1, lane);
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        __syncwarp();
+        const int j = g.stage_of(c, s), xi = g.x_index_of(c, s);
+        const int k = lane; // this lane's entry of the nux-vector
+        // y_k -= ([LB ALQ]' lam_f)_k ; idg_k = 1 / LH_kk
+        double gk = 0.0;
+#pragma unroll
+        for (int q = 0; q < NX; ++q)
+            gk += (k < NUX ? buf[L::at(TOP + q, 0) + (k / 8) * kTileElems + k % 8] : 0.0) * lf[q];
+        double Y = (k < NUX) ? buf[L::OFF_Y + (k < NUX ? k : 0)] - gk : 0.0;
+        const double idg = (k < NUX) ? 1.0 / buf[L::at(k < NUX ? k : 0, k < NUX ? k : 0)] : 0.0;
+        if (s == n - 1) {
+            // x += L_Q^{-1} lam_b  (T' lam_b, kkt_solve.cpp:218-223); lane i holds t_i
+            double t = (lane < NX) ? lbk : 0.0;
+#pragma unroll
+            for (int kk = 0; kk < NX; ++kk) {
+                const double idk = __shfl_sync(0xffffffffu, idg, NU + kk);
+                const double xk = __shfl_sync(0xffffffffu, t, kk) * idk;
+                if (lane == kk)
+                    t = xk;
+                else if (lane > kk && lane < NX)
+                    t -= buf[L::at(NU + (lane < NX ? lane : 0), NU + kk)] * xk;
+            }
+            // move t_i (lane i) to Y_{nu+i} (lane nu+i)
+            const double ti = __shfl_sync(0xffffffffu, t, (lane - NU) & 31);
+            if (k >= NU && k < NUX)
+                Y += ti;
+        } else {
+            const int j1 = g.stage_of(c, s + 1);
+            // w_i = -wl_i - g_{nu+i}; zn_i = (B z_u + A z_x)_i ; lane i
+            const double gx = __shfl_sync(0xffffffffu, gk, (lane + NU) & 31);
+            double zn = 0.0;
+            if (lane < NX) {
+#pragma unroll
+                for (int q = 0; q < NU; ++q)
+                    zn += buf[L::OFF_B + lane * NU + q] * z[q];
+#pragma unroll
+                for (int q = 0; q < NX; ++q)
+                    zn += buf[L::OFF_A + lane * NX + q] * z[NU + q];
+            }
+            const double w = (lane < NX) ? -buf[L::OFF_WL + (lane < NX ? lane : 0)] - gx : 0.0;
+            // t_i = w_i - sum_{k >= i} L_Q[k][i] zn_k
+            double t = w;
+#pragma unroll
+            for (int kk = 0; kk < NX; ++kk) {
+                const double znk = __shfl_sync(0xffffffffu, zn, kk);
+                if (lane <= kk && lane < NX)
+                    t -= buf[L::at(NU + kk, NU + (lane < NX ? lane : 0))] * znk;
+            }
+            // lam^{j(s+1)}_i = -sum_{k <= i} L_Q[i][k] t_k
+            double lam = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < NX; ++kk) {
+                const double tk = __shfl_sync(0xffffffffu, t, kk);
+                if (lane >= kk && lane < NX)
+                    lam -= buf[L::at(NU + (lane < NX ? lane : 0), NU + kk)] * tk;
+            }
+            if (lane < NX && j1 < g.N)
+                a.sol.lam[((size_t)b * g.N + j1) * NX + lane] = lam;
+            const double ti = __shfl_sync(0xffffffffu, t, (lane - NU) & 31);
+            if (k >= NU && k < NUX)
+                Y -= ti;
+        }
+        // z = LH^{-T} Y : back substitution over the top block, lane k owns Y_k
+#pragma unroll
+        for (int r = NUX - 1; r >= 0; --r) {
+            const double zr = __shfl_sync(0xffffffffu, Y * idg, r);
+            if (lane == r)
+                Y = zr;
+            else if (lane < r)
+                Y -= buf[L::at(r, 0) + (lane / 8) * kTileElems + lane % 8] * zr;
+        }
+        __syncwarp();
+        if (k < NUX) {
+            z[k] = Y;
+            if (k < NU) {
+                if (j < g.N)
+                    a.sol.u[((size_t)b * g.N + j) * NU + k] = Y;
+            } else if (xi <= g.N) {
+                a.sol.x[((size_t)b * (g.N + 1) + xi) * NX + (k - NU)] = Y;
+            }
+        }
+        __syncwarp();
+    }
+    if (c == 0 && lane < NX)
+        a.sol.x[(size_t)b * (g.N + 1) * NX + lane] = __ldg(a.p.x_init + (size_t)b * NX + lane);
+}
+
+namespace {
+template <int NU, int NX, int WPB> bool launch_b(const Geo &g, cudaStream_t st, const BacksubArgs &ba) {
+    if (g.nu != NU || g.nx != NX)
+        return false;
+    const size_t smem = (size_t)WPB * BS<NU, NX>::PER_WARP * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(backsub_warp_kernel<NU, NX, WPB>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const int chains = g.batch * g.P;
+    backsub_warp_kernel<NU, NX, WPB><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ba);
+    return true;
+}
+} // namespace
+
+bool launch_backsub_warp(const Geo &g, cudaStream_t st, const BacksubArgs &ba) {
+    if (getenv("CYQ_NO_BACKSUB_WARP"))
+        return false;
+    return launch_b<10, 20, 2>(g, st, ba) || launch_b<8, 16, 2>(g, st, ba) ||
+           launch_b<4, 12, 2>(g, st, ba) || launch_b<5, 10, 2>(g, st, ba);
+}
+
+} // namespace cyqb

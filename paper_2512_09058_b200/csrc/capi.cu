@@ -343,9 +343,11 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
         BacksubArgs ba{g, p, ws.fac, ws.y, ws.wl, ws.lamc, *sol};
         {
             Timed t(ctx, 2);
-            const int wpb = backsub_wpb(g);
-            backsub_kernel<<<(chains + wpb - 1) / wpb, 32 * wpb, backsub_smem_bytes(g),
-                             ctx->stream>>>(ba);
+            if (!launch_backsub_warp(g, ctx->stream, ba)) {
+                const int wpb = backsub_wpb(g);
+                backsub_kernel<<<(chains + wpb - 1) / wpb, 32 * wpb, backsub_smem_bytes(g),
+                                 ctx->stream>>>(ba);
+            }
         }
         CU(cudaGetLastError());
     }

@@ -95,6 +95,8 @@ bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
 bool launch_riccati_cta2(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
 // tile-based Schur assembly + CR factorization (compile-time nx); false if n/a
 bool launch_schur_tiles(const Geo &g, cudaStream_t st, const SchurArgs &sa);
+// compile-time (nu, nx) warp-per-chain back substitution; false if n/a
+bool launch_backsub_warp(const Geo &g, cudaStream_t st, const BacksubArgs &ba);
 __global__ void schur_cr_kernel(SchurArgs a);
 __global__ void backsub_kernel(BacksubArgs a);
 
