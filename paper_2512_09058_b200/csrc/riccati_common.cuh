@@ -26,9 +26,10 @@ template <int NU, int NX> struct Shp {
     static constexpr int BB = NX * NU + NX * NX + NX;
     static constexpr int HBp = (HB + 1) & ~1, BBp = (BB + 1) & ~1;
     static constexpr int SMEM_STAGED =
-        (TT * NXT + NLQ) * kTileElems + HBp + BBp + 2 * ((NX + 1) & ~1);
+        (TT * NXT + NLQ) * kTileElems + HBp + BBp + 2 * ((NX + 1) & ~1) + kTileElems;
     // direct mode: stage data read from global (L2-prefetched one stage ahead)
-    static constexpr int SMEM_DIRECT = (TT * NXT + NLQ) * kTileElems + 2 * ((NU + 1) & ~1);
+    static constexpr int SMEM_DIRECT =
+        (TT * NXT + NLQ) * kTileElems + 2 * ((NU + 1) & ~1) + kTileElems;
     __host__ __device__ static constexpr int T(int i, int j) { return i * (i + 1) / 2 + j; }
 };
 

@@ -26,7 +26,7 @@ namespace cyqb {
 
 using namespace cyqb::ric;
 
-template <int NU, int NX, int WPB, bool DIRECT>
+template <int NU, int NX, int WPB, bool DIRECT, bool INV>
 __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_kernel(RiccatiArgs a) {
     using S = Shp<NU, NX>;
     extern __shared__ __align__(16) double sm[];
@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
 
     constexpr int SMEM_DBL = DIRECT ? S::SMEM_DIRECT : S::SMEM_STAGED;
     double *base = sm + (size_t)wib * SMEM_DBL;
+    double *tscr = base + SMEM_DBL - kTileElems; // 8x8 transpose scratch
     double *Wsm = base;                                   // TT x NXT tiles
     double *Lsm = Wsm + S::TT * S::NXT * kTileElems;      // NLQ tiles (x-x block of L)
     Stage<NU, NX> st;
@@ -165,6 +166,7 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
 #pragma unroll
         for (int kb = 0; kb < S::CT; ++kb) {
             Frag &dg = P[S::T(kb, kb)];
+            Frag idt{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0};
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 constexpr unsigned FULL = 0xffffffffu;
@@ -190,21 +192,49 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
                     dg.a = (q2 == src) ? nv : dg.a;
                 dg.a -= lrk * lc0;
                 dg.b -= lrk * lc1;
+                if (!INV) {
 #pragma unroll
-                for (int ti = kb + 1; ti < S::TT; ++ti) {
-                    Frag &x = P[S::T(ti, kb)];
-                    const double vq = (k & 1) ? x.b : x.a;
+                    for (int ti = kb + 1; ti < S::TT; ++ti) {
+                        Frag &x = P[S::T(ti, kb)];
+                        const double vq = (k & 1) ? x.b : x.a;
+                        const double xrq = __shfl_sync(FULL, vq, 4 * rq + src) * iv;
+                        if (k & 1)
+                            x.b = (q2 == src) ? xrq : x.b;
+                        else
+                            x.a = (q2 == src) ? xrq : x.a;
+                        x.a -= xrq * lc0;
+                        x.b -= xrq * lc1;
+                    }
+                } else { // same step on one identity tile: ends as L_kk^{-T}
+                    const double vq = (k & 1) ? idt.b : idt.a;
                     const double xrq = __shfl_sync(FULL, vq, 4 * rq + src) * iv;
                     if (k & 1)
-                        x.b = (q2 == src) ? xrq : x.b;
+                        idt.b = (q2 == src) ? xrq : idt.b;
                     else
-                        x.a = (q2 == src) ? xrq : x.a;
-                    x.a -= xrq * lc0;
-                    x.b -= xrq * lc1;
+                        idt.a = (q2 == src) ? xrq : idt.a;
+                    idt.a -= xrq * lc0;
+                    idt.b -= xrq * lc1;
                 }
             }
             if (cq > rq) dg.a = 0.0;
             if (cq + 1 > rq) dg.b = 0.0;
+            if (INV) {
+                // L^{-1} = (L^{-T})' through a shared-memory transpose, then
+                // every sub-diagonal tile at once: X <- X L^{-T} = X (L^{-1})'
+                // (two DMMAs per tile instead of eight dependent pivot steps)
+                st_frag(tscr, lane, idt);
+                __syncwarp();
+                Frag linv;
+                linv.a = tscr[cq * 8 + rq];
+                linv.b = tscr[(cq + 1) * 8 + rq];
+                __syncwarp();
+#pragma unroll
+                for (int ti = kb + 1; ti < S::TT; ++ti) {
+                    Frag x = P[S::T(ti, kb)], r{0.0, 0.0};
+                    tile_gemm_nt(r, x, linv);
+                    P[S::T(ti, kb)] = r;
+                }
+            }
             // trailing update C(ti,tj) -= L(ti,kb) L(tj,kb)': the next diagonal
             // tile first (its factorization can start early), then both k
             // slices over all tiles so consecutive DMMAs are independent
@@ -389,25 +419,30 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
 
 // ---- dispatch ----------------------------------------------------------------
 namespace {
-template <int NU, int NX, int WPB, bool DIRECT>
+template <int NU, int NX, int WPB, bool DIRECT, bool INV>
 bool launch_wd(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
     using S = Shp<NU, NX>;
     const size_t smem = (size_t)WPB * (DIRECT ? S::SMEM_DIRECT : S::SMEM_STAGED) * sizeof(double);
+    static_assert(S::SMEM_STAGED % 2 == 0 && S::SMEM_DIRECT % 2 == 0, "16-byte aligned warps");
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(riccati_warp_kernel<NU, NX, WPB, DIRECT>,
+        cudaFuncSetAttribute(riccati_warp_kernel<NU, NX, WPB, DIRECT, INV>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     const int chains = g.batch * g.P;
-    riccati_warp_kernel<NU, NX, WPB, DIRECT><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ra);
+    riccati_warp_kernel<NU, NX, WPB, DIRECT, INV><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ra);
     return true;
 }
 template <int NU, int NX, int WPB> bool launch_w(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
     if (g.nu != NU || g.nx != NX)
         return false;
     static const bool direct = getenv("CYQ_RICCATI_DIRECT") != nullptr;
-    return direct ? launch_wd<NU, NX, WPB, true>(g, st, ra) : launch_wd<NU, NX, WPB, false>(g, st, ra);
+    static const bool noinv = getenv("CYQ_RICCATI_NOINV") != nullptr;
+    if (direct)
+        return launch_wd<NU, NX, WPB, true, true>(g, st, ra);
+    return noinv ? launch_wd<NU, NX, WPB, false, false>(g, st, ra)
+                 : launch_wd<NU, NX, WPB, false, true>(g, st, ra);
 }
 } // namespace
 
