@@ -142,11 +142,14 @@ def cpu_reference_rate(p, P, target_s, impl_kind=None, threads=None):
         run = lambda n: orc.bench(p, P, n, threads)  # noqa: E731
     key = (id(p), kind, threads)
     if key not in _CAL:
-        n0 = max(threads, 16)
+        # two-stage calibration: the first short run includes thread start-up
+        n0 = max(4 * threads, 64)
         t0 = run(n0)
         if t0 <= 0:
             raise RuntimeError("CPU baseline failed")
-        _CAL[key] = max(n0, int(n0 * target_s / max(t0, 1e-6)))
+        n1 = max(n0, int(n0 * min(2.0, target_s / 4) / max(t0, 1e-6)))
+        t1 = run(n1)
+        _CAL[key] = max(n1, int(n1 * target_s / max(t1, 1e-6)))
     n = _CAL[key]
     t = run(n)
     if t <= 0:

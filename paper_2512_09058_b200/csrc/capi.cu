@@ -29,6 +29,7 @@ struct cyq_ctx {
     size_t hbuf_bytes = 0;
     void *wsbuf = nullptr;
     size_t wsbuf_bytes = 0;
+    cudaStream_t copy_stream = nullptr; // host->device staging of chunked calls
     // per-kernel timing (cyq_ctx_profile)
     bool profile = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
@@ -354,6 +355,44 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
     return CYQ_OK;
 }
 
+// kkt::solve over an existing factor: forward sweep (forward.cu), Schur/CR
+// solve, back substitution. `p` carries the explicit rhs.
+int launch_solve(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &ws,
+                 const SolView &sol) {
+    static bool attr = false;
+    if (!attr) {
+        CU(cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                227 * 1024));
+        attr = true;
+    }
+    const int chains = g.batch * g.P;
+    BacksubArgs ba{g, p, ws.fac, ws.y, ws.wl, ws.lamc, sol};
+    {
+        Timed t(ctx, 3);
+        const int wpb = 2 * forward_smem_per_warp(g) <= 200 * 1024 ? 2 : 1;
+        forward_kernel<<<(chains + wpb - 1) / wpb, 32 * wpb, wpb * forward_smem_per_warp(g),
+                         ctx->stream>>>(ba, ws.y, ws.wl, ws.trail);
+    }
+    CU(cudaGetLastError());
+    SchurArgs sa{g, p, ws.fac, ws.y, ws.trail, ws.schur, ws.lamc, sol.lam, ws.fail, 0, 1};
+    {
+        Timed t(ctx, 1);
+        const int nw = schur_warps_solve(g);
+        schur_cr_kernel<<<g.batch, 32 * nw, schur_smem_for(g, nw), ctx->stream>>>(sa);
+    }
+    CU(cudaGetLastError());
+    {
+        Timed t(ctx, 2);
+        if (!launch_backsub_warp(g, ctx->stream, ba)) {
+            const int wpb = backsub_wpb(g);
+            backsub_kernel<<<(chains + wpb - 1) / wpb, 32 * wpb, backsub_smem_bytes(g),
+                             ctx->stream>>>(ba);
+        }
+    }
+    CU(cudaGetLastError());
+    return CYQ_OK;
+}
+
 int decode_status(cyq_ctx *ctx, const Geo &g, const unsigned long long *dfail,
                   cyq_status *status) {
     std::vector<unsigned long long> h(g.batch);
@@ -440,6 +479,8 @@ int cyq_ctx_destroy(cyq_ctx *ctx) {
         cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream)
         cudaStreamDestroy(ctx->stream);
+    if (ctx->copy_stream)
+        cudaStreamDestroy(ctx->copy_stream);
     delete ctx;
     return CYQ_OK;
 }
@@ -491,28 +532,88 @@ int cyq_solve_problem_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_ba
             return rc;
         return decode_status(ctx, g, ws.fail, status);
     }
-    // host memory: stage through device buffers
+    // host memory: the batch is split into chunks whose host->device copies
+    // (copy stream) overlap the previous chunk's kernels (compute stream);
+    // each chunk's solution is copied back on the compute stream.
     const size_t pd = prob_doubles(g), sd = sol_doubles(g);
     rc = ensure(ctx, &ctx->hbuf, &ctx->hbuf_bytes, (pd + sd) * sizeof(double));
     if (rc)
         return rc;
+    if (!ctx->copy_stream)
+        CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     double *base = static_cast<double *>(ctx->hbuf);
-    ProbView dp = carve_prob(base, g);
-    rc = copy_prob_h2d(ctx, g, prob, dp);
+    const ProbView dp = carve_prob(base, g);
+    const size_t B = g.batch, N = g.N, nx = g.nx, nu = g.nu;
+    const SolView svall{base + pd, base + pd + B * N * nu, base + pd + B * N * nu + B * (N + 1) * nx};
+    const int nch = B >= 256 ? 8 : (B >= 32 ? 4 : 1);
+    const int per = (int)((B + nch - 1) / nch);
+    Geo gc = g;
+    gc.batch = per;
+    const WsSizes wc = ws_sizes(gc);
+    rc = ensure(ctx, &ctx->wsbuf, &ctx->wsbuf_bytes, (size_t)nch * wc.total);
     if (rc)
         return rc;
-    const size_t B = g.batch, N = g.N;
-    SolView sv{base + pd, base + pd + B * N * g.nu, base + pd + B * N * g.nu + B * (N + 1) * g.nx};
-    rc = launch_pipeline(ctx, g, dp, ws, &sv, true);
-    if (rc)
-        return rc;
-    CU(cudaMemcpyAsync(sol->u, sv.u, B * N * g.nu * sizeof(double), cudaMemcpyDeviceToHost,
-                       ctx->stream));
-    CU(cudaMemcpyAsync(sol->x, sv.x, B * (N + 1) * g.nx * sizeof(double),
-                       cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaMemcpyAsync(sol->lam, sv.lam, B * N * g.nx * sizeof(double), cudaMemcpyDeviceToHost,
-                       ctx->stream));
-    return decode_status(ctx, g, ws.fail, status);
+    const std::pair<const double *, size_t> hp[9] = {
+        {prob->A, N * nx * nx}, {prob->B, N * nx * nu}, {prob->R, N * nu * nu},
+        {prob->S, N * nu * nx}, {prob->Q, (N + 1) * nx * nx}, {prob->f, N * nx},
+        {prob->r, N * nu},      {prob->q, (N + 1) * nx},     {prob->x_init, nx}};
+    const double *dpa[9] = {dp.A, dp.B, dp.R, dp.S, dp.Q, dp.f, dp.r, dp.q, dp.x_init};
+    for (int i = 0; i < 9; ++i)
+        if (!hp[i].first)
+            return set_err(ctx, CYQ_INVALID_ARG, "null problem array");
+    std::vector<cudaEvent_t> evs;
+    int worst = CYQ_OK;
+    for (int ch = 0; ch < nch; ++ch) {
+        const size_t b0 = (size_t)ch * per;
+        if (b0 >= B)
+            break;
+        const size_t cb = std::min<size_t>(per, B - b0);
+        for (int i = 0; i < 9; ++i)
+            CU(cudaMemcpyAsync(const_cast<double *>(dpa[i]) + b0 * hp[i].second,
+                               hp[i].first + b0 * hp[i].second, cb * hp[i].second * sizeof(double),
+                               cudaMemcpyHostToDevice, ctx->copy_stream));
+        cudaEvent_t ev = take_event(ctx);
+        CU(cudaEventRecord(ev, ctx->copy_stream));
+        CU(cudaStreamWaitEvent(ctx->stream, ev, 0));
+        evs.push_back(ev);
+        Geo gi = g;
+        gi.batch = (int)cb;
+        ProbView pv{};
+        const double **pvp[9] = {&pv.A, &pv.B, &pv.R, &pv.S, &pv.Q, &pv.f, &pv.r, &pv.q, &pv.x_init};
+        for (int i = 0; i < 9; ++i)
+            *pvp[i] = dpa[i] + b0 * hp[i].second;
+        SolView sv{svall.u + b0 * N * nu, svall.x + b0 * (N + 1) * nx, svall.lam + b0 * N * nx};
+        FactorWS wsi = carve(static_cast<char *>(ctx->wsbuf) + (size_t)ch * wc.total, wc);
+        rc = launch_pipeline(ctx, gi, pv, wsi, &sv, true);
+        if (rc)
+            return rc;
+        CU(cudaMemcpyAsync(sol->u + b0 * N * nu, sv.u, cb * N * nu * sizeof(double),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaMemcpyAsync(sol->x + b0 * (N + 1) * nx, sv.x, cb * (N + 1) * nx * sizeof(double),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaMemcpyAsync(sol->lam + b0 * N * nx, sv.lam, cb * N * nx * sizeof(double),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    for (int ch = 0; ch < nch; ++ch) {
+        const size_t b0 = (size_t)ch * per;
+        if (b0 >= B)
+            break;
+        Geo gi = g;
+        gi.batch = (int)std::min<size_t>(per, B - b0);
+        FactorWS wsi = carve(static_cast<char *>(ctx->wsbuf) + (size_t)ch * wc.total, wc);
+        const int r2 = decode_status(ctx, gi, wsi.fail, status ? status + b0 : nullptr);
+        if (status)
+            for (size_t k = 0; k < (size_t)gi.batch; ++k)
+                status[b0 + k].instance = (int64_t)(b0 + k);
+        if (r2 == CYQ_CUDA_ERR)
+            return r2;
+        worst = std::max(worst, r2);
+    }
+    for (auto e : evs)
+        ctx->pool.push_back(e);
+    if (worst != CYQ_OK)
+        set_err(ctx, worst, "factorization pivot failure (see status)");
+    return worst;
 }
 
 int cyq_factor_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_batch *prob, int mem,
@@ -600,9 +701,7 @@ int cyq_solve_batch(cyq_ctx *ctx, const cyq_factor *f, const cyq_ocp_batch *prob
         double *s0 = base + rd;
         sv = SolView{s0, s0 + B * N * nu, s0 + B * N * nu + B * (N + 1) * nx};
     }
-    // TODO(perf): a forward-sweep-only kernel over the stored factor; this
-    // re-runs the stage-panel kernel with the new right-hand side row.
-    rc = launch_pipeline(ctx, g, p, f->ws, &sv, true);
+    rc = launch_solve(ctx, g, p, f->ws, sv);
     if (rc)
         return rc;
     if (mem != CYQ_MEM_DEVICE) {

@@ -97,6 +97,9 @@ bool launch_riccati_cta2(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
 bool launch_schur_tiles(const Geo &g, cudaStream_t st, const SchurArgs &sa);
 // compile-time (nu, nx) warp-per-chain back substitution; false if n/a
 bool launch_backsub_warp(const Geo &g, cudaStream_t st, const BacksubArgs &ba);
+// forward substitution over a stored factor (kkt::solve with a new rhs)
+__global__ void forward_kernel(BacksubArgs a, double *y_out, double *wl_out, double *trail);
+__host__ __device__ size_t forward_smem_per_warp(const Geo &g);
 __global__ void schur_cr_kernel(SchurArgs a);
 __global__ void backsub_kernel(BacksubArgs a);
 
