@@ -279,7 +279,7 @@ def run_ours(args):
     # ---- roofline of the dominant kernel --------------------------------
     ph = fma_phases(cfg.N, cfg.nx, cfg.nu, cfg.P)
     k_ms, k_n = kern["riccati_panel"]
-    k_avg = k_ms / max(k_n, 1)
+    k_avg = k_ms / max(k_n, 1)  # one stage-panel launch per step
     k_flops = 2.0 * ph["kernel_riccati_panel"] * B
     peak, peak_src = fp64_peak()
     achieved = k_flops / (k_avg * 1e-3) / 1e12

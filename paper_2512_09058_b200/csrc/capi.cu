@@ -36,6 +36,7 @@ struct cyq_ctx {
     std::vector<cudaEvent_t> pool;
     double ms[4] = {0, 0, 0, 0};
     int64_t launches[4] = {0, 0, 0, 0};
+    int64_t kernels[4] = {0, 0, 0, 0}; // kernel launches per kind
 };
 
 struct cyq_factor {
@@ -252,6 +253,7 @@ struct Timed {
     cyq_ctx *ctx;
     int kind;
     cudaEvent_t a = nullptr, b = nullptr;
+    int kernels = 1; // kernel launches inside the bracket (set by the caller)
     Timed(cyq_ctx *c, int k) : ctx(c), kind(k) {
         if (ctx->profile) {
             a = take_event(ctx);
@@ -263,6 +265,7 @@ struct Timed {
         if (ctx->profile) {
             cudaEventRecord(b, ctx->stream);
             ctx->ev.push_back({kind, {a, b}});
+            ctx->kernels[kind] += kernels;
         }
     }
 };
@@ -318,6 +321,7 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
     {
         Timed t(ctx, 1);
         if (launch_schur_tiles(g, ctx->stream, sa)) { // DMMA-tile factorization
+            t.kernels = 2 + SchurLayout::make(g.P, g.nx).levels + (do_solve ? 1 : 0);
             if (do_solve) {
                 SchurArgs sv = sa;
                 sv.do_factor = 0;
@@ -776,6 +780,8 @@ int cyq_ctx_profile(cyq_ctx *ctx, int enable) {
 }
 
 int cyq_ctx_profile_read(cyq_ctx *ctx, double *ms, int64_t *launches, int reset) {
+    // launches[k] = kernel launches of kind k (several kernels may share one
+    // timed bracket, e.g. the per-level CR kernels); ms[k] = their time
     if (!ctx)
         return CYQ_INVALID_ARG;
     CU(cudaStreamSynchronize(ctx->stream));
@@ -783,7 +789,6 @@ int cyq_ctx_profile_read(cyq_ctx *ctx, double *ms, int64_t *launches, int reset)
         float t = 0;
         CU(cudaEventElapsedTime(&t, e.second.first, e.second.second));
         ctx->ms[e.first] += t;
-        ctx->launches[e.first] += 1;
         ctx->pool.push_back(e.second.first);
         ctx->pool.push_back(e.second.second);
     }
@@ -792,10 +797,10 @@ int cyq_ctx_profile_read(cyq_ctx *ctx, double *ms, int64_t *launches, int reset)
         if (ms)
             ms[k] = ctx->ms[k];
         if (launches)
-            launches[k] = ctx->launches[k];
+            launches[k] = ctx->kernels[k];
         if (reset) {
             ctx->ms[k] = 0;
-            ctx->launches[k] = 0;
+            ctx->kernels[k] = 0;
         }
     }
     return CYQ_OK;

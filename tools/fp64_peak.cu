@@ -68,6 +68,37 @@ __global__ void dmma_kernel(double *out, int iters, double a, double b) {
         out[0] = s;
 }
 
+// DMMA and DFMA interleaved in one instruction stream: tells whether the
+// FP64 tensor path and the FP64 FMA pipe are separate resources.
+__global__ void mixed_kernel(double *out, int iters, double a, double b) {
+    double c[8][2];
+    double acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        c[i][0] = c[i][1] = threadIdx.x * 1e-3 + i;
+        acc[i] = i;
+    }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                dmma(c[i][0], c[i][1], a, b);
+                // 8 DFMA warp-instructions = 256 FMAs, the work of one DMMA
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    acc[q] = fma(acc[q], a, b);
+            }
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        s += c[i][0] + c[i][1] + acc[i];
+    if (s == 12345.678)
+        out[0] = s;
+}
+
 // Single-thread dependent-chain latencies (cycles).
 __global__ void latency_kernel(long long *cyc, double *sink, double x0) {
     double x = x0;
@@ -163,6 +194,26 @@ int main() {
                 best_dmma = tf;
         }
     }
+    // mixed DMMA + DFMA (equal FMA counts); FLOPs counted for both
+    double best_mixed = 0;
+    for (int threads : {128, 256}) {
+        for (int bps : {2, 4}) {
+            int iters = 1000;
+            int grid  = sms * bps;
+            mixed_kernel<<<grid, threads>>>(out, 10, 1.0, 1e-9);
+            CK(cudaDeviceSynchronize());
+            cudaEventRecord(e0);
+            mixed_kernel<<<grid, threads>>>(out, iters, 1.0, 1e-9);
+            cudaEventRecord(e1);
+            CK(cudaEventSynchronize(e1));
+            cudaEventElapsedTime(&ms, e0, e1);
+            double warps = double(grid) * threads / 32;
+            double fl    = 2.0 * warps * iters * 4 * 8 * (256 + 8 * 32);
+            double tf    = fl / (ms * 1e-3) / 1e12;
+            if (tf > best_mixed)
+                best_mixed = tf;
+        }
+    }
     long long *cyc;
     CK(cudaMallocManaged(&cyc, 16 * sizeof(long long)));
     latency_kernel<<<1, 32>>>(cyc, out, 2.0);
@@ -172,10 +223,10 @@ int main() {
     int clk_khz = 0;
     cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
     printf("{\"sms\": %d, \"clock_mhz\": %d, \"dfma_tflops\": %.3f, "
-           "\"dmma_tflops\": %.3f, \"lat_cycles\": {\"dfma\": %lld, "
+           "\"dmma_tflops\": %.3f, \"mixed_dmma_dfma_tflops\": %.3f, \"lat_cycles\": {\"dfma\": %lld, "
            "\"sqrt\": %lld, \"rsqrt\": %lld, \"div\": %lld, \"shfl_f64\": %lld, "
            "\"dmma\": %lld}}\n",
-           sms, clk_khz / 1000, best_dfma, best_dmma, cyc[0], cyc[1], cyc[2],
+           sms, clk_khz / 1000, best_dfma, best_dmma, best_mixed, cyc[0], cyc[1], cyc[2],
            cyc[3], cyc[4], cyc[5]);
     return 0;
 }
