@@ -29,7 +29,8 @@ template <int NU, int NX> struct BS {
     static constexpr int OFF_A = OFF_B + ((NX * NU + 1) & ~1);
     static constexpr int BUF = OFF_A + ((NX * NX + 1) & ~1);
     static constexpr int VEC = 64; // z (nux), lf/lb scratch
-    static constexpr int PER_WARP = 2 * BUF + VEC;
+    static constexpr int NBUF = 1; // single buffer: more resident warps hide the loads
+    static constexpr int PER_WARP = NBUF * BUF + VEC;
     // stored-tile offset of panel entry (r, col), r/col compile-time or not
     __host__ __device__ static constexpr int at(int r, int col) {
         return ((r / 8) < S::CT ? S::T(r / 8, col / 8)
@@ -75,8 +76,8 @@ __global__ void __launch_bounds__(32 * WPB) backsub_warp_kernel(BacksubArgs a) {
         return;
     const int b = (int)(chain / g.P), c = (int)(chain % g.P), n = g.n;
     double *base = sm + (size_t)wib * L::PER_WARP;
-    double *bufs[2] = {base, base + L::BUF};
-    double *z = base + 2 * L::BUF; // nux: z_{s+1}
+    double *bufs[2] = {base, base + (L::NBUF > 1 ? L::BUF : 0)};
+    double *z = base + L::NBUF * L::BUF; // nux: z_{s+1}
     double *lf = z + 32;           // nx: lam_f (smem broadcast)
 
     const double lfk = lane < NX ? a.lamc[((size_t)b * g.P + c) * NX + lane] : 0.0;
@@ -87,7 +88,7 @@ __global__ void __launch_bounds__(32 * WPB) backsub_warp_kernel(BacksubArgs a) {
 
     for (int s = n - 1; s >= 0; --s) {
         const double *buf = bufs[(n - 1 - s) & 1];
-        if (s > 0) {
+        if (L::NBUF > 1 && s > 0) {
             bs_stage<NU, NX>(a, bufs[(n - s) & 1], chain, b, c, s - 1, lane);
             cp_wait<1>();
         } else {
@@ -165,6 +166,10 @@ __global__ void __launch_bounds__(32 * WPB) backsub_warp_kernel(BacksubArgs a) {
                 Y -= buf[L::at(r, 0) + (lane / 8) * kTileElems + lane % 8] * zr;
         }
         __syncwarp();
+        if (L::NBUF == 1 && s > 0) { // buffer consumed: fetch stage s-1
+            __syncwarp();
+            bs_stage<NU, NX>(a, bufs[0], chain, b, c, s - 1, lane);
+        }
         if (k < NUX) {
             z[k] = Y;
             if (k < NU) {
@@ -200,8 +205,8 @@ template <int NU, int NX, int WPB> bool launch_b(const Geo &g, cudaStream_t st, 
 bool launch_backsub_warp(const Geo &g, cudaStream_t st, const BacksubArgs &ba) {
     if (getenv("CYQ_NO_BACKSUB_WARP"))
         return false;
-    return launch_b<10, 20, 2>(g, st, ba) || launch_b<8, 16, 2>(g, st, ba) ||
-           launch_b<4, 12, 2>(g, st, ba) || launch_b<5, 10, 2>(g, st, ba);
+    return launch_b<10, 20, 4>(g, st, ba) || launch_b<8, 16, 4>(g, st, ba) ||
+           launch_b<4, 12, 4>(g, st, ba) || launch_b<5, 10, 4>(g, st, ba);
 }
 
 } // namespace cyqb
