@@ -109,7 +109,8 @@ WsSizes ws_sizes(const Geo &g) {
     s.y = al(chains * g.n * g.nux);
     s.wl = al(chains * g.n * g.nx);
     s.trail = al(chains * g.NTT * kTileElems);
-    s.schur = al((size_t)g.batch * SchurLayout::make(g.P, g.nx).total);
+    s.schur = al((size_t)g.batch * std::max<size_t>(SchurLayout::make(g.P, g.nx).total,
+                                                    schur_fused_doubles(g)));
     s.lamc = al((size_t)g.batch * g.P * g.nx);
     s.fail = al((size_t)g.batch); // 8-byte keys
     s.consts = al(riccati_consts_doubles(g));
@@ -318,9 +319,12 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
     CU(cudaGetLastError());
     SchurArgs sa{g, p, ws.fac, ws.y, ws.trail, ws.schur, ws.lamc,
                  sol ? sol->lam : nullptr, ws.fail, 1, do_solve ? 1 : 0};
+    sa.phase = ra.phase ? ra.phase + 8 * (g.n + 1) + 8 : nullptr;
     {
         Timed t(ctx, 1);
-        if (launch_schur_tiles(g, ctx->stream, sa)) { // DMMA-tile factorization
+        if (launch_schur_fused(g, ctx->stream, sa)) { // one fused kernel per batch
+            t.kernels = 1;
+        } else if (launch_schur_tiles(g, ctx->stream, sa)) { // DMMA-tile factorization
             t.kernels = 2 + SchurLayout::make(g.P, g.nx).levels + (do_solve ? 1 : 0);
             if (do_solve) {
                 SchurArgs sv = sa;
@@ -343,6 +347,16 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
                     h[s * 8 + 1] - h[s * 8 + 0], h[s * 8 + 2] - h[s * 8 + 1],
                     h[s * 8 + 3] - h[s * 8 + 2], h[s * 8 + 4] - h[s * 8 + 3],
                     (s + 1 < g.n ? h[(s + 1) * 8] : h[g.n * 8]) - h[s * 8 + 4]);
+        std::vector<long long> q(32);
+        CU(cudaMemcpyAsync(q.data(), sa.phase, 32 * sizeof(long long), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        if (q[31] > 1 && q[31] < 31) {
+            fprintf(stderr, "schur phases (instance 0):");
+            for (long long k = 1; k < q[31]; ++k)
+                fprintf(stderr, " %lld", q[k] - q[k - 1]);
+            fprintf(stderr, "  total %lld\n", q[q[31] - 1] - q[0]);
+        }
     }
     if (do_solve) {
         BacksubArgs ba{g, p, ws.fac, ws.y, ws.wl, ws.lamc, *sol};
@@ -381,8 +395,10 @@ int launch_solve(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &
     SchurArgs sa{g, p, ws.fac, ws.y, ws.trail, ws.schur, ws.lamc, sol.lam, ws.fail, 0, 1};
     {
         Timed t(ctx, 1);
-        const int nw = schur_warps_solve(g);
-        schur_cr_kernel<<<g.batch, 32 * nw, schur_smem_for(g, nw), ctx->stream>>>(sa);
+        if (!launch_schur_fused(g, ctx->stream, sa)) {
+            const int nw = schur_warps_solve(g);
+            schur_cr_kernel<<<g.batch, 32 * nw, schur_smem_for(g, nw), ctx->stream>>>(sa);
+        }
     }
     CU(cudaGetLastError());
     {

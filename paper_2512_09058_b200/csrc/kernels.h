@@ -37,6 +37,7 @@ struct SchurArgs {
     double *lam_out; // solution lam (nullable)
     unsigned long long *fail;
     int do_factor, do_solve;
+    long long *phase = nullptr; // optional phase clocks of instance 0 (profiling)
 };
 
 struct BacksubArgs {
@@ -95,6 +96,11 @@ bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
 bool launch_riccati_cta2(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
 // tile-based Schur assembly + CR factorization (compile-time nx); false if n/a
 bool launch_schur_tiles(const Geo &g, cudaStream_t st, const SchurArgs &sa);
+// fused Schur + CR factor (+ solve) kernel, one CTA per instance (schur_fused.cu);
+// false if the shape / batch is not served (the caller falls back)
+bool schur_fused_ok(const Geo &g);
+bool launch_schur_fused(const Geo &g, cudaStream_t st, const SchurArgs &sa);
+size_t schur_fused_doubles(const Geo &g);
 // compile-time (nu, nx) warp-per-chain back substitution; false if n/a
 bool launch_backsub_warp(const Geo &g, cudaStream_t st, const BacksubArgs &ba);
 // forward substitution over a stored factor (kkt::solve with a new rhs)

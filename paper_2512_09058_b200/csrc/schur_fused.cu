@@ -1,0 +1,632 @@
+// Schur complement + cyclic reduction, factor and solve, fused into ONE
+// kernel per batch: one CTA per OCP instance, NW warps taking the
+// independent block operations of each phase, __syncthreads between the
+// phases/levels. All per-instance blocks are 8x8-tile-ordered (C-fragment
+// order, XT x XT tiles per nx x nx block) so every load/store is a coalesced
+// 512-byte tile, and the whole instance's working set stays hot in L2 for
+// the few microseconds the CTA lives (the per-level batch-wide kernels in
+// schur_tiles.cu stream it through HBM instead).
+//
+// Restates:
+//   kkt_factor.cpp:163-178    T = L_Q^{-T}, Mbwd = T T', W = T LA'
+//   kkt_factor.cpp:194-212    assemble_schur: diag[c] = Mfwd_c + Mbwd_{c+1},
+//                             subdiag[c-1] = -W_c' = -LA_c T_c'
+//   block_tridiag.cpp:126-171 cr_level: L = chol(M_k), U = K_{k-1}' L^{-T},
+//                             Y = K_k L^{-T}, M' = M - U U' - Y_prev Y_prev',
+//                             K' = -Y U'
+//   block_tridiag.cpp:173-197 cr_factor_base
+//   kkt_solve.cpp:137-182     Schur rhs b_i = fd[n i] - fwd_i + bwd_neg_{i+1}
+//   block_tridiag.cpp:252-333 CRFactor::forward / backward, then negate
+//
+// B200 reformulation: each elimination forms Linv = L^{-1} once (the tile
+// trsm on an identity block plus an 8x8 transpose through shared memory),
+// so U, Y are DMMA products (U = K_{k-1}' Linv', Y = K_k Linv') instead of
+// two dependent triangular solves, and the CR solve is matrix-vector
+// products only (L^{-1} v = Linv v, L^{-T} v = Linv' v): no sequential
+// trsv on the solve path. K_{k-1}' is read as transposed tiles directly from
+// the tile-ordered workspace (two 8-byte loads per lane per tile).
+#include "kernels.h"
+#include "tiles.cuh"
+
+#include <cstdlib>
+
+namespace cyqb {
+
+using tiles::T;
+
+namespace {
+
+template <int NX> struct SF {
+    static constexpr int XT = (NX + 7) / 8;
+    static constexpr int NL = XT * (XT + 1) / 2; // tiles of a lower block
+    static constexpr int NF = XT * XT;           // tiles of a full block
+    static constexpr int XP = 8 * XT;            // padded vector length
+};
+
+__device__ __forceinline__ int fidx(int XT, int i, int j) { return i * XT + j; }
+
+// transposed 8x8 tile load from the tile-ordered workspace: returns the
+// C-fragment of tile' (lane holds X'[rq][cq], X'[rq][cq+1] = X[cq][rq], X[cq+1][rq])
+__device__ __forceinline__ Frag ld_frag_t(const double *tile, int lane) {
+    const int rq = lane >> 2, cq = 2 * (lane & 3);
+    return {tile[cq * 8 + rq], tile[(cq + 1) * 8 + rq]};
+}
+
+__device__ __forceinline__ Frag fadd(Frag x, Frag y) { return {x.a + y.a, x.b + y.b}; }
+__device__ __forceinline__ Frag fsub(Frag x, Frag y) { return {x.a - y.a, x.b - y.b}; }
+
+__device__ __forceinline__ double fac_elem(const Geo &g, const double *st, int r, int col) {
+    const int ti = r / 8, tj = col / 8;
+    const int t = ti < g.CT ? tri_index(ti, tj) : g.CT * (g.CT + 1) / 2 + (ti - g.CT) * g.CT + tj;
+    return __ldg(st + t * kTileElems + (r % 8) * 8 + col % 8);
+}
+
+// y = M v (FULL: XT x XT tiles; else lower tiles T(i, j)); v: XP doubles in
+// shared memory; out[i] = row 8 i + rq, valid in every lane of the quad
+template <int XT, bool FULL>
+__device__ __forceinline__ void matvec(const double *M, const double *v, double (&out)[XT], int lane) {
+    const int cq = 2 * (lane & 3);
+#pragma unroll
+    for (int i = 0; i < XT; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < XT; ++j) {
+            if (!FULL && j > i)
+                continue;
+            const Frag f = ld_frag(M + (FULL ? fidx(XT, i, j) : T(i, j)) * kTileElems, lane);
+            acc = fma(f.a, v[8 * j + cq], acc);
+            acc = fma(f.b, v[8 * j + cq + 1], acc);
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        out[i] = acc;
+    }
+}
+// y = M' v; out[j][h] = entry 8 j + cq + h, valid in every lane with that cq
+template <int XT, bool FULL>
+__device__ __forceinline__ void matvec_t(const double *M, const double *v, double (&out)[XT][2],
+                                         int lane) {
+    const int rq = lane >> 2;
+#pragma unroll
+    for (int j = 0; j < XT; ++j) {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < XT; ++i) {
+            if (!FULL && j > i)
+                continue;
+            const Frag f = ld_frag(M + (FULL ? fidx(XT, i, j) : T(i, j)) * kTileElems, lane);
+            const double vi = v[8 * i + rq];
+            a0 = fma(f.a, vi, a0);
+            a1 = fma(f.b, vi, a1);
+        }
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+            a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+            a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+        }
+        out[j][0] = a0;
+        out[j][1] = a1;
+    }
+}
+
+// Z = L^{-T} (trsm on the identity), transposed through the warp's shared
+// scratch into Li = L^{-1} (lower tiles T(i, j))
+template <int XT, int NL>
+__device__ __forceinline__ void lower_inverse(const Frag (&L)[NL], Frag (&Li)[NL], double *scr,
+                                              int lane) {
+    const int rq = lane >> 2, cq = 2 * (lane & 3);
+    Frag Z[XT * XT];
+#pragma unroll
+    for (int i = 0; i < XT; ++i)
+#pragma unroll
+        for (int j = 0; j < XT; ++j)
+            Z[i * XT + j] = (i == j) ? Frag{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0}
+                                     : Frag{0.0, 0.0};
+    tiles::trsm_rows<XT, XT>(Z, L, lane); // Z = L^{-T}: upper, Z[i][j] = 0 for i > j
+#pragma unroll
+    for (int i = 0; i < XT; ++i)
+#pragma unroll
+        for (int j = i; j < XT; ++j)
+            st_frag(scr + (i * XT + j) * kTileElems, lane, Z[i * XT + j]);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < XT; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j) // Li(i, j) = Z(j, i)'
+            Li[T(i, j)] = ld_frag_t(scr + (j * XT + i) * kTileElems, lane);
+    __syncwarp();
+}
+
+} // namespace
+
+// Per-instance workspace of the fused path, in 8x8 tiles (64 doubles).
+//   Tt[P] full      T_c = L_Q(last stage)^{-T} per column  (persistent)
+//   Li[P-1] lower   L^{-1} of every odd-block elimination   (persistent)
+//   U[P-1], Y[P-1]  full                                     (persistent)
+//   Lb lower        L_base^{-1}                              (persistent)
+//   D[P], Mb[P]     lower: Mfwd_c, Mbwd_c                    (scratch)
+//   K[P] full       level-0 subdiagonal                      (scratch)
+//   M2[P-1], CY[P-1] lower; K2[P-1] full                      (scratch)
+//   bn[P * XP]      bwd_neg = T x' per column
+// Level l (half = P >> (l+1) blocks) starts at block P - (P >> l) of each
+// per-level array.
+struct SFLayout {
+    long long Tt, Li, U, Y, Lb, D, Mb, K, M2, CY, K2, bn, total; // doubles
+    int XT, NL, NF, XP, levels;
+    __host__ __device__ static SFLayout make(int P, int nx) {
+        SFLayout s;
+        s.XT = (nx + 7) / 8;
+        s.NL = s.XT * (s.XT + 1) / 2;
+        s.NF = s.XT * s.XT;
+        s.XP = 8 * s.XT;
+        int lg = 0;
+        while ((1 << lg) < P)
+            ++lg;
+        s.levels = lg;
+        const long long tl = 64LL * s.NL, tf = 64LL * s.NF;
+        long long o = 0;
+        s.Tt = o; o += P * tf;
+        s.Li = o; o += (P - 1) * tl;
+        s.U = o; o += (P - 1) * tf;
+        s.Y = o; o += (P - 1) * tf;
+        s.Lb = o; o += tl;
+        s.D = o; o += P * tl;
+        s.Mb = o; o += P * tl;
+        s.K = o; o += P * tf;
+        s.M2 = o; o += (P - 1) * tl;
+        s.CY = o; o += (P - 1) * tl;
+        s.K2 = o; o += (P - 1) * tf;
+        s.bn = o; o += (long long)P * s.XP;
+        s.total = o;
+        return s;
+    }
+};
+
+size_t schur_fused_doubles(const Geo &g) { return (size_t)SFLayout::make(g.P, g.nx).total; }
+
+namespace {
+
+template <int NX, int NW> __global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs a) {
+    using F = SF<NX>;
+    constexpr int XT = F::XT, NL = F::NL, NF = F::NF, XP = F::XP;
+    constexpr long long TL = 64LL * NL, TF = 64LL * NF;
+    extern __shared__ __align__(16) double sm[];
+    const Geo &g = a.g;
+    const int b = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int rq = lane >> 2, cq = 2 * (lane & 3), q2 = lane & 3;
+    const int P = g.P, nu = g.nu, n = g.n, top = 8 * g.CT;
+    const SFLayout Lo = SFLayout::make(P, NX);
+    double *ws = a.schur + (size_t)b * Lo.total;
+    double *scr = sm + (size_t)warp * NF * kTileElems; // per-warp transpose scratch
+    double *xs = sm + (size_t)NW * NF * kTileElems;    // P x XP: CR solve vector
+    unsigned long long my_fail = ~0ull;
+    const double *Tt = ws + Lo.Tt, *bn = ws + Lo.bn;
+    long long *ph = (a.phase && b == 0 && threadIdx.x == 0) ? a.phase : nullptr;
+    int php = 0;
+    if (ph) ph[php++] = clock64();
+
+    // ---- phase 1: per-column T, Mbwd, K, Mfwd (and bwd_neg) -------------
+    if (a.do_factor) {
+        for (int c = warp; c < P; c += NW) {
+            const size_t chain = (size_t)b * P + c;
+            const double *st = a.fac + (chain * n + (n - 1)) * g.NPT * kTileElems;
+            Frag Lq[NL], X[NF];
+#pragma unroll
+            for (int i = 0; i < XT; ++i)
+#pragma unroll
+                for (int j = 0; j <= i; ++j) {
+                    Frag f;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int r = 8 * i + rq, k = 8 * j + cq + h;
+                        (h ? f.b : f.a) = (r < NX && k < NX)
+                                              ? (k <= r ? fac_elem(g, st, nu + r, nu + k) : 0.0)
+                                              : (r == k ? 1.0 : 0.0);
+                    }
+                    Lq[T(i, j)] = f;
+                }
+#pragma unroll
+            for (int i = 0; i < XT; ++i)
+#pragma unroll
+                for (int j = 0; j < XT; ++j)
+                    X[i * XT + j] = (i == j) ? Frag{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0}
+                                             : Frag{0.0, 0.0};
+            tiles::trsm_rows<XT, XT>(X, Lq, lane); // X = T = L_Q^{-T} (rows)
+            double *Tc = ws + Lo.Tt + c * TF;
+#pragma unroll
+            for (int t = 0; t < NF; ++t)
+                st_frag(Tc + t * kTileElems, lane, X[t]);
+            // Mbwd = T T' (kkt_factor.cpp:174), lower tiles
+            double *Mbc = ws + Lo.Mb + c * TL;
+#pragma unroll
+            for (int i = 0; i < XT; ++i)
+#pragma unroll
+                for (int j = 0; j <= i; ++j) {
+                    Frag acc{0.0, 0.0};
+#pragma unroll
+                    for (int t = 0; t < XT; ++t)
+                        tile_gemm_nt(acc, X[i * XT + t], X[j * XT + t]);
+                    st_frag(Mbc + T(i, j) * kTileElems, lane, acc);
+                }
+            // subdiag[c-1] = -W_c' = -LA T' (kkt_factor.cpp:203-209); K[P-1] = 0
+            double *Kc = ws + Lo.K + (size_t)((c + P - 1) % P) * TF;
+            if (c > 0) {
+                Frag LA[NF];
+#pragma unroll
+                for (int i = 0; i < XT; ++i)
+#pragma unroll
+                    for (int j = 0; j < XT; ++j) {
+                        Frag f;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int r = 8 * i + rq, k = 8 * j + cq + h;
+                            (h ? f.b : f.a) = (r < NX && k < NX) ? fac_elem(g, st, top + r, nu + k) : 0.0;
+                        }
+                        LA[i * XT + j] = f;
+                    }
+#pragma unroll
+                for (int i = 0; i < XT; ++i)
+#pragma unroll
+                    for (int j = 0; j < XT; ++j) {
+                        Frag acc{0.0, 0.0};
+#pragma unroll
+                        for (int t = 0; t < XT; ++t)
+                            tile_gemm_nt_sub(acc, LA[i * XT + t], X[j * XT + t]);
+                        st_frag(Kc + (i * XT + j) * kTileElems, lane, acc);
+                    }
+            } else {
+#pragma unroll
+                for (int t = 0; t < NF; ++t)
+                    st_frag(Kc + t * kTileElems, lane, Frag{0.0, 0.0});
+            }
+            // Mfwd_c = -(trailing coupling block), padded with a unit diagonal
+            const double *tr = a.trail + chain * g.NTT * kTileElems;
+            double *Dc = ws + Lo.D + c * TL;
+#pragma unroll
+            for (int i = 0; i < XT; ++i)
+#pragma unroll
+                for (int j = 0; j <= i; ++j) {
+                    Frag f;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int r = 8 * i + rq, k = 8 * j + cq + h;
+                        const int rr = r > k ? r : k, kk = r > k ? k : r;
+                        (h ? f.b : f.a) =
+                            (r < NX && k < NX)
+                                ? -__ldg(tr + tri_index(rr / 8, kk / 8) * kTileElems + (rr % 8) * 8 + kk % 8)
+                                : (r == k ? 1.0 : 0.0);
+                    }
+                    st_frag(Dc + T(i, j) * kTileElems, lane, f);
+                }
+            if (a.do_solve) { // bwd_neg_c = T x'_{n-1} (kkt_solve.cpp:128-131)
+                const double *yv = a.y + (chain * n + (n - 1)) * g.nux + nu;
+#pragma unroll
+                for (int i = 0; i < XT; ++i) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int j = 0; j < XT; ++j) {
+                        const int k = 8 * j + cq;
+                        acc = fma(X[i * XT + j].a, k < NX ? __ldg(yv + k) : 0.0, acc);
+                        acc = fma(X[i * XT + j].b, k + 1 < NX ? __ldg(yv + k + 1) : 0.0, acc);
+                    }
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+                    if (q2 == 0)
+                        ws[Lo.bn + c * XP + 8 * i + rq] = acc;
+                }
+            }
+        }
+        __syncthreads();
+        if (ph) ph[php++] = clock64();
+
+        // ---- phase 2: CR levels (block_tridiag.cpp:126-238) -------------
+        for (int l = 0, s = P; l < Lo.levels; ++l, s >>= 1) {
+            const int half = s / 2;
+            const long long in0 = P - (P >> (l > 0 ? l - 1 : 0)); // level l-1 block base
+            const long long out0 = P - (P >> l);                  // level l block base
+            // level-l diagonal block i, lower tiles (assembled on the fly)
+            auto m_tile = [&](int i, int ti, int tj) -> Frag {
+                if (l == 0)
+                    return fadd(ld_frag(ws + Lo.D + i * TL + T(ti, tj) * kTileElems, lane),
+                                ld_frag(ws + Lo.Mb + ((i + 1) % P) * TL + T(ti, tj) * kTileElems, lane));
+                Frag f = ld_frag(ws + Lo.M2 + (in0 + i) * TL + T(ti, tj) * kTileElems, lane);
+                if (i > 0)
+                    f = fsub(f, ld_frag(ws + Lo.CY + (in0 + i - 1) * TL + T(ti, tj) * kTileElems, lane));
+                return f;
+            };
+            auto k_blk = [&](int i) -> const double * {
+                return l == 0 ? ws + Lo.K + i * TF : ws + Lo.K2 + (in0 + i) * TF;
+            };
+            for (int mm = warp; mm < half; mm += NW) {
+                const int k = 2 * mm + 1;
+                Frag Lt[NL];
+#pragma unroll
+                for (int i = 0; i < XT; ++i)
+#pragma unroll
+                    for (int j = 0; j <= i; ++j)
+                        Lt[T(i, j)] = m_tile(k, i, j);
+                const double dfloor = 1e-14 * tiles::diag_absmax<XT>(Lt, NX, lane);
+                int pf = -1;
+                tiles::panel_cholesky<XT, XT>(Lt, NX, dfloor, lane, pf);
+                if (pf >= 0)
+                    my_fail = min(my_fail, fail_key(kKindCR, l, k, pf));
+                Frag Li[NL];
+                lower_inverse<XT, NL>(Lt, Li, scr, lane);
+                double *Lio = ws + Lo.Li + (out0 + mm) * TL;
+#pragma unroll
+                for (int t = 0; t < NL; ++t)
+                    st_frag(Lio + t * kTileElems, lane, Li[t]);
+                // U = K_{k-1}' Linv', Y = K_k Linv' (Y = 0 at the last slot)
+                const bool has_y = k < s - 1;
+                const double *Kp = k_blk(k - 1), *Kk = k_blk(k);
+                Frag U[NF], Y[NF];
+#pragma unroll
+                for (int i = 0; i < XT; ++i) {
+                    Frag kp[XT], kk[XT];
+#pragma unroll
+                    for (int t = 0; t < XT; ++t) {
+                        kp[t] = ld_frag_t(Kp + fidx(XT, t, i) * kTileElems, lane); // (K_{k-1}')(i, t)
+                        kk[t] = has_y ? ld_frag(Kk + fidx(XT, i, t) * kTileElems, lane) : Frag{0.0, 0.0};
+                    }
+#pragma unroll
+                    for (int j = 0; j < XT; ++j) {
+                        Frag u{0.0, 0.0}, y{0.0, 0.0};
+#pragma unroll
+                        for (int t = 0; t <= j; ++t) {
+                            tile_gemm_nt(u, kp[t], Li[T(j, t)]);
+                            tile_gemm_nt(y, kk[t], Li[T(j, t)]);
+                        }
+                        U[i * XT + j] = u;
+                        Y[i * XT + j] = y;
+                    }
+                }
+                double *Uo = ws + Lo.U + (out0 + mm) * TF, *Yo = ws + Lo.Y + (out0 + mm) * TF;
+#pragma unroll
+                for (int t = 0; t < NF; ++t) {
+                    st_frag(Uo + t * kTileElems, lane, U[t]);
+                    st_frag(Yo + t * kTileElems, lane, Y[t]);
+                }
+                // M'_mm = M_{2mm} - U U' (the Y_{mm-1} term is subtracted when the
+                // next level loads it), CY_mm = Y Y', K'_mm = -Y U'
+                double *M2o = ws + Lo.M2 + (out0 + mm) * TL, *CYo = ws + Lo.CY + (out0 + mm) * TL;
+                double *K2o = ws + Lo.K2 + (out0 + mm) * TF;
+                const bool last = mm == half - 1;
+#pragma unroll
+                for (int i = 0; i < XT; ++i)
+#pragma unroll
+                    for (int j = 0; j < XT; ++j) {
+                        Frag uu{0.0, 0.0}, yy{0.0, 0.0}, yu{0.0, 0.0};
+#pragma unroll
+                        for (int t = 0; t < XT; ++t) {
+                            if (j <= i) {
+                                tile_gemm_nt(uu, U[i * XT + t], U[j * XT + t]);
+                                tile_gemm_nt(yy, Y[i * XT + t], Y[j * XT + t]);
+                            }
+                            if (!last)
+                                tile_gemm_nt_sub(yu, Y[i * XT + t], U[j * XT + t]);
+                        }
+                        if (j <= i) {
+                            st_frag(M2o + T(i, j) * kTileElems, lane, fsub(m_tile(2 * mm, i, j), uu));
+                            st_frag(CYo + T(i, j) * kTileElems, lane, yy);
+                        }
+                        st_frag(K2o + fidx(XT, i, j) * kTileElems, lane, yu);
+                    }
+            }
+            __syncthreads();
+            if (ph) ph[php++] = clock64();
+        }
+        // ---- cr_factor_base (block_tridiag.cpp:173-197) ------------------
+        if (warp == 0) {
+            Frag Lt[NL];
+            const long long in0 = P - (P >> (Lo.levels > 0 ? Lo.levels - 1 : 0));
+#pragma unroll
+            for (int i = 0; i < XT; ++i)
+#pragma unroll
+                for (int j = 0; j <= i; ++j)
+                    Lt[T(i, j)] =
+                        Lo.levels == 0
+                            ? fadd(ld_frag(ws + Lo.D + T(i, j) * kTileElems, lane),
+                                   ld_frag(ws + Lo.Mb + T(i, j) * kTileElems, lane))
+                            : ld_frag(ws + Lo.M2 + in0 * TL + T(i, j) * kTileElems, lane);
+            const double dfloor = 1e-14 * tiles::diag_absmax<XT>(Lt, NX, lane);
+            int pf = -1;
+            tiles::panel_cholesky<XT, XT>(Lt, NX, dfloor, lane, pf);
+            if (pf >= 0)
+                my_fail = min(my_fail, fail_key(kKindCR, Lo.levels, 0, pf));
+            Frag Li[NL];
+            lower_inverse<XT, NL>(Lt, Li, scr, lane);
+#pragma unroll
+            for (int t = 0; t < NL; ++t)
+                st_frag(ws + Lo.Lb + t * kTileElems, lane, Li[t]);
+        }
+        __syncthreads();
+        if (ph) ph[php++] = clock64();
+    }
+
+    // ---- phase 3: Schur rhs, CR solve, negate --------------------------
+    if (a.do_solve) {
+        if (!a.do_factor) { // bwd_neg_c = T_c x'_{n-1} from the stored T
+            for (int c = warp; c < P; c += NW) {
+                const size_t chain = (size_t)b * P + c;
+                const double *yv = a.y + (chain * n + (n - 1)) * g.nux + nu;
+                double *v = scr;
+                if (lane < XP)
+                    v[lane] = lane < NX ? __ldg(yv + lane) : 0.0;
+                __syncwarp();
+                double o[XT];
+                matvec<XT, true>(Tt + c * TF, v, o, lane);
+#pragma unroll
+                for (int i = 0; i < XT; ++i)
+                    if (q2 == 0)
+                        ws[Lo.bn + c * XP + 8 * i + rq] = o[i];
+                __syncwarp();
+            }
+            __syncthreads();
+        }
+        // b_i = fd[n i] - fwd_i + bwd_neg_{(i+1) % P}  (kkt_solve.cpp:137-160)
+        {
+            ProbAcc pa{a.p, g, b};
+            for (int e = threadIdx.x; e < P * XP; e += blockDim.x) {
+                const int i = e / XP, k = e % XP;
+                double v = 0.0;
+                if (k < NX) {
+                    const int jst = n * i;
+                    v = pa.fd(jst, k);
+                    if (jst == 0 && a.p.fd == nullptr) // fd[0] -= A_0 x_init
+                        for (int m = 0; m < NX; ++m)
+                            v -= pa.A(0, k, m) * __ldg(a.p.x_init + (size_t)b * NX + m);
+                    const double *tr = a.trail + ((size_t)b * P + i) * g.NTT * kTileElems;
+                    v += __ldg(tr + tri_index(NX / 8, k / 8) * kTileElems + (NX % 8) * 8 + k % 8);
+                    v += bn[((i + 1) % P) * XP + k];
+                }
+                xs[e] = v;
+            }
+        }
+        __syncthreads();
+        if (ph) ph[php++] = clock64();
+        // CRFactor::forward (block_tridiag.cpp:252-296)
+        for (int l = 0, s = P; l < Lo.levels; ++l, s >>= 1) {
+            const int half = s / 2, stride = P / s;
+            const long long o0 = P - (P >> l);
+            for (int mm = warp; mm < half; mm += NW) { // x_k <- L^{-1} x_k
+                double *xk = xs + (size_t)(2 * mm + 1) * stride * XP;
+                double o[XT];
+                matvec<XT, false>(ws + Lo.Li + (o0 + mm) * TL, xk, o, lane);
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < XT; ++i)
+                    if (q2 == 0)
+                        xk[8 * i + rq] = o[i];
+            }
+            __syncthreads();
+            for (int mm = warp; mm < half; mm += NW) { // x_e -= U x_k + Y_prev x_k'
+                double *xe = xs + (size_t)2 * mm * stride * XP;
+                double o[XT], o2[XT];
+                matvec<XT, true>(ws + Lo.U + (o0 + mm) * TF, xs + (size_t)(2 * mm + 1) * stride * XP, o,
+                                 lane);
+                if (mm > 0)
+                    matvec<XT, true>(ws + Lo.Y + (o0 + mm - 1) * TF,
+                                     xs + (size_t)(2 * mm - 1) * stride * XP, o2, lane);
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < XT; ++i)
+                    if (q2 == 0)
+                        xe[8 * i + rq] -= mm > 0 ? o[i] + o2[i] : o[i];
+            }
+            __syncthreads();
+        }
+        if (warp == 0) { // base: x_0 <- L_b^{-T} L_b^{-1} x_0
+            double o[XT], o2[XT][2];
+            matvec<XT, false>(ws + Lo.Lb, xs, o, lane);
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < XT; ++i)
+                if (q2 == 0)
+                    xs[8 * i + rq] = o[i];
+            __syncwarp();
+            matvec_t<XT, false>(ws + Lo.Lb, xs, o2, lane);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < XT; ++j)
+                if (rq == 0) {
+                    xs[8 * j + cq] = o2[j][0];
+                    xs[8 * j + cq + 1] = o2[j][1];
+                }
+        }
+        __syncthreads();
+        if (ph) ph[php++] = clock64();
+        // CRFactor::backward (block_tridiag.cpp:298-333)
+        for (int l = Lo.levels - 1; l >= 0; --l) {
+            const int sl = P >> l, half = sl / 2, stride = P / sl;
+            const long long o0 = P - (P >> l);
+            for (int mm = warp; mm < half; mm += NW) {
+                double *xo = xs + (size_t)(2 * mm + 1) * stride * XP;
+                double t1[XT][2], t2[XT][2];
+                matvec_t<XT, true>(ws + Lo.U + (o0 + mm) * TF, xs + (size_t)2 * mm * stride * XP, t1,
+                                   lane);
+                const bool has_y = 2 * mm + 2 < sl;
+                if (has_y)
+                    matvec_t<XT, true>(ws + Lo.Y + (o0 + mm) * TF,
+                                       xs + (size_t)((2 * mm + 2) * stride % P) * XP, t2, lane);
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < XT; ++j)
+                    if (rq == 0) {
+                        xo[8 * j + cq] -= has_y ? t1[j][0] + t2[j][0] : t1[j][0];
+                        xo[8 * j + cq + 1] -= has_y ? t1[j][1] + t2[j][1] : t1[j][1];
+                    }
+                __syncwarp();
+                matvec_t<XT, false>(ws + Lo.Li + (o0 + mm) * TL, xo, t1, lane); // L^{-T} xo
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < XT; ++j)
+                    if (rq == 0) {
+                        xo[8 * j + cq] = t1[j][0];
+                        xo[8 * j + cq + 1] = t1[j][1];
+                    }
+            }
+            __syncthreads();
+        }
+        if (ph) ph[php++] = clock64();
+        for (int e = threadIdx.x; e < P * NX; e += blockDim.x) {
+            const int i = e / NX, k = e % NX;
+            const double lam = -xs[i * XP + k];
+            a.lamc[(size_t)b * P * NX + e] = lam;
+            if (a.lam_out && n * i < g.N)
+                a.lam_out[((size_t)b * g.N + n * i) * NX + k] = lam;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1)
+        my_fail = min(my_fail, __shfl_xor_sync(0xffffffffu, my_fail, o));
+    if (lane == 0 && my_fail != ~0ull)
+        atomicMin(a.fail + b, my_fail);
+    if (ph) {
+        ph[php++] = clock64();
+        ph[31] = php;
+    }
+}
+
+template <int NX> bool launch_sf(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
+    if (g.nx != NX)
+        return false;
+    constexpr int NW = 4;
+    const size_t smem = ((size_t)NW * SF<NX>::NF * kTileElems + (size_t)g.P * SF<NX>::XP) * sizeof(double);
+    if (smem > 200 * 1024)
+        return false;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(schur_fused_kernel<NX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attr = true;
+    }
+    schur_fused_kernel<NX, NW><<<g.batch, 32 * NW, smem, st>>>(sa);
+    return true;
+}
+
+} // namespace
+
+// The fused path serves batches large enough to fill the GPU with one CTA
+// per instance; small batches (a single long horizon, config 2) keep the
+// per-level batch-wide kernels, whose parallelism is the blocks of a level.
+bool schur_fused_ok(const Geo &g) {
+    // CYQ_SCHUR=levels|fused overrides the choice (read per call: tests
+    // exercise both paths in one process)
+    const char *e = getenv("CYQ_SCHUR");
+    if (e && e[0] == 'l')
+        return false;
+    const bool shape = g.nx == 20 || g.nx == 16 || g.nx == 12 || g.nx == 10;
+    if (!shape)
+        return false;
+    if (e && e[0] == 'f')
+        return true;
+    return g.batch >= 64;
+}
+
+bool launch_schur_fused(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
+    if (!schur_fused_ok(g))
+        return false;
+    return launch_sf<20>(g, st, sa) || launch_sf<16>(g, st, sa) || launch_sf<12>(g, st, sa) ||
+           launch_sf<10>(g, st, sa);
+}
+
+} // namespace cyqb
