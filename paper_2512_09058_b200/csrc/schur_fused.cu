@@ -18,9 +18,10 @@
 //   kkt_solve.cpp:137-182     Schur rhs b_i = fd[n i] - fwd_i + bwd_neg_{i+1}
 //   block_tridiag.cpp:252-333 CRFactor::forward / backward, then negate
 //
-// B200 reformulation: each elimination forms Linv = L^{-1} once (the tile
-// trsm on an identity block plus an 8x8 transpose through shared memory),
-// so U, Y are DMMA products (U = K_{k-1}' Linv', Y = K_k Linv') instead of
+// B200 reformulation: each elimination forms Linv = L^{-1} once -- the
+// Cholesky carries an identity tile through its pivot steps (diagonal-tile
+// inverses for free), the off-diagonal inverse tiles are NT-form DMMA
+// products (tiles::blocked_inverse) -- so U, Y are DMMA products (U = K_{k-1}' Linv', Y = K_k Linv') instead of
 // two dependent triangular solves, and the CR solve is matrix-vector
 // products only (L^{-1} v = Linv v, L^{-T} v = Linv' v): no sequential
 // trsv on the solve path. K_{k-1}' is read as transposed tiles directly from
@@ -109,49 +110,76 @@ __device__ __forceinline__ void matvec_t(const double *M, const double *v, doubl
     }
 }
 
-// Z = L^{-T} (trsm on the identity), transposed through the warp's shared
-// scratch into Li = L^{-1} (lower tiles T(i, j))
-template <int XT, int NL>
-__device__ __forceinline__ void lower_inverse(const Frag (&L)[NL], Frag (&Li)[NL], double *scr,
-                                              int lane) {
-    const int rq = lane >> 2, cq = 2 * (lane & 3);
-    Frag Z[XT * XT];
+
+// tile slot of block tile (i, j) for the three storage modes
+enum : int { kFull = 0, kLower = 1, kUpper = 2 };
+template <int XT, int MODE> __device__ __forceinline__ constexpr bool tile_present(int i, int j) {
+    return MODE == kFull || (MODE == kLower ? j <= i : j >= i);
+}
+template <int XT, int MODE> __device__ __forceinline__ constexpr int tile_slot(int i, int j) {
+    return MODE == kFull ? i * XT + j : (MODE == kLower ? T(i, j) : T(j, i));
+}
+
+// y = M v with M in registers (same conventions as matvec)
+template <int XT, int MODE, int N>
+__device__ __forceinline__ void matvec_r(const Frag (&M)[N], const double *v, double (&out)[XT],
+                                         int lane) {
+    const int cq = 2 * (lane & 3);
 #pragma unroll
-    for (int i = 0; i < XT; ++i)
+    for (int i = 0; i < XT; ++i) {
+        double acc = 0.0;
 #pragma unroll
-        for (int j = 0; j < XT; ++j)
-            Z[i * XT + j] = (i == j) ? Frag{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0}
-                                     : Frag{0.0, 0.0};
-    tiles::trsm_rows<XT, XT>(Z, L, lane); // Z = L^{-T}: upper, Z[i][j] = 0 for i > j
+        for (int j = 0; j < XT; ++j) {
+            if (!tile_present<XT, MODE>(i, j))
+                continue;
+            const Frag f = M[tile_slot<XT, MODE>(i, j)];
+            acc = fma(f.a, v[8 * j + cq], acc);
+            acc = fma(f.b, v[8 * j + cq + 1], acc);
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        out[i] = acc;
+    }
+}
+// y = M v with M upper triangular stored as tiles T(j, i) (memory)
+template <int XT>
+__device__ __forceinline__ void matvec_upper(const double *M, const double *v, double (&out)[XT],
+                                             int lane) {
+    const int cq = 2 * (lane & 3);
 #pragma unroll
-    for (int i = 0; i < XT; ++i)
+    for (int i = 0; i < XT; ++i) {
+        double acc = 0.0;
 #pragma unroll
-        for (int j = i; j < XT; ++j)
-            st_frag(scr + (i * XT + j) * kTileElems, lane, Z[i * XT + j]);
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < XT; ++i)
-#pragma unroll
-        for (int j = 0; j <= i; ++j) // Li(i, j) = Z(j, i)'
-            Li[T(i, j)] = ld_frag_t(scr + (j * XT + i) * kTileElems, lane);
-    __syncwarp();
+        for (int j = i; j < XT; ++j) {
+            const Frag f = ld_frag(M + T(j, i) * kTileElems, lane);
+            acc = fma(f.a, v[8 * j + cq], acc);
+            acc = fma(f.b, v[8 * j + cq + 1], acc);
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        out[i] = acc;
+    }
 }
 
 } // namespace
 
-// Per-instance workspace of the fused path, in 8x8 tiles (64 doubles).
-//   Tt[P] full      T_c = L_Q(last stage)^{-T} per column  (persistent)
-//   Li[P-1] lower   L^{-1} of every odd-block elimination   (persistent)
-//   U[P-1], Y[P-1]  full                                     (persistent)
-//   Lb lower        L_base^{-1}                              (persistent)
-//   D[P], Mb[P]     lower: Mfwd_c, Mbwd_c                    (scratch)
-//   K[P] full       level-0 subdiagonal                      (scratch)
-//   M2[P-1], CY[P-1] lower; K2[P-1] full                      (scratch)
-//   bn[P * XP]      bwd_neg = T x' per column
-// Level l (half = P >> (l+1) blocks) starts at block P - (P >> l) of each
-// per-level array.
+// Per-instance workspace of the fused path, in 8x8 tiles (64 doubles):
+//   Tt[P]   upper   T_c = L_Q(last stage)^{-T} per column, tile (i, j) at
+//                   slot T(j, i)                             (persistent)
+//   Li[P-1] lower   L^{-1} of every odd-block elimination    (persistent)
+//   U[P-1], Y[P-1]  full                                      (persistent)
+//   Lb      lower   L_base^{-1}                               (persistent)
+//   D[P], Mb[P]     lower: Mfwd_c, Mbwd_c                     (scratch)
+//   K[P]    full    level-0 subdiagonal                       (scratch)
+// Li/U/Y of level l (half = P >> (l+1) blocks) start at block P - (P >> l).
+// The CR levels run in place in D / K: at level l, block i is
+//   M_i = D[i << l] - D[(i << l) - 2^(l-1)]  (l > 0, i > 0; the CY term)
+//   M_i = D[i] + Mb[(i + 1) % P]             (l = 0)
+//   K_i = K[i << l]
+// and elimination mm writes M' -> D[2mm << l], CY -> D[(2mm+1) << l],
+// K' -> K[2mm << l]: every slot is read and rewritten by one warp only.
 struct SFLayout {
-    long long Tt, Li, U, Y, Lb, D, Mb, K, M2, CY, K2, bn, total; // doubles
+    long long Tt, Li, U, Y, Lb, D, Mb, K, total; // doubles
     int XT, NL, NF, XP, levels;
     __host__ __device__ static SFLayout make(int P, int nx) {
         SFLayout s;
@@ -165,7 +193,7 @@ struct SFLayout {
         s.levels = lg;
         const long long tl = 64LL * s.NL, tf = 64LL * s.NF;
         long long o = 0;
-        s.Tt = o; o += P * tf;
+        s.Tt = o; o += P * tl;
         s.Li = o; o += (P - 1) * tl;
         s.U = o; o += (P - 1) * tf;
         s.Y = o; o += (P - 1) * tf;
@@ -173,10 +201,6 @@ struct SFLayout {
         s.D = o; o += P * tl;
         s.Mb = o; o += P * tl;
         s.K = o; o += P * tf;
-        s.M2 = o; o += (P - 1) * tl;
-        s.CY = o; o += (P - 1) * tl;
-        s.K2 = o; o += (P - 1) * tf;
-        s.bn = o; o += (long long)P * s.XP;
         s.total = o;
         return s;
     }
@@ -186,7 +210,12 @@ size_t schur_fused_doubles(const Geo &g) { return (size_t)SFLayout::make(g.P, g.
 
 namespace {
 
-template <int NX, int NW> __global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs a) {
+template <int XP> __host__ __device__ constexpr size_t sf_smem_doubles(int NW, int NF, int P) {
+    return (size_t)NW * NF * kTileElems + 3 * (size_t)P * XP;
+}
+
+template <int NX, int NW>
+__global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs a) {
     using F = SF<NX>;
     constexpr int XT = F::XT, NL = F::NL, NF = F::NF, XP = F::XP;
     constexpr long long TL = 64LL * NL, TF = 64LL * NF;
@@ -199,146 +228,178 @@ template <int NX, int NW> __global__ void __launch_bounds__(32 * NW, 12 / NW) sc
     double *ws = a.schur + (size_t)b * Lo.total;
     double *scr = sm + (size_t)warp * NF * kTileElems; // per-warp transpose scratch
     double *xs = sm + (size_t)NW * NF * kTileElems;    // P x XP: CR solve vector
+    double *bns = xs + (size_t)P * XP;                 // P x XP: bwd_neg per column
+    double *cu = bns + (size_t)P * XP;                 // P/2 x XP each: even-block
+    double *cy = cu + (size_t)(P / 2) * XP;            //   contributions U x_k, Y x_k
+    double *D = ws + Lo.D, *Mb = ws + Lo.Mb, *K = ws + Lo.K;
     unsigned long long my_fail = ~0ull;
-    const double *Tt = ws + Lo.Tt, *bn = ws + Lo.bn;
+    const bool fwd_fused = a.do_factor && a.do_solve; // CR forward inside the factor levels
     long long *ph = (a.phase && b == 0 && threadIdx.x == 0) ? a.phase : nullptr;
     int php = 0;
     if (ph) ph[php++] = clock64();
 
-    // ---- phase 1: per-column T, Mbwd, K, Mfwd (and bwd_neg) -------------
-    if (a.do_factor) {
-        for (int c = warp; c < P; c += NW) {
-            const size_t chain = (size_t)b * P + c;
+    // ---- phase 1: per-column T, Mbwd, K, Mfwd and bwd_neg ----------------
+    // (kkt_factor.cpp:163-178, 194-212; kkt_solve.cpp:128-131)
+    for (int c = warp; c < P; c += NW) {
+        const size_t chain = (size_t)b * P + c;
+        const double *yv = a.y + (chain * n + (n - 1)) * g.nux + nu;
+        if (a.do_factor) {
             const double *st = a.fac + (chain * n + (n - 1)) * g.NPT * kTileElems;
-            Frag Lq[NL], X[NF];
+            const double *tr = a.trail + chain * g.NTT * kTileElems;
+            Frag Lq[NL];
+            double *Dc = D + c * TL;
 #pragma unroll
             for (int i = 0; i < XT; ++i)
 #pragma unroll
                 for (int j = 0; j <= i; ++j) {
-                    Frag f;
+                    Frag dm;
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int r = 8 * i + rq, k = 8 * j + cq + h;
-                        (h ? f.b : f.a) = (r < NX && k < NX)
-                                              ? (k <= r ? fac_elem(g, st, nu + r, nu + k) : 0.0)
-                                              : (r == k ? 1.0 : 0.0);
+                        const bool in = r < NX && k < NX;
+                        (h ? Lq[T(i, j)].b : Lq[T(i, j)].a) =
+                            in ? (k <= r ? fac_elem(g, st, nu + r, nu + k) : 0.0) : (r == k ? 1.0 : 0.0);
+                        // Mfwd_c = -(trailing coupling block), unit padding diagonal
+                        const int rr = r > k ? r : k, kk = r > k ? k : r;
+                        (h ? dm.b : dm.a) =
+                            in ? -__ldg(tr + tri_index(rr / 8, kk / 8) * kTileElems + (rr % 8) * 8 + kk % 8)
+                               : (r == k ? 1.0 : 0.0);
                     }
-                    Lq[T(i, j)] = f;
+                    st_frag(Dc + T(i, j) * kTileElems, lane, dm);
                 }
+            double yx[XT][2];
+            if (a.do_solve)
+#pragma unroll
+                for (int j = 0; j < XT; ++j) {
+                    const int k = 8 * j + cq;
+                    yx[j][0] = k < NX ? __ldg(yv + k) : 0.0;
+                    yx[j][1] = k + 1 < NX ? __ldg(yv + k + 1) : 0.0;
+                }
+            Frag X[NF]; // T = L_Q^{-T} (rows): diagonal-tile inverses + blocked DMMA inverse
+            {
+                Frag Zd[XT], Ld[XT], Li[NL];
+                tiles::diag_inverses<XT, NL>(Lq, Zd, Ld, lane, scr);
+                tiles::blocked_inverse<XT, NL>(Lq, Zd, Ld, Li, X);
+            }
+            double *Tc = ws + Lo.Tt + c * TL;
 #pragma unroll
             for (int i = 0; i < XT; ++i)
 #pragma unroll
-                for (int j = 0; j < XT; ++j)
-                    X[i * XT + j] = (i == j) ? Frag{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0}
-                                             : Frag{0.0, 0.0};
-            tiles::trsm_rows<XT, XT>(X, Lq, lane); // X = T = L_Q^{-T} (rows)
-            double *Tc = ws + Lo.Tt + c * TF;
-#pragma unroll
-            for (int t = 0; t < NF; ++t)
-                st_frag(Tc + t * kTileElems, lane, X[t]);
+                for (int j = i; j < XT; ++j)
+                    st_frag(Tc + T(j, i) * kTileElems, lane, X[i * XT + j]);
             // Mbwd = T T' (kkt_factor.cpp:174), lower tiles
-            double *Mbc = ws + Lo.Mb + c * TL;
+            double *Mbc = Mb + c * TL;
 #pragma unroll
             for (int i = 0; i < XT; ++i)
 #pragma unroll
                 for (int j = 0; j <= i; ++j) {
                     Frag acc{0.0, 0.0};
 #pragma unroll
-                    for (int t = 0; t < XT; ++t)
+                    for (int t = i; t < XT; ++t) // T upper: X[i][t] = 0 for t < i
                         tile_gemm_nt(acc, X[i * XT + t], X[j * XT + t]);
                     st_frag(Mbc + T(i, j) * kTileElems, lane, acc);
                 }
             // subdiag[c-1] = -W_c' = -LA T' (kkt_factor.cpp:203-209); K[P-1] = 0
-            double *Kc = ws + Lo.K + (size_t)((c + P - 1) % P) * TF;
-            if (c > 0) {
-                Frag LA[NF];
+            double *Kc = K + (size_t)((c + P - 1) % P) * TF;
 #pragma unroll
-                for (int i = 0; i < XT; ++i)
+            for (int i = 0; i < XT; ++i) {
+                Frag la[XT];
 #pragma unroll
-                    for (int j = 0; j < XT; ++j) {
-                        Frag f;
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int r = 8 * i + rq, k = 8 * j + cq + h;
-                            (h ? f.b : f.a) = (r < NX && k < NX) ? fac_elem(g, st, top + r, nu + k) : 0.0;
-                        }
-                        LA[i * XT + j] = f;
-                    }
-#pragma unroll
-                for (int i = 0; i < XT; ++i)
-#pragma unroll
-                    for (int j = 0; j < XT; ++j) {
-                        Frag acc{0.0, 0.0};
-#pragma unroll
-                        for (int t = 0; t < XT; ++t)
-                            tile_gemm_nt_sub(acc, LA[i * XT + t], X[j * XT + t]);
-                        st_frag(Kc + (i * XT + j) * kTileElems, lane, acc);
-                    }
-            } else {
-#pragma unroll
-                for (int t = 0; t < NF; ++t)
-                    st_frag(Kc + t * kTileElems, lane, Frag{0.0, 0.0});
-            }
-            // Mfwd_c = -(trailing coupling block), padded with a unit diagonal
-            const double *tr = a.trail + chain * g.NTT * kTileElems;
-            double *Dc = ws + Lo.D + c * TL;
-#pragma unroll
-            for (int i = 0; i < XT; ++i)
-#pragma unroll
-                for (int j = 0; j <= i; ++j) {
-                    Frag f;
+                for (int t = 0; t < XT; ++t)
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const int r = 8 * i + rq, k = 8 * j + cq + h;
-                        const int rr = r > k ? r : k, kk = r > k ? k : r;
-                        (h ? f.b : f.a) =
-                            (r < NX && k < NX)
-                                ? -__ldg(tr + tri_index(rr / 8, kk / 8) * kTileElems + (rr % 8) * 8 + kk % 8)
-                                : (r == k ? 1.0 : 0.0);
+                        const int r = 8 * i + rq, k = 8 * t + cq + h;
+                        (h ? la[t].b : la[t].a) =
+                            (c > 0 && r < NX && k < NX) ? fac_elem(g, st, top + r, nu + k) : 0.0;
                     }
-                    st_frag(Dc + T(i, j) * kTileElems, lane, f);
+#pragma unroll
+                for (int j = 0; j < XT; ++j) {
+                    Frag acc{0.0, 0.0};
+#pragma unroll
+                    for (int t = j; t < XT; ++t)
+                        tile_gemm_nt_sub(acc, la[t], X[j * XT + t]);
+                    st_frag(Kc + (i * XT + j) * kTileElems, lane, acc);
                 }
-            if (a.do_solve) { // bwd_neg_c = T x'_{n-1} (kkt_solve.cpp:128-131)
-                const double *yv = a.y + (chain * n + (n - 1)) * g.nux + nu;
+            }
+            if (a.do_solve) { // bwd_neg_c = T x'_{n-1}
 #pragma unroll
                 for (int i = 0; i < XT; ++i) {
                     double acc = 0.0;
 #pragma unroll
-                    for (int j = 0; j < XT; ++j) {
-                        const int k = 8 * j + cq;
-                        acc = fma(X[i * XT + j].a, k < NX ? __ldg(yv + k) : 0.0, acc);
-                        acc = fma(X[i * XT + j].b, k + 1 < NX ? __ldg(yv + k + 1) : 0.0, acc);
+                    for (int j = i; j < XT; ++j) {
+                        acc = fma(X[i * XT + j].a, yx[j][0], acc);
+                        acc = fma(X[i * XT + j].b, yx[j][1], acc);
                     }
                     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
                     acc += __shfl_xor_sync(0xffffffffu, acc, 2);
                     if (q2 == 0)
-                        ws[Lo.bn + c * XP + 8 * i + rq] = acc;
+                        bns[c * XP + 8 * i + rq] = acc;
                 }
             }
+        } else if (a.do_solve) { // solve only: bwd_neg_c from the stored T
+            if (lane < XP)
+                scr[lane] = lane < NX ? __ldg(yv + lane) : 0.0;
+            __syncwarp();
+            double o[XT];
+            matvec_upper<XT>(ws + Lo.Tt + c * TL, scr, o, lane);
+#pragma unroll
+            for (int i = 0; i < XT; ++i)
+                if (q2 == 0)
+                    bns[c * XP + 8 * i + rq] = o[i];
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    if (ph) ph[php++] = clock64();
+
+    // ---- Schur rhs b_i = fd[n i] - fwd_i + bwd_neg_{(i+1) % P} -----------
+    // (kkt_solve.cpp:137-160); fd[0] of EqRhs::of_problem carries -A_0 x_init
+    if (a.do_solve) {
+        ProbAcc pa{a.p, g, b};
+        for (int e = threadIdx.x; e < P * XP; e += blockDim.x) {
+            const int i = e / XP, k = e % XP;
+            double v = 0.0;
+            if (k < NX) {
+                const int jst = n * i;
+                v = pa.fd(jst, k);
+                if (jst == 0 && a.p.fd == nullptr) {
+                    double ax = 0.0;
+#pragma unroll
+                    for (int m = 0; m < NX; ++m)
+                        ax = fma(pa.A(0, k, m), __ldg(a.p.x_init + (size_t)b * NX + m), ax);
+                    v -= ax;
+                }
+                const double *tr = a.trail + ((size_t)b * P + i) * g.NTT * kTileElems;
+                v += __ldg(tr + tri_index(NX / 8, k / 8) * kTileElems + (NX % 8) * 8 + k % 8);
+                v += bns[((i + 1) % P) * XP + k];
+            }
+            xs[e] = v;
         }
         __syncthreads();
-        if (ph) ph[php++] = clock64();
+    }
 
-        // ---- phase 2: CR levels (block_tridiag.cpp:126-238) -------------
+    // ---- phase 2: CR levels (block_tridiag.cpp:126-238), in place ---------
+    // With a right-hand side at hand the CR forward sweep
+    // (block_tridiag.cpp:252-296) runs inside the levels on the register
+    // tiles: x_k <- L^{-1} x_k, then U x_k / Y x_k go to the even blocks.
+    if (a.do_factor) {
         for (int l = 0, s = P; l < Lo.levels; ++l, s >>= 1) {
             const int half = s / 2;
-            const long long in0 = P - (P >> (l > 0 ? l - 1 : 0)); // level l-1 block base
-            const long long out0 = P - (P >> l);                  // level l block base
-            // level-l diagonal block i, lower tiles (assembled on the fly)
+            const long long out0 = P - (P >> l);
+            const int hcy = l > 0 ? 1 << (l - 1) : 0;
             auto m_tile = [&](int i, int ti, int tj) -> Frag {
                 if (l == 0)
-                    return fadd(ld_frag(ws + Lo.D + i * TL + T(ti, tj) * kTileElems, lane),
-                                ld_frag(ws + Lo.Mb + ((i + 1) % P) * TL + T(ti, tj) * kTileElems, lane));
-                Frag f = ld_frag(ws + Lo.M2 + (in0 + i) * TL + T(ti, tj) * kTileElems, lane);
+                    return fadd(ld_frag(D + i * TL + T(ti, tj) * kTileElems, lane),
+                                ld_frag(Mb + ((i + 1) % P) * TL + T(ti, tj) * kTileElems, lane));
+                Frag f = ld_frag(D + (i << l) * TL + T(ti, tj) * kTileElems, lane);
                 if (i > 0)
-                    f = fsub(f, ld_frag(ws + Lo.CY + (in0 + i - 1) * TL + T(ti, tj) * kTileElems, lane));
+                    f = fsub(f, ld_frag(D + ((i << l) - hcy) * TL + T(ti, tj) * kTileElems, lane));
                 return f;
-            };
-            auto k_blk = [&](int i) -> const double * {
-                return l == 0 ? ws + Lo.K + i * TF : ws + Lo.K2 + (in0 + i) * TF;
             };
             for (int mm = warp; mm < half; mm += NW) {
                 const int k = 2 * mm + 1;
+                const bool has_y = k < s - 1;
+                const double *Kp = K + ((k - 1) << l) * TF, *Kk = K + (k << l) * TF;
                 Frag Lt[NL];
 #pragma unroll
                 for (int i = 0; i < XT; ++i)
@@ -347,18 +408,30 @@ template <int NX, int NW> __global__ void __launch_bounds__(32 * NW, 12 / NW) sc
                         Lt[T(i, j)] = m_tile(k, i, j);
                 const double dfloor = 1e-14 * tiles::diag_absmax<XT>(Lt, NX, lane);
                 int pf = -1;
-                tiles::panel_cholesky<XT, XT>(Lt, NX, dfloor, lane, pf);
+                Frag Li[NL];
+                {
+                    Frag Zd[XT], Ld[XT], Z[NF];
+                    tiles::chol_inv<XT, NL>(Lt, Zd, Ld, NX, dfloor, lane, pf, scr);
+                    tiles::blocked_inverse<XT, NL>(Lt, Zd, Ld, Li, Z);
+                }
                 if (pf >= 0)
                     my_fail = min(my_fail, fail_key(kKindCR, l, k, pf));
-                Frag Li[NL];
-                lower_inverse<XT, NL>(Lt, Li, scr, lane);
                 double *Lio = ws + Lo.Li + (out0 + mm) * TL;
 #pragma unroll
                 for (int t = 0; t < NL; ++t)
                     st_frag(Lio + t * kTileElems, lane, Li[t]);
+                double *xk = xs + (size_t)(k << l) * XP;
+                if (fwd_fused) { // x_k <- L^{-1} x_k
+                    double o[XT];
+                    matvec_r<XT, kLower>(Li, xk, o, lane);
+                    __syncwarp();
+#pragma unroll
+                    for (int i = 0; i < XT; ++i)
+                        if (q2 == 0)
+                            xk[8 * i + rq] = o[i];
+                    __syncwarp();
+                }
                 // U = K_{k-1}' Linv', Y = K_k Linv' (Y = 0 at the last slot)
-                const bool has_y = k < s - 1;
-                const double *Kp = k_blk(k - 1), *Kk = k_blk(k);
                 Frag U[NF], Y[NF];
 #pragma unroll
                 for (int i = 0; i < XT; ++i) {
@@ -386,10 +459,22 @@ template <int NX, int NW> __global__ void __launch_bounds__(32 * NW, 12 / NW) sc
                     st_frag(Uo + t * kTileElems, lane, U[t]);
                     st_frag(Yo + t * kTileElems, lane, Y[t]);
                 }
-                // M'_mm = M_{2mm} - U U' (the Y_{mm-1} term is subtracted when the
-                // next level loads it), CY_mm = Y Y', K'_mm = -Y U'
-                double *M2o = ws + Lo.M2 + (out0 + mm) * TL, *CYo = ws + Lo.CY + (out0 + mm) * TL;
-                double *K2o = ws + Lo.K2 + (out0 + mm) * TF;
+                if (fwd_fused) { // contributions U x_k -> x_{2mm}, Y x_k -> x_{2mm+2}
+                    double ou[XT], oy[XT];
+                    matvec_r<XT, kFull>(U, xk, ou, lane);
+                    matvec_r<XT, kFull>(Y, xk, oy, lane);
+#pragma unroll
+                    for (int i = 0; i < XT; ++i)
+                        if (q2 == 0) {
+                            cu[mm * XP + 8 * i + rq] = ou[i];
+                            cy[mm * XP + 8 * i + rq] = oy[i];
+                        }
+                }
+                // M' = M_{2mm} - U U' -> D[2mm << l] (the Y_{mm-1} term is
+                // subtracted by the next level's loads), CY = Y Y' ->
+                // D[(2mm+1) << l], K' = -Y U' -> K[2mm << l]
+                double *M2o = D + ((2 * mm) << l) * TL, *CYo = D + (k << l) * TL;
+                double *K2o = K + ((2 * mm) << l) * TF;
                 const bool last = mm == half - 1;
 #pragma unroll
                 for (int i = 0; i < XT; ++i)
@@ -413,127 +498,119 @@ template <int NX, int NW> __global__ void __launch_bounds__(32 * NW, 12 / NW) sc
                     }
             }
             __syncthreads();
+            if (fwd_fused) { // x_{2mm} -= U_mm x_{2mm+1} + Y_{mm-1} x_{2mm-1}
+                for (int e = threadIdx.x; e < half * XP; e += blockDim.x) {
+                    const int mm = e / XP, r = e % XP;
+                    double d = cu[e];
+                    if (mm > 0)
+                        d += cy[e - XP];
+                    xs[(size_t)((2 * mm) << l) * XP + r] -= d;
+                }
+                __syncthreads();
+            }
             if (ph) ph[php++] = clock64();
         }
-        // ---- cr_factor_base (block_tridiag.cpp:173-197) ------------------
+        // ---- cr_factor_base (block_tridiag.cpp:173-197) --------------------
         if (warp == 0) {
             Frag Lt[NL];
-            const long long in0 = P - (P >> (Lo.levels > 0 ? Lo.levels - 1 : 0));
 #pragma unroll
             for (int i = 0; i < XT; ++i)
 #pragma unroll
                 for (int j = 0; j <= i; ++j)
-                    Lt[T(i, j)] =
-                        Lo.levels == 0
-                            ? fadd(ld_frag(ws + Lo.D + T(i, j) * kTileElems, lane),
-                                   ld_frag(ws + Lo.Mb + T(i, j) * kTileElems, lane))
-                            : ld_frag(ws + Lo.M2 + in0 * TL + T(i, j) * kTileElems, lane);
+                    Lt[T(i, j)] = Lo.levels == 0
+                                      ? fadd(ld_frag(D + T(i, j) * kTileElems, lane),
+                                             ld_frag(Mb + T(i, j) * kTileElems, lane))
+                                      : ld_frag(D + T(i, j) * kTileElems, lane);
             const double dfloor = 1e-14 * tiles::diag_absmax<XT>(Lt, NX, lane);
             int pf = -1;
-            tiles::panel_cholesky<XT, XT>(Lt, NX, dfloor, lane, pf);
+            Frag Li[NL];
+            {
+                Frag Zd[XT], Ld[XT], Z[NF];
+                tiles::chol_inv<XT, NL>(Lt, Zd, Ld, NX, dfloor, lane, pf, scr);
+                tiles::blocked_inverse<XT, NL>(Lt, Zd, Ld, Li, Z);
+            }
             if (pf >= 0)
                 my_fail = min(my_fail, fail_key(kKindCR, Lo.levels, 0, pf));
-            Frag Li[NL];
-            lower_inverse<XT, NL>(Lt, Li, scr, lane);
 #pragma unroll
             for (int t = 0; t < NL; ++t)
                 st_frag(ws + Lo.Lb + t * kTileElems, lane, Li[t]);
+            if (fwd_fused) { // base solve x_0 <- L_b^{-T} L_b^{-1} x_0
+                double o[XT], o2[XT][2];
+                matvec_r<XT, kLower>(Li, xs, o, lane);
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < XT; ++i)
+                    if (q2 == 0)
+                        xs[8 * i + rq] = o[i];
+                __syncwarp();
+                matvec_t<XT, false>(ws + Lo.Lb, xs, o2, lane);
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < XT; ++j)
+                    if (rq == 0) {
+                        xs[8 * j + cq] = o2[j][0];
+                        xs[8 * j + cq + 1] = o2[j][1];
+                    }
+            }
         }
         __syncthreads();
         if (ph) ph[php++] = clock64();
     }
 
-    // ---- phase 3: Schur rhs, CR solve, negate --------------------------
+    // ---- phase 3: CR solve over the stored factor, negate ----------------
     if (a.do_solve) {
-        if (!a.do_factor) { // bwd_neg_c = T_c x'_{n-1} from the stored T
-            for (int c = warp; c < P; c += NW) {
-                const size_t chain = (size_t)b * P + c;
-                const double *yv = a.y + (chain * n + (n - 1)) * g.nux + nu;
-                double *v = scr;
-                if (lane < XP)
-                    v[lane] = lane < NX ? __ldg(yv + lane) : 0.0;
-                __syncwarp();
-                double o[XT];
-                matvec<XT, true>(Tt + c * TF, v, o, lane);
+        if (!fwd_fused) {
+            // CRFactor::forward (block_tridiag.cpp:252-296)
+            for (int l = 0, s = P; l < Lo.levels; ++l, s >>= 1) {
+                const int half = s / 2, stride = P / s;
+                const long long o0 = P - (P >> l);
+                for (int mm = warp; mm < half; mm += NW) { // x_k <- L^{-1} x_k
+                    double *xk = xs + (size_t)(2 * mm + 1) * stride * XP;
+                    double o[XT];
+                    matvec<XT, false>(ws + Lo.Li + (o0 + mm) * TL, xk, o, lane);
+                    __syncwarp();
 #pragma unroll
-                for (int i = 0; i < XT; ++i)
-                    if (q2 == 0)
-                        ws[Lo.bn + c * XP + 8 * i + rq] = o[i];
-                __syncwarp();
-            }
-            __syncthreads();
-        }
-        // b_i = fd[n i] - fwd_i + bwd_neg_{(i+1) % P}  (kkt_solve.cpp:137-160)
-        {
-            ProbAcc pa{a.p, g, b};
-            for (int e = threadIdx.x; e < P * XP; e += blockDim.x) {
-                const int i = e / XP, k = e % XP;
-                double v = 0.0;
-                if (k < NX) {
-                    const int jst = n * i;
-                    v = pa.fd(jst, k);
-                    if (jst == 0 && a.p.fd == nullptr) // fd[0] -= A_0 x_init
-                        for (int m = 0; m < NX; ++m)
-                            v -= pa.A(0, k, m) * __ldg(a.p.x_init + (size_t)b * NX + m);
-                    const double *tr = a.trail + ((size_t)b * P + i) * g.NTT * kTileElems;
-                    v += __ldg(tr + tri_index(NX / 8, k / 8) * kTileElems + (NX % 8) * 8 + k % 8);
-                    v += bn[((i + 1) % P) * XP + k];
+                    for (int i = 0; i < XT; ++i)
+                        if (q2 == 0)
+                            xk[8 * i + rq] = o[i];
                 }
-                xs[e] = v;
-            }
-        }
-        __syncthreads();
-        if (ph) ph[php++] = clock64();
-        // CRFactor::forward (block_tridiag.cpp:252-296)
-        for (int l = 0, s = P; l < Lo.levels; ++l, s >>= 1) {
-            const int half = s / 2, stride = P / s;
-            const long long o0 = P - (P >> l);
-            for (int mm = warp; mm < half; mm += NW) { // x_k <- L^{-1} x_k
-                double *xk = xs + (size_t)(2 * mm + 1) * stride * XP;
-                double o[XT];
-                matvec<XT, false>(ws + Lo.Li + (o0 + mm) * TL, xk, o, lane);
-                __syncwarp();
+                __syncthreads();
+                for (int mm = warp; mm < half; mm += NW) { // x_e -= U x_k + Y_prev x_k'
+                    double *xe = xs + (size_t)2 * mm * stride * XP;
+                    double o[XT], o2[XT];
+                    matvec<XT, true>(ws + Lo.U + (o0 + mm) * TF, xs + (size_t)(2 * mm + 1) * stride * XP,
+                                     o, lane);
+                    if (mm > 0)
+                        matvec<XT, true>(ws + Lo.Y + (o0 + mm - 1) * TF,
+                                         xs + (size_t)(2 * mm - 1) * stride * XP, o2, lane);
+                    __syncwarp();
 #pragma unroll
-                for (int i = 0; i < XT; ++i)
-                    if (q2 == 0)
-                        xk[8 * i + rq] = o[i];
-            }
-            __syncthreads();
-            for (int mm = warp; mm < half; mm += NW) { // x_e -= U x_k + Y_prev x_k'
-                double *xe = xs + (size_t)2 * mm * stride * XP;
-                double o[XT], o2[XT];
-                matvec<XT, true>(ws + Lo.U + (o0 + mm) * TF, xs + (size_t)(2 * mm + 1) * stride * XP, o,
-                                 lane);
-                if (mm > 0)
-                    matvec<XT, true>(ws + Lo.Y + (o0 + mm - 1) * TF,
-                                     xs + (size_t)(2 * mm - 1) * stride * XP, o2, lane);
-                __syncwarp();
-#pragma unroll
-                for (int i = 0; i < XT; ++i)
-                    if (q2 == 0)
-                        xe[8 * i + rq] -= mm > 0 ? o[i] + o2[i] : o[i];
-            }
-            __syncthreads();
-        }
-        if (warp == 0) { // base: x_0 <- L_b^{-T} L_b^{-1} x_0
-            double o[XT], o2[XT][2];
-            matvec<XT, false>(ws + Lo.Lb, xs, o, lane);
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < XT; ++i)
-                if (q2 == 0)
-                    xs[8 * i + rq] = o[i];
-            __syncwarp();
-            matvec_t<XT, false>(ws + Lo.Lb, xs, o2, lane);
-            __syncwarp();
-#pragma unroll
-            for (int j = 0; j < XT; ++j)
-                if (rq == 0) {
-                    xs[8 * j + cq] = o2[j][0];
-                    xs[8 * j + cq + 1] = o2[j][1];
+                    for (int i = 0; i < XT; ++i)
+                        if (q2 == 0)
+                            xe[8 * i + rq] -= mm > 0 ? o[i] + o2[i] : o[i];
                 }
+                __syncthreads();
+            }
+            if (warp == 0) { // base: x_0 <- L_b^{-T} L_b^{-1} x_0
+                double o[XT], o2[XT][2];
+                matvec<XT, false>(ws + Lo.Lb, xs, o, lane);
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < XT; ++i)
+                    if (q2 == 0)
+                        xs[8 * i + rq] = o[i];
+                __syncwarp();
+                matvec_t<XT, false>(ws + Lo.Lb, xs, o2, lane);
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < XT; ++j)
+                    if (rq == 0) {
+                        xs[8 * j + cq] = o2[j][0];
+                        xs[8 * j + cq + 1] = o2[j][1];
+                    }
+            }
+            __syncthreads();
         }
-        __syncthreads();
         if (ph) ph[php++] = clock64();
         // CRFactor::backward (block_tridiag.cpp:298-333)
         for (int l = Lo.levels - 1; l >= 0; --l) {
@@ -541,10 +618,10 @@ template <int NX, int NW> __global__ void __launch_bounds__(32 * NW, 12 / NW) sc
             const long long o0 = P - (P >> l);
             for (int mm = warp; mm < half; mm += NW) {
                 double *xo = xs + (size_t)(2 * mm + 1) * stride * XP;
-                double t1[XT][2], t2[XT][2];
+                double t1[XT][2], t2[XT][2], t3[XT][2];
+                const bool has_y = 2 * mm + 2 < sl;
                 matvec_t<XT, true>(ws + Lo.U + (o0 + mm) * TF, xs + (size_t)2 * mm * stride * XP, t1,
                                    lane);
-                const bool has_y = 2 * mm + 2 < sl;
                 if (has_y)
                     matvec_t<XT, true>(ws + Lo.Y + (o0 + mm) * TF,
                                        xs + (size_t)((2 * mm + 2) * stride % P) * XP, t2, lane);
@@ -556,13 +633,13 @@ template <int NX, int NW> __global__ void __launch_bounds__(32 * NW, 12 / NW) sc
                         xo[8 * j + cq + 1] -= has_y ? t1[j][1] + t2[j][1] : t1[j][1];
                     }
                 __syncwarp();
-                matvec_t<XT, false>(ws + Lo.Li + (o0 + mm) * TL, xo, t1, lane); // L^{-T} xo
+                matvec_t<XT, false>(ws + Lo.Li + (o0 + mm) * TL, xo, t3, lane); // L^{-T} xo
                 __syncwarp();
 #pragma unroll
                 for (int j = 0; j < XT; ++j)
                     if (rq == 0) {
-                        xo[8 * j + cq] = t1[j][0];
-                        xo[8 * j + cq + 1] = t1[j][1];
+                        xo[8 * j + cq] = t3[j][0];
+                        xo[8 * j + cq + 1] = t3[j][1];
                     }
             }
             __syncthreads();
@@ -590,7 +667,7 @@ template <int NX> bool launch_sf(const Geo &g, cudaStream_t st, const SchurArgs 
     if (g.nx != NX)
         return false;
     constexpr int NW = 4;
-    const size_t smem = ((size_t)NW * SF<NX>::NF * kTileElems + (size_t)g.P * SF<NX>::XP) * sizeof(double);
+    const size_t smem = sf_smem_doubles<SF<NX>::XP>(NW, SF<NX>::NF, g.P) * sizeof(double);
     if (smem > 200 * 1024)
         return false;
     static bool attr = false;
