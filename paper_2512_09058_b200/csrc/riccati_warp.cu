@@ -10,25 +10,196 @@
 // warp's registers as 8x8 DMMA C-fragments (tile indices are compile-time,
 // so all index arithmetic folds away); the rank-8 block updates are DMMAs
 // whose A/B operands are the register tiles themselves (k permuted, no
-// shuffles). Shared memory holds only what must be re-read in another
-// layout: W = [V; ALQ; -wl] (operands of the next stage's W W' update),
-// L_Q (the transposed B operand of V = BA' L_Q) and the cp.async staging
-// buffers for the next stage's R, S, Q, B, A, r, q, f (issued one stage
-// ahead; full-sector 16-byte copies when aligned).
+// shuffles).
+//
+// Shared memory per warp:
+//  * the next stage's data, staged by cp.async straight into the layouts the
+//    compute reads: R and Q land in a tile-ordered image of the panel's
+//    pivot block (padding diagonal preset once), so initialising a panel
+//    tile is one 16-byte shared load per lane; [B A] lands as one padded
+//    row-major block (the A operand of V = BA' L_Q, no selects); S (its
+//    transpose fills the S' tiles), [r; q] and f as plain vectors;
+//  * W = [V; ALQ; -wl] with its x-columns COMPACTED and permuted (the last
+//    partial tile's columns on even positions), so W W' and V run over
+//    ceil(nx/4) k-slices instead of the panel's x-tile span (5 instead of 6
+//    at config 1) -- W W' is invariant under a column permutation;
+//  * L_Q as a row-major x-space block (the B operand of V).
 #include "kkt_common.cuh"
 #include "kernels.h"
 
 #include "riccati_common.cuh"
 
 #include <cstdlib>
+#include <type_traits>
 
 namespace cyqb {
 
 using namespace cyqb::ric;
 
-template <int NU, int NX, int WPB, bool DIRECT, bool INV>
-__global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_kernel(RiccatiArgs a) {
+namespace {
+
+template <int NU, int NX> struct WS {
     using S = Shp<NU, NX>;
+    static constexpr int NUX = S::NUX, CT = S::CT, BT = S::BT, TT = S::TT, NT = S::NT;
+    static constexpr int TOP = S::TOP, RHS = S::RHS, RT = RHS / 8, RR = RHS % 8;
+    static constexpr int XT0 = S::XT0, NXT = S::NXT; // panel tile columns holding x columns
+    static constexpr int NXF = NX / 8, REM = NX % 8;
+    static constexpr bool HALF = REM > 0 && REM <= 4; // remainder on even positions only
+    static constexpr int NXC = (NX + 7) / 8;           // compact W tile columns
+    static constexpr int KQ = (NX + 3) / 4;            // V k-steps over x rows
+    static constexpr int NXR = 4 * KQ;                 // padded x rows (LQ, BA)
+    static constexpr int PW = 8 * CT;                  // padded panel width
+    static constexpr int NIMG = CT * (CT + 1) / 2;     // image tiles
+    // compact position of x-column kk / x-column at position p (-1 = none)
+    __host__ __device__ static constexpr int pos(int kk) {
+        return kk < 8 * NXF ? kk : 8 * NXF + (HALF ? 2 : 1) * (kk - 8 * NXF);
+    }
+    __host__ __device__ static constexpr int col_of(int p) {
+        return p < 8 * NXF ? p
+                           : (HALF ? ((((p - 8 * NXF) & 1) == 0 && (p - 8 * NXF) / 2 < REM)
+                                          ? 8 * NXF + (p - 8 * NXF) / 2
+                                          : -1)
+                                   : ((p - 8 * NXF) < REM ? p : -1));
+    }
+    // per-warp shared memory (doubles); every offset is even (16-byte aligned)
+    static constexpr int O_W = 0;
+    static constexpr int O_LQ = O_W + TT * NXC * kTileElems;
+    static constexpr int O_IMG = O_LQ + NXR * NX;
+    static constexpr int O_IMR = O_IMG + NIMG * kTileElems;
+    static constexpr int O_S = O_IMR + PW;
+    static constexpr int O_BA = O_S + ((NU * NX + 1) & ~1);
+    static constexpr int O_F = O_BA + NXR * PW;
+    static constexpr int O_RU0 = O_F + ((NX + 1) & ~1);
+    static constexpr int O_SCR = O_RU0 + ((NU + 1) & ~1);
+    static constexpr int SMEM = O_SCR + kTileElems;
+    static_assert((O_LQ | O_IMG | O_IMR | O_S | O_BA | O_F | O_RU0 | O_SCR | SMEM) % 2 == 0, "align");
+};
+
+// %laneid through a volatile asm: lane-dependent addresses derived from it
+// are recomputed where used instead of being hoisted out of the stage loop
+// (and spilled -- the long-scoreboard stalls of a first version)
+__device__ __forceinline__ int lane_v() {
+    int l;
+    asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+    return l;
+}
+
+__device__ __forceinline__ bool aligned16(const void *p) {
+    return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
+
+// H_s: R -> panel (r, c), Q -> panel (NU + r, NU + c) of the tile image
+// (lower tiles only), S raw, [r; q] -> imr. Padding stages get R = Q = I,
+// S = 0, r = q = 0 (pad_problem, kkt_factor.cpp:27-47).
+template <int NU, int NX>
+__device__ __forceinline__ void stage_H(const Geo &g, const ProbView &p, int b, int j, int xi,
+                                        double *base, int) {
+    using W = WS<NU, NX>;
+    using S = Shp<NU, NX>;
+    const int N = g.N;
+    const int lane = lane_v();
+    double *img = base + W::O_IMG;
+    const bool in = j < N, qin = xi <= N;
+    auto at = [&](int r, int c) { return img + S::T(r / 8, c / 8) * kTileElems + (r % 8) * 8 + c % 8; };
+    const double *Rs = in ? p.R + ((size_t)b * N + j) * NU * NU : nullptr;
+    const double *Qs = qin ? p.Q + ((size_t)b * (N + 1) + xi) * NX * NX : nullptr;
+    // R
+    if (Rs && (NU % 2 == 0) && aligned16(Rs)) {
+#pragma unroll
+        for (int e = 2 * lane; e < NU * NU; e += 64) {
+            const int r = e / NU, c = e % NU;
+            if (c / 8 <= r / 8)
+                cp16(at(r, c), Rs + e);
+        }
+    } else {
+#pragma unroll
+        for (int e = lane; e < NU * NU; e += 32) {
+            const int r = e / NU, c = e % NU;
+            if (c / 8 <= r / 8) {
+                if (Rs)
+                    cp8(at(r, c), Rs + e);
+                else
+                    *at(r, c) = r == c ? 1.0 : 0.0;
+            }
+        }
+    }
+    // Q
+    if (Qs && (NU % 2 == 0) && (NX % 2 == 0) && aligned16(Qs)) {
+#pragma unroll
+        for (int e = 2 * lane; e < NX * NX; e += 64) {
+            const int r = NU + e / NX, c = NU + e % NX;
+            if (c / 8 <= r / 8)
+                cp16(at(r, c), Qs + e);
+        }
+    } else {
+#pragma unroll
+        for (int e = lane; e < NX * NX; e += 32) {
+            const int r = NU + e / NX, c = NU + e % NX;
+            if (c / 8 <= r / 8) {
+                if (Qs)
+                    cp8(at(r, c), Qs + e);
+                else
+                    *at(r, c) = r == c ? 1.0 : 0.0;
+            }
+        }
+    }
+    wcopy<NU * NX, 0>(base + W::O_S, in ? p.S + ((size_t)b * N + j) * NU * NX : nullptr, lane);
+    const double *rs = p.ru ? p.ru : p.r;
+    const double *qs = p.qx ? p.qx : p.q;
+    wcopy<NU, 0>(base + W::O_IMR, in ? rs + ((size_t)b * N + j) * NU : nullptr, lane);
+    wcopy<NX, 0>(base + W::O_IMR + NU, qin ? qs + ((size_t)b * (N + 1) + xi) * NX : nullptr, lane);
+}
+
+// BA_j = [B A] -> rows of the padded block (A omitted for j = 0, zero for
+// padding stages), f -> vector
+template <int NU, int NX>
+__device__ __forceinline__ void stage_BA(const Geo &g, const ProbView &p, int b, int j, double *base,
+                                         int) {
+    using W = WS<NU, NX>;
+    const int N = g.N;
+    const int lane = lane_v();
+    double *ba = base + W::O_BA;
+    const bool in = j < N;
+    const double *Bs = in ? p.B + ((size_t)b * N + j) * NX * NU : nullptr;
+    const double *As = (in && j != 0) ? p.A + ((size_t)b * N + j) * NX * NX : nullptr;
+    if (Bs && NU % 2 == 0 && aligned16(Bs)) {
+#pragma unroll
+        for (int e = 2 * lane; e < NX * NU; e += 64)
+            cp16(ba + (e / NU) * W::PW + e % NU, Bs + e);
+    } else {
+#pragma unroll
+        for (int e = lane; e < NX * NU; e += 32) {
+            double *d = ba + (e / NU) * W::PW + e % NU;
+            if (Bs)
+                cp8(d, Bs + e);
+            else
+                *d = 0.0;
+        }
+    }
+    if (As && NU % 2 == 0 && NX % 2 == 0 && aligned16(As)) {
+#pragma unroll
+        for (int e = 2 * lane; e < NX * NX; e += 64)
+            cp16(ba + (e / NX) * W::PW + NU + e % NX, As + e);
+    } else {
+#pragma unroll
+        for (int e = lane; e < NX * NX; e += 32) {
+            double *d = ba + (e / NX) * W::PW + NU + e % NX;
+            if (As)
+                cp8(d, As + e);
+            else
+                *d = 0.0;
+        }
+    }
+    const double *fs = p.fd ? p.fd : p.f;
+    wcopy<NX, 0>(base + W::O_F, in ? fs + ((size_t)b * N + j) * NX : nullptr, lane);
+}
+
+} // namespace
+
+template <int NU, int NX, int WPB>
+__global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a) {
+    using S = Shp<NU, NX>;
+    using W = WS<NU, NX>;
     extern __shared__ __align__(16) double sm[];
     const Geo &g = a.g;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -36,37 +207,32 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
     if (chain >= g.batch * g.P)
         return;
     const int b = chain / g.P, c = chain % g.P, n = g.n;
-    const int rq = lane >> 2, cq = 2 * (lane & 3);
+    const int rq = lane >> 2, cq = 2 * (lane & 3), q2 = lane & 3;
 
-    constexpr int SMEM_DBL = DIRECT ? S::SMEM_DIRECT : S::SMEM_STAGED;
-    double *base = sm + (size_t)wib * SMEM_DBL;
-    double *tscr = base + SMEM_DBL - kTileElems; // 8x8 transpose scratch
-    double *Wsm = base;                                   // TT x NXT tiles
-    double *Lsm = Wsm + S::TT * S::NXT * kTileElems;      // NLQ tiles (x-x block of L)
-    Stage<NU, NX> st;
-    st.R = Lsm + S::NLQ * kTileElems;
-    st.S = st.R + NU * NU;
-    st.Q = st.S + NU * NX;
-    st.r = st.Q + NX * NX;
-    st.q = st.r + NU;
-    st.B = st.R + S::HBp;
-    st.A = st.B + NX * NU;
-    st.f = st.A + NX * NX;
-    double *ru0 = DIRECT ? st.R : st.B + S::BBp; // NU: S_0 x_init
+    double *base = sm + (size_t)wib * W::SMEM;
+    double *Wsm = base + W::O_W, *LQ = base + W::O_LQ, *img = base + W::O_IMG;
+    double *imr = base + W::O_IMR, *Sb = base + W::O_S, *BA = base + W::O_BA;
+    double *fb = base + W::O_F, *ru0 = base + W::O_RU0, *tscr = base + W::O_SCR;
     const bool implicit_rhs = (a.p.ru == nullptr);
     const double sgn = implicit_rhs ? -1.0 : 1.0;
     int fail_piv = -1, fail_stage = 0;
 
+    // one-time init: everything zero, unit padding diagonal in the image
+    // (the stage copies never touch padding / permutation-gap positions)
+    for (int i = lane; i < W::SMEM; i += 32)
+        base[i] = 0.0;
+    __syncwarp();
+    if (lane < W::PW - W::NUX) {
+        const int r = W::NUX + lane;
+        img[S::T(r / 8, r / 8) * kTileElems + (r % 8) * 9] = 1.0;
+    }
+    __syncwarp();
+
     // prologue: H_0, BA_0 and the x_init term of ru[0]
     {
         const int j0 = g.stage_of(c, 0);
-        if (DIRECT) {
-            point_H<NU, NX>(g, a.p, a.consts, b, j0, g.x_index_of(c, 0), st, lane);
-            point_BA<NU, NX>(g, a.p, a.consts, b, j0, st, lane);
-        } else {
-            load_H<NU, NX>(g, a.p, b, j0, g.x_index_of(c, 0), st, lane);
-            load_BA<NU, NX>(g, a.p, b, j0, st, lane);
-        }
+        stage_H<NU, NX>(g, a.p, b, j0, g.x_index_of(c, 0), base, lane);
+        stage_BA<NU, NX>(g, a.p, b, j0, base, lane);
         cp_commit();
         if (implicit_rhs && c == 0 && lane < NU) {
             double s0 = 0;
@@ -84,60 +250,74 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
     for (int t = 0; t < S::NT; ++t)
         P[t] = Frag{0.0, 0.0};
 
-    // optional phase timing (CYQ_PHASE_PROF): chain 0's lane 0 records
-    // clock64 at the phase boundaries of every stage
     long long *ph = (a.phase && chain == 0 && lane == 0) ? a.phase : nullptr;
     for (int s = 0; s < n; ++s) {
         if (ph) ph[s * 8 + 0] = clock64();
         const int j = g.stage_of(c, s);
-        const double *ru0p = (implicit_rhs && j == 0) ? ru0 : nullptr;
+        const bool j0 = j == 0;
+        const double *ru0p = (implicit_rhs && j0) ? ru0 : nullptr;
         if (s > 0) {
             cp_wait<1>(); // H_s has landed (the newest group may still fly)
             __syncwarp();
         }
-        // ---- init pivot tiles, += W W' ------------------------------------
+        // ---- init: H_s image (+ S' gather), BA_0 rows at s = 0, rhs row ----
 #pragma unroll
-        for (int ti = 0; ti < S::TT; ++ti) {
+        for (int ti = 0; ti < S::TT; ++ti)
 #pragma unroll
             for (int tj = 0; tj <= ti && tj < S::CT; ++tj) {
-                Frag &f = P[S::T(ti, tj)];
-                const int r = 8 * ti + rq, col = 8 * tj + cq;
-                f.a = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, ti, r, col);
-                f.b = pinit<NU, NX>(st, s == 0, j == 0, sgn, ru0p, ti, r, col + 1);
-            }
-        }
-        if (s > 0) {
-            // k-slice outer, tiles inner: consecutive DMMAs hit different
-            // accumulators (no dependent-DMMA stalls); each W fragment is
-            // read from shared memory once per slice
+                Frag f{0.0, 0.0};
+                if (8 * ti < S::TOP) {
+                    f = ld_frag(img + S::T(ti, tj) * kTileElems, lane);
+                    if (8 * ti + 7 >= NU && 8 * tj < NU && !j0) { // tile meets the S' block
 #pragma unroll
-            for (int kt = 0; kt < S::NXT; ++kt) {
+                        for (int h = 0; h < 2; ++h) {
+                            const int r = 8 * ti + rq, col = 8 * tj + cq + h;
+                            const bool isS = r >= NU && r < S::NUX && col < NU;
+                            const double v = Sb[isS ? col * NX + (r - NU) : 0];
+                            (h ? f.b : f.a) += isS ? v : 0.0;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int rb = 8 * ti + rq - S::TOP, col = 8 * tj + cq + h;
+                        double v = 0.0;
+                        if (s == 0 && rb < NX)
+                            v = BA[rb * W::PW + col];
+                        if (rb == NX)
+                            v = sgn * imr[col] - ((ru0p && col < NU) ? ru0p[col] : 0.0);
+                        (h ? f.b : f.a) = v;
+                    }
+                }
+                P[S::T(ti, tj)] = f;
+            }
+        if (s > 0) {
+            // += W W' over the compact x-columns: k-slice outer, tiles inner
+            // (consecutive DMMAs hit different accumulators)
+#pragma unroll
+            for (int kt = 0; kt < W::NXC; ++kt) {
                 Frag w[S::TT];
 #pragma unroll
                 for (int i = 0; i < S::TT; ++i)
-                    w[i] = ld_frag(Wsm + (i * S::NXT + kt) * kTileElems, lane);
+                    w[i] = ld_frag(Wsm + (i * W::NXC + kt) * kTileElems, lane);
 #pragma unroll
-                for (int h = 0; h < 2; ++h)
+                for (int h = 0; h < 2; ++h) {
+                    if (kt == W::NXF && W::HALF && h == 1)
+                        continue; // odd positions of the last tile are empty
 #pragma unroll
                     for (int ti = 0; ti < S::TT; ++ti)
 #pragma unroll
                         for (int tj = 0; tj <= ti; ++tj)
                             dmma(P[S::T(ti, tj)], h ? w[ti].b : w[ti].a, h ? w[tj].b : w[tj].a);
+                }
             }
         }
         __syncwarp();
-        // the H buffer is free: prefetch H_{s+1} (and BA_1 at s = 0)
+        // the H buffers are free: prefetch H_{s+1} (and BA_1 at s = 0)
         if (s + 1 < n) {
-            if (DIRECT) {
-                point_H<NU, NX>(g, a.p, a.consts, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1),
-                                st, lane);
-                if (s == 0)
-                    point_BA<NU, NX>(g, a.p, a.consts, b, g.stage_of(c, 1), st, lane);
-            } else {
-                load_H<NU, NX>(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), st, lane);
-                if (s == 0)
-                    load_BA<NU, NX>(g, a.p, b, g.stage_of(c, 1), st, lane);
-            }
+            stage_H<NU, NX>(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), base, lane);
+            if (s == 0)
+                stage_BA<NU, NX>(g, a.p, b, g.stage_of(c, 1), base, lane);
         }
         cp_commit();
 
@@ -157,12 +337,12 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
         const double dfloor = 1e-14 * dmax;
 
         // ---- blocked Cholesky of the pivot columns -------------------------
-        // Step k of the diagonal tile and step k of every sub-diagonal tile of
-        // block column kb are interleaved, so the independent sub-diagonal
-        // work fills the latency of the pivot chain (broadcast, rsqrt) and
-        // no per-column arrays stay live. Updates are unconditional FMAs with
-        // zeroed multipliers instead of predicated branches.
-        const int q2 = lane & 3; // this lane holds columns 2*q2, 2*q2 + 1
+        // The diagonal tile's pivot steps carry an identity tile (ends as
+        // L_kk^{-T}); the sub-diagonal tiles are then solved by two DMMAs
+        // each against L_kk^{-1}, and the trailing updates are DMMAs.
+        // (Issuing the trailing / W W' DMMAs between the pivot steps instead
+        // was measured slower: the DMMA pipe, shared by the SM sub-partition's
+        // two resident warps, then throttles the pivot chain's issue.)
 #pragma unroll
         for (int kb = 0; kb < S::CT; ++kb) {
             Frag &dg = P[S::T(kb, kb)];
@@ -192,48 +372,30 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
                     dg.a = (q2 == src) ? nv : dg.a;
                 dg.a -= lrk * lc0;
                 dg.b -= lrk * lc1;
-                if (!INV) {
-#pragma unroll
-                    for (int ti = kb + 1; ti < S::TT; ++ti) {
-                        Frag &x = P[S::T(ti, kb)];
-                        const double vq = (k & 1) ? x.b : x.a;
-                        const double xrq = __shfl_sync(FULL, vq, 4 * rq + src) * iv;
-                        if (k & 1)
-                            x.b = (q2 == src) ? xrq : x.b;
-                        else
-                            x.a = (q2 == src) ? xrq : x.a;
-                        x.a -= xrq * lc0;
-                        x.b -= xrq * lc1;
-                    }
-                } else { // same step on one identity tile: ends as L_kk^{-T}
-                    const double vq = (k & 1) ? idt.b : idt.a;
-                    const double xrq = __shfl_sync(FULL, vq, 4 * rq + src) * iv;
-                    if (k & 1)
-                        idt.b = (q2 == src) ? xrq : idt.b;
-                    else
-                        idt.a = (q2 == src) ? xrq : idt.a;
-                    idt.a -= xrq * lc0;
-                    idt.b -= xrq * lc1;
-                }
+                const double vq = (k & 1) ? idt.b : idt.a;
+                const double xrq = __shfl_sync(FULL, vq, 4 * rq + src) * iv;
+                if (k & 1)
+                    idt.b = (q2 == src) ? xrq : idt.b;
+                else
+                    idt.a = (q2 == src) ? xrq : idt.a;
+                idt.a -= xrq * lc0;
+                idt.b -= xrq * lc1;
             }
             if (cq > rq) dg.a = 0.0;
             if (cq + 1 > rq) dg.b = 0.0;
-            if (INV) {
-                // L^{-1} = (L^{-T})' through a shared-memory transpose, then
-                // every sub-diagonal tile at once: X <- X L^{-T} = X (L^{-1})'
-                // (two DMMAs per tile instead of eight dependent pivot steps)
-                st_frag(tscr, lane, idt);
-                __syncwarp();
-                Frag linv;
-                linv.a = tscr[cq * 8 + rq];
-                linv.b = tscr[(cq + 1) * 8 + rq];
-                __syncwarp();
+            // L^{-1} = (L^{-T})' through a shared-memory transpose, then every
+            // sub-diagonal tile at once: X <- X L^{-T} = X (L^{-1})'
+            st_frag(tscr, lane, idt);
+            __syncwarp();
+            Frag linv;
+            linv.a = tscr[cq * 8 + rq];
+            linv.b = tscr[(cq + 1) * 8 + rq];
+            __syncwarp();
 #pragma unroll
-                for (int ti = kb + 1; ti < S::TT; ++ti) {
-                    Frag x = P[S::T(ti, kb)], r{0.0, 0.0};
-                    tile_gemm_nt(r, x, linv);
-                    P[S::T(ti, kb)] = r;
-                }
+            for (int ti = kb + 1; ti < S::TT; ++ti) {
+                Frag x = P[S::T(ti, kb)], r{0.0, 0.0};
+                tile_gemm_nt(r, x, linv);
+                P[S::T(ti, kb)] = r;
             }
             // trailing update C(ti,tj) -= L(ti,kb) L(tj,kb)': the next diagonal
             // tile first (its factorization can start early), then both k
@@ -265,14 +427,13 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
                         st_frag(dst + o * kTileElems, lane, P[S::T(ti, tj)]);
                         ++o;
                     }
-            constexpr int RT = S::RHS / 8, RR = S::RHS % 8;
-            if (rq == RR) {
+            if (rq == W::RR) {
                 double *yv = a.y + ((size_t)chain * n + s) * S::NUX;
 #pragma unroll
                 for (int tj = 0; tj < S::CT; ++tj) {
                     const int col = 8 * tj + cq;
-                    if (col < S::NUX) yv[col] = P[S::T(RT, tj)].a;
-                    if (col + 1 < S::NUX) yv[col + 1] = P[S::T(RT, tj)].b;
+                    if (col < S::NUX) yv[col] = P[S::T(W::RT, tj)].a;
+                    if (col + 1 < S::NUX) yv[col + 1] = P[S::T(W::RT, tj)].b;
                 }
             }
         }
@@ -298,14 +459,13 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
                         const int K = 8 * ti + rq;
                         const double lv = e ? P[S::T(ti, ct)].b : P[S::T(ti, ct)].a;
                         if (K >= NU && K < S::NUX && K >= C && C >= NU && C < S::NUX)
-                            acc += lv * (sgn * st.f[K - NU]);
+                            acc += lv * (sgn * fb[K - NU]);
                     }
                     acc += __shfl_xor_sync(0xffffffffu, acc, 4);
                     acc += __shfl_xor_sync(0xffffffffu, acc, 8);
                     acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-                    constexpr int RT = S::RHS / 8, RR = S::RHS % 8;
-                    const double xr = e ? P[S::T(RT, ct)].b : P[S::T(RT, ct)].a;
-                    const double xp = __shfl_sync(0xffffffffu, xr, 4 * RR + (lane & 3));
+                    const double xr = e ? P[S::T(W::RT, ct)].b : P[S::T(W::RT, ct)].a;
+                    const double xp = __shfl_sync(0xffffffffu, xr, 4 * W::RR + (lane & 3));
                     mw[kt][e] = (C >= NU && C < S::NUX) ? acc + xp : 0.0;
                 }
             }
@@ -320,82 +480,76 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
                             wl[C - NU] = -mw[kt][e];
                     }
             }
-            // W bottom rows: ALQ (x columns of the coupling rows), rhs row -wl
+            // W bottom rows: ALQ (x columns of the coupling rows) and the rhs
+            // row -wl, scattered to the compact column positions; L_Q -> LQ
+            {
+            const int lv = lane_v(), rq = lv >> 2, cq = 2 * (lv & 3);
 #pragma unroll
             for (int ti = S::CT; ti < S::TT; ++ti)
 #pragma unroll
                 for (int kt = 0; kt < S::NXT; ++kt) {
-                    const int ct = S::XT0 + kt;
-                    Frag w = P[S::T(ti, ct)];
-                    const int r = 8 * ti + rq, c0 = 8 * ct + cq;
-                    if (r == S::RHS) {
-                        w.a = mw[kt][0];
-                        w.b = mw[kt][1];
-                    } else if (r > S::RHS) {
-                        w.a = w.b = 0.0;
+                    const int ct = S::XT0 + kt, r = 8 * ti + rq;
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int C = 8 * ct + cq + e;
+                        if (C >= NU && C < S::NUX && r <= S::RHS) {
+                            const double v = (r == S::RHS) ? mw[kt][e]
+                                                           : (e ? P[S::T(ti, ct)].b : P[S::T(ti, ct)].a);
+                            const int p = W::pos(C - NU);
+                            Wsm[(ti * W::NXC + p / 8) * kTileElems + (r % 8) * 8 + p % 8] = v;
+                        }
                     }
-                    if (c0 < NU || c0 >= S::NUX) w.a = 0.0;
-                    if (c0 + 1 < NU || c0 + 1 >= S::NUX) w.b = 0.0;
-                    st_frag(Wsm + (ti * S::NXT + kt) * kTileElems, lane, w);
                 }
-            // L_Q tiles (x rows/cols, masked) -> Lsm for the transposed access
 #pragma unroll
             for (int u = 0; u < S::NXT; ++u)
 #pragma unroll
                 for (int v = 0; v <= u; ++v) {
-                    Frag w = P[S::T(S::XT0 + u, S::XT0 + v)];
-                    const int K = 8 * (S::XT0 + u) + rq, C0 = 8 * (S::XT0 + v) + cq;
-                    const bool rin = K >= NU && K < S::NUX;
-                    if (!(rin && C0 >= NU && C0 < S::NUX && C0 <= K)) w.a = 0.0;
-                    if (!(rin && C0 + 1 >= NU && C0 + 1 < S::NUX && C0 + 1 <= K)) w.b = 0.0;
-                    st_frag(Lsm + S::T(u, v) * kTileElems, lane, w);
+                    const Frag w = P[S::T(S::XT0 + u, S::XT0 + v)];
+                    const int K = 8 * (S::XT0 + u) + rq;
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int C = 8 * (S::XT0 + v) + cq + e;
+                        if (K >= NU && K < S::NUX && C >= NU && C <= K)
+                            LQ[(K - NU) * NX + (C - NU)] = e ? w.b : w.a;
+                    }
                 }
+            }
             __syncwarp();
             if (ph) ph[s * 8 + 4] = clock64();
-            // V = BA_{s+1}' L_Q : rows 0..nux-1 of W (DMMA), k-slice outer
+            // V = BA_{s+1}' L_Q : rows 0..nux-1 of W (DMMA over x rows K)
             {
-                Frag vacc[S::CT * S::NXT];
+                Frag vacc[S::CT * W::NXC];
 #pragma unroll
-                for (int v = 0; v < S::CT * S::NXT; ++v)
+                for (int v = 0; v < S::CT * W::NXC; ++v)
                     vacc[v] = Frag{0.0, 0.0};
 #pragma unroll
-                for (int ks = 2 * S::XT0; ks < 2 * (S::XT1 + 1); ++ks) {
+                for (int ks = 0; ks < W::KQ; ++ks) {
                     const int K = 4 * ks + (lane & 3);
-                    const bool kin = K >= NU && K < S::NUX;
-                    double av[S::CT], bv[S::NXT];
+                    double av[S::CT], bv[W::NXC];
 #pragma unroll
-                    for (int ti = 0; ti < S::CT; ++ti) {
-                        const int r = 8 * ti + rq;
-                        av[ti] = (kin && r < S::NUX)
-                                     ? (r < NU ? st.B[(K - NU) * NU + r] : st.A[(K - NU) * NX + (r - NU)])
-                                     : 0.0;
-                    }
+                    for (int ti = 0; ti < S::CT; ++ti)
+                        av[ti] = BA[K * W::PW + 8 * ti + rq];
 #pragma unroll
-                    for (int kt = 0; kt < S::NXT; ++kt) {
-                        // B[kk][n] = L[K][8ct + n]: tile (K/8, ct) of Lsm
-                        const int u = ks / 2 - S::XT0;
-                        bv[kt] = (u >= kt) ? Lsm[S::T(u >= kt ? u : kt, kt) * kTileElems +
-                                                 (4 * (ks & 1) + (lane & 3)) * 8 + (lane >> 2)]
-                                           : 0.0;
+                    for (int kt = 0; kt < W::NXC; ++kt) { // x-column of this lane's B column
+                        const int vc = W::col_of(8 * kt + rq);
+                        bv[kt] = vc >= 0 ? LQ[K * NX + (vc >= 0 ? vc : 0)] : 0.0; // rows >= nx: 0
                     }
 #pragma unroll
                     for (int ti = 0; ti < S::CT; ++ti)
 #pragma unroll
-                        for (int kt = 0; kt < S::NXT; ++kt)
-                            if (4 * ks + 3 >= 8 * (S::XT0 + kt)) // L_Q upper part is zero
-                                dmma(vacc[ti * S::NXT + kt], av[ti], bv[kt]);
+                        for (int kt = 0; kt < W::NXC; ++kt)
+                            if (4 * ks + 3 >= 8 * kt) // L_Q upper part is zero
+                                dmma(vacc[ti * W::NXC + kt], av[ti], bv[kt]);
                 }
 #pragma unroll
-                for (int v = 0; v < S::CT * S::NXT; ++v)
-                    st_frag(Wsm + v * kTileElems, lane, vacc[v]);
+                for (int ti = 0; ti < S::CT; ++ti)
+#pragma unroll
+                    for (int kt = 0; kt < W::NXC; ++kt)
+                        st_frag(Wsm + (ti * W::NXC + kt) * kTileElems, lane, vacc[ti * W::NXC + kt]);
             }
             __syncwarp();
-            if (s + 2 < n) {
-                if (DIRECT)
-                    point_BA<NU, NX>(g, a.p, a.consts, b, g.stage_of(c, s + 2), st, lane);
-                else
-                    load_BA<NU, NX>(g, a.p, b, g.stage_of(c, s + 2), st, lane);
-            }
+            if (s + 2 < n)
+                stage_BA<NU, NX>(g, a.p, b, g.stage_of(c, s + 2), base, lane);
             cp_commit();
         }
     }
@@ -419,30 +573,20 @@ __global__ void __launch_bounds__(32 * WPB, DIRECT ? 12 / WPB : 1) riccati_warp_
 
 // ---- dispatch ----------------------------------------------------------------
 namespace {
-template <int NU, int NX, int WPB, bool DIRECT, bool INV>
-bool launch_wd(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
-    using S = Shp<NU, NX>;
-    const size_t smem = (size_t)WPB * (DIRECT ? S::SMEM_DIRECT : S::SMEM_STAGED) * sizeof(double);
-    static_assert(S::SMEM_STAGED % 2 == 0 && S::SMEM_DIRECT % 2 == 0, "16-byte aligned warps");
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(riccati_warp_kernel<NU, NX, WPB, DIRECT, INV>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    const int chains = g.batch * g.P;
-    riccati_warp_kernel<NU, NX, WPB, DIRECT, INV><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ra);
-    return true;
-}
 template <int NU, int NX, int WPB> bool launch_w(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
     if (g.nu != NU || g.nx != NX)
         return false;
-    static const bool direct = getenv("CYQ_RICCATI_DIRECT") != nullptr;
-    static const bool noinv = getenv("CYQ_RICCATI_NOINV") != nullptr;
-    if (direct)
-        return launch_wd<NU, NX, WPB, true, true>(g, st, ra);
-    return noinv ? launch_wd<NU, NX, WPB, false, false>(g, st, ra)
-                 : launch_wd<NU, NX, WPB, false, true>(g, st, ra);
+    using W = WS<NU, NX>;
+    const size_t smem = (size_t)WPB * W::SMEM * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(riccati_warp_kernel<NU, NX, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attr = true;
+    }
+    const int chains = g.batch * g.P;
+    riccati_warp_kernel<NU, NX, WPB><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ra);
+    return true;
 }
 } // namespace
 
