@@ -37,7 +37,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_2512_09058_b200 import synth  # noqa: E402
+from paper_2512_09058_b200 import shard, synth  # noqa: E402
 from paper_2512_09058_b200.flops import (fma_phases, flops_per_solve, problem_bytes,  # noqa: E402
                                          solution_bytes)
 
@@ -207,7 +207,7 @@ def run_ours(args):
     cfg = synth.CONFIGS[args.config]
     B = cfg.batch
     t0 = time.time()
-    p = synth.generate(args.config, seed=args.seed, batch=B, start=rank * B)
+    p, _ = shard.generate_shard(args.config, args.seed, rank, ws, per_rank=B)  # weak scaling
     log(f"[rank {rank}] generated {B} instances ({p.nbytes() / 1e9:.2f} GB) in "
         f"{time.time() - t0:.1f}s")
     opts = kkt.FactorOptions(P=cfg.P)
@@ -222,11 +222,7 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
-        if ws == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        return float(t.item())
+        return shard.max_over_ranks(x, device="cuda")
 
     # ---- device-resident inputs -----------------------------------------
     dev = EqOCPBatch.__new__(EqOCPBatch)

@@ -41,5 +41,36 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+HOST_SOURCES = ["host/ocp.cpp", "host/kkt_solver.cpp"]
+HOST_OUT = os.path.join(HERE, "libcyqlone_b200_host.so")
+ROOT = os.path.dirname(HERE)
+HOST_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_kkt_host.cpp")
+HOST_TEST_OUT = os.path.join(ROOT, "tests", "cpp", "test_kkt_host")
+CXX = os.environ.get("CXX", "g++")
+
+
+def build_host(verbose: bool = False) -> str:
+    """The C++ mirror of the reference interface (cyqlone::kkt / cyqlone::ocp,
+    include/cyqlone_b200/*.hpp) as libcyqlone_b200_host.so over the CUDA
+    library, plus the C++ test driver tests/cpp/test_kkt_host. Host-only g++
+    (no CUDA headers): the kernels are reached through the C ABI."""
+    cmds = [
+        [CXX, "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall", "-Wextra", "-o", HOST_OUT,
+         *[os.path.join(HERE, s) for s in HOST_SOURCES], "-L" + HERE, "-lcyqlone_b200",
+         "-Wl,-rpath,$ORIGIN"],
+        [CXX, "-O2", "-std=c++17", "-Wall", "-I" + os.path.join(ROOT, "include"), "-o", HOST_TEST_OUT,
+         HOST_TEST_SRC, "-L" + HERE, "-lcyqlone_b200_host", "-lcyqlone_b200",
+         "-Wl,-rpath,$ORIGIN/../../paper_2512_09058_b200"],
+    ]
+    for cmd in cmds:
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if verbose or r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+        if r.returncode != 0:
+            raise RuntimeError("g++ failed: " + " ".join(cmd[:8]))
+    return HOST_OUT
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    print(build_host(verbose=True))
