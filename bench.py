@@ -110,6 +110,18 @@ def fp64_peak():
         return 37.0, "fallback: B200 FP64 tensor datasheet ~37 TFLOP/s"
 
 
+def ncu_traffic(kernel_tag, cfg_idx, batch):
+    """DRAM bytes per launch of a kernel from the committed `ncu --set full`
+    summary (profiles/ncu_r01_<tag>.json, tools/ncu_summary.py) -- only for
+    the workload it was captured on (config 1, 1024 instances)."""
+    path = os.path.join(ROOT, "profiles", f"ncu_r01_{kernel_tag}.json")
+    if cfg_idx != 1 or batch != 1024 or not os.path.exists(path):
+        return None, None
+    with open(path) as fh:
+        d = json.load(fh)
+    return d.get("dram_bytes"), f"profiles/ncu_r01_{kernel_tag}.json ({d.get('report')})"
+
+
 def hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -283,6 +295,28 @@ def run_ours(args):
     shares = {k: round(v[0] / max(sum(x[0] for x in kern.values()), 1e-9), 4)
               for k, v in kern.items() if v[1]}
     hbm, hbm_src = hbm_peak()
+    traffic, traffic_src = ncu_traffic("riccati", cfg.idx, B)
+    # the other two kernels against their own bounds (algorithmic bytes:
+    # DESIGN.md §6; the CR/Schur kernel is latency-bound, reported in FLOP/s)
+    kms = {k: v[0] / max(v[1], 1) for k, v in kern.items() if v[1]}
+    n_per = (cfg.N + cfg.P - 1) // cfg.P
+    chains = B * cfg.P
+    fac_bytes = chains * n_per * (-(-(cfg.nx + cfg.nu) // 8) * (-(-(cfg.nx + cfg.nu) // 8) + 1) // 2
+                                  + -(-(cfg.nx + 1) // 8) * -(-(cfg.nx + cfg.nu) // 8)) * 512
+    back_bytes = fac_bytes + B * cfg.N * (cfg.nx * cfg.nx + cfg.nx * cfg.nu) * 8 \
+        + solution_bytes(cfg.N, cfg.nx, cfg.nu) * B
+    kernel_rooflines = {}
+    if "backsub" in kms:
+        kernel_rooflines["backsub"] = {
+            "bound": "hbm", "unit": "GB/s", "algo_bytes": back_bytes,
+            "achieved": back_bytes / (kms["backsub"] * 1e-3) / 1e9, "peak": hbm,
+            "frac": back_bytes / (kms["backsub"] * 1e-3) / 1e9 / hbm}
+    if "schur_cr" in kms:
+        sf = 2.0 * ph["kernel_schur_cr"] * B
+        kernel_rooflines["schur_cr"] = {
+            "bound": "latency (CR tree depth)", "unit": "TFLOP/s", "algo_flops": sf,
+            "achieved": sf / (kms["schur_cr"] * 1e-3) / 1e12, "peak": peak,
+            "frac": sf / (kms["schur_cr"] * 1e-3) / 1e12 / peak}
     line = {
         "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -295,7 +329,8 @@ def run_ours(args):
                 "ms_per_step": ms_e2e},
         "roofline": {"bound": "tensor", "kernel": "riccati_panel_kernel",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_source": peak_src,
                      "flops_per_launch": k_flops, "launch_ms": k_avg},
         "step_roofline": {
             "flops_per_step": flops_per_solve(cfg.N, cfg.nx, cfg.nu, cfg.P) * B,
@@ -305,6 +340,7 @@ def run_ours(args):
             "compulsory_bytes": (problem_bytes(cfg.N, cfg.nx, cfg.nu)
                                  + solution_bytes(cfg.N, cfg.nx, cfg.nu)) * B,
             "hbm_gbs_peak": hbm, "hbm_source": hbm_src},
+        "kernel_rooflines": kernel_rooflines,
         "kernel_shares": shares, "kernel_ms_per_step": {k: v[0] / max(args.steps, 1)
                                                         for k, v in kern.items() if v[1]},
         "kernel_sum_ms_per_step": step_ms_k,
