@@ -663,10 +663,7 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs
     }
 }
 
-template <int NX> bool launch_sf(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
-    if (g.nx != NX)
-        return false;
-    constexpr int NW = 4;
+template <int NX, int NW> bool launch_sfw(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
     const size_t smem = sf_smem_doubles<SF<NX>::XP>(NW, SF<NX>::NF, g.P) * sizeof(double);
     if (smem > 200 * 1024)
         return false;
@@ -680,11 +677,23 @@ template <int NX> bool launch_sf(const Geo &g, cudaStream_t st, const SchurArgs 
     return true;
 }
 
+// 4 warps per instance when the batch fills the GPU with CTAs; a wide CTA
+// (the level's blocks spread over 8-16 warps) for a few long-horizon
+// instances (config 2: one instance, P = 256)
+template <int NX> bool launch_sf(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
+    if (g.nx != NX)
+        return false;
+    constexpr int WIDE = NX > 16 ? 8 : 16;
+    if (g.batch >= 64 || g.P <= 8)
+        return launch_sfw<NX, 4>(g, st, sa);
+    return launch_sfw<NX, WIDE>(g, st, sa);
+}
+
 } // namespace
 
-// The fused path serves batches large enough to fill the GPU with one CTA
-// per instance; small batches (a single long horizon, config 2) keep the
-// per-level batch-wide kernels, whose parallelism is the blocks of a level.
+// The fused kernel serves every batch size (one CTA per instance; wide CTAs
+// for small batches); CYQ_SCHUR=levels selects the per-level batch-wide
+// kernels of schur_tiles.cu instead (kept as the cross-check path).
 bool schur_fused_ok(const Geo &g) {
     // CYQ_SCHUR=levels|fused overrides the choice (read per call: tests
     // exercise both paths in one process)
@@ -694,9 +703,7 @@ bool schur_fused_ok(const Geo &g) {
     const bool shape = g.nx == 20 || g.nx == 16 || g.nx == 12 || g.nx == 10;
     if (!shape)
         return false;
-    if (e && e[0] == 'f')
-        return true;
-    return g.batch >= 64;
+    return true;
 }
 
 bool launch_schur_fused(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
