@@ -313,6 +313,8 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
             done = launch_riccati_cta2(g, ctx->stream, ra);
         if (!want_gen && !done)
             done = launch_riccati_warp(g, ctx->stream, ra);
+        if (!want_gen && !done)
+            done = launch_riccati_cta(g, ctx->stream, ra);
         if (!done)
             launch_riccati(g, ctx->stream, ra);
     }
