@@ -34,6 +34,9 @@ using namespace cyqb::ric;
 
 namespace {
 
+// (ti << 8 | tj) of lower-triangular tile t = ti (ti + 1) / 2 + tj
+__constant__ unsigned short c_tij[1024];
+
 template <int NU, int NX, int NW> struct CS {
     static_assert(NU % 8 == 0 && NX % 8 == 0, "tile-aligned shapes only");
     static constexpr int NUX = NU + NX;
@@ -57,8 +60,8 @@ template <int NU, int NX, int NW> struct CS {
     static constexpr int O_MW = O_YX + NX;                         // NX (-wl_new)
     static constexpr int O_RU0 = O_MW + NX;                        // NU
     static constexpr int O_RED = O_RU0 + NU;                       // 32 (pivot floor)
-    static constexpr int O_SCR = O_RED + 32;                       // 64 (transpose)
-    static constexpr int SMEM = O_SCR + kTileElems;
+    static constexpr int O_SCR = O_RED + 32;                       // 2 x 64 (transpose, by parity)
+    static constexpr int SMEM = O_SCR + 2 * kTileElems;
     __host__ __device__ static constexpr int T(int i, int j) { return i * (i + 1) / 2 + j; }
     // stored-factor tile index of panel tile (i, j), j < CT
     __host__ __device__ static constexpr int PI(int i, int j) {
@@ -133,23 +136,12 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
     const double sgn = implicit_rhs ? -1.0 : 1.0;
     int fail_piv = -1, fail_stage = 0;
 
-    // my tiles: t = warp + k NW -> (ti, tj), recomputed where used (no
-    // per-tile index registers)
-    auto mti_f = [&](int k) -> int {
-        const int t = warp + k * NW;
-        if (t >= NT)
-            return -1;
-        int ti = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-        ti += (C::T(ti + 1, 0) <= t) ? 1 : 0;
-        ti -= (C::T(ti, 0) > t) ? 1 : 0;
-        return ti;
-    };
-    auto mtj_f = [&](int k) -> int {
-        const int t = warp + k * NW, ti = mti_f(k);
-        return ti < 0 ? -1 : t - C::T(ti, 0);
-    };
-#define mti(k) mti_f(k)
-#define mtj(k) mtj_f(k)
+    // my tiles: t = warp + k NW -> (ti, tj) from the constant-memory table
+    // of the triangular enumeration (warp-uniform loads, no index registers)
+#define mtt(k) (warp + (k) * NW)
+#define mt(k) (mtt(k) < NT ? (int)c_tij[mtt(k)] : -1)
+#define mti(k) (mtt(k) < NT ? (int)(c_tij[mtt(k)] >> 8) : -1)
+#define mtj(k) (mtt(k) < NT ? (int)(c_tij[mtt(k)] & 255) : -1)
     for (int i = tid; i < C::SMEM; i += NTH)
         sm[i] = 0.0;
     __syncthreads();
@@ -279,64 +271,77 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         // ---- blocked Cholesky with look-ahead ----------------------------
         // factor_diag: the owner's (kb, kb) tile -> L_kk (upper zeroed) and
         // L_kk^{-1} -> linv[kb & 1], L_kk -> column buffer slot kb.
+        // factor_diag: the diagonal tile (kb, kb), handed over in the column
+        // buffer slot kb by its owner, is factored in place there (L_kk, upper
+        // zeroed) and L_kk^{-1} goes to linv[kb & 1]; one code copy, no
+        // register-array indexing (the owner reloads L_kk into its register
+        // tile in the next sub-diagonal phase)
         auto factor_diag = [&](int kb) {
+            if (C::T(kb, kb) % NW != warp)
+                return;
+            double *slot = colb + ((kb & 1) * TT + kb) * kTileElems;
+            Frag dg = ld_frag(slot, lane);
+            Frag idt{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0};
 #pragma unroll
-            for (int k = 0; k < MAXT; ++k) {
-                if (mti(k) != kb || mtj(k) != kb)
-                    continue;
-                Frag dg = acc[k];
-                Frag idt{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0};
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const int src = kk / 2;
-                    const double vk = (kk & 1) ? dg.b : dg.a;
-                    const double pv = __shfl_sync(0xffffffffu, vk, 4 * kk + src);
-                    const double urk = __shfl_sync(0xffffffffu, vk, 4 * rq + src);
-                    const double uc0 = __shfl_sync(0xffffffffu, vk, 4 * cq + src);
-                    const double uc1 = __shfl_sync(0xffffffffu, vk, 4 * (cq + 1) + src);
-                    const bool first = !(pv > dfloor && isfinite(pv)) && fail_piv < 0;
-                    fail_piv = first ? 8 * kb + kk : fail_piv;
-                    fail_stage = first ? s : fail_stage;
-                    const double iv = rsqrt_nr(pv);
-                    const double lc0 = (cq > kk) ? uc0 * iv : 0.0;
-                    const double lc1 = (cq + 1 > kk) ? uc1 * iv : 0.0;
-                    const double lrk = urk * iv;
-                    const double nv = (rq == kk) ? pv * iv : lrk;
-                    if (kk & 1)
-                        dg.b = (q2 == src) ? nv : dg.b;
-                    else
-                        dg.a = (q2 == src) ? nv : dg.a;
-                    dg.a -= lrk * lc0;
-                    dg.b -= lrk * lc1;
-                    const double vq = (kk & 1) ? idt.b : idt.a;
-                    const double xrq = __shfl_sync(0xffffffffu, vq, 4 * rq + src) * iv;
-                    if (kk & 1)
-                        idt.b = (q2 == src) ? xrq : idt.b;
-                    else
-                        idt.a = (q2 == src) ? xrq : idt.a;
-                    idt.a -= xrq * lc0;
-                    idt.b -= xrq * lc1;
-                }
-                if (cq > rq) dg.a = 0.0;
-                if (cq + 1 > rq) dg.b = 0.0;
-                acc[k] = dg;
-                st_frag(colb + ((kb & 1) * TT + kb) * kTileElems, lane, dg);
-                st_frag(tscr, lane, idt); // L^{-1} = (L^{-T})'
-                __syncwarp();
-                st_frag(linvb + (kb & 1) * kTileElems, lane,
-                        Frag{tscr[cq * 8 + rq], tscr[(cq + 1) * 8 + rq]});
-                __syncwarp();
+            for (int kk = 0; kk < 8; ++kk) {
+                const int src = kk / 2;
+                const double vk = (kk & 1) ? dg.b : dg.a;
+                const double pv = __shfl_sync(0xffffffffu, vk, 4 * kk + src);
+                const double urk = __shfl_sync(0xffffffffu, vk, 4 * rq + src);
+                const double uc0 = __shfl_sync(0xffffffffu, vk, 4 * cq + src);
+                const double uc1 = __shfl_sync(0xffffffffu, vk, 4 * (cq + 1) + src);
+                const bool first = !(pv > dfloor && isfinite(pv)) && fail_piv < 0;
+                fail_piv = first ? 8 * kb + kk : fail_piv;
+                fail_stage = first ? s : fail_stage;
+                const double iv = rsqrt_nr(pv);
+                const double lc0 = (cq > kk) ? uc0 * iv : 0.0;
+                const double lc1 = (cq + 1 > kk) ? uc1 * iv : 0.0;
+                const double lrk = urk * iv;
+                const double nv = (rq == kk) ? pv * iv : lrk;
+                if (kk & 1)
+                    dg.b = (q2 == src) ? nv : dg.b;
+                else
+                    dg.a = (q2 == src) ? nv : dg.a;
+                dg.a -= lrk * lc0;
+                dg.b -= lrk * lc1;
+                const double vq = (kk & 1) ? idt.b : idt.a;
+                const double xrq = __shfl_sync(0xffffffffu, vq, 4 * rq + src) * iv;
+                if (kk & 1)
+                    idt.b = (q2 == src) ? xrq : idt.b;
+                else
+                    idt.a = (q2 == src) ? xrq : idt.a;
+                idt.a -= xrq * lc0;
+                idt.b -= xrq * lc1;
             }
+            if (cq > rq) dg.a = 0.0;
+            if (cq + 1 > rq) dg.b = 0.0;
+            st_frag(slot, lane, dg);
+            double *ts = tscr + (kb & 1) * kTileElems;
+            st_frag(ts, lane, idt); // L^{-1} = (L^{-T})'
+            __syncwarp();
+            st_frag(linvb + (kb & 1) * kTileElems, lane, Frag{ts[cq * 8 + rq], ts[(cq + 1) * 8 + rq]});
+            __syncwarp();
         };
+        // the owner of (0, 0) hands it over
+#pragma unroll
+        for (int k = 0; k < MAXT; ++k)
+            if (mt(k) == 0)
+                st_frag(colb, lane, acc[k]);
+        __syncwarp();
         factor_diag(0);
         __syncthreads();
 #pragma unroll 1
         for (int kb = 0; kb < CT; ++kb) {
             const int par = kb & 1;
             double *col = colb + par * TT * kTileElems;
-            // sub-diagonal tiles of column kb: X <- X L_kk^{-T} = X (L_kk^{-1})'
+            // sub-diagonal tiles of column kb: X <- X L_kk^{-T} = X (L_kk^{-1})';
+            // the owner of (kb, kb) takes L_kk back into its register tile
             {
                 const Frag linv = ld_frag(linvb + par * kTileElems, lane);
+#pragma unroll
+                for (int k = 0; k < MAXT; ++k)
+                    if (mt(k) == ((kb << 8) | kb))
+                        acc[k] = ld_frag(col + kb * kTileElems, lane);
 #pragma unroll
                 for (int k = 0; k < MAXT; ++k)
                     if (mtj(k) == kb && mti(k) > kb) {
@@ -349,12 +354,15 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
             __syncthreads(); // column kb published
             // look-ahead: (kb+1, kb+1) first, then factor it
             if (kb + 1 < CT) {
+                const int pk = ((kb + 1) << 8) | (kb + 1);
 #pragma unroll
                 for (int k = 0; k < MAXT; ++k)
-                    if (mti(k) == kb + 1 && mtj(k) == kb + 1) {
+                    if (mt(k) == pk) {
                         const Frag li = ld_frag(col + (kb + 1) * kTileElems, lane);
                         tile_gemm_nt_sub(acc[k], li, li);
+                        st_frag(colb + (((kb + 1) & 1) * TT + kb + 1) * kTileElems, lane, acc[k]);
                     }
+                __syncwarp();
                 factor_diag(kb + 1);
             }
             // trailing update of my other tiles: C(ti, tj) -= L(ti, kb) L(tj, kb)'
@@ -460,6 +468,8 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         atomicMin(a.fail + b, my_fail);
 #undef mti
 #undef mtj
+#undef mt
+#undef mtt
 }
 
 namespace {
@@ -472,6 +482,13 @@ template <int NU, int NX, int NW> bool launch_c(const Geo &g, cudaStream_t st, c
     if (!attr) {
         cudaFuncSetAttribute(riccati_cta_kernel<NU, NX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
+        unsigned short h[1024];
+        for (int t = 0, ti = 0; t < 1024; ++t) {
+            while ((ti + 1) * (ti + 2) / 2 <= t)
+                ++ti;
+            h[t] = (unsigned short)((ti << 8) | (t - ti * (ti + 1) / 2));
+        }
+        cudaMemcpyToSymbol(c_tij, h, sizeof h);
         attr = true;
     }
     riccati_cta_kernel<NU, NX, NW><<<g.batch * g.P, 32 * NW, smem, st>>>(ra);
