@@ -109,8 +109,9 @@ WsSizes ws_sizes(const Geo &g) {
     s.y = al(chains * g.n * g.nux);
     s.wl = al(chains * g.n * g.nx);
     s.trail = al(chains * g.NTT * kTileElems);
-    s.schur = al((size_t)g.batch * std::max<size_t>(SchurLayout::make(g.P, g.nx).total,
-                                                    schur_fused_doubles(g)));
+    s.schur = al((size_t)g.batch * std::max<size_t>(std::max<size_t>(SchurLayout::make(g.P, g.nx).total,
+                                                                      schur_fused_doubles(g)),
+                                                    schur_big_doubles(g)));
     s.lamc = al((size_t)g.batch * g.P * g.nx);
     s.fail = al((size_t)g.batch); // 8-byte keys
     s.consts = al(riccati_consts_doubles(g));
@@ -324,8 +325,8 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
     sa.phase = ra.phase ? ra.phase + 8 * (g.n + 1) + 8 : nullptr;
     {
         Timed t(ctx, 1);
-        if (launch_schur_fused(g, ctx->stream, sa)) { // one fused kernel per batch
-            t.kernels = 1;
+        if (launch_schur_fused(g, ctx->stream, sa) || launch_schur_big(g, ctx->stream, sa)) {
+            t.kernels = 1; // one fused kernel per batch
         } else if (launch_schur_tiles(g, ctx->stream, sa)) { // DMMA-tile factorization
             t.kernels = 2 + SchurLayout::make(g.P, g.nx).levels + (do_solve ? 1 : 0);
             if (do_solve) {
@@ -397,7 +398,7 @@ int launch_solve(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &
     SchurArgs sa{g, p, ws.fac, ws.y, ws.trail, ws.schur, ws.lamc, sol.lam, ws.fail, 0, 1};
     {
         Timed t(ctx, 1);
-        if (!launch_schur_fused(g, ctx->stream, sa)) {
+        if (!launch_schur_fused(g, ctx->stream, sa) && !launch_schur_big(g, ctx->stream, sa)) {
             const int nw = schur_warps_solve(g);
             schur_cr_kernel<<<g.batch, 32 * nw, schur_smem_for(g, nw), ctx->stream>>>(sa);
         }

@@ -103,6 +103,9 @@ bool launch_schur_tiles(const Geo &g, cudaStream_t st, const SchurArgs &sa);
 bool schur_fused_ok(const Geo &g);
 bool launch_schur_fused(const Geo &g, cudaStream_t st, const SchurArgs &sa);
 size_t schur_fused_doubles(const Geo &g);
+// CTA-level Schur + CR for large tile-aligned nx (schur_big.cu); false if n/a
+bool launch_schur_big(const Geo &g, cudaStream_t st, const SchurArgs &sa);
+size_t schur_big_doubles(const Geo &g);
 // compile-time (nu, nx) warp-per-chain back substitution; false if n/a
 bool launch_backsub_warp(const Geo &g, cudaStream_t st, const BacksubArgs &ba);
 // forward substitution over a stored factor (kkt::solve with a new rhs)

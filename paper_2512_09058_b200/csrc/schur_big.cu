@@ -1,0 +1,342 @@
+// Schur complement + cyclic reduction (factor and solve) for LARGE,
+// tile-aligned nx (nx % 8 == 0, nx >= 32; BASELINE config 3: 64 x 64
+// blocks): one CTA per OCP instance, every block operation spread over the
+// CTA's warps (cta_tiles.cuh). Same algorithm and workspace semantics as the
+// register-tile fused kernel for small nx (schur_fused.cu):
+//   kkt_factor.cpp:163-178    T = L_Q^{-T}, Mbwd = T T', W = T LA'
+//   kkt_factor.cpp:194-212    assemble_schur
+//   block_tridiag.cpp:126-238 cr_level / cr_factor_base
+//   kkt_solve.cpp:137-182     Schur rhs, CRFactor::forward / backward
+// with explicit inverse factors Li = L^{-1} (so U, Y are DMMA GEMMs and the
+// CR solve is matrix-vector products) and the forward CR sweep fused into
+// the factor levels when the rhs is known (solve_problem).
+#include "cta_tiles.cuh"
+#include "kernels.h"
+
+#include <cstdlib>
+
+namespace cyqb {
+
+namespace {
+
+// Per-instance workspace, full XT x XT tile blocks (NF tiles):
+//   Tt[P]  L_Q^{-1} per column (T = Tt')          (persistent)
+//   Li[P-1], U[P-1], Y[P-1], Lb                    (persistent)
+//   D[P], Mb[P], K[P]                              (scratch, CR in place)
+//   S1, S2                                         (scratch blocks)
+struct SBLayout {
+    long long Tt, Li, U, Y, Lb, D, Mb, K, S1, S2, total;
+    int levels;
+    __host__ __device__ static SBLayout make(int P, int nx) {
+        SBLayout s;
+        const long long tf = 64LL * (nx / 8) * (nx / 8);
+        int lg = 0;
+        while ((1 << lg) < P)
+            ++lg;
+        s.levels = lg;
+        long long o = 0;
+        s.Tt = o; o += P * tf;
+        s.Li = o; o += (P - 1) * tf;
+        s.U = o; o += (P - 1) * tf;
+        s.Y = o; o += (P - 1) * tf;
+        s.Lb = o; o += tf;
+        s.D = o; o += P * tf;
+        s.Mb = o; o += P * tf;
+        s.K = o; o += P * tf;
+        s.S1 = o; o += tf;
+        s.S2 = o; o += tf;
+        s.total = o;
+        return s;
+    }
+};
+
+template <int XT, int NW>
+__device__ __forceinline__ void blk_zero(double *C, int warp, int lane) {
+    for (int t = warp; t < XT * XT; t += NW)
+        st_frag(C + t * kTileElems, lane, Frag{0.0, 0.0});
+}
+// C = A + sgn B over the lower tiles (B nullable)
+template <int XT, int NW>
+__device__ __forceinline__ void blk_axpy_lower(double *C, const double *A, const double *B, double sgn,
+                                               int warp, int lane) {
+    for (int o = warp; o < XT * (XT + 1) / 2; o += NW) {
+        int i = 0;
+        while ((i + 1) * (i + 2) / 2 <= o)
+            ++i;
+        const int t = i * XT + (o - i * (i + 1) / 2);
+        Frag f = ld_frag(A + t * kTileElems, lane);
+        if (B) {
+            const Frag h = ld_frag(B + t * kTileElems, lane);
+            f.a += sgn * h.a;
+            f.b += sgn * h.b;
+        }
+        st_frag(C + t * kTileElems, lane, f);
+    }
+}
+
+template <int NX, int NW>
+__global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
+    constexpr int XT = NX / 8, NF = XT * XT;
+    constexpr long long TF = 64LL * NF;
+    extern __shared__ __align__(16) double sm[];
+    const Geo &g = a.g;
+    const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int P = g.P, nu = g.nu, n = g.n, CT = g.CT;
+    const SBLayout Lo = SBLayout::make(P, NX);
+    double *ws = a.schur + (size_t)b * Lo.total;
+    double *Tt = ws + Lo.Tt, *D = ws + Lo.D, *Mb = ws + Lo.Mb, *K = ws + Lo.K, *S1 = ws + Lo.S1,
+           *S2 = ws + Lo.S2;
+    double *scr = sm;                       // NW x 64
+    double *xs = scr + NW * kTileElems;     // P x NX
+    double *bns = xs + (size_t)P * NX;      // P x NX
+    double *cu = bns + (size_t)P * NX;      // P/2 x NX
+    double *cy = cu + (size_t)(P / 2 + 1) * NX;
+    double *v1 = cy + (size_t)(P / 2 + 1) * NX, *v2 = v1 + NX; // NX each
+    const bool fwd_fused = a.do_factor && a.do_solve;
+    int fail = -1, fail_l = 0, fail_k = 0;
+
+    // ---- phase 1: per column T, Mbwd, K, Mfwd, bwd_neg ------------------
+    for (int c = 0; c < P; ++c) {
+        const size_t chain = (size_t)b * P + c;
+        const double *st = a.fac + (chain * n + (n - 1)) * g.NPT * kTileElems;
+        auto ftile = [&](int i, int j) { // stored pivot tile (i, j < CT)
+            return st + (i < CT ? tri_index(i, j) : CT * (CT + 1) / 2 + (i - CT) * CT + j) * kTileElems;
+        };
+        const int xt0 = nu / 8;
+        double *Tc = Tt + c * TF;
+        if (a.do_factor) {
+            // L_Q -> S1 (lower), LA -> S2 (full), -Mfwd -> D[c] (lower)
+            const double *tr = a.trail + chain * g.NTT * kTileElems;
+            for (int t = warp; t < NF; t += NW) {
+                const int i = t / XT, j = t % XT;
+                st_frag(S2 + t * kTileElems, lane, ld_frag_g(ftile(CT + i, xt0 + j), lane));
+                if (j <= i) {
+                    st_frag(S1 + t * kTileElems, lane, ld_frag_g(ftile(xt0 + i, xt0 + j), lane));
+                    Frag m = ld_frag_g(tr + tri_index(i, j) * kTileElems, lane);
+                    st_frag(D + c * TF + t * kTileElems, lane, Frag{-m.a, -m.b});
+                }
+            }
+            __syncthreads();
+            ctat::cta_trtri<XT, NW>(S1, Tc, scr, warp, lane); // Tt = L_Q^{-1}
+            // Mbwd = T T' (T(i,k) = Tt(k,i)', upper) ; K[c-1] = -LA T'
+            ctat::cta_gemm<XT, NW, true, true, ctat::kGeMaxIJ, true>(Mb + c * TF, nullptr, 1.0, Tc, Tc, warp, lane);
+            double *Kc = K + (size_t)((c + P - 1) % P) * TF;
+            if (c > 0)
+                ctat::cta_gemm<XT, NW, false, true, ctat::kGeJ, false>(Kc, nullptr, -1.0, S2, Tc, warp, lane);
+            else
+                blk_zero<XT, NW>(Kc, warp, lane);
+        }
+        if (a.do_solve) { // bwd_neg_c = T x'_{n-1} = Tt' x'
+            const double *yv = a.y + (chain * n + (n - 1)) * g.nux + nu;
+            for (int k = tid; k < NX; k += 32 * NW)
+                v1[k] = __ldg(yv + k);
+            __syncthreads();
+            ctat::cta_matvec<XT, NW, true, true>(Tc, v1, bns + c * NX, 1.0, false, warp, lane);
+        }
+        __syncthreads();
+    }
+
+    // ---- Schur rhs b_i = fd[n i] - fwd_i + bwd_neg_{(i+1) % P} ------------
+    if (a.do_solve) {
+        ProbAcc pa{a.p, g, b};
+        for (int e = tid; e < P * NX; e += 32 * NW) {
+            const int i = e / NX, k = e % NX, jst = n * i;
+            double v = pa.fd(jst, k);
+            if (jst == 0 && a.p.fd == nullptr) {
+                double ax = 0.0;
+                for (int m = 0; m < NX; ++m)
+                    ax = fma(pa.A(0, k, m), __ldg(a.p.x_init + (size_t)b * NX + m), ax);
+                v -= ax;
+            }
+            const double *tr = a.trail + ((size_t)b * P + i) * g.NTT * kTileElems;
+            v += __ldg(tr + tri_index(XT, k / 8) * kTileElems + k % 8);
+            v += bns[((i + 1) % P) * NX + k];
+            xs[e] = v;
+        }
+        __syncthreads();
+    }
+
+    // ---- CR levels (in place in D / K, as schur_fused.cu) -----------------
+    if (a.do_factor) {
+        for (int l = 0, s = P; l < Lo.levels; ++l, s >>= 1) {
+            const int half = s / 2, hcy = l > 0 ? 1 << (l - 1) : 0;
+            const long long out0 = P - (P >> l);
+            auto assemble = [&](double *dst, int i) { // level-l diagonal block i -> dst
+                if (l == 0)
+                    blk_axpy_lower<XT, NW>(dst, D + i * TF, Mb + ((i + 1) % P) * TF, 1.0, warp, lane);
+                else
+                    blk_axpy_lower<XT, NW>(dst, D + (size_t)(i << l) * TF,
+                                           i > 0 ? D + (size_t)((i << l) - hcy) * TF : nullptr, -1.0,
+                                           warp, lane);
+            };
+            for (int mm = 0; mm < half; ++mm) {
+                const int k = 2 * mm + 1;
+                const bool has_y = k < s - 1, last = mm == half - 1;
+                double *Li = ws + Lo.Li + (out0 + mm) * TF, *U = ws + Lo.U + (out0 + mm) * TF;
+                double *Y = ws + Lo.Y + (out0 + mm) * TF;
+                const double *Kp = K + (size_t)((k - 1) << l) * TF, *Kk = K + (size_t)(k << l) * TF;
+                assemble(S1, k);
+                assemble(S2, 2 * mm); // the even block, used after the products
+                __syncthreads();
+                int f = -1;
+                ctat::cta_potrf_inv<XT, NW>(S1, Li, scr, NX, warp, lane, tid, f);
+                if (warp == 0 && f >= 0 && fail < 0) {
+                    fail = f;
+                    fail_l = l;
+                    fail_k = k;
+                }
+                // U = K_{k-1}' Li', Y = K_k Li' (Li lower: k-range <= j)
+                ctat::cta_gemm<XT, NW, true, false, ctat::kLeJ, false>(U, nullptr, 1.0, Kp, Li, warp, lane);
+                if (has_y)
+                    ctat::cta_gemm<XT, NW, false, false, ctat::kLeJ, false>(Y, nullptr, 1.0, Kk, Li, warp, lane);
+                else
+                    blk_zero<XT, NW>(Y, warp, lane);
+                __syncthreads();
+                if (fwd_fused) { // x_k <- Li x_k ; contributions U x_k, Y x_k
+                    double *xk = xs + (size_t)(k << l) * NX;
+                    ctat::cta_matvec<XT, NW, false, true>(Li, xk, v1, 1.0, false, warp, lane);
+                    __syncthreads();
+                    for (int e = tid; e < NX; e += 32 * NW)
+                        xk[e] = v1[e];
+                    __syncthreads();
+                    ctat::cta_matvec<XT, NW, false, false>(U, xk, cu + mm * NX, 1.0, false, warp, lane);
+                    ctat::cta_matvec<XT, NW, false, false>(Y, xk, cy + mm * NX, 1.0, false, warp, lane);
+                }
+                // M' = M_2mm - U U' -> D[2mm << l]; CY = Y Y' -> D[k << l]; K' = -Y U' -> K[2mm << l]
+                ctat::cta_gemm<XT, NW, false, false, ctat::kAll, true>(D + (size_t)((2 * mm) << l) * TF, S2, -1.0,
+                                                                      U, U, warp, lane);
+                ctat::cta_gemm<XT, NW, false, false, ctat::kAll, true>(D + (size_t)(k << l) * TF, nullptr, 1.0, Y,
+                                                                      Y, warp, lane);
+                if (!last)
+                    ctat::cta_gemm<XT, NW, false, false, ctat::kAll, false>(K + (size_t)((2 * mm) << l) * TF,
+                                                                           nullptr, -1.0, Y, U, warp, lane);
+                else
+                    blk_zero<XT, NW>(K + (size_t)((2 * mm) << l) * TF, warp, lane);
+                __syncthreads();
+            }
+            if (fwd_fused) { // x_{2mm} -= U_mm x_{2mm+1} + Y_{mm-1} x_{2mm-1}
+                for (int e = tid; e < half * NX; e += 32 * NW) {
+                    const int mm = e / NX, r = e % NX;
+                    double d = cu[e];
+                    if (mm > 0)
+                        d += cy[e - NX];
+                    xs[(size_t)((2 * mm) << l) * NX + r] -= d;
+                }
+                __syncthreads();
+            }
+        }
+        // cr_factor_base
+        if (Lo.levels == 0)
+            blk_axpy_lower<XT, NW>(S1, D, Mb, 1.0, warp, lane);
+        else
+            blk_axpy_lower<XT, NW>(S1, D, nullptr, 0.0, warp, lane);
+        __syncthreads();
+        int f = -1;
+        ctat::cta_potrf_inv<XT, NW>(S1, ws + Lo.Lb, scr, NX, warp, lane, tid, f);
+        if (warp == 0 && f >= 0 && fail < 0) {
+            fail = f;
+            fail_l = Lo.levels;
+            fail_k = 0;
+        }
+        __syncthreads();
+    }
+
+    // ---- CR solve over the stored factor, negate --------------------------
+    if (a.do_solve) {
+        if (!fwd_fused) {
+            for (int l = 0, s = P; l < Lo.levels; ++l, s >>= 1) {
+                const int half = s / 2, stride = P / s;
+                const long long o0 = P - (P >> l);
+                for (int mm = 0; mm < half; ++mm) {
+                    double *xk = xs + (size_t)(2 * mm + 1) * stride * NX;
+                    ctat::cta_matvec<XT, NW, false, true>(ws + Lo.Li + (o0 + mm) * TF, xk, v1, 1.0, false, warp,
+                                                         lane);
+                    __syncthreads();
+                    for (int e = tid; e < NX; e += 32 * NW)
+                        xk[e] = v1[e];
+                    __syncthreads();
+                }
+                for (int mm = 0; mm < half; ++mm) {
+                    double *xe = xs + (size_t)2 * mm * stride * NX;
+                    ctat::cta_matvec<XT, NW, false, false>(ws + Lo.U + (o0 + mm) * TF,
+                                                          xs + (size_t)(2 * mm + 1) * stride * NX, v1, 1.0, false,
+                                                          warp, lane);
+                    if (mm > 0)
+                        ctat::cta_matvec<XT, NW, false, false>(ws + Lo.Y + (o0 + mm - 1) * TF,
+                                                              xs + (size_t)(2 * mm - 1) * stride * NX, v1, 1.0,
+                                                              true, warp, lane);
+                    __syncthreads();
+                    for (int e = tid; e < NX; e += 32 * NW)
+                        xe[e] -= v1[e];
+                    __syncthreads();
+                }
+            }
+        }
+        // base: x_0 <- Lb^{-T} Lb^{-1} x_0
+        ctat::cta_matvec<XT, NW, false, true>(ws + Lo.Lb, xs, v1, 1.0, false, warp, lane);
+        __syncthreads();
+        ctat::cta_matvec<XT, NW, true, true>(ws + Lo.Lb, v1, xs, 1.0, false, warp, lane);
+        __syncthreads();
+        // CRFactor::backward
+        for (int l = Lo.levels - 1; l >= 0; --l) {
+            const int sl = P >> l, half = sl / 2, stride = P / sl;
+            const long long o0 = P - (P >> l);
+            for (int mm = 0; mm < half; ++mm) {
+                double *xo = xs + (size_t)(2 * mm + 1) * stride * NX;
+                ctat::cta_matvec<XT, NW, true, false>(ws + Lo.U + (o0 + mm) * TF,
+                                                     xs + (size_t)2 * mm * stride * NX, v1, 1.0, false, warp, lane);
+                if (2 * mm + 2 < sl)
+                    ctat::cta_matvec<XT, NW, true, false>(ws + Lo.Y + (o0 + mm) * TF,
+                                                         xs + (size_t)((2 * mm + 2) * stride % P) * NX, v1, 1.0,
+                                                         true, warp, lane);
+                __syncthreads();
+                for (int e = tid; e < NX; e += 32 * NW)
+                    v2[e] = xo[e] - v1[e];
+                __syncthreads();
+                ctat::cta_matvec<XT, NW, true, true>(ws + Lo.Li + (o0 + mm) * TF, v2, xo, 1.0, false, warp, lane);
+                __syncthreads();
+            }
+        }
+        for (int e = tid; e < P * NX; e += 32 * NW) {
+            const int i = e / NX, k = e % NX;
+            const double lam = -xs[e];
+            a.lamc[(size_t)b * P * NX + e] = lam;
+            if (a.lam_out && n * i < g.N)
+                a.lam_out[((size_t)b * g.N + n * i) * NX + k] = lam;
+        }
+    }
+    if (warp == 0 && lane == 0 && fail >= 0)
+        atomicMin(a.fail + b, fail_key(kKindCR, fail_l, fail_k, fail));
+}
+
+template <int NX> bool launch_sb(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
+    if (g.nx != NX)
+        return false;
+    constexpr int NW = 8;
+    const size_t smem = ((size_t)NW * kTileElems + (size_t)g.P * NX * 2 + (size_t)(g.P / 2 + 1) * NX * 2 +
+                         2 * NX) * sizeof(double);
+    if (smem > 200 * 1024)
+        return false;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(schur_big_kernel<NX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attr = true;
+    }
+    schur_big_kernel<NX, NW><<<g.batch, 32 * NW, smem, st>>>(sa);
+    return true;
+}
+
+} // namespace
+
+size_t schur_big_doubles(const Geo &g) {
+    return (g.nx % 8 == 0) ? (size_t)SBLayout::make(g.P, g.nx).total : 0;
+}
+
+bool launch_schur_big(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
+    if (getenv("CYQ_NO_SCHUR_BIG") || g.nu % 8 != 0)
+        return false;
+    return launch_sb<64>(g, st, sa) || launch_sb<32>(g, st, sa);
+}
+
+} // namespace cyqb
