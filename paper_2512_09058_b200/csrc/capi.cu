@@ -365,7 +365,7 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
         BacksubArgs ba{g, p, ws.fac, ws.y, ws.wl, ws.lamc, *sol};
         {
             Timed t(ctx, 2);
-            if (!launch_backsub_warp(g, ctx->stream, ba)) {
+            if (!launch_backsub_warp(g, ctx->stream, ba) && !launch_backsub_tile(g, ctx->stream, ba)) {
                 const int wpb = backsub_wpb(g);
                 backsub_kernel<<<(chains + wpb - 1) / wpb, 32 * wpb, backsub_smem_bytes(g),
                                  ctx->stream>>>(ba);
@@ -406,7 +406,7 @@ int launch_solve(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &
     CU(cudaGetLastError());
     {
         Timed t(ctx, 2);
-        if (!launch_backsub_warp(g, ctx->stream, ba)) {
+        if (!launch_backsub_warp(g, ctx->stream, ba) && !launch_backsub_tile(g, ctx->stream, ba)) {
             const int wpb = backsub_wpb(g);
             backsub_kernel<<<(chains + wpb - 1) / wpb, 32 * wpb, backsub_smem_bytes(g),
                              ctx->stream>>>(ba);

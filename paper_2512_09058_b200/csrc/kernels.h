@@ -108,6 +108,8 @@ bool launch_schur_big(const Geo &g, cudaStream_t st, const SchurArgs &sa);
 size_t schur_big_doubles(const Geo &g);
 // compile-time (nu, nx) warp-per-chain back substitution; false if n/a
 bool launch_backsub_warp(const Geo &g, cudaStream_t st, const BacksubArgs &ba);
+// warp-per-chain back substitution streaming tiles from global (tile-aligned large shapes)
+bool launch_backsub_tile(const Geo &g, cudaStream_t st, const BacksubArgs &ba);
 // forward substitution over a stored factor (kkt::solve with a new rhs)
 __global__ void forward_kernel(BacksubArgs a, double *y_out, double *wl_out, double *trail);
 __host__ __device__ size_t forward_smem_per_warp(const Geo &g);
