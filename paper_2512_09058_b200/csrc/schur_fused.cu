@@ -29,6 +29,8 @@
 #include "kernels.h"
 #include "tiles.cuh"
 
+#include <cooperative_groups.h>
+
 #include <cstdlib>
 
 namespace cyqb {
@@ -53,6 +55,17 @@ __device__ __forceinline__ Frag ld_frag_t(const double *tile, int lane) {
     return {tile[cq * 8 + rq], tile[(cq + 1) * 8 + rq]};
 }
 
+// workspace loads bypass L1 (ld.global.cg): blocks are rewritten in place by
+// other warps -- and, in the cluster variant, by other SMs -- between phases
+__device__ __forceinline__ Frag ldw(const double *tile, int lane) {
+    const double2 v = __ldcg(reinterpret_cast<const double2 *>(tile) + lane);
+    return {v.x, v.y};
+}
+__device__ __forceinline__ Frag ldw_t(const double *tile, int lane) {
+    const int rq = lane >> 2, cq = 2 * (lane & 3);
+    return {__ldcg(tile + cq * 8 + rq), __ldcg(tile + (cq + 1) * 8 + rq)};
+}
+
 __device__ __forceinline__ Frag fadd(Frag x, Frag y) { return {x.a + y.a, x.b + y.b}; }
 __device__ __forceinline__ Frag fsub(Frag x, Frag y) { return {x.a - y.a, x.b - y.b}; }
 
@@ -74,7 +87,7 @@ __device__ __forceinline__ void matvec(const double *M, const double *v, double 
         for (int j = 0; j < XT; ++j) {
             if (!FULL && j > i)
                 continue;
-            const Frag f = ld_frag(M + (FULL ? fidx(XT, i, j) : T(i, j)) * kTileElems, lane);
+            const Frag f = ldw(M + (FULL ? fidx(XT, i, j) : T(i, j)) * kTileElems, lane);
             acc = fma(f.a, v[8 * j + cq], acc);
             acc = fma(f.b, v[8 * j + cq + 1], acc);
         }
@@ -95,7 +108,7 @@ __device__ __forceinline__ void matvec_t(const double *M, const double *v, doubl
         for (int i = 0; i < XT; ++i) {
             if (!FULL && j > i)
                 continue;
-            const Frag f = ld_frag(M + (FULL ? fidx(XT, i, j) : T(i, j)) * kTileElems, lane);
+            const Frag f = ldw(M + (FULL ? fidx(XT, i, j) : T(i, j)) * kTileElems, lane);
             const double vi = v[8 * i + rq];
             a0 = fma(f.a, vi, a0);
             a1 = fma(f.b, vi, a1);
@@ -151,7 +164,7 @@ __device__ __forceinline__ void matvec_upper(const double *M, const double *v, d
         double acc = 0.0;
 #pragma unroll
         for (int j = i; j < XT; ++j) {
-            const Frag f = ld_frag(M + T(j, i) * kTileElems, lane);
+            const Frag f = ldw(M + T(j, i) * kTileElems, lane);
             acc = fma(f.a, v[8 * j + cq], acc);
             acc = fma(f.b, v[8 * j + cq + 1], acc);
         }
@@ -211,36 +224,56 @@ size_t schur_fused_doubles(const Geo &g) { return (size_t)SFLayout::make(g.P, g.
 namespace {
 
 template <int XP> __host__ __device__ constexpr size_t sf_smem_doubles(int NW, int NF, int P) {
-    return (size_t)NW * NF * kTileElems + 3 * (size_t)P * XP;
+    return (size_t)NW * NF * kTileElems + 2 * (size_t)P * XP;
 }
 
-template <int NX, int NW>
-__global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs a) {
+// CL > 1: one thread-block CLUSTER per instance (a single long horizon,
+// config 2): the tasks of every phase / CR level are spread over the CL * NW
+// warps of the cluster, phases are separated by cluster barriers (release /
+// acquire: the global workspace writes of one CTA are visible to the
+// others), and the solve vectors live in rank 0's shared memory, reached
+// through distributed shared memory.
+template <int NX, int NW, int CL>
+__global__ void __launch_bounds__(32 * NW, NW <= 4 ? 12 / NW : 1) schur_fused_kernel(SchurArgs a) {
     using F = SF<NX>;
     constexpr int XT = F::XT, NL = F::NL, NF = F::NF, XP = F::XP;
     constexpr long long TL = 64LL * NL, TF = 64LL * NF;
     extern __shared__ __align__(16) double sm[];
     const Geo &g = a.g;
-    const int b = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    namespace cg = cooperative_groups;
+    const int crank = CL > 1 ? (int)cg::this_cluster().block_rank() : 0;
+    const int b = blockIdx.x / CL, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int vwarp = crank * NW + warp, vtid = crank * 32 * NW + threadIdx.x;
+    constexpr int VNW = CL * NW, VNTH = CL * 32 * NW;
+    auto csync = [&]() {
+        if (CL > 1)
+            cg::this_cluster().sync();
+        else
+            __syncthreads();
+    };
     const int rq = lane >> 2, cq = 2 * (lane & 3), q2 = lane & 3;
     const int P = g.P, nu = g.nu, n = g.n, top = 8 * g.CT;
     const SFLayout Lo = SFLayout::make(P, NX);
     double *ws = a.schur + (size_t)b * Lo.total;
     double *scr = sm + (size_t)warp * NF * kTileElems; // per-warp transpose scratch
     double *xs = sm + (size_t)NW * NF * kTileElems;    // P x XP: CR solve vector
+    if (CL > 1) // rank 0's copy (DSMEM)
+        xs = cg::this_cluster().map_shared_rank(xs, 0);
+    // bwd_neg is dead once the Schur rhs is assembled: it shares its buffer
+    // with the even-block contributions U x_k | Y x_k of the CR levels
     double *bns = xs + (size_t)P * XP;                 // P x XP: bwd_neg per column
-    double *cu = bns + (size_t)P * XP;                 // P/2 x XP each: even-block
+    double *cu = bns;                                  // P/2 x XP each: even-block
     double *cy = cu + (size_t)(P / 2) * XP;            //   contributions U x_k, Y x_k
     double *D = ws + Lo.D, *Mb = ws + Lo.Mb, *K = ws + Lo.K;
     unsigned long long my_fail = ~0ull;
     const bool fwd_fused = a.do_factor && a.do_solve; // CR forward inside the factor levels
-    long long *ph = (a.phase && b == 0 && threadIdx.x == 0) ? a.phase : nullptr;
+    long long *ph = (a.phase && b == 0 && crank == 0 && threadIdx.x == 0) ? a.phase : nullptr;
     int php = 0;
     if (ph) ph[php++] = clock64();
 
     // ---- phase 1: per-column T, Mbwd, K, Mfwd and bwd_neg ----------------
     // (kkt_factor.cpp:163-178, 194-212; kkt_solve.cpp:128-131)
-    for (int c = warp; c < P; c += NW) {
+    for (int c = vwarp; c < P; c += VNW) {
         const size_t chain = (size_t)b * P + c;
         const double *yv = a.y + (chain * n + (n - 1)) * g.nux + nu;
         if (a.do_factor) {
@@ -349,14 +382,14 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs
             __syncwarp();
         }
     }
-    __syncthreads();
+    csync();
     if (ph) ph[php++] = clock64();
 
     // ---- Schur rhs b_i = fd[n i] - fwd_i + bwd_neg_{(i+1) % P} -----------
     // (kkt_solve.cpp:137-160); fd[0] of EqRhs::of_problem carries -A_0 x_init
     if (a.do_solve) {
         ProbAcc pa{a.p, g, b};
-        for (int e = threadIdx.x; e < P * XP; e += blockDim.x) {
+        for (int e = vtid; e < P * XP; e += VNTH) {
             const int i = e / XP, k = e % XP;
             double v = 0.0;
             if (k < NX) {
@@ -375,7 +408,7 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs
             }
             xs[e] = v;
         }
-        __syncthreads();
+        csync();
     }
 
     // ---- phase 2: CR levels (block_tridiag.cpp:126-238), in place ---------
@@ -389,14 +422,14 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs
             const int hcy = l > 0 ? 1 << (l - 1) : 0;
             auto m_tile = [&](int i, int ti, int tj) -> Frag {
                 if (l == 0)
-                    return fadd(ld_frag(D + i * TL + T(ti, tj) * kTileElems, lane),
-                                ld_frag(Mb + ((i + 1) % P) * TL + T(ti, tj) * kTileElems, lane));
-                Frag f = ld_frag(D + (i << l) * TL + T(ti, tj) * kTileElems, lane);
+                    return fadd(ldw(D + i * TL + T(ti, tj) * kTileElems, lane),
+                                ldw(Mb + ((i + 1) % P) * TL + T(ti, tj) * kTileElems, lane));
+                Frag f = ldw(D + (i << l) * TL + T(ti, tj) * kTileElems, lane);
                 if (i > 0)
-                    f = fsub(f, ld_frag(D + ((i << l) - hcy) * TL + T(ti, tj) * kTileElems, lane));
+                    f = fsub(f, ldw(D + ((i << l) - hcy) * TL + T(ti, tj) * kTileElems, lane));
                 return f;
             };
-            for (int mm = warp; mm < half; mm += NW) {
+            for (int mm = vwarp; mm < half; mm += VNW) {
                 const int k = 2 * mm + 1;
                 const bool has_y = k < s - 1;
                 const double *Kp = K + ((k - 1) << l) * TF, *Kk = K + (k << l) * TF;
@@ -438,8 +471,8 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs
                     Frag kp[XT], kk[XT];
 #pragma unroll
                     for (int t = 0; t < XT; ++t) {
-                        kp[t] = ld_frag_t(Kp + fidx(XT, t, i) * kTileElems, lane); // (K_{k-1}')(i, t)
-                        kk[t] = has_y ? ld_frag(Kk + fidx(XT, i, t) * kTileElems, lane) : Frag{0.0, 0.0};
+                        kp[t] = ldw_t(Kp + fidx(XT, t, i) * kTileElems, lane); // (K_{k-1}')(i, t)
+                        kk[t] = has_y ? ldw(Kk + fidx(XT, i, t) * kTileElems, lane) : Frag{0.0, 0.0};
                     }
 #pragma unroll
                     for (int j = 0; j < XT; ++j) {
@@ -497,30 +530,30 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs
                         st_frag(K2o + fidx(XT, i, j) * kTileElems, lane, yu);
                     }
             }
-            __syncthreads();
+            csync();
             if (fwd_fused) { // x_{2mm} -= U_mm x_{2mm+1} + Y_{mm-1} x_{2mm-1}
-                for (int e = threadIdx.x; e < half * XP; e += blockDim.x) {
+                for (int e = vtid; e < half * XP; e += VNTH) {
                     const int mm = e / XP, r = e % XP;
                     double d = cu[e];
                     if (mm > 0)
                         d += cy[e - XP];
                     xs[(size_t)((2 * mm) << l) * XP + r] -= d;
                 }
-                __syncthreads();
+                csync();
             }
             if (ph) ph[php++] = clock64();
         }
         // ---- cr_factor_base (block_tridiag.cpp:173-197) --------------------
-        if (warp == 0) {
+        if (vwarp == 0) {
             Frag Lt[NL];
 #pragma unroll
             for (int i = 0; i < XT; ++i)
 #pragma unroll
                 for (int j = 0; j <= i; ++j)
                     Lt[T(i, j)] = Lo.levels == 0
-                                      ? fadd(ld_frag(D + T(i, j) * kTileElems, lane),
-                                             ld_frag(Mb + T(i, j) * kTileElems, lane))
-                                      : ld_frag(D + T(i, j) * kTileElems, lane);
+                                      ? fadd(ldw(D + T(i, j) * kTileElems, lane),
+                                             ldw(Mb + T(i, j) * kTileElems, lane))
+                                      : ldw(D + T(i, j) * kTileElems, lane);
             const double dfloor = 1e-14 * tiles::diag_absmax<XT>(Lt, NX, lane);
             int pf = -1;
             Frag Li[NL];
@@ -553,7 +586,7 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs
                     }
             }
         }
-        __syncthreads();
+        csync();
         if (ph) ph[php++] = clock64();
     }
 
@@ -564,7 +597,7 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs
             for (int l = 0, s = P; l < Lo.levels; ++l, s >>= 1) {
                 const int half = s / 2, stride = P / s;
                 const long long o0 = P - (P >> l);
-                for (int mm = warp; mm < half; mm += NW) { // x_k <- L^{-1} x_k
+                for (int mm = vwarp; mm < half; mm += VNW) { // x_k <- L^{-1} x_k
                     double *xk = xs + (size_t)(2 * mm + 1) * stride * XP;
                     double o[XT];
                     matvec<XT, false>(ws + Lo.Li + (o0 + mm) * TL, xk, o, lane);
@@ -574,8 +607,8 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs
                         if (q2 == 0)
                             xk[8 * i + rq] = o[i];
                 }
-                __syncthreads();
-                for (int mm = warp; mm < half; mm += NW) { // x_e -= U x_k + Y_prev x_k'
+                csync();
+                for (int mm = vwarp; mm < half; mm += VNW) { // x_e -= U x_k + Y_prev x_k'
                     double *xe = xs + (size_t)2 * mm * stride * XP;
                     double o[XT], o2[XT];
                     matvec<XT, true>(ws + Lo.U + (o0 + mm) * TF, xs + (size_t)(2 * mm + 1) * stride * XP,
@@ -589,9 +622,9 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs
                         if (q2 == 0)
                             xe[8 * i + rq] -= mm > 0 ? o[i] + o2[i] : o[i];
                 }
-                __syncthreads();
+                csync();
             }
-            if (warp == 0) { // base: x_0 <- L_b^{-T} L_b^{-1} x_0
+            if (vwarp == 0) { // base: x_0 <- L_b^{-T} L_b^{-1} x_0
                 double o[XT], o2[XT][2];
                 matvec<XT, false>(ws + Lo.Lb, xs, o, lane);
                 __syncwarp();
@@ -609,14 +642,14 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs
                         xs[8 * j + cq + 1] = o2[j][1];
                     }
             }
-            __syncthreads();
+            csync();
         }
         if (ph) ph[php++] = clock64();
         // CRFactor::backward (block_tridiag.cpp:298-333)
         for (int l = Lo.levels - 1; l >= 0; --l) {
             const int sl = P >> l, half = sl / 2, stride = P / sl;
             const long long o0 = P - (P >> l);
-            for (int mm = warp; mm < half; mm += NW) {
+            for (int mm = vwarp; mm < half; mm += VNW) {
                 double *xo = xs + (size_t)(2 * mm + 1) * stride * XP;
                 double t1[XT][2], t2[XT][2], t3[XT][2];
                 const bool has_y = 2 * mm + 2 < sl;
@@ -642,10 +675,10 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs
                         xo[8 * j + cq + 1] = t3[j][1];
                     }
             }
-            __syncthreads();
+            csync();
         }
         if (ph) ph[php++] = clock64();
-        for (int e = threadIdx.x; e < P * NX; e += blockDim.x) {
+        for (int e = vtid; e < P * NX; e += VNTH) {
             const int i = e / NX, k = e % NX;
             const double lam = -xs[i * XP + k];
             a.lamc[(size_t)b * P * NX + e] = lam;
@@ -661,32 +694,52 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) schur_fused_kernel(SchurArgs
         ph[php++] = clock64();
         ph[31] = php;
     }
+    if (CL > 1)
+        cg::this_cluster().sync();
 }
 
-template <int NX, int NW> bool launch_sfw(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
+template <int NX, int NW, int CL> bool launch_sfw(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
     const size_t smem = sf_smem_doubles<SF<NX>::XP>(NW, SF<NX>::NF, g.P) * sizeof(double);
-    if (smem > 200 * 1024)
+    if (smem > 220 * 1024)
         return false;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(schur_fused_kernel<NX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
+        cudaFuncSetAttribute(schur_fused_kernel<NX, NW, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             220 * 1024);
         attr = true;
     }
-    schur_fused_kernel<NX, NW><<<g.batch, 32 * NW, smem, st>>>(sa);
-    return true;
+    if (CL == 1) {
+        schur_fused_kernel<NX, NW, CL><<<g.batch, 32 * NW, smem, st>>>(sa);
+        return true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g.batch * CL);
+    cfg.blockDim = dim3(32 * NW);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, schur_fused_kernel<NX, NW, CL>, sa) == cudaSuccess;
 }
 
-// 4 warps per instance when the batch fills the GPU with CTAs; a wide CTA
-// (the level's blocks spread over 8-16 warps) for a few long-horizon
-// instances (config 2: one instance, P = 256)
+// 4 warps per instance when the batch fills the GPU with CTAs; for a few
+// long-horizon instances (config 2: one instance, P = 256) a cluster of 8
+// wide CTAs per instance, so a CR level's eliminations run in one round
 template <int NX> bool launch_sf(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
     if (g.nx != NX)
         return false;
     constexpr int WIDE = NX > 16 ? 8 : 16;
     if (g.batch >= 64 || g.P <= 8)
-        return launch_sfw<NX, 4>(g, st, sa);
-    return launch_sfw<NX, WIDE>(g, st, sa);
+        return launch_sfw<NX, 4, 1>(g, st, sa);
+    if (g.P >= 64 && g.batch * 8 <= 148 && !getenv("CYQ_NO_SCHUR_CLUSTER"))
+        if (launch_sfw<NX, WIDE, 8>(g, st, sa))
+            return true;
+    return launch_sfw<NX, WIDE, 1>(g, st, sa);
 }
 
 } // namespace

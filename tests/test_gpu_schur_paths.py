@@ -102,3 +102,28 @@ def test_schur_paths_bitwise_deterministic(schur_mode):
     b = kkt.solve_problem(p, kkt.FactorOptions(P=8))
     for k in ("u", "x", "lam"):
         assert np.array_equal(getattr(a, k), getattr(b, k))
+
+
+@pytest.mark.parametrize("P", [64, 256, 512])
+def test_cluster_schur_single_long_horizon(P):
+    # one instance: the CR tree runs on a cluster of 8 CTAs (DSMEM solve
+    # vectors, cluster barriers); must match the single-CTA kernel and the
+    # C oracle
+    N = 16 * P
+    p = synth.generate(2, seed=31, batch=1, N=N)
+    os.environ.pop("CYQ_NO_SCHUR_CLUSTER", None)
+    s_cl = kkt.solve_problem(p, kkt.FactorOptions(P=P))
+    os.environ["CYQ_NO_SCHUR_CLUSTER"] = "1"
+    try:
+        s_one = kkt.solve_problem(p, kkt.FactorOptions(P=P))
+    finally:
+        os.environ.pop("CYQ_NO_SCHUR_CLUSTER", None)
+    assert rel_error(s_cl, s_one).max() <= 1e-12
+    ref, rc, _ = Oracle().solve_problem(p, P)
+    assert rc == 0
+    assert rel_error(s_cl, ref).max() <= REL_TOL
+    assert kkt_residual(p, EqRhsBatch.of_problem(p), s_cl).max() <= RES_TOL
+    # kkt::solve over the stored factor (solve-only branch on the cluster)
+    f = kkt.factor(p, kkt.FactorOptions(P=P))
+    s2 = kkt.solve(f, p, EqRhsBatch.of_problem(p))
+    assert rel_error(s2, s_cl).max() <= 1e-13
