@@ -256,14 +256,18 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 12 / NW : 1) schur_fused_ke
     const SFLayout Lo = SFLayout::make(P, NX);
     double *ws = a.schur + (size_t)b * Lo.total;
     double *scr = sm + (size_t)warp * NF * kTileElems; // per-warp transpose scratch
-    double *xs = sm + (size_t)NW * NF * kTileElems;    // P x XP: CR solve vector
-    if (CL > 1) // rank 0's copy (DSMEM)
-        xs = cg::this_cluster().map_shared_rank(xs, 0);
-    // bwd_neg is dead once the Schur rhs is assembled: it shares its buffer
-    // with the even-block contributions U x_k | Y x_k of the CR levels
-    double *bns = xs + (size_t)P * XP;                 // P x XP: bwd_neg per column
-    double *cu = bns;                                  // P/2 x XP each: even-block
-    double *cy = cu + (size_t)(P / 2) * XP;            //   contributions U x_k, Y x_k
+    // solve vectors: xs (P x XP) and bwd_neg (P x XP), the latter dead once
+    // the Schur rhs is assembled and reused for the even-block contributions
+    // U x_k | Y x_k of the CR levels; in a cluster xs lives in rank 0's and
+    // bwd_neg in rank 1's shared memory (DSMEM)
+    double *vecs = sm + (size_t)NW * NF * kTileElems;
+    double *xs = vecs, *bns = vecs + (size_t)P * XP;
+    if (CL > 1) {
+        xs = cg::this_cluster().map_shared_rank(vecs, 0);
+        bns = cg::this_cluster().map_shared_rank(vecs, 1);
+    }
+    double *cu = bns;                                  // P/2 x XP each
+    double *cy = cu + (size_t)(P / 2) * XP;
     double *D = ws + Lo.D, *Mb = ws + Lo.Mb, *K = ws + Lo.K;
     unsigned long long my_fail = ~0ull;
     const bool fwd_fused = a.do_factor && a.do_solve; // CR forward inside the factor levels
@@ -699,7 +703,8 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 12 / NW : 1) schur_fused_ke
 }
 
 template <int NX, int NW, int CL> bool launch_sfw(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
-    const size_t smem = sf_smem_doubles<SF<NX>::XP>(NW, SF<NX>::NF, g.P) * sizeof(double);
+    const size_t smem = (sf_smem_doubles<SF<NX>::XP>(NW, SF<NX>::NF, g.P) -
+                         (CL > 1 ? (size_t)g.P * SF<NX>::XP : 0)) * sizeof(double);
     if (smem > 220 * 1024)
         return false;
     static bool attr = false;
