@@ -309,7 +309,10 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
         // (CYQ_RICCATI=g, and every shape without a specialisation)
         static const char *sel = getenv("CYQ_RICCATI");
         const bool want_c2 = sel && sel[0] == 'c', want_gen = sel && sel[0] == 'g';
+        const bool want_pc = sel && sel[0] == 'p';
         bool done = false;
+        if (!want_gen && want_pc)
+            done = launch_riccati_pc(g, ctx->stream, ra);
         if (!want_gen && want_c2)
             done = launch_riccati_cta2(g, ctx->stream, ra);
         if (!want_gen && !done)
@@ -322,7 +325,7 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
     CU(cudaGetLastError());
     SchurArgs sa{g, p, ws.fac, ws.y, ws.trail, ws.schur, ws.lamc,
                  sol ? sol->lam : nullptr, ws.fail, 1, do_solve ? 1 : 0};
-    sa.phase = ra.phase ? ra.phase + 8 * (g.n + 1) + 8 : nullptr;
+    sa.phase = ra.phase ? ra.phase + 16 * (g.n + 1) + 8 : nullptr;
     {
         Timed t(ctx, 1);
         if (launch_schur_fused(g, ctx->stream, sa) || launch_schur_big(g, ctx->stream, sa)) {
@@ -340,7 +343,22 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
         }
     }
     CU(cudaGetLastError());
-    if (ra.phase) { // dump chain 0's phase clocks (profiling aid)
+    if (ra.phase && getenv("CYQ_PC_PROF")) { // producer/consumer kernel: raw stamps
+        std::vector<long long> h(16 * g.n);
+        CU(cudaMemcpyAsync(h.data(), ra.phase, h.size() * sizeof(long long), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        const long long t0 = h[0];
+        for (int s = 0; s < g.n; ++s) {
+            fprintf(stderr, "pc s=%d P:", s);
+            for (int k = 0; k < 8; ++k)
+                fprintf(stderr, " %lld", h[s * 16 + k] ? h[s * 16 + k] - t0 : -1);
+            fprintf(stderr, " | C:");
+            for (int k = 8; k < 15; ++k)
+                fprintf(stderr, " %lld", h[s * 16 + k] ? h[s * 16 + k] - t0 : -1);
+            fprintf(stderr, "\n");
+        }
+    } else if (ra.phase) { // dump chain 0's phase clocks (profiling aid)
         std::vector<long long> h(8 * (g.n + 1));
         CU(cudaMemcpyAsync(h.data(), ra.phase, h.size() * sizeof(long long),
                            cudaMemcpyDeviceToHost, ctx->stream));

@@ -96,6 +96,8 @@ bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
 bool launch_riccati_cta2(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
 // CTA-per-chain kernel for large tile-aligned panels (riccati_cta.cu); false if n/a
 bool launch_riccati_cta(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
+// producer/consumer two-warp-per-chain kernel (riccati_pc.cu); false if n/a
+bool launch_riccati_pc(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
 // tile-based Schur assembly + CR factorization (compile-time nx); false if n/a
 bool launch_schur_tiles(const Geo &g, cudaStream_t st, const SchurArgs &sa);
 // fused Schur + CR factor (+ solve) kernel, one CTA per instance (schur_fused.cu);

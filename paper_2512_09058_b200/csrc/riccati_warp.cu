@@ -28,6 +28,7 @@
 #include "kernels.h"
 
 #include "riccati_common.cuh"
+#include "riccati_stage.cuh"
 
 #include <cstdlib>
 #include <type_traits>
@@ -38,29 +39,9 @@ using namespace cyqb::ric;
 
 namespace {
 
-template <int NU, int NX> struct WS {
-    using S = Shp<NU, NX>;
-    static constexpr int NUX = S::NUX, CT = S::CT, BT = S::BT, TT = S::TT, NT = S::NT;
-    static constexpr int TOP = S::TOP, RHS = S::RHS, RT = RHS / 8, RR = RHS % 8;
-    static constexpr int XT0 = S::XT0, NXT = S::NXT; // panel tile columns holding x columns
-    static constexpr int NXF = NX / 8, REM = NX % 8;
-    static constexpr bool HALF = REM > 0 && REM <= 4; // remainder on even positions only
-    static constexpr int NXC = (NX + 7) / 8;           // compact W tile columns
-    static constexpr int KQ = (NX + 3) / 4;            // V k-steps over x rows
-    static constexpr int NXR = 4 * KQ;                 // padded x rows (LQ, BA)
-    static constexpr int PW = 8 * CT;                  // padded panel width
-    static constexpr int NIMG = CT * (CT + 1) / 2;     // image tiles
-    // compact position of x-column kk / x-column at position p (-1 = none)
-    __host__ __device__ static constexpr int pos(int kk) {
-        return kk < 8 * NXF ? kk : 8 * NXF + (HALF ? 2 : 1) * (kk - 8 * NXF);
-    }
-    __host__ __device__ static constexpr int col_of(int p) {
-        return p < 8 * NXF ? p
-                           : (HALF ? ((((p - 8 * NXF) & 1) == 0 && (p - 8 * NXF) / 2 < REM)
-                                          ? 8 * NXF + (p - 8 * NXF) / 2
-                                          : -1)
-                                   : ((p - 8 * NXF) < REM ? p : -1));
-    }
+template <int NU, int NX> struct WS : PanelShape<NU, NX> {
+    using P_ = PanelShape<NU, NX>;
+    static constexpr int TT = P_::TT, NXC = P_::NXC, NXR = P_::NXR, NIMG = P_::NIMG, PW = P_::PW;
     // per-warp shared memory (doubles); every offset is even (16-byte aligned)
     static constexpr int O_W = 0;
     static constexpr int O_LQ = O_W + TT * NXC * kTileElems;
@@ -74,125 +55,6 @@ template <int NU, int NX> struct WS {
     static constexpr int SMEM = O_SCR + kTileElems;
     static_assert((O_LQ | O_IMG | O_IMR | O_S | O_BA | O_F | O_RU0 | O_SCR | SMEM) % 2 == 0, "align");
 };
-
-// %laneid through a volatile asm: lane-dependent addresses derived from it
-// are recomputed where used instead of being hoisted out of the stage loop
-// (and spilled -- the long-scoreboard stalls of a first version)
-__device__ __forceinline__ int lane_v() {
-    int l;
-    asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
-    return l;
-}
-
-__device__ __forceinline__ bool aligned16(const void *p) {
-    return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
-}
-
-// H_s: R -> panel (r, c), Q -> panel (NU + r, NU + c) of the tile image
-// (lower tiles only), S raw, [r; q] -> imr. Padding stages get R = Q = I,
-// S = 0, r = q = 0 (pad_problem, kkt_factor.cpp:27-47).
-template <int NU, int NX>
-__device__ __forceinline__ void stage_H(const Geo &g, const ProbView &p, int b, int j, int xi,
-                                        double *base, int) {
-    using W = WS<NU, NX>;
-    using S = Shp<NU, NX>;
-    const int N = g.N;
-    const int lane = lane_v();
-    double *img = base + W::O_IMG;
-    const bool in = j < N, qin = xi <= N;
-    auto at = [&](int r, int c) { return img + S::T(r / 8, c / 8) * kTileElems + (r % 8) * 8 + c % 8; };
-    const double *Rs = in ? p.R + ((size_t)b * N + j) * NU * NU : nullptr;
-    const double *Qs = qin ? p.Q + ((size_t)b * (N + 1) + xi) * NX * NX : nullptr;
-    // R
-    if (Rs && (NU % 2 == 0) && aligned16(Rs)) {
-#pragma unroll
-        for (int e = 2 * lane; e < NU * NU; e += 64) {
-            const int r = e / NU, c = e % NU;
-            if (c / 8 <= r / 8)
-                cp16(at(r, c), Rs + e);
-        }
-    } else {
-#pragma unroll
-        for (int e = lane; e < NU * NU; e += 32) {
-            const int r = e / NU, c = e % NU;
-            if (c / 8 <= r / 8) {
-                if (Rs)
-                    cp8(at(r, c), Rs + e);
-                else
-                    *at(r, c) = r == c ? 1.0 : 0.0;
-            }
-        }
-    }
-    // Q
-    if (Qs && (NU % 2 == 0) && (NX % 2 == 0) && aligned16(Qs)) {
-#pragma unroll
-        for (int e = 2 * lane; e < NX * NX; e += 64) {
-            const int r = NU + e / NX, c = NU + e % NX;
-            if (c / 8 <= r / 8)
-                cp16(at(r, c), Qs + e);
-        }
-    } else {
-#pragma unroll
-        for (int e = lane; e < NX * NX; e += 32) {
-            const int r = NU + e / NX, c = NU + e % NX;
-            if (c / 8 <= r / 8) {
-                if (Qs)
-                    cp8(at(r, c), Qs + e);
-                else
-                    *at(r, c) = r == c ? 1.0 : 0.0;
-            }
-        }
-    }
-    wcopy<NU * NX, 0>(base + W::O_S, in ? p.S + ((size_t)b * N + j) * NU * NX : nullptr, lane);
-    const double *rs = p.ru ? p.ru : p.r;
-    const double *qs = p.qx ? p.qx : p.q;
-    wcopy<NU, 0>(base + W::O_IMR, in ? rs + ((size_t)b * N + j) * NU : nullptr, lane);
-    wcopy<NX, 0>(base + W::O_IMR + NU, qin ? qs + ((size_t)b * (N + 1) + xi) * NX : nullptr, lane);
-}
-
-// BA_j = [B A] -> rows of the padded block (A omitted for j = 0, zero for
-// padding stages), f -> vector
-template <int NU, int NX>
-__device__ __forceinline__ void stage_BA(const Geo &g, const ProbView &p, int b, int j, double *base,
-                                         int) {
-    using W = WS<NU, NX>;
-    const int N = g.N;
-    const int lane = lane_v();
-    double *ba = base + W::O_BA;
-    const bool in = j < N;
-    const double *Bs = in ? p.B + ((size_t)b * N + j) * NX * NU : nullptr;
-    const double *As = (in && j != 0) ? p.A + ((size_t)b * N + j) * NX * NX : nullptr;
-    if (Bs && NU % 2 == 0 && aligned16(Bs)) {
-#pragma unroll
-        for (int e = 2 * lane; e < NX * NU; e += 64)
-            cp16(ba + (e / NU) * W::PW + e % NU, Bs + e);
-    } else {
-#pragma unroll
-        for (int e = lane; e < NX * NU; e += 32) {
-            double *d = ba + (e / NU) * W::PW + e % NU;
-            if (Bs)
-                cp8(d, Bs + e);
-            else
-                *d = 0.0;
-        }
-    }
-    if (As && NU % 2 == 0 && NX % 2 == 0 && aligned16(As)) {
-#pragma unroll
-        for (int e = 2 * lane; e < NX * NX; e += 64)
-            cp16(ba + (e / NX) * W::PW + NU + e % NX, As + e);
-    } else {
-#pragma unroll
-        for (int e = lane; e < NX * NX; e += 32) {
-            double *d = ba + (e / NX) * W::PW + NU + e % NX;
-            if (As)
-                cp8(d, As + e);
-            else
-                *d = 0.0;
-        }
-    }
-    const double *fs = p.fd ? p.fd : p.f;
-    wcopy<NX, 0>(base + W::O_F, in ? fs + ((size_t)b * N + j) * NX : nullptr, lane);
-}
 
 } // namespace
 
@@ -231,8 +93,8 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
     // prologue: H_0, BA_0 and the x_init term of ru[0]
     {
         const int j0 = g.stage_of(c, 0);
-        stage_H<NU, NX>(g, a.p, b, j0, g.x_index_of(c, 0), base, lane);
-        stage_BA<NU, NX>(g, a.p, b, j0, base, lane);
+        stage_H<NU, NX>(g, a.p, b, j0, g.x_index_of(c, 0), img, imr, Sb);
+        stage_BA<NU, NX>(g, a.p, b, j0, BA, fb);
         cp_commit();
         if (implicit_rhs && c == 0 && lane < NU) {
             double s0 = 0;
@@ -315,9 +177,9 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
         __syncwarp();
         // the H buffers are free: prefetch H_{s+1} (and BA_1 at s = 0)
         if (s + 1 < n) {
-            stage_H<NU, NX>(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), base, lane);
+            stage_H<NU, NX>(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), img, imr, Sb);
             if (s == 0)
-                stage_BA<NU, NX>(g, a.p, b, g.stage_of(c, 1), base, lane);
+                stage_BA<NU, NX>(g, a.p, b, g.stage_of(c, 1), BA, fb);
         }
         cp_commit();
 
@@ -549,7 +411,7 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
             }
             __syncwarp();
             if (s + 2 < n)
-                stage_BA<NU, NX>(g, a.p, b, g.stage_of(c, s + 2), base, lane);
+                stage_BA<NU, NX>(g, a.p, b, g.stage_of(c, s + 2), BA, fb);
             cp_commit();
         }
     }
