@@ -199,10 +199,14 @@ def run_reference(args):
 
 
 def config_dict(args, cfg):
-    return {"workload": f"config {cfg.idx}: {cfg.name}", "batch_per_gpu": cfg.batch,
-            "N": cfg.N, "nx": cfg.nx, "nu": cfg.nu, "P": cfg.P, "seed": args.seed,
-            "parallelism": f"instance-sharded x{args.gpus}",
-            "l2": "inputs larger than L2 (no flush)"}
+    d = {"workload": f"config {cfg.idx}: {cfg.name}", "batch_per_gpu": cfg.batch,
+         "N": cfg.N, "nx": cfg.nx, "nu": cfg.nu, "P": cfg.P, "seed": args.seed,
+         "parallelism": f"instance-sharded x{args.gpus}",
+         "l2": "inputs larger than L2 (no flush)"}
+    if cfg.iters > 1:
+        d.update({"newton_iters_per_step": cfg.iters, "ny": cfg.ny,
+                  "step": "per iteration: GPU Newton-system assembly + factor + solve"})
+    return d
 
 
 def run_ours(args):
@@ -237,12 +241,31 @@ def run_ours(args):
         return shard.max_over_ranks(x, device="cuda")
 
     # ---- device-resident inputs -----------------------------------------
+    # config 4 (QPALM Newton systems): one step = `iters` successive
+    # refactorizations per instance, each = GPU Newton-system assembly
+    # (qpalm::assemble_newton, Σ of that iteration) + factor + solve; D, C and
+    # the whole Σ sequence are resident like the problem data.
+    iters = cfg.iters
     dev = EqOCPBatch.__new__(EqOCPBatch)
     for k in OCP_FIELDS:
         setattr(dev, k, torch.from_numpy(getattr(p, k)).to("cuda"))
+    if iters > 1:
+        Dh, Eh, sigh = synth.qpalm_data(p, seed=args.seed, iters=iters, ny=cfg.ny,
+                                        start=rank * B)
+        Dd, Ed, sigd = (torch.from_numpy(a).to("cuda") for a in (Dh, Eh, sigh))
+        aug = kkt.augment_hessians(dev, Dd, Ed, sigd[0], ctx=ctx)
+
+    def one_step(src, out):
+        if iters == 1:
+            kkt.solve_problem(src, opts, ctx=ctx, out=out)
+            return
+        for it in range(iters):
+            kkt.augment_hessians(src, Dd, Ed, sigd[it], ctx=ctx, out=aug)
+            kkt.solve_problem(aug, opts, ctx=ctx, out=out)
+
     sol = kkt._alloc_sol(dev, True)
     for _ in range(args.warmup):
-        kkt.solve_problem(dev, opts, ctx=ctx, out=sol)
+        one_step(dev, sol)
     barrier()
     ctx.profile(True)
     ctx.profile_read(reset=True)
@@ -251,14 +274,14 @@ def run_ours(args):
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            kkt.solve_problem(dev, opts, ctx=ctx, out=sol)
+            one_step(dev, sol)
         e1.record(stream)
         barrier()
     ms = e0.elapsed_time(e1) / args.steps
     kern = ctx.profile_read(reset=True)
     ctx.profile(False)
     ms = max_over_ranks(ms)
-    value = ws * B / (ms * 1e-3)
+    value = ws * B * iters / (ms * 1e-3)
 
     # ---- end to end: pinned host buffers, H2D + D2H inside the timed region
     pin = EqOCPBatch.__new__(EqOCPBatch)
@@ -266,16 +289,38 @@ def run_ours(args):
         setattr(pin, k, torch.from_numpy(getattr(p, k)).pin_memory().numpy())
     hsol = kkt.EqSolutionBatch(*[torch.zeros(getattr(sol, k).shape, dtype=torch.float64)
                                  .pin_memory().numpy() for k in ("u", "x", "lam")])
+    h2d_extra = 0
+    if iters == 1:
+        def e2e_step():
+            kkt.solve_problem(pin, opts, ctx=ctx, out=hsol)
+    else:
+        # host problem, D, C and Σ sequence pinned; H2D inside the step, every
+        # iteration's solution copied back to the host
+        pins = [torch.from_numpy(a).pin_memory() for a in (Dh, Eh, sigh)]
+        h2d_extra = sum(t.numel() * 8 for t in pins)
+        dsol = kkt._alloc_sol(dev, True)
+        hsols = [torch.zeros(dsol.u.shape, dtype=torch.float64).pin_memory() for _ in range(3)]
+
+        def e2e_step():
+            for k in OCP_FIELDS:
+                getattr(dev, k).copy_(torch.from_numpy(getattr(pin, k)), non_blocking=True)
+            for dst, src in zip((Dd, Ed, sigd), pins):
+                dst.copy_(src, non_blocking=True)
+            for it in range(iters):
+                kkt.augment_hessians(dev, Dd, Ed, sigd[it], ctx=ctx, out=aug)
+                kkt.solve_problem(aug, opts, ctx=ctx, out=dsol)
+                for h, d in zip((hsol.u, hsol.x, hsol.lam), (dsol.u, dsol.x, dsol.lam)):
+                    torch.from_numpy(h).copy_(d, non_blocking=True)
     for _ in range(max(1, args.warmup // 2)):
-        kkt.solve_problem(pin, opts, ctx=ctx, out=hsol)
+        e2e_step()
     barrier()
     e0.record(stream)
     for _ in range(args.steps):
-        kkt.solve_problem(pin, opts, ctx=ctx, out=hsol)
+        e2e_step()
     e1.record(stream)
     barrier()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-    e2e = ws * B / (ms_e2e * 1e-3)
+    e2e = ws * B * iters / (ms_e2e * 1e-3)
     # spot parity of this run's result against the device run
     assert np.array_equal(hsol.u[:4], sol.u[:4].cpu().numpy())
 
@@ -324,8 +369,8 @@ def run_ours(args):
         "data": "synthetic (seeded BASELINE config generators, synth.py)",
         "config": config_dict(args, cfg),
         "e2e": {"value": e2e, "unit": "solves/s",
-                "h2d_bytes_per_step": problem_bytes(cfg.N, cfg.nx, cfg.nu) * B,
-                "d2h_bytes_per_step": solution_bytes(cfg.N, cfg.nx, cfg.nu) * B,
+                "h2d_bytes_per_step": problem_bytes(cfg.N, cfg.nx, cfg.nu) * B + h2d_extra,
+                "d2h_bytes_per_step": solution_bytes(cfg.N, cfg.nx, cfg.nu) * B * iters,
                 "ms_per_step": ms_e2e},
         "roofline": {"bound": "tensor", "kernel": "riccati_panel_kernel",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -333,9 +378,9 @@ def run_ours(args):
                      "peak_source": peak_src,
                      "flops_per_launch": k_flops, "launch_ms": k_avg},
         "step_roofline": {
-            "flops_per_step": flops_per_solve(cfg.N, cfg.nx, cfg.nu, cfg.P) * B,
-            "tflops": flops_per_solve(cfg.N, cfg.nx, cfg.nu, cfg.P) * B / (ms * 1e-3) / 1e12,
-            "frac_fp64": flops_per_solve(cfg.N, cfg.nx, cfg.nu, cfg.P) * B / (ms * 1e-3)
+            "flops_per_step": flops_per_solve(cfg.N, cfg.nx, cfg.nu, cfg.P) * B * iters,
+            "tflops": flops_per_solve(cfg.N, cfg.nx, cfg.nu, cfg.P) * B * iters / (ms * 1e-3) / 1e12,
+            "frac_fp64": flops_per_solve(cfg.N, cfg.nx, cfg.nu, cfg.P) * B * iters / (ms * 1e-3)
             / 1e12 / peak,
             "compulsory_bytes": (problem_bytes(cfg.N, cfg.nx, cfg.nu)
                                  + solution_bytes(cfg.N, cfg.nx, cfg.nu)) * B,
@@ -349,6 +394,8 @@ def run_ours(args):
     }
     if ws == 1 and not args.no_cpu:
         sample = p.subset(np.arange(min(64, B)))
+        if iters > 1:  # CPU reference on iteration 0's Newton systems (assembly not timed)
+            sample = next(synth.qpalm_sequence(sample, seed=args.seed, iters=1, ny=cfg.ny))
         rate, kind, threads, n, t = cpu_reference_rate(sample, cfg.P, args.cpu_seconds)
         line["cpu_baseline"] = {
             "value": rate, "unit": "solves/s", "cores": threads, "kind": kind,

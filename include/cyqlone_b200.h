@@ -112,10 +112,28 @@ int cyq_factor_destroy(cyq_factor *factor);
 int cyq_factor_materialize(const cyq_factor *factor, int64_t inst, double *LH,
                            double *LB, double *Acl, double *LA);
 
+/* Newton-system assembly of the QPALM inner loop (qpalm::assemble_newton,
+ * qpalm.cpp:167-225, equality part; BASELINE config 4): for every instance
+ * and stage j
+ *   R_out = R + D_j' diag(sigma_j) D_j + gamma_inv I          (j < N)
+ *   S_out = S + D_j' diag(sigma_j) C_j                        (j < N)
+ *   Q_out = Q + C_j' diag(sigma_j) C_j + gamma_inv I (j >= 1) (j <= N)
+ * with D[b][N][ny][nu], C[b][N+1][ny][nx] (C[N] = the terminal rows),
+ * sigma[b][N+1][ny] (0 for inactive rows), R/S/Q in the problem layout.
+ * DEVICE pointers on the context's GPU; stream-ordered, asynchronous. The
+ * outputs plus the unchanged A, B, f, r, q, x_init form the Newton problem
+ * for cyq_solve_problem_batch / cyq_factor_batch. ny <= 64, nx + nu <= 64. */
+int cyq_augment_hessians_batch(cyq_ctx *ctx, const cyq_dims *dims, int64_t ny,
+                               const double *R, const double *S, const double *Q,
+                               const double *D, const double *C,
+                               const double *sigma, double gamma_inv,
+                               double *R_out, double *S_out, double *Q_out);
+
 /* Per-kernel device timing: when enabled, every launch of the pipeline is
  * bracketed by CUDA events on the context stream. `read` synchronizes and
  * returns, per kernel (0 riccati_panel, 1 schur_cr, 2 backsub, 3 forward
- * sweep), the summed milliseconds and launch counts since the last reset. */
+ * sweep, 4 Newton-system assembly) -- ms[5], launches[5] -- the summed
+ * milliseconds and launch counts since the last reset. */
 int cyq_ctx_profile(cyq_ctx *ctx, int enable);
 int cyq_ctx_profile_read(cyq_ctx *ctx, double *ms, int64_t *launches,
                          int reset);

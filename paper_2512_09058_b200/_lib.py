@@ -62,6 +62,8 @@ SIGNATURES = {
     "cyq_ctx_profile_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(i64),
                                        C.c_int]),
     "cyq_version": (C.c_char_p, []),
+    "cyq_augment_hessians_batch": (C.c_int, [C.c_void_p, C.POINTER(CyqDims), i64] + [C.c_void_p] * 6
+                                   + [C.c_double] + [C.c_void_p] * 3),
 }
 
 _lib = None

@@ -34,9 +34,9 @@ struct cyq_ctx {
     bool profile = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
     std::vector<cudaEvent_t> pool;
-    double ms[4] = {0, 0, 0, 0};
-    int64_t launches[4] = {0, 0, 0, 0};
-    int64_t kernels[4] = {0, 0, 0, 0}; // kernel launches per kind
+    double ms[5] = {0, 0, 0, 0, 0};
+    int64_t launches[5] = {0, 0, 0, 0, 0};
+    int64_t kernels[5] = {0, 0, 0, 0, 0}; // kernel launches per kind
 };
 
 struct cyq_factor {
@@ -476,6 +476,10 @@ int ensure(cyq_ctx *ctx, void **buf, size_t *have, size_t need) {
 
 namespace cyqb {
 
+cudaStream_t ctx_prepare(cyq_ctx *ctx) {
+    cudaSetDevice(ctx->device);
+    return ctx->stream;
+}
 
 } // namespace cyqb
 
@@ -830,7 +834,7 @@ int cyq_ctx_profile_read(cyq_ctx *ctx, double *ms, int64_t *launches, int reset)
         ctx->pool.push_back(e.second.second);
     }
     ctx->ev.clear();
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 5; ++k) {
         if (ms)
             ms[k] = ctx->ms[k];
         if (launches)
@@ -840,6 +844,25 @@ int cyq_ctx_profile_read(cyq_ctx *ctx, double *ms, int64_t *launches, int reset)
             ctx->kernels[k] = 0;
         }
     }
+    return CYQ_OK;
+}
+
+int cyq_augment_hessians_batch(cyq_ctx *ctx, const cyq_dims *dims, int64_t ny, const double *R,
+                               const double *S, const double *Q, const double *D, const double *C,
+                               const double *sigma, double gamma_inv, double *R_out, double *S_out,
+                               double *Q_out) {
+    if (!ctx || !dims || !R || !S || !Q || !D || !C || !sigma || !R_out || !S_out || !Q_out)
+        return set_err(ctx, CYQ_INVALID_ARG, "null argument");
+    if (dims->N < 1 || dims->nx < 1 || dims->nu < 1 || dims->batch < 1 || ny < 1)
+        return set_err(ctx, CYQ_INVALID_ARG, "dims: N, nx, nu, batch, ny must be >= 1");
+    CU(cudaSetDevice(ctx->device));
+    {
+        Timed t(ctx, 4);
+        if (!launch_augment(ctx->stream, (int)dims->batch, (int)dims->N, (int)dims->nx, (int)dims->nu,
+                            (int)ny, R, S, Q, D, C, sigma, gamma_inv, R_out, S_out, Q_out))
+            return set_err(ctx, CYQ_INVALID_ARG, "augment: ny <= 64 and nx + nu <= 64 supported");
+    }
+    CU(cudaGetLastError());
     return CYQ_OK;
 }
 

@@ -5,6 +5,8 @@
 
 #include <cuda_runtime.h>
 
+struct cyq_ctx; // include/cyqlone_b200.h
+
 namespace cyqb {
 
 // Device workspace of one factorization of a batch (all chains).
@@ -119,6 +121,14 @@ __global__ void schur_cr_kernel(SchurArgs a);
 __global__ void backsub_kernel(BacksubArgs a);
 
 size_t riccati_smem_bytes(const Geo &g);
+// context helpers for entry points outside capi.cu: selects the context's
+// device, returns its stream
+cudaStream_t ctx_prepare(::cyq_ctx *ctx);
+// Newton-system assembly (augment.cu); false if the shape is not supported
+bool launch_augment(cudaStream_t st, int batch, int N, int nx, int nu, int ny, const double *R,
+                    const double *S, const double *Q, const double *D, const double *C,
+                    const double *sigma, double gamma_inv, double *R_out, double *S_out,
+                    double *Q_out);
 bool riccati_staged(const Geo &g);
 size_t riccati_consts_doubles(const Geo &g);
 size_t backsub_smem_bytes(const Geo &g);

@@ -96,14 +96,14 @@ class Context:
     def synchronize(self):
         self.lib.cyq_ctx_synchronize(self.h)
 
-    KERNELS = ("riccati_panel", "schur_cr", "backsub", "forward_sweep")
+    KERNELS = ("riccati_panel", "schur_cr", "backsub", "forward_sweep", "augment")
 
     def profile(self, enable: bool = True):
         self.lib.cyq_ctx_profile(self.h, int(enable))
 
     def profile_read(self, reset: bool = True):
-        ms = (C.c_double * 4)()
-        n = (C.c_int64 * 4)()
+        ms = (C.c_double * 5)()
+        n = (C.c_int64 * 5)()
         self.lib.cyq_ctx_profile_read(self.h, ms, n, int(reset))
         return {k: (ms[i], n[i]) for i, k in enumerate(self.KERNELS)}
 
@@ -265,5 +265,36 @@ def solve(f: Factor, p, rhs) -> EqSolutionBatch:
     return sol
 
 
-__all__ = ["FactorOptions", "Factor", "FactorizeError", "CudaError", "Context", "factor",
+def augment_hessians(p, D, Cm, sigma, gamma_inv: float = 0.0, out=None,
+                     ctx: Context | None = None) -> EqOCPBatch:
+    """Newton-system assembly of the QPALM inner loop (qpalm::assemble_newton,
+    qpalm.cpp:167-225, equality part) on the GPU: returns the batch with
+    R + D'ΣD + γ⁻¹I, S + D'ΣC, Q + C'ΣC + γ⁻¹I (stage-wise; C[:, N] the
+    terminal rows) and the other fields shared with `p`. Device (CUDA torch)
+    arrays only: D (b, N, ny, nu), Cm (b, N+1, ny, nx), sigma (b, N+1, ny).
+    `out` may pass a preallocated EqOCPBatch whose R, S, Q are overwritten."""
+    import torch
+
+    ctx = ctx or Context.default()
+    for a in (p.R, p.S, p.Q, D, Cm, sigma):
+        if not _is_torch(a):
+            raise ValueError("augment_hessians takes CUDA torch tensors")
+    b, N, nx, nu = p.A.shape[0], p.A.shape[1], p.A.shape[2], p.B.shape[3]
+    ny = D.shape[2]
+    if out is None:
+        out = EqOCPBatch.__new__(EqOCPBatch)
+        for k in OCP_FIELDS:
+            setattr(out, k, getattr(p, k))
+        out.R, out.S, out.Q = torch.empty_like(p.R), torch.empty_like(p.S), torch.empty_like(p.Q)
+    rc = ctx.lib.cyq_augment_hessians_batch(
+        ctx.h, C.byref(_lib.CyqDims(N, nx, nu, 1, b)), ny, *[_ptr(a) for a in
+                                                             (p.R, p.S, p.Q, D, Cm, sigma)],
+        float(gamma_inv), _ptr(out.R), _ptr(out.S), _ptr(out.Q))
+    if rc != _lib.CYQ_OK:
+        raise (ValueError if rc == _lib.CYQ_INVALID_ARG else CudaError)(
+            f"cyq_augment_hessians_batch failed ({rc}): {ctx.last_error()}")
+    return out
+
+
+__all__ = ["augment_hessians", "FactorOptions", "Factor", "FactorizeError", "CudaError", "Context", "factor",
            "solve", "solve_problem", "nu2", "EqOCPBatch", "EqRhsBatch", "EqSolutionBatch"]

@@ -95,6 +95,25 @@ def generate(cfg_idx: int, seed: int = 0, batch: int | None = None,
     return EqOCPBatch(*[np.stack(c) for c in cols])
 
 
+def qpalm_data(base: EqOCPBatch, seed: int = 0, iters: int = 20, ny: int = 24, start: int = 0):
+    """Config 4 inputs of the Newton sequence: D (b, N, ny, nu), E (b, N+1,
+    ny, nx) and the iters x (b, N+1, ny) Σ diagonals of `qpalm_sequence`
+    (same random streams)."""
+    b, N, nx, nu = base.batch, base.N, base.nx, base.nu
+    rngs = [np.random.default_rng([seed, 4, start + i, 7]) for i in range(b)]
+    D = np.stack([g.standard_normal((N, ny, nu)) for g in rngs])
+    E = np.stack([g.standard_normal((N + 1, ny, nx)) for g in rngs])
+    logs = np.stack([g.uniform(-2, 4, (N + 1, ny)) for g in rngs])
+    sig = []
+    for it in range(iters):
+        if it > 0:
+            for k, g in enumerate(rngs):
+                mask = g.random((N + 1, ny)) < 0.3
+                logs[k][mask] = g.uniform(-2, 4, int(mask.sum()))
+        sig.append(10.0 ** logs)
+    return D, E, np.stack(sig)
+
+
 def qpalm_sequence(base: EqOCPBatch, seed: int = 0, iters: int = 20, ny: int = 24,
                    start: int = 0):
     """Config 4: yields `iters` augmented Newton systems per instance,
