@@ -13,6 +13,7 @@
 // row-major (both triangles) next to the unchanged A, B, f, r, q. Memory
 // bound: it streams D, C, σ and the base Hessians once.
 #include "kernels.h"
+#include "riccati_common.cuh" // cp8 / cp_commit / cp_wait
 
 #include <string>
 
@@ -20,8 +21,33 @@ namespace cyqb {
 
 namespace {
 
-constexpr int kAugWarps = 4;
+constexpr int kAugWarps = 8;
 constexpr int kAugMaxY = 64, kAugMaxUX = 64; // ny, nu + nx limits (shared memory)
+
+// out[i] = in[i] + G(row(i), col(i)) (+ gamma_inv on the diagonal), i over a
+// contiguous row-major block of `rows x cols`, 16-byte coalesced when aligned
+__device__ __forceinline__ void add_block(double *out, const double *in, const double *G, int ldg,
+                                          int r0, int c0, int rows, int cols, double dg, int lane) {
+    const int cnt = rows * cols;
+    const bool al = (((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(in)) & 15) == 0) &&
+                    (cols % 2 == 0);
+    if (al) {
+#pragma unroll 4
+        for (int e = 2 * lane; e < cnt; e += 64) {
+            const int r = e / cols, c = e % cols;
+            const double2 v = __ldg(reinterpret_cast<const double2 *>(in + e));
+            double2 o;
+            o.x = v.x + G[(r0 + r) * ldg + c0 + c] + (r == c ? dg : 0.0);
+            o.y = v.y + G[(r0 + r) * ldg + c0 + c + 1] + (r == c + 1 ? dg : 0.0);
+            *reinterpret_cast<double2 *>(out + e) = o;
+        }
+    } else {
+        for (int e = lane; e < cnt; e += 32) {
+            const int r = e / cols, c = e % cols;
+            out[e] = __ldg(in + e) + G[(r0 + r) * ldg + c0 + c] + (r == c ? dg : 0.0);
+        }
+    }
+}
 
 __global__ void __launch_bounds__(32 * kAugWarps) augment_kernel(
     int batch, int N, int nx, int nu, int ny, const double *R, const double *S, const double *Q,
@@ -34,65 +60,64 @@ __global__ void __launch_bounds__(32 * kAugWarps) augment_kernel(
         return;
     const int b = (int)(task / (N + 1)), j = (int)(task % (N + 1));
     const int nux = nu + nx, TT = (nux + 7) / 8, KS = (ny + 3) / 4;
-    const int ldc = 8 * TT;                 // padded row length of [D C]
+    const int ldc = 8 * TT;                 // padded row length of [D C] and G
     double *Cm = sm + (size_t)wib * per_warp;
-    double *sg = Cm + (size_t)4 * KS * ldc; // ny (padded to 4 KS)
+    double *sg = Cm + (size_t)4 * KS * ldc; // 4 KS
+    double *G = sg + 4 * KS;                // ldc x ldc (symmetric, both triangles)
     const bool has_d = j < N;
-    // stage [D_j C_j] rows (zero padding rows / columns) and σ_j
-    for (int e = lane; e < 4 * KS * ldc; e += 32) {
-        const int i = e / ldc, m = e % ldc;
-        double v = 0.0;
-        if (i < ny && m < nux) {
-            if (m < nu)
-                v = has_d ? __ldg(D + (((size_t)b * N + j) * ny + i) * nu + m) : 0.0;
+    // stage [D_j C_j] rows and σ_j with cp.async (every copy in flight at
+    // once); zero padding rows / columns written directly
+    {
+        const double *Dj = D + ((size_t)b * N + j) * ny * nu;
+        const double *Ej = E + ((size_t)b * (N + 1) + j) * ny * nx;
+        for (int e = lane; e < 4 * KS * ldc; e += 32) {
+            const int i = e / ldc, m = e % ldc;
+            if (i < ny && m < nu && has_d)
+                ric::cp8(Cm + e, Dj + i * nu + m);
+            else if (i < ny && m >= nu && m < nux)
+                ric::cp8(Cm + e, Ej + i * nx + (m - nu));
             else
-                v = __ldg(E + (((size_t)b * (N + 1) + j) * ny + i) * nx + (m - nu));
+                Cm[e] = 0.0;
         }
-        Cm[e] = v;
+        for (int i = lane; i < 4 * KS; i += 32) {
+            if (i < ny)
+                ric::cp8(sg + i, sig + ((size_t)b * (N + 1) + j) * ny + i);
+            else
+                sg[i] = 0.0;
+        }
+        ric::cp_commit();
+        ric::cp_wait<0>();
     }
-    for (int i = lane; i < 4 * KS; i += 32)
-        sg[i] = i < ny ? __ldg(sig + ((size_t)b * (N + 1) + j) * ny + i) : 0.0;
     __syncwarp();
+    // G = [D C]' diag(σ) [D C] on DMMA tiles (lower tiles, mirrored into smem)
     const int rq = lane >> 2, cq = 2 * (lane & 3), kq = lane & 3;
     for (int ti = 0; ti < TT; ++ti)
         for (int tj = 0; tj <= ti; ++tj) {
             Frag acc{0.0, 0.0};
             for (int ks = 0; ks < KS; ++ks) {
                 const int k = 4 * ks + kq;
-                const double av = sg[k] * Cm[k * ldc + 8 * ti + rq]; // (σ C)'(m, k)
-                const double bv = Cm[k * ldc + 8 * tj + rq];         // C(k, n)
-                dmma(acc, av, bv);
+                dmma(acc, sg[k] * Cm[k * ldc + 8 * ti + rq], Cm[k * ldc + 8 * tj + rq]);
             }
-            // scatter G(r, c) (and its mirror) into R / S / Q with the base values
+            // every entry written once, from its lower-triangle value (the
+            // upper half of a diagonal tile differs in rounding: deterministic)
+            const int r = 8 * ti + rq, c = 8 * tj + cq;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int r = 8 * ti + rq, c = 8 * tj + cq + h;
-                const double gv = h ? acc.b : acc.a;
-                if (r >= nux || c >= nux || c > r)
-                    continue;
-                if (r < nu) { // R (j < N)
-                    if (has_d) {
-                        const size_t o = ((size_t)b * N + j) * nu * nu;
-                        const double dg = (r == c) ? gamma_inv : 0.0;
-                        Ro[o + r * nu + c] = __ldg(R + o + r * nu + c) + gv + dg;
-                        if (r != c)
-                            Ro[o + c * nu + r] = __ldg(R + o + c * nu + r) + gv;
-                    }
-                } else if (c < nu) { // S(c, r - nu) = G(c, r) = G(r, c)
-                    if (has_d) {
-                        const size_t o = ((size_t)b * N + j) * nu * nx;
-                        So[o + c * nx + (r - nu)] = __ldg(S + o + c * nx + (r - nu)) + gv;
-                    }
-                } else { // Q
-                    const int qr = r - nu, qc = c - nu;
-                    const size_t o = ((size_t)b * (N + 1) + j) * nx * nx;
-                    const double dg = (qr == qc && j >= 1) ? gamma_inv : 0.0;
-                    Qo[o + qr * nx + qc] = __ldg(Q + o + qr * nx + qc) + gv + dg;
-                    if (qr != qc)
-                        Qo[o + qc * nx + qr] = __ldg(Q + o + qc * nx + qr) + gv;
+            for (int h = 0; h < 2; ++h)
+                if (c + h <= r) {
+                    const double v = h ? acc.b : acc.a;
+                    G[r * ldc + c + h] = v;
+                    G[(c + h) * ldc + r] = v;
                 }
-            }
         }
+    __syncwarp();
+    // coalesced read-add-write of the stage's R, S, Q blocks
+    if (has_d) {
+        const size_t oR = ((size_t)b * N + j) * nu * nu, oS = ((size_t)b * N + j) * nu * nx;
+        add_block(Ro + oR, R + oR, G, ldc, 0, 0, nu, nu, gamma_inv, lane);
+        add_block(So + oS, S + oS, G, ldc, 0, nu, nu, nx, 0.0, lane);
+    }
+    const size_t oQ = ((size_t)b * (N + 1) + j) * nx * nx;
+    add_block(Qo + oQ, Q + oQ, G, ldc, nu, nu, nx, nx, j >= 1 ? gamma_inv : 0.0, lane);
 }
 
 } // namespace
@@ -104,7 +129,7 @@ bool launch_augment(cudaStream_t st, int batch, int N, int nx, int nu, int ny, c
     if (ny < 1 || ny > kAugMaxY || nx + nu > kAugMaxUX)
         return false;
     const int nux = nx + nu, ldc = 8 * ((nux + 7) / 8), ks = (ny + 3) / 4;
-    const int per_warp = (4 * ks * ldc + 4 * ks + 1) & ~1;
+    const int per_warp = (4 * ks * ldc + 4 * ks + ldc * ldc + 1) & ~1;
     const long long tasks = (long long)batch * (N + 1);
     const int grid = (int)((tasks + kAugWarps - 1) / kAugWarps);
     const size_t smem = (size_t)kAugWarps * per_warp * sizeof(double);
