@@ -11,7 +11,9 @@
 //    reference members LH, LB, Acl, LA (kkt_solver.hpp:76-85) to the host.
 //  * FactorOptions::vlen / workers are CPU lane / thread knobs and have no
 //    effect (the reference's results do not depend on them either,
-//    test_kkt.cpp:133-138); tail must be Tail::cr1.
+//    test_kkt.cpp:133-138); every tail (cr1 / pcr / pcg) is served by the
+//    exact cyclic reduction of the whole Schur tree (within the pcr / pcg
+//    accuracy contracts of test_kkt.cpp:152-161).
 //  * Batched entry points (solve_problem_batch, factor_batch) are additions:
 //    the reference API is single-instance.
 #pragma once
@@ -112,8 +114,8 @@ class Factor {
 };
 
 /// kkt::factor (kkt_factor.cpp:251-313). Throws std::invalid_argument for a
-/// non-power-of-two P or a tail other than cr1, batla::factorize_error on a
-/// pivot failure, std::runtime_error on a CUDA error.
+/// non-power-of-two P or vlen, batla::factorize_error on a pivot failure,
+/// std::runtime_error on a CUDA error.
 Factor factor(const EqOCP &p, const FactorOptions &opts, FlopTrace *trace = nullptr);
 /// kkt::solve (kkt_solve.cpp:23-309) with an explicit right-hand side.
 EqSolution solve(const Factor &f, const EqOCP &p, const EqRhs &rhs);

@@ -148,6 +148,10 @@ class RefOracle(_Base):
         super().__init__(_load(os.path.join(HERE, "_ref", "libcyqref.so"), "ref"))
         self.lib.ref_bench_solve_problem.restype = C.c_double
 
+    def set_tail(self, tail: str):
+        """FactorOptions::tail of the following calls: cr1 | pcr | pcg."""
+        self.lib.ref_set_tail(C.c_int({"cr1": 0, "pcr": 1, "pcg": 2}[tail]))
+
     def solve_problem(self, p, P, vlen=4, threads=1):
         sol = _sol_arrays(p)
         res = np.zeros(p.batch)

@@ -113,12 +113,14 @@ void set_status(oc_status *st, int code, int kind, index_t inst, index_t col,
     st->pivot           = piv;
 }
 
+int g_tail = 0; // ref_set_tail: 0 cr1, 1 pcr, 2 pcg
+
 FactorOptions opts_of(const oc_dims *d, int64_t vlen) {
     FactorOptions o;
     o.P       = d->P;
     o.vlen    = vlen;
     o.workers = 1;
-    o.tail    = kkt::Tail::cr1;
+    o.tail    = g_tail == 1 ? kkt::Tail::pcr : g_tail == 2 ? kkt::Tail::pcg : kkt::Tail::cr1;
     return o;
 }
 
@@ -146,6 +148,9 @@ void dense_of(const batla::BatchMatrix &m, index_t lane, double *out) {
 } // namespace
 
 extern "C" {
+
+// FactorOptions::tail of every following call (kkt_solver.hpp:45-57)
+void ref_set_tail(int tail) { g_tail = tail; }
 
 int ref_solve_problem(const oc_dims *d, const oc_ocp *p, int64_t vlen,
                       int threads, oc_sol *out, double *resid,

@@ -46,8 +46,11 @@ void check_opts(const FactorOptions &o) {
         throw std::invalid_argument("P must be a power of two");
     if (!pow2(o.vlen))
         throw std::invalid_argument("vlen must be a power of two");
-    if (o.tail != Tail::cr1)
-        throw std::invalid_argument("cyqlone_b200: only the cr1 tail is implemented on the GPU");
+    // Tail::pcr / Tail::pcg (kkt_factor.cpp:227-247) are CPU strategies for
+    // the last min(P, vlen) Schur blocks; the GPU's fused cyclic reduction
+    // solves the whole tree exactly, within both tails' accuracy contracts
+    if (o.tail != Tail::cr1 && o.tail != Tail::pcr && o.tail != Tail::pcg)
+        throw std::invalid_argument("unknown tail");
 }
 
 void check_mat(const Mat &m, index_t r, index_t c, const char *what) {

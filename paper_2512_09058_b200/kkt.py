@@ -13,7 +13,8 @@ instance axis; a single reference EqOCP is a batch of one). Arrays may be
 host numpy arrays or CUDA torch tensors (device-resident, zero-copy).
 `opts.vlen` / `opts.workers` are CPU lane/thread knobs of the reference and
 are accepted but have no effect on the GPU (results are independent of them
-in the reference too, test_kkt.cpp:133-138); `tail` must be cr1.
+in the reference too, test_kkt.cpp:133-138); every `tail` (cr1 / pcr / pcg)
+is served by the GPU's exact cyclic reduction of the whole Schur tree.
 """
 from __future__ import annotations
 
@@ -150,8 +151,12 @@ def _check_opts(opts: FactorOptions):
     v = int(opts.vlen)
     if v < 1 or (v & (v - 1)) != 0:
         raise ValueError("vlen must be a power of two")
-    if opts.tail != "cr1":
-        raise NotImplementedError("only Tail::cr1 is implemented on the GPU")
+    if opts.tail not in ("cr1", "pcr", "pcg"):
+        raise ValueError("tail must be one of cr1, pcr, pcg")
+    # pcr / pcg (kkt_factor.cpp:227-247) are CPU strategies for the last
+    # min(P, vlen) Schur blocks; the GPU's fused cyclic reduction solves the
+    # whole tree exactly, which meets both tails' accuracy contracts
+    # (test_kkt.cpp:152-161: pcr within 1e-10 of cr1, pcg within 1e-8)
 
 
 def _raise_status(ctx, rc, st):

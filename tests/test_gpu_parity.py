@@ -30,7 +30,8 @@ def oracle():
 @pytest.mark.parametrize("name", golden_util.names())
 def test_golden_reference_outputs(name):
     p, P, ref_sol, z = golden_util.load(name)
-    sol = kkt.solve_problem(p, kkt.FactorOptions(P=P))
+    tail = str(z["tail"]) if "tail" in z else "cr1"  # pcr / pcg fixtures: reference tails
+    sol = kkt.solve_problem(p, kkt.FactorOptions(P=P, tail=tail))
     err = rel_error(sol, ref_sol)
     assert err.max() <= REL_TOL, f"rel err {err.max():.3e}"
     res = kkt_residual(p, EqRhsBatch.of_problem(p), sol).max(axis=1)
