@@ -28,16 +28,35 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """One nvcc -c per source (in parallel, into build/), then one link."""
     if not force and not needs_build():
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT, *[os.path.join(CSRC, s) for s in SOURCES]]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if verbose or r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-    if r.returncode != 0:
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"]
+
+    def compile_one(src: str):
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        r = subprocess.run([NVCC, *cflags, "-c", "-o", obj, os.path.join(CSRC, src)],
+                           capture_output=True, text=True)
+        return obj, r
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    log = "".join(r.stdout + r.stderr for _, r in results)
+    if verbose or any(r.returncode for _, r in results):
+        sys.stderr.write(log)
+    if any(r.returncode for _, r in results):
         raise RuntimeError("nvcc failed building libcyqlone_b200.so")
+    r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT,
+                        *[o for o, _ in results]], capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc link failed for libcyqlone_b200.so")
     with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
-        fh.write(r.stderr)
+        fh.write(log)
     return OUT
 
 

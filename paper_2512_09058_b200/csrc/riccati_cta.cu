@@ -7,17 +7,27 @@
 //   kkt_solve.cpp:72-134    forward substitution + coupling rows (rhs row)
 //
 // Execution model (one CTA of NW warps per partition column):
-//  * the extended panel (TT x TT lower tiles, 231 at config 3) is owned
-//    tile-by-tile by the warps (tile t -> warp t % NW) and lives in their
-//    registers for the stage (coupling x coupling tiles for the chain);
-//  * blocked Cholesky, per pivot block column kb: the owner of (kb, kb)
-//    factors it with an identity tile carried through the pivot steps
-//    (L_kk^{-1} for free) and publishes L_kk^{-1}; the owners of the
-//    sub-diagonal tiles solve them by two DMMAs and publish the column;
-//    every owner applies C -= L_i L_j' to its trailing tiles. The owner of
-//    (kb+1, kb+1) updates and factors it FIRST (look-ahead), so the next
-//    pivot chain overlaps this column's trailing DMMAs; the column buffer
-//    is double-buffered by kb parity -> two __syncthreads per block column;
+//  * the extended panel (TT x TT lower tiles, 231 at config 3) lives in the
+//    warps' registers for the stage. Warp kb (< CT) owns the pivot diagonal
+//    tile (kb, kb) in a dedicated register tile; every other tile is on a
+//    LIST ordered by tile column descending (and tile row descending inside
+//    a column), dealt round-robin to the warps. So at block column kb the
+//    tiles a warp must update (tj > kb) are a PREFIX of its list and the
+//    update loop leaves through a warp-uniform branch: no predicated-off
+//    DMMA is ever issued (they occupy the DMMA pipe like real ones; the
+//    previous triangular-order ownership issued 58% of its DMMAs
+//    predicated off);
+//  * blocked right-looking Cholesky with look-ahead, per block column kb:
+//    (A) the raw column-kb tiles, published in shared memory by their owners
+//        at the end of the previous step, are solved in place there
+//        (X <- X L_kk^{-T} = X (L_kk^{-1})', two DMMAs) by any warp -- a
+//        runtime loop over the column, no register-array indexing;
+//    (B) warp kb+1 applies column kb to its diagonal tile and factors it
+//        (identity tile carried through the pivot steps -> L^{-1} for free),
+//        while every warp takes its solved column-kb tiles back into
+//        registers, applies C -= L_i L_j' to its list prefix and publishes
+//        its (now complete) column-(kb+1) tiles into the other buffer;
+//    two __syncthreads per block column;
 //  * shared memory holds W = [V; ALQ; -wl] (the next stage's W W' operand),
 //    [B A] of the next stage (cp.async, one stage ahead), L_Q in x-space
 //    (the B operand of V = BA' L_Q) and the column buffers; H_s is read
@@ -26,6 +36,7 @@
 #include "kernels.h"
 #include "riccati_common.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace cyqb {
@@ -34,8 +45,13 @@ using namespace cyqb::ric;
 
 namespace {
 
-// (ti << 8 | tj) of lower-triangular tile t = ti (ti + 1) / 2 + tj
-__constant__ unsigned short c_tij[1024];
+// per-warp tile lists (host-built, launch_c): c_list[w][k] = (ti << 8 | tj),
+// tile columns non-increasing in k; c_cnt[w][kb + 1] = number of my tiles
+// with tile column > kb (the update prefix at block column kb), c_cnt[w][0]
+// = all my tiles
+constexpr int kMaxW = 16, kMaxL = 32, kMaxCT = 31;
+__constant__ unsigned short c_list[kMaxW * kMaxL];
+__constant__ unsigned char c_cnt[kMaxW * (kMaxCT + 1)];
 
 template <int NU, int NX, int NW> struct CS {
     static_assert(NU % 8 == 0 && NX % 8 == 0, "tile-aligned shapes only");
@@ -44,24 +60,30 @@ template <int NU, int NX, int NW> struct CS {
     static constexpr int BT = (NX + 1 + 7) / 8;   // coupling + rhs tile rows
     static constexpr int TT = CT + BT;
     static constexpr int NT = TT * (TT + 1) / 2;
+    static constexpr int NL = NT - CT;            // list tiles (all but pivot diagonals)
+    static_assert(NW >= CT + 1 && NW <= kMaxW && CT <= kMaxCT, "one warp per pivot diagonal tile");
     static constexpr int TOP = 8 * CT, RHS = TOP + NX, RT = RHS / 8, RR = RHS % 8;
     static constexpr int XT0 = NU / 8, NXC = NX / 8; // x columns: tiles XT0 .. CT-1
     static constexpr int NPT = CT * (CT + 1) / 2 + BT * CT;
-    static constexpr int MAXT = (NT + NW - 1) / NW;
-    static constexpr int PW = NUX;                 // [B A] row length
+    static constexpr int MAXL = (NL + NW - 1) / NW;  // tiles per warp (the host plan meets it)
+    static_assert(MAXL <= kMaxL, "list table size");
+    // [B A] and L_Q row strides, padded by 8 doubles: the V = BA' L_Q
+    // operand loads (4 rows x 8 columns per warp) then need the minimum two
+    // shared-memory wavefronts instead of four
+    static constexpr int PW = NUX + 8, LQS = NX + 8;
     // shared memory (doubles)
     static constexpr int O_W = 0;                                  // TT x NXC tiles
     static constexpr int O_COL = O_W + TT * NXC * kTileElems;      // 2 x TT tiles
     static constexpr int O_LINV = O_COL + 2 * TT * kTileElems;     // 2 tiles (by kb parity)
     static constexpr int O_BA = O_LINV + 2 * kTileElems;           // NX x PW
-    static constexpr int O_LQ = O_BA + NX * PW;                    // NX x NX (x-space L_Q)
-    static constexpr int O_F = O_LQ + NX * NX;                     // NX
+    static constexpr int O_LQ = O_BA + NX * PW;                    // NX x LQS (x-space L_Q)
+    static constexpr int O_F = O_LQ + NX * LQS;                    // NX
     static constexpr int O_YX = O_F + NX;                          // NX (x part of y)
     static constexpr int O_MW = O_YX + NX;                         // NX (-wl_new)
     static constexpr int O_RU0 = O_MW + NX;                        // NU
     static constexpr int O_RED = O_RU0 + NU;                       // 32 (pivot floor)
-    static constexpr int O_SCR = O_RED + 32;                       // 2 x 64 (transpose, by parity)
-    static constexpr int SMEM = O_SCR + 2 * kTileElems;
+    static constexpr int O_SCR = O_RED + 32;                       // 64 (transpose)
+    static constexpr int SMEM = O_SCR + kTileElems;
     __host__ __device__ static constexpr int T(int i, int j) { return i * (i + 1) / 2 + j; }
     // stored-factor tile index of panel tile (i, j), j < CT
     __host__ __device__ static constexpr int PI(int i, int j) {
@@ -115,12 +137,62 @@ __device__ __forceinline__ void stage_BA_cta(const Geo &g, const ProbView &p, in
     }
 }
 
+// initial value of panel tile (ti, tj), tj < CT: H_s (top), [B A]_0 rows at
+// s = 0 and the rhs row (bottom)
+template <int NU, int NX, int NW>
+__device__ __forceinline__ Frag init_tile(int ti, int tj, int rq, int cq, int s, double sgn,
+                                          const double *Rg, const double *Sg, const double *Qg,
+                                          const double *rg, const double *qg, const double *ru0p,
+                                          const double *BA, bool aligned) {
+    using C = CS<NU, NX, NW>;
+    Frag f{0.0, 0.0};
+    const int r = 8 * ti + rq, c0 = 8 * tj + cq;
+    if (ti < C::CT) {
+        if (r < NU && c0 < NU) { // R (full block; upper parts are don't-care)
+            if (Rg && !aligned) {
+                f = {__ldg(Rg + r * NU + c0), __ldg(Rg + r * NU + c0 + 1)};
+            } else if (Rg) {
+                const double2 v = __ldg(reinterpret_cast<const double2 *>(Rg + r * NU + c0));
+                f = {v.x, v.y};
+            } else
+                f = {r == c0 ? 1.0 : 0.0, r == c0 + 1 ? 1.0 : 0.0};
+        } else if (r >= NU && c0 >= NU) { // Q
+            if (Qg && !aligned) {
+                f = {__ldg(Qg + (r - NU) * NX + (c0 - NU)), __ldg(Qg + (r - NU) * NX + (c0 - NU) + 1)};
+            } else if (Qg) {
+                const double2 v = __ldg(reinterpret_cast<const double2 *>(Qg + (r - NU) * NX + (c0 - NU)));
+                f = {v.x, v.y};
+            } else
+                f = {r == c0 ? 1.0 : 0.0, r == c0 + 1 ? 1.0 : 0.0};
+        } else if (r >= NU && c0 < NU && Sg) { // S' (lower-left), transposed read
+            f = {__ldg(Sg + c0 * NX + (r - NU)), __ldg(Sg + (c0 + 1) * NX + (r - NU))};
+        }
+    } else {
+        const int rb = r - C::TOP;
+        if (s == 0 && rb < NX)
+            f = {BA[rb * C::PW + c0], BA[rb * C::PW + c0 + 1]};
+        else if (rb == NX) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int col = c0 + h;
+                double v = 0.0;
+                if (col < NU)
+                    v = (rg ? sgn * __ldg(rg + col) : 0.0) - (ru0p ? ru0p[col] : 0.0);
+                else
+                    v = qg ? sgn * __ldg(qg + col - NU) : 0.0;
+                (h ? f.b : f.a) = v;
+            }
+        }
+    }
+    return f;
+}
+
 } // namespace
 
 template <int NU, int NX, int NW>
 __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) {
     using C = CS<NU, NX, NW>;
-    constexpr int NTH = 32 * NW, MAXT = C::MAXT, CT = C::CT, TT = C::TT, NT = C::NT;
+    constexpr int NTH = 32 * NW, MAXL = C::MAXL, CT = C::CT, TT = C::TT;
     extern __shared__ __align__(16) double sm[];
     const Geo &g = a.g;
     const int chain = blockIdx.x;
@@ -135,13 +207,14 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
     const bool implicit_rhs = (a.p.ru == nullptr);
     const double sgn = implicit_rhs ? -1.0 : 1.0;
     int fail_piv = -1, fail_stage = 0;
-
-    // my tiles: t = warp + k NW -> (ti, tj) from the constant-memory table
-    // of the triangular enumeration (warp-uniform loads, no index registers)
-#define mtt(k) (warp + (k) * NW)
-#define mt(k) (mtt(k) < NT ? (int)c_tij[mtt(k)] : -1)
-#define mti(k) (mtt(k) < NT ? (int)(c_tij[mtt(k)] >> 8) : -1)
-#define mtj(k) (mtt(k) < NT ? (int)(c_tij[mtt(k)] & 255) : -1)
+    // warp w = 1..CT owns the pivot diagonal tile (w-1, w-1)
+    const int dkb = warp - 1;
+    const bool diag_owner = dkb >= 0 && dkb < CT;
+    // my list tiles (ti, tj) from constant memory (warp-uniform loads, no
+    // index registers)
+    const int mycnt = c_cnt[warp * (kMaxCT + 1)];
+#define LTI(k) ((int)(c_list[warp * kMaxL + (k)] >> 8))
+#define LTJ(k) ((int)(c_list[warp * kMaxL + (k)] & 255))
     for (int i = tid; i < C::SMEM; i += NTH)
         sm[i] = 0.0;
     __syncthreads();
@@ -162,12 +235,59 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
     }
     __syncthreads();
 
-    Frag acc[MAXT];
+    Frag acc[MAXL];
 #pragma unroll
-    for (int k = 0; k < MAXT; ++k)
+    for (int k = 0; k < MAXL; ++k)
         acc[k] = Frag{0.0, 0.0};
+    Frag dg{0.0, 0.0};
 
+    // the owner factors its diagonal tile dg (L_kk, upper zeroed) and
+    // publishes L_kk^{-1} -> linv[kb & 1] (identity tile carried through the
+    // pivot steps gives L^{-T}; transposed through shared memory)
+    auto factor_diag = [&](int kb, double dfloor, int s) {
+        Frag idt{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0};
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            const int src = kk / 2;
+            const double vk = (kk & 1) ? dg.b : dg.a;
+            const double pv = __shfl_sync(0xffffffffu, vk, 4 * kk + src);
+            const double urk = __shfl_sync(0xffffffffu, vk, 4 * rq + src);
+            const double uc0 = __shfl_sync(0xffffffffu, vk, 4 * cq + src);
+            const double uc1 = __shfl_sync(0xffffffffu, vk, 4 * (cq + 1) + src);
+            const bool first = !(pv > dfloor && isfinite(pv)) && fail_piv < 0;
+            fail_piv = first ? 8 * kb + kk : fail_piv;
+            fail_stage = first ? s : fail_stage;
+            const double iv = rsqrt_nr(pv);
+            const double lc0 = (cq > kk) ? uc0 * iv : 0.0;
+            const double lc1 = (cq + 1 > kk) ? uc1 * iv : 0.0;
+            const double lrk = urk * iv;
+            const double nv = (rq == kk) ? pv * iv : lrk;
+            if (kk & 1)
+                dg.b = (q2 == src) ? nv : dg.b;
+            else
+                dg.a = (q2 == src) ? nv : dg.a;
+            dg.a -= lrk * lc0;
+            dg.b -= lrk * lc1;
+            const double vq = (kk & 1) ? idt.b : idt.a;
+            const double xrq = __shfl_sync(0xffffffffu, vq, 4 * rq + src) * iv;
+            if (kk & 1)
+                idt.b = (q2 == src) ? xrq : idt.b;
+            else
+                idt.a = (q2 == src) ? xrq : idt.a;
+            idt.a -= xrq * lc0;
+            idt.b -= xrq * lc1;
+        }
+        if (cq > rq) dg.a = 0.0;
+        if (cq + 1 > rq) dg.b = 0.0;
+        st_frag(tscr, lane, idt); // L^{-1} = (L^{-T})'
+        __syncwarp();
+        st_frag(linvb + (kb & 1) * kTileElems, lane, Frag{tscr[cq * 8 + rq], tscr[(cq + 1) * 8 + rq]});
+        __syncwarp();
+    };
+
+    long long *ph = (a.phase && chain == 0 && tid == 0) ? a.phase : nullptr;
     for (int s = 0; s < n; ++s) {
+        if (ph) ph[s * 8 + 0] = clock64();
         const int j = g.stage_of(c, s), xi = g.x_index_of(c, s);
         const bool j0 = j == 0, in = j < N, qin = xi <= N;
         const double *Rg = in ? a.p.R + ((size_t)b * N + j) * NU * NU : nullptr;
@@ -179,64 +299,34 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         const bool aligned = ((reinterpret_cast<uintptr_t>(a.p.R) | reinterpret_cast<uintptr_t>(a.p.Q)) & 15) == 0;
         // ---- init (H_s from global, coupling rows BA_0 at s = 0, rhs row) ---
 #pragma unroll
-        for (int k = 0; k < MAXT; ++k) {
-            const int ti = mti(k), tj = mtj(k);
-            if (ti < 0 || tj >= CT)
-                continue;
-            Frag f{0.0, 0.0};
-            const int r = 8 * ti + rq, c0 = 8 * tj + cq;
-            if (ti < CT) {
-                if (r < NU && c0 < NU) { // R (full block; upper parts are don't-care)
-                    if (Rg && !aligned) {
-                        f = {__ldg(Rg + r * NU + c0), __ldg(Rg + r * NU + c0 + 1)};
-                    } else if (Rg) {
-                        const double2 v = __ldg(reinterpret_cast<const double2 *>(Rg + r * NU + c0));
-                        f = {v.x, v.y};
-                    } else
-                        f = {r == c0 ? 1.0 : 0.0, r == c0 + 1 ? 1.0 : 0.0};
-                } else if (r >= NU && c0 >= NU) { // Q
-                    if (Qg && !aligned) {
-                        f = {__ldg(Qg + (r - NU) * NX + (c0 - NU)), __ldg(Qg + (r - NU) * NX + (c0 - NU) + 1)};
-                    } else if (Qg) {
-                        const double2 v =
-                            __ldg(reinterpret_cast<const double2 *>(Qg + (r - NU) * NX + (c0 - NU)));
-                        f = {v.x, v.y};
-                    } else
-                        f = {r == c0 ? 1.0 : 0.0, r == c0 + 1 ? 1.0 : 0.0};
-                } else if (r >= NU && c0 < NU && Sg) { // S' (lower-left), transposed read
-                    f = {__ldg(Sg + c0 * NX + (r - NU)), __ldg(Sg + (c0 + 1) * NX + (r - NU))};
-                }
-            } else {
-                const int rb = r - C::TOP;
-                if (s == 0 && rb < NX)
-                    f = {BA[rb * C::PW + c0], BA[rb * C::PW + c0 + 1]};
-                else if (rb == NX) {
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int col = c0 + h;
-                        double v = 0.0;
-                        if (col < NU)
-                            v = (rg ? sgn * __ldg(rg + col) : 0.0) - (ru0p ? ru0p[col] : 0.0);
-                        else
-                            v = qg ? sgn * __ldg(qg + col - NU) : 0.0;
-                        (h ? f.b : f.a) = v;
-                    }
-                }
-            }
-            acc[k] = f;
+        for (int k = 0; k < MAXL; ++k) {
+            if (k >= mycnt)
+                break;
+            const int ti = LTI(k), tj = LTJ(k);
+            if (tj < CT)
+                acc[k] = init_tile<NU, NX, NW>(ti, tj, rq, cq, s, sgn, Rg, Sg, Qg, rg, qg, ru0p, BA, aligned);
         }
+        if (diag_owner)
+            dg = init_tile<NU, NX, NW>(dkb, dkb, rq, cq, s, sgn, Rg, Sg, Qg, rg, qg, ru0p, BA, aligned);
         // ---- += W W' (s > 0) --------------------------------------------
         if (s > 0) {
 #pragma unroll
-            for (int k = 0; k < MAXT; ++k) {
-                const int ti = mti(k), tj = mtj(k);
-                if (ti < 0)
-                    continue;
+            for (int k = 0; k < MAXL; ++k) {
+                if (k >= mycnt)
+                    break;
+                const int ti = LTI(k), tj = LTJ(k);
 #pragma unroll
                 for (int kt = 0; kt < C::NXC; ++kt) {
                     const Frag wi = ld_frag(Wsm + (ti * C::NXC + kt) * kTileElems, lane);
                     const Frag wj = ld_frag(Wsm + (tj * C::NXC + kt) * kTileElems, lane);
                     tile_gemm_nt(acc[k], wi, wj);
+                }
+            }
+            if (diag_owner) {
+#pragma unroll
+                for (int kt = 0; kt < C::NXC; ++kt) {
+                    const Frag wi = ld_frag(Wsm + (dkb * C::NXC + kt) * kTileElems, lane);
+                    tile_gemm_nt(dg, wi, wi);
                 }
             }
         }
@@ -250,143 +340,112 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
             if (x1 <= N)
                 pf_lines(a.p.Q + ((size_t)b * (N + 1) + x1) * NX * NX, NX * NX * 8, tid, NTH);
         }
-        __syncthreads(); // W and BA_0 reads done
+        if (ph) ph[s * 8 + 1] = clock64();
+        // ---- pivot floor: max |diag| (kernels.cpp:21-29) ---------------------
+        if (diag_owner) {
+            double v = (rq & 1) ? dg.b : dg.a;
+            v = ((lane & 3) == rq / 2) ? fabs(v) : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+                v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+            if (lane == 0)
+                atomicMax(red, (unsigned long long)__double_as_longlong(v));
+        }
+        // raw column-0 tiles -> column buffer 0 (the last list positions)
+#pragma unroll
+        for (int k = 0; k < MAXL; ++k) {
+            if (k >= mycnt)
+                break;
+            if (LTJ(k) == 0)
+                st_frag(colb + LTI(k) * kTileElems, lane, acc[k]);
+        }
+        __syncthreads(); // W and BA_0 reads done, pivot floor, column 0 published
         if (s == 0 && n > 1)
             stage_BA_cta<NU, NX, NW>(g, a.p, b, g.stage_of(c, 1), sm, tid);
         cp_commit();
-        // ---- pivot floor: max |diag| (kernels.cpp:21-29) ---------------------
-#pragma unroll
-        for (int k = 0; k < MAXT; ++k)
-            if (mti(k) >= 0 && mti(k) == mtj(k) && mti(k) < CT && (lane & 3) == rq / 2) {
-                const double v = (rq & 1) ? acc[k].b : acc[k].a;
-                atomicMax(red + (lane & 31), (unsigned long long)__double_as_longlong(fabs(v)));
-            }
-        __syncthreads();
-        double dm = __longlong_as_double((long long)red[lane]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-            dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
-        const double dfloor = 1e-14 * dm;
+        const double dfloor = 1e-14 * __longlong_as_double((long long)red[0]);
+        if (dkb == 0)
+            factor_diag(0, dfloor, s);
+        __syncthreads(); // linv[0]
 
         // ---- blocked Cholesky with look-ahead ----------------------------
-        // factor_diag: the owner's (kb, kb) tile -> L_kk (upper zeroed) and
-        // L_kk^{-1} -> linv[kb & 1], L_kk -> column buffer slot kb.
-        // factor_diag: the diagonal tile (kb, kb), handed over in the column
-        // buffer slot kb by its owner, is factored in place there (L_kk, upper
-        // zeroed) and L_kk^{-1} goes to linv[kb & 1]; one code copy, no
-        // register-array indexing (the owner reloads L_kk into its register
-        // tile in the next sub-diagonal phase)
-        auto factor_diag = [&](int kb) {
-            if (C::T(kb, kb) % NW != warp)
-                return;
-            double *slot = colb + ((kb & 1) * TT + kb) * kTileElems;
-            Frag dg = ld_frag(slot, lane);
-            Frag idt{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0};
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-                const int src = kk / 2;
-                const double vk = (kk & 1) ? dg.b : dg.a;
-                const double pv = __shfl_sync(0xffffffffu, vk, 4 * kk + src);
-                const double urk = __shfl_sync(0xffffffffu, vk, 4 * rq + src);
-                const double uc0 = __shfl_sync(0xffffffffu, vk, 4 * cq + src);
-                const double uc1 = __shfl_sync(0xffffffffu, vk, 4 * (cq + 1) + src);
-                const bool first = !(pv > dfloor && isfinite(pv)) && fail_piv < 0;
-                fail_piv = first ? 8 * kb + kk : fail_piv;
-                fail_stage = first ? s : fail_stage;
-                const double iv = rsqrt_nr(pv);
-                const double lc0 = (cq > kk) ? uc0 * iv : 0.0;
-                const double lc1 = (cq + 1 > kk) ? uc1 * iv : 0.0;
-                const double lrk = urk * iv;
-                const double nv = (rq == kk) ? pv * iv : lrk;
-                if (kk & 1)
-                    dg.b = (q2 == src) ? nv : dg.b;
-                else
-                    dg.a = (q2 == src) ? nv : dg.a;
-                dg.a -= lrk * lc0;
-                dg.b -= lrk * lc1;
-                const double vq = (kk & 1) ? idt.b : idt.a;
-                const double xrq = __shfl_sync(0xffffffffu, vq, 4 * rq + src) * iv;
-                if (kk & 1)
-                    idt.b = (q2 == src) ? xrq : idt.b;
-                else
-                    idt.a = (q2 == src) ? xrq : idt.a;
-                idt.a -= xrq * lc0;
-                idt.b -= xrq * lc1;
-            }
-            if (cq > rq) dg.a = 0.0;
-            if (cq + 1 > rq) dg.b = 0.0;
-            st_frag(slot, lane, dg);
-            double *ts = tscr + (kb & 1) * kTileElems;
-            st_frag(ts, lane, idt); // L^{-1} = (L^{-T})'
-            __syncwarp();
-            st_frag(linvb + (kb & 1) * kTileElems, lane, Frag{ts[cq * 8 + rq], ts[(cq + 1) * 8 + rq]});
-            __syncwarp();
-        };
-        // the owner of (0, 0) hands it over
-#pragma unroll
-        for (int k = 0; k < MAXT; ++k)
-            if (mt(k) == 0)
-                st_frag(colb, lane, acc[k]);
-        __syncwarp();
-        factor_diag(0);
-        __syncthreads();
 #pragma unroll 1
         for (int kb = 0; kb < CT; ++kb) {
             const int par = kb & 1;
-            double *col = colb + par * TT * kTileElems;
-            // sub-diagonal tiles of column kb: X <- X L_kk^{-T} = X (L_kk^{-1})';
-            // the owner of (kb, kb) takes L_kk back into its register tile
+            double *col = colb + par * TT * kTileElems, *nxt = colb + (par ^ 1) * TT * kTileElems;
+            // (A) solve the column-kb tiles in place: X <- X (L_kk^{-1})'
             {
                 const Frag linv = ld_frag(linvb + par * kTileElems, lane);
-#pragma unroll
-                for (int k = 0; k < MAXT; ++k)
-                    if (mt(k) == ((kb << 8) | kb))
-                        acc[k] = ld_frag(col + kb * kTileElems, lane);
-#pragma unroll
-                for (int k = 0; k < MAXT; ++k)
-                    if (mtj(k) == kb && mti(k) > kb) {
-                        Frag r{0.0, 0.0};
-                        tile_gemm_nt(r, acc[k], linv);
-                        acc[k] = r;
-                        st_frag(col + mti(k) * kTileElems, lane, r);
-                    }
-            }
-            __syncthreads(); // column kb published
-            // look-ahead: (kb+1, kb+1) first, then factor it
-            if (kb + 1 < CT) {
-                const int pk = ((kb + 1) << 8) | (kb + 1);
-#pragma unroll
-                for (int k = 0; k < MAXT; ++k)
-                    if (mt(k) == pk) {
-                        const Frag li = ld_frag(col + (kb + 1) * kTileElems, lane);
-                        tile_gemm_nt_sub(acc[k], li, li);
-                        st_frag(colb + (((kb + 1) & 1) * TT + kb + 1) * kTileElems, lane, acc[k]);
-                    }
-                __syncwarp();
-                factor_diag(kb + 1);
-            }
-            // trailing update of my other tiles: C(ti, tj) -= L(ti, kb) L(tj, kb)'
-#pragma unroll
-            for (int k = 0; k < MAXT; ++k) {
-                const int ti = mti(k), tj = mtj(k);
-                if (tj > kb && !(ti == kb + 1 && tj == kb + 1 && kb + 1 < CT)) {
-                    const Frag li = ld_frag(col + ti * kTileElems, lane);
-                    const Frag lj = ld_frag(col + tj * kTileElems, lane);
-                    tile_gemm_nt_sub(acc[k], li, lj);
+                for (int ti = kb + 1 + warp; ti < TT; ti += NW) {
+                    const Frag x = ld_frag(col + ti * kTileElems, lane);
+                    Frag r{0.0, 0.0};
+                    tile_gemm_nt(r, x, linv);
+                    st_frag(col + ti * kTileElems, lane, r);
                 }
             }
-            __syncthreads(); // column kb consumed, L_{kb+1} / linv published
+            __syncthreads(); // column kb solved
+            // (B) look-ahead: the owner of (kb+1, kb+1) updates and factors it
+            // (its list holds few tiles right of column kb: the host plan)
+            if (dkb == kb + 1 && kb + 1 < CT) {
+                const Frag li = ld_frag(col + (kb + 1) * kTileElems, lane);
+                tile_gemm_nt_sub(dg, li, li);
+                factor_diag(kb + 1, dfloor, s);
+            } else if (diag_owner && dkb > kb + 1) {
+                const Frag li = ld_frag(col + dkb * kTileElems, lane);
+                tile_gemm_nt_sub(dg, li, li);
+            }
+            // my solved column-kb tiles back into registers: list positions
+            // [cnt, hi) (right after the update prefix)
+            const int cnt = c_cnt[warp * (kMaxCT + 1) + kb + 1];
+            const int hi = c_cnt[warp * (kMaxCT + 1) + kb];
+#pragma unroll
+            for (int k = 0; k < MAXL; ++k) {
+                if (k >= hi)
+                    break;
+                if (k >= cnt)
+                    acc[k] = ld_frag(col + LTI(k) * kTileElems, lane);
+            }
+            // trailing update of my prefix: C(ti, tj) -= L(ti, kb) L(tj, kb)';
+            // completed column-(kb+1) tiles are published for step kb+1. The
+            // next tile's operands are loaded one iteration ahead (a read of
+            // a valid column slot even past the prefix)
+            {
+                int tj = LTJ(0);
+                Frag li = ld_frag(col + LTI(0) * kTileElems, lane), lj = ld_frag(col + tj * kTileElems, lane);
+#pragma unroll
+                for (int k = 0; k < MAXL; ++k) {
+                    if (k >= cnt)
+                        break;
+                    Frag nli{0.0, 0.0}, nlj{0.0, 0.0};
+                    int ntj = 0;
+                    if (k + 1 < MAXL) {
+                        ntj = LTJ(k + 1);
+                        nli = ld_frag(col + LTI(k + 1) * kTileElems, lane);
+                        nlj = ld_frag(col + ntj * kTileElems, lane);
+                    }
+                    tile_gemm_nt_sub(acc[k], li, lj);
+                    if (tj == kb + 1)
+                        st_frag(nxt + LTI(k) * kTileElems, lane, acc[k]);
+                    li = nli;
+                    lj = nlj;
+                    tj = ntj;
+                }
+            }
+            __syncthreads(); // column kb consumed, column kb+1 / linv published
         }
-        if (tid < 32)
-            red[tid] = 0ull;
+        if (tid == 0)
+            red[0] = 0ull;
+        if (ph) ph[s * 8 + 2] = clock64();
 
         // ---- store the factor tiles and y_s' ---------------------------------
         {
             double *dst = a.fac + ((size_t)chain * n + s) * C::NPT * kTileElems;
 #pragma unroll
-            for (int k = 0; k < MAXT; ++k) {
-                const int ti = mti(k), tj = mtj(k);
-                if (ti >= 0 && tj < CT) {
+            for (int k = 0; k < MAXL; ++k) {
+                if (k >= mycnt)
+                    break;
+                const int ti = LTI(k), tj = LTJ(k);
+                if (tj < CT) {
                     st_frag(dst + C::PI(ti, tj) * kTileElems, lane, acc[k]);
                     if (ti == C::RT && rq == C::RR) {
                         double *yv = a.y + ((size_t)chain * n + s) * C::NUX;
@@ -399,45 +458,69 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                     }
                 }
             }
+            if (diag_owner)
+                st_frag(dst + C::PI(dkb, dkb) * kTileElems, lane, dg);
         }
+        if (ph) ph[s * 8 + 3] = clock64();
 
         if (s + 1 < n) {
             // ---- W for stage s+1 -------------------------------------------
             // L_Q (x block of the pivot tiles) -> LQ (x-space, row-major)
 #pragma unroll
-            for (int k = 0; k < MAXT; ++k) {
-                const int ti = mti(k), tj = mtj(k);
+            for (int k = 0; k < MAXL; ++k) {
+                if (k >= mycnt)
+                    break;
+                const int ti = LTI(k), tj = LTJ(k);
                 if (ti >= C::XT0 && ti < CT && tj >= C::XT0) {
                     const int r = 8 * ti + rq - NU, c0 = 8 * tj + cq - NU;
-                    LQ[r * NX + c0] = acc[k].a;
-                    LQ[r * NX + c0 + 1] = acc[k].b;
+                    LQ[r * C::LQS + c0] = acc[k].a;
+                    LQ[r * C::LQS + c0 + 1] = acc[k].b;
                 }
                 // ALQ rows (coupling rows, x columns) -> W tile rows >= CT
                 if (ti >= CT && tj >= C::XT0 && tj < CT)
                     st_frag(Wsm + (ti * C::NXC + (tj - C::XT0)) * kTileElems, lane, acc[k]);
             }
+            if (diag_owner && dkb >= C::XT0) {
+                const int r = 8 * dkb + rq - NU, c0 = 8 * dkb + cq - NU;
+                LQ[r * C::LQS + c0] = dg.a;
+                LQ[r * C::LQS + c0 + 1] = dg.b;
+            }
             cp_wait<0>(); // BA_{s+1}, f_{s+1}
             __syncthreads();
-            // -wl_new = L_Q' (sgn f) + x'   (kkt_solve.cpp:85-90)
-            for (int t = tid; t < NX; t += NTH) {
+            if (ph) ph[s * 8 + 4] = clock64();
+            // -wl_new = L_Q' (sgn f) + x'   (kkt_solve.cpp:85-90): 8 lanes per
+            // entry (split k, shuffle-reduced), spread over all warps
+            for (int t0 = 4 * warp; t0 < NX; t0 += 4 * NW) {
+                const int t = t0 + (lane >> 3), part = lane & 7;
                 double q = 0.0;
-                for (int k = t; k < NX; ++k)
-                    q += LQ[k * NX + t] * (sgn * fb[k]);
-                q += yx[t];
-                mw[t] = q;
-                a.wl[((size_t)chain * n + s) * NX + t] = -q;
+                if (t < NX)
+                    for (int k = t + part; k < NX; k += 8)
+                        q += LQ[k * C::LQS + t] * (sgn * fb[k]);
+                q += __shfl_xor_sync(0xffffffffu, q, 1);
+                q += __shfl_xor_sync(0xffffffffu, q, 2);
+                q += __shfl_xor_sync(0xffffffffu, q, 4);
+                if (t < NX && part == 0) {
+                    q += yx[t];
+                    mw[t] = q;
+                    a.wl[((size_t)chain * n + s) * NX + t] = -q;
+                }
             }
-            // V = BA_{s+1}' L_Q -> W tile rows 0..CT-1 (DMMA, one tile per warp pass)
+            // V = BA_{s+1}' L_Q -> W tile rows 0..CT-1 (DMMA, one tile per warp
+            // pass, two accumulators to halve the dependent DMMA chain)
             for (int v = warp; v < CT * C::NXC; v += NW) {
                 const int ti = v / C::NXC, kt = v % C::NXC;
-                Frag f{0.0, 0.0};
-                for (int ks = 2 * kt; ks < NX / 4; ++ks) { // L_Q upper part is zero
-                    const int K = 4 * ks + (lane & 3);
-                    const double av = BA[K * C::PW + 8 * ti + rq];
-                    const double bv = LQ[K * NX + 8 * kt + rq];
-                    dmma(f, av, bv);
+                Frag f0{0.0, 0.0}, f1{0.0, 0.0};
+                int ks = 2 * kt; // L_Q upper part is zero
+                for (; ks + 1 < NX / 4; ks += 2) {
+                    const int K0 = 4 * ks + (lane & 3), K1 = K0 + 4;
+                    dmma(f0, BA[K0 * C::PW + 8 * ti + rq], LQ[K0 * C::LQS + 8 * kt + rq]);
+                    dmma(f1, BA[K1 * C::PW + 8 * ti + rq], LQ[K1 * C::LQS + 8 * kt + rq]);
                 }
-                st_frag(Wsm + (ti * C::NXC + kt) * kTileElems, lane, f);
+                if (ks < NX / 4) {
+                    const int K0 = 4 * ks + (lane & 3);
+                    dmma(f0, BA[K0 * C::PW + 8 * ti + rq], LQ[K0 * C::LQS + 8 * kt + rq]);
+                }
+                st_frag(Wsm + (ti * C::NXC + kt) * kTileElems, lane, Frag{f0.a + f1.a, f0.b + f1.b});
             }
             __syncthreads(); // mw ready, V written, BA / LQ reads done
             // rhs row of W: -wl in row RHS of tile row RT (other rows of
@@ -451,10 +534,13 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         }
     }
 
+    if (ph) ph[n * 8] = clock64();
     // trailing tiles (coupling x coupling = -Mfwd, rhs x coupling = -fwd)
 #pragma unroll
-    for (int k = 0; k < MAXT; ++k) {
-        const int ti = mti(k), tj = mtj(k);
+    for (int k = 0; k < MAXL; ++k) {
+        if (k >= mycnt)
+            break;
+        const int ti = LTI(k), tj = LTJ(k);
         if (tj >= CT)
             st_frag(a.trail + ((size_t)chain * g.NTT + C::T(ti - CT, tj - CT)) * kTileElems, lane,
                     acc[k]);
@@ -466,10 +552,8 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         my_fail = min(my_fail, __shfl_xor_sync(0xffffffffu, my_fail, o));
     if (lane == 0 && my_fail != ~0ull)
         atomicMin(a.fail + b, my_fail);
-#undef mti
-#undef mtj
-#undef mt
-#undef mtt
+#undef LTI
+#undef LTJ
 }
 
 namespace {
@@ -482,13 +566,60 @@ template <int NU, int NX, int NW> bool launch_c(const Geo &g, cudaStream_t st, c
     if (!attr) {
         cudaFuncSetAttribute(riccati_cta_kernel<NU, NX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        unsigned short h[1024];
-        for (int t = 0, ti = 0; t < 1024; ++t) {
-            while ((ti + 1) * (ti + 2) / 2 <= t)
-                ++ti;
-            h[t] = (unsigned short)((ti << 8) | (t - ti * (ti + 1) / 2));
+        // tile plan: every list tile (all but the pivot diagonals) goes,
+        // in tile-column-descending order, to the warp that minimises the
+        // modelled Cholesky time sum_kb max(DMMA issue per SM sub-partition,
+        // look-ahead warp's factorization + its own updates): the owner of
+        // (kb+1, kb+1) is then left with few tiles right of column kb
+        unsigned short h[kMaxW * kMaxL] = {};
+        unsigned char cnt[kMaxW * (kMaxCT + 1)] = {};
+        double load[kMaxW][kMaxCT] = {};
+        int nown[kMaxW] = {};
+        const double kUpd = 2 * 16.0, kFac = 1400.0; // cycles: one tile update, one diagonal factorization
+        auto cost = [&]() {
+            double t = 0;
+            for (int kb = 0; kb < C::CT; ++kb) {
+                double sp[4] = {}, la = 0;
+                for (int w = 0; w < NW; ++w)
+                    sp[w % 4] += load[w][kb];
+                if (kb + 1 < C::CT)
+                    la = kFac + load[kb + 2][kb] * 4; // (kb+1, kb+1) is owned by warp kb+2
+                t += std::max(std::max(std::max(sp[0], sp[1]), std::max(sp[2], sp[3])), la);
+            }
+            return t;
+        };
+        for (int tj = C::TT - 1; tj >= 0; --tj)
+            for (int ti = C::TT - 1; ti >= tj; --ti) {
+                if (ti == tj && tj < C::CT)
+                    continue;
+                int best = -1;
+                double bc = 0;
+                for (int w = 0; w < NW; ++w) {
+                    if (nown[w] >= C::MAXL)
+                        continue;
+                    for (int kb = 0; kb < std::min(tj, C::CT); ++kb)
+                        load[w][kb] += kUpd;
+                    const double cw = cost() + 1e-3 * nown[w];
+                    for (int kb = 0; kb < std::min(tj, C::CT); ++kb)
+                        load[w][kb] -= kUpd;
+                    if (best < 0 || cw < bc)
+                        best = w, bc = cw;
+                }
+                for (int kb = 0; kb < std::min(tj, C::CT); ++kb)
+                    load[best][kb] += kUpd;
+                h[best * kMaxL + nown[best]++] = (unsigned short)((ti << 8) | tj);
+            }
+        for (int w = 0; w < NW; ++w) {
+            cnt[w * (kMaxCT + 1)] = (unsigned char)nown[w];
+            for (int kb = 0; kb < C::CT; ++kb) {
+                int m = 0;
+                for (int k = 0; k < nown[w]; ++k)
+                    m += (h[w * kMaxL + k] & 255) > kb;
+                cnt[w * (kMaxCT + 1) + kb + 1] = (unsigned char)m;
+            }
         }
-        cudaMemcpyToSymbol(c_tij, h, sizeof h);
+        cudaMemcpyToSymbol(c_list, h, sizeof h);
+        cudaMemcpyToSymbol(c_cnt, cnt, sizeof cnt);
         attr = true;
     }
     riccati_cta_kernel<NU, NX, NW><<<g.batch * g.P, 32 * NW, smem, st>>>(ra);
