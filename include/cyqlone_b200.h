@@ -129,6 +129,21 @@ int cyq_augment_hessians_batch(cyq_ctx *ctx, const cyq_dims *dims, int64_t ny,
                                const double *sigma, double gamma_inv,
                                double *R_out, double *S_out, double *Q_out);
 
+/* The Newton system of the QPALM inner loop solved in one call:
+ * kkt::solve_problem (kkt_solve.cpp:311-317) of the problem whose Hessians
+ * are augmented as cyq_augment_hessians_batch describes (qpalm::
+ * assemble_newton, qpalm.cpp:167-225, then qpalm.cpp:368-413's factor +
+ * solve). For the stage shapes the warp-level panel kernel covers
+ * (nu = 8, nx = 16, ny = 24: BASELINE config 4) the assembly is fused into
+ * the factorization's stage loads and the augmented Hessians never reach
+ * HBM; other shapes run the assembly kernel into context scratch first.
+ * DEVICE pointers only (prob, D, C, sigma, sol); stream-ordered. */
+int cyq_solve_newton_batch(cyq_ctx *ctx, const cyq_dims *dims,
+                           const cyq_ocp_batch *prob, int64_t ny,
+                           const double *D, const double *C,
+                           const double *sigma, double gamma_inv,
+                           const cyq_sol_batch *sol, cyq_status *status);
+
 /* Per-kernel device timing: when enabled, every launch of the pipeline is
  * bracketed by CUDA events on the context stream. `read` synchronizes and
  * returns, per kernel (0 riccati_panel, 1 schur_cr, 2 backsub, 3 forward

@@ -29,6 +29,8 @@ struct cyq_ctx {
     size_t hbuf_bytes = 0;
     void *wsbuf = nullptr;
     size_t wsbuf_bytes = 0;
+    void *augbuf = nullptr; // augmented R, S, Q of cyq_solve_newton_batch's two-kernel path
+    size_t augbuf_bytes = 0;
     cudaStream_t copy_stream = nullptr; // host->device staging of chunked calls
     // per-kernel timing (cyq_ctx_profile)
     bool profile = false;
@@ -311,9 +313,14 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
         const bool want_c2 = sel && sel[0] == 'c', want_gen = sel && sel[0] == 'g';
         const bool want_pc = sel && sel[0] == 'p';
         bool done = false;
-        if (!want_gen && want_pc)
+        if (p.aD) { // fused Newton-system augmentation: the warp kernel only
+            if (!launch_riccati_warp(g, ctx->stream, ra))
+                return set_err(ctx, CYQ_INVALID_ARG, "fused augmentation: no kernel for this shape");
+            done = true;
+        }
+        if (!done && !want_gen && want_pc)
             done = launch_riccati_pc(g, ctx->stream, ra);
-        if (!want_gen && want_c2)
+        if (!done && !want_gen && want_c2)
             done = launch_riccati_cta2(g, ctx->stream, ra);
         if (!want_gen && !done)
             done = launch_riccati_warp(g, ctx->stream, ra);
@@ -516,6 +523,8 @@ int cyq_ctx_destroy(cyq_ctx *ctx) {
         cudaFree(ctx->hbuf);
     if (ctx->wsbuf)
         cudaFree(ctx->wsbuf);
+    if (ctx->augbuf)
+        cudaFree(ctx->augbuf);
     for (auto &e : ctx->ev) {
         cudaEventDestroy(e.second.first);
         cudaEventDestroy(e.second.second);
@@ -864,6 +873,58 @@ int cyq_augment_hessians_batch(cyq_ctx *ctx, const cyq_dims *dims, int64_t ny, c
     }
     CU(cudaGetLastError());
     return CYQ_OK;
+}
+
+int cyq_solve_newton_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_batch *prob, int64_t ny,
+                           const double *D, const double *C, const double *sigma, double gamma_inv,
+                           const cyq_sol_batch *sol, cyq_status *status) {
+    if (!ctx || !prob || !sol || !D || !C || !sigma)
+        return set_err(ctx, CYQ_INVALID_ARG, "null argument");
+    if (ny < 1 || ny > 64)
+        return set_err(ctx, CYQ_INVALID_ARG, "ny must be in [1, 64]");
+    Geo g;
+    int rc = make_geo(ctx, dims, g);
+    if (rc)
+        return rc;
+    CU(cudaSetDevice(ctx->device));
+    const WsSizes wsz = ws_sizes(g);
+    rc = ensure(ctx, &ctx->wsbuf, &ctx->wsbuf_bytes, wsz.total);
+    if (rc)
+        return rc;
+    FactorWS ws = carve(ctx->wsbuf, wsz);
+    ProbView pv = view_of(prob);
+    if (riccati_warp_fuses_aug(g, (int)ny)) {
+        // assembly fused into the stage-panel loads: the augmented Hessians
+        // never touch HBM
+        pv.aD = D;
+        pv.aC = C;
+        pv.asig = sigma;
+        pv.ny = (int)ny;
+        pv.gamma_inv = gamma_inv;
+    } else {
+        // assembly kernel into context scratch, then the plain pipeline
+        const size_t B = g.batch, N = g.N, nx = g.nx, nu = g.nu;
+        const size_t nR = B * N * nu * nu, nS = B * N * nu * nx, nQ = B * (N + 1) * nx * nx;
+        rc = ensure(ctx, &ctx->augbuf, &ctx->augbuf_bytes, (nR + nS + nQ) * sizeof(double));
+        if (rc)
+            return rc;
+        double *Ro = static_cast<double *>(ctx->augbuf), *So = Ro + nR, *Qo = So + nS;
+        {
+            Timed t(ctx, 4);
+            if (!launch_augment(ctx->stream, g.batch, g.N, g.nx, g.nu, (int)ny, pv.R, pv.S, pv.Q, D, C,
+                                sigma, gamma_inv, Ro, So, Qo))
+                return set_err(ctx, CYQ_INVALID_ARG, "augment: ny <= 64 and nx + nu <= 64 supported");
+        }
+        CU(cudaGetLastError());
+        pv.R = Ro;
+        pv.S = So;
+        pv.Q = Qo;
+    }
+    SolView sv{sol->u, sol->x, sol->lam};
+    rc = launch_pipeline(ctx, g, pv, ws, &sv, true);
+    if (rc)
+        return rc;
+    return decode_status(ctx, g, ws.fail, status);
 }
 
 const char *cyq_version(void) {

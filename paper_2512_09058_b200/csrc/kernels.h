@@ -95,6 +95,9 @@ struct SchurLayout {
 template <int MAXT> __global__ void riccati_panel_kernel_t(RiccatiArgs a);
 // compile-time (nu, nx) warp-per-chain fast path; false if not instantiated
 bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
+// true when the warp kernel has a fused Newton-system augmentation variant
+// for this stage shape and ny (ProbView::aD path)
+bool riccati_warp_fuses_aug(const Geo &g, int ny);
 bool launch_riccati_cta2(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
 // CTA-per-chain kernel for large tile-aligned panels (riccati_cta.cu); false if n/a
 bool launch_riccati_cta(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);

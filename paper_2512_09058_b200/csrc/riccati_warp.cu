@@ -39,7 +39,7 @@ using namespace cyqb::ric;
 
 namespace {
 
-template <int NU, int NX> struct WS : PanelShape<NU, NX> {
+template <int NU, int NX, int NY = 0> struct WS : PanelShape<NU, NX> {
     using P_ = PanelShape<NU, NX>;
     static constexpr int TT = P_::TT, NXC = P_::NXC, NXR = P_::NXR, NIMG = P_::NIMG, PW = P_::PW;
     // per-warp shared memory (doubles); every offset is even (16-byte aligned)
@@ -52,16 +52,68 @@ template <int NU, int NX> struct WS : PanelShape<NU, NX> {
     static constexpr int O_F = O_BA + NXR * PW;
     static constexpr int O_RU0 = O_F + ((NX + 1) & ~1);
     static constexpr int O_SCR = O_RU0 + ((NU + 1) & ~1);
-    static constexpr int SMEM = O_SCR + kTileElems;
-    static_assert((O_LQ | O_IMG | O_IMR | O_S | O_BA | O_F | O_RU0 | O_SCR | SMEM) % 2 == 0, "align");
+    // Newton-system augmentation (NY > 0): [D_j C_xi] rows (NY x nux),
+    // sigma of the u rows and of the x rows
+    static constexpr int NUX_ = NU + NX, NYP = (NY + 7) / 8 * 8;
+    static constexpr int O_X = O_SCR + kTileElems;
+    static constexpr int O_SGU = O_X + ((NY * NUX_ + 1) & ~1);
+    static constexpr int O_SGX = O_SGU + NYP;
+    static constexpr int SMEM = NY > 0 ? O_SGX + NYP : O_SCR + kTileElems;
+    static_assert((O_LQ | O_IMG | O_IMR | O_S | O_BA | O_F | O_RU0 | O_SCR | O_X | O_SGU | O_SGX | SMEM) % 2 == 0,
+                  "align");
 };
+
+// Newton-system augmentation rows of stage position (j, xi): X[k][0..nu) =
+// D_j row k (j < N), X[k][nu..nux) = C_xi row k (1 <= xi <= N), and their
+// sigma vectors (zero rows / sigma where a block does not apply)
+template <int NU, int NX, int NY>
+__device__ __forceinline__ void stage_aug(const Geo &g, const ProbView &p, int b, int j, int xi, double *X,
+                                          double *sgu, double *sgx) {
+    constexpr int NUX = NU + NX;
+    const int N = g.N;
+    const int lane = lane_v();
+    const bool du = j < N, dx = xi >= 1 && xi <= N;
+    const double *Dj = du ? p.aD + ((size_t)b * N + j) * NY * NU : nullptr;
+    const double *Cj = dx ? p.aC + ((size_t)b * (N + 1) + xi) * NY * NX : nullptr;
+    constexpr bool V2 = NU % 2 == 0 && NX % 2 == 0;
+    if (Dj && V2 && aligned16(Dj)) {
+#pragma unroll
+        for (int e = 2 * lane; e < NY * NU; e += 64)
+            cp16(X + (e / NU) * NUX + e % NU, Dj + e);
+    } else {
+#pragma unroll
+        for (int e = lane; e < NY * NU; e += 32) {
+            double *d = X + (e / NU) * NUX + e % NU;
+            if (Dj)
+                cp8(d, Dj + e);
+            else
+                *d = 0.0;
+        }
+    }
+    if (Cj && V2 && aligned16(Cj)) {
+#pragma unroll
+        for (int e = 2 * lane; e < NY * NX; e += 64)
+            cp16(X + (e / NX) * NUX + NU + e % NX, Cj + e);
+    } else {
+#pragma unroll
+        for (int e = lane; e < NY * NX; e += 32) {
+            double *d = X + (e / NX) * NUX + NU + e % NX;
+            if (Cj)
+                cp8(d, Cj + e);
+            else
+                *d = 0.0;
+        }
+    }
+    wcopy<NY, 0>(sgu, du ? p.asig + ((size_t)b * (N + 1) + j) * NY : nullptr, lane);
+    wcopy<NY, 0>(sgx, dx ? p.asig + ((size_t)b * (N + 1) + xi) * NY : nullptr, lane);
+}
 
 } // namespace
 
-template <int NU, int NX, int WPB>
+template <int NU, int NX, int WPB, int NY>
 __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a) {
     using S = Shp<NU, NX>;
-    using W = WS<NU, NX>;
+    using W = WS<NU, NX, NY>;
     extern __shared__ __align__(16) double sm[];
     const Geo &g = a.g;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -75,6 +127,7 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
     double *Wsm = base + W::O_W, *LQ = base + W::O_LQ, *img = base + W::O_IMG;
     double *imr = base + W::O_IMR, *Sb = base + W::O_S, *BA = base + W::O_BA;
     double *fb = base + W::O_F, *ru0 = base + W::O_RU0, *tscr = base + W::O_SCR;
+    double *Xa = base + W::O_X, *sgu = base + W::O_SGU, *sgx = base + W::O_SGX; // NY > 0 only
     const bool implicit_rhs = (a.p.ru == nullptr);
     const double sgn = implicit_rhs ? -1.0 : 1.0;
     int fail_piv = -1, fail_stage = 0;
@@ -95,12 +148,31 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
         const int j0 = g.stage_of(c, 0);
         stage_H<NU, NX>(g, a.p, b, j0, g.x_index_of(c, 0), img, imr, Sb);
         stage_BA<NU, NX>(g, a.p, b, j0, BA, fb);
+        if constexpr (NY > 0)
+            stage_aug<NU, NX, NY>(g, a.p, b, j0, g.x_index_of(c, 0), Xa, sgu, sgx);
         cp_commit();
+        if constexpr (NY > 0) {
+            // augmented S_0 = S_0 + D_0' Σ_0 C_0 enters ru[0] through S_0 x_init:
+            // tscr[m] = σ_0[m] (C_0 x_init)[m]
+            if (implicit_rhs && c == 0) {
+                for (int m = lane; m < NY; m += 32) {
+                    double t = 0;
+                    for (int k = 0; k < NX; ++k)
+                        t += __ldg(a.p.aC + (size_t)b * (g.N + 1) * NY * NX + m * NX + k) *
+                             __ldg(a.p.x_init + (size_t)b * NX + k);
+                    tscr[m] = t * __ldg(a.p.asig + (size_t)b * (g.N + 1) * NY + m);
+                }
+                __syncwarp();
+            }
+        }
         if (implicit_rhs && c == 0 && lane < NU) {
             double s0 = 0;
             for (int k = 0; k < NX; ++k)
                 s0 += __ldg(a.p.S + (size_t)b * g.N * NU * NX + lane * NX + k) *
                       __ldg(a.p.x_init + (size_t)b * NX + k);
+            if constexpr (NY > 0)
+                for (int m = 0; m < NY; ++m)
+                    s0 += __ldg(a.p.aD + (size_t)b * g.N * NY * NU + m * NU + lane) * tscr[m];
             ru0[lane] = s0;
         }
         cp_wait<0>();
@@ -153,6 +225,54 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
                 }
                 P[S::T(ti, tj)] = f;
             }
+        if constexpr (NY > 0) {
+            // Newton-system augmentation of the pivot block, fused into the
+            // stage load: += X' diag(σ) X (qpalm.cpp:184-221) on DMMA tiles,
+            // A operand = σ-scaled X' tiles, B operand = X' tiles (the
+            // reference's D'(ΣD) association). Stage j != 0 < N: one pass
+            // over [D_j C_j] with σ_j (R, S', Q blocks). Otherwise the u
+            // and x rows come from different stages (j = 0: D_0 and the
+            // terminal C_N) and take one pass each, no cross block.
+            const bool cross = j < g.N && !j0;
+            constexpr int KT = (NY + 7) / 8;
+            for (int pass = 0; pass < (cross ? 1 : 2); ++pass) {
+                const int c0 = (cross || pass == 0) ? 0 : NU, c1 = (!cross && pass == 0) ? NU : S::NUX;
+                const double *sg = (cross || pass == 0) ? sgu : sgx;
+#pragma unroll
+                for (int kt = 0; kt < KT; ++kt) {
+                    const int k0 = 8 * kt + cq;
+                    const double s0 = k0 < NY ? sg[k0] : 0.0, s1 = k0 + 1 < NY ? sg[k0 + 1] : 0.0;
+                    Frag y[S::CT], ys[S::CT];
+#pragma unroll
+                    for (int ti = 0; ti < S::CT; ++ti) {
+                        const int col = 8 * ti + rq;
+                        const bool in = col >= c0 && col < c1;
+                        const double v0 = (in && k0 < NY) ? Xa[(k0 < NY ? k0 : 0) * S::NUX + (in ? col : 0)] : 0.0;
+                        const double v1 =
+                            (in && k0 + 1 < NY) ? Xa[(k0 + 1 < NY ? k0 + 1 : 0) * S::NUX + (in ? col : 0)] : 0.0;
+                        y[ti] = Frag{v0, v1};
+                        ys[ti] = Frag{v0 * s0, v1 * s1};
+                    }
+#pragma unroll
+                    for (int ti = 0; ti < S::CT; ++ti)
+#pragma unroll
+                        for (int tj = 0; tj <= ti; ++tj)
+                            tile_gemm_nt(P[S::T(ti, tj)], ys[ti], y[tj]);
+                }
+            }
+            if (a.p.gamma_inv != 0.0) { // + gamma^-1 I on R (j < N) and Q (1 <= xi <= N)
+                const int xi = g.x_index_of(c, s);
+                const double gu = j < g.N ? a.p.gamma_inv : 0.0;
+                const double gx = (xi >= 1 && xi <= g.N) ? a.p.gamma_inv : 0.0;
+#pragma unroll
+                for (int kb = 0; kb < S::CT; ++kb) {
+                    const int r = 8 * kb + rq;
+                    const double gv = r < NU ? gu : (r < S::NUX ? gx : 0.0);
+                    P[S::T(kb, kb)].a += rq == cq ? gv : 0.0;
+                    P[S::T(kb, kb)].b += rq == cq + 1 ? gv : 0.0;
+                }
+            }
+        }
         if (s > 0) {
             // += W W' over the compact x-columns: k-slice outer, tiles inner
             // (consecutive DMMAs hit different accumulators)
@@ -178,6 +298,8 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
         // the H buffers are free: prefetch H_{s+1} (and BA_1 at s = 0)
         if (s + 1 < n) {
             stage_H<NU, NX>(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), img, imr, Sb);
+            if constexpr (NY > 0)
+                stage_aug<NU, NX, NY>(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), Xa, sgu, sgx);
             if (s == 0)
                 stage_BA<NU, NX>(g, a.p, b, g.stage_of(c, 1), BA, fb);
         }
@@ -435,32 +557,40 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
 
 // ---- dispatch ----------------------------------------------------------------
 namespace {
-template <int NU, int NX, int WPB> bool launch_w(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
+template <int NU, int NX, int WPB, int NY> bool launch_w(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
     if (g.nu != NU || g.nx != NX)
         return false;
-    using W = WS<NU, NX>;
+    if ((NY > 0) != (ra.p.aD != nullptr) || (NY > 0 && ra.p.ny != NY))
+        return false;
+    using W = WS<NU, NX, NY>;
     const size_t smem = (size_t)WPB * W::SMEM * sizeof(double);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(riccati_warp_kernel<NU, NX, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(riccati_warp_kernel<NU, NX, WPB, NY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attr = true;
     }
     const int chains = g.batch * g.P;
-    riccati_warp_kernel<NU, NX, WPB><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ra);
+    riccati_warp_kernel<NU, NX, WPB, NY><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ra);
     return true;
 }
 } // namespace
 
+bool riccati_warp_fuses_aug(const Geo &g, int ny) {
+    return !getenv("CYQ_NO_WARP_KERNEL") && !getenv("CYQ_NO_FUSED_AUG") && g.nu == 8 && g.nx == 16 && ny == 24;
+}
+
 bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
     if (getenv("CYQ_NO_WARP_KERNEL"))
         return false;
+    if (ra.p.aD) // fused Newton-system augmentation (config 4 stage shape)
+        return launch_w<8, 16, 1, 24>(g, st, ra);
     static const int wpb = getenv("CYQ_RICCATI_WPB") ? atoi(getenv("CYQ_RICCATI_WPB")) : 1;
     if (wpb == 2)
-        return launch_w<10, 20, 2>(g, st, ra) || launch_w<8, 16, 2>(g, st, ra) ||
-               launch_w<4, 12, 2>(g, st, ra) || launch_w<5, 10, 2>(g, st, ra);
-    return launch_w<10, 20, 1>(g, st, ra) || launch_w<8, 16, 1>(g, st, ra) ||
-           launch_w<4, 12, 1>(g, st, ra) || launch_w<5, 10, 1>(g, st, ra);
+        return launch_w<10, 20, 2, 0>(g, st, ra) || launch_w<8, 16, 2, 0>(g, st, ra) ||
+               launch_w<4, 12, 2, 0>(g, st, ra) || launch_w<5, 10, 2, 0>(g, st, ra);
+    return launch_w<10, 20, 1, 0>(g, st, ra) || launch_w<8, 16, 1, 0>(g, st, ra) ||
+           launch_w<4, 12, 1, 0>(g, st, ra) || launch_w<5, 10, 1, 0>(g, st, ra);
 }
 
 } // namespace cyqb

@@ -118,6 +118,16 @@ def flops_per_solve(N: int, nx: int, nu: int, P: int) -> float:
     return 2.0 * (ph["factor"] + ph["solve"])
 
 
+def assembly_flops(N: int, nx: int, nu: int, ny: int) -> float:
+    """Newton-system assembly of one instance (qpalm::assemble_newton,
+    qpalm.cpp:184-221, equality part), symmetric blocks counted once:
+    R_j + D_j' Σ D_j (lower), S_j + D_j' Σ C_j for j < N, Q_j + C_j' Σ C_j
+    (lower) for 1 <= j <= N. FLOPs = 2 x FMA (the Σ scaling folded into
+    the products, as the GPU kernels do)."""
+    fma = N * (ny * _tri(nu) + ny * nu * nx) + N * ny * _tri(nx)
+    return 2.0 * fma
+
+
 def problem_bytes(N: int, nx: int, nu: int) -> int:
     """Compulsory input bytes of one EqOCP as the C ABI reads it (full
     row-major blocks; SURVEY §8d counts packed R, Q)."""

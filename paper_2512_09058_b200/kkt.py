@@ -301,5 +301,29 @@ def augment_hessians(p, D, Cm, sigma, gamma_inv: float = 0.0, out=None,
     return out
 
 
-__all__ = ["augment_hessians", "FactorOptions", "Factor", "FactorizeError", "CudaError", "Context", "factor",
+def solve_newton(p, D, Cm, sigma, opts: FactorOptions, gamma_inv: float = 0.0, out=None,
+                 ctx: Context | None = None, raise_on_error: bool = True):
+    """One Newton system of the QPALM inner loop per instance: assembly as in
+    `augment_hessians` (qpalm::assemble_newton, qpalm.cpp:167-225) followed by
+    kkt::solve_problem (qpalm.cpp:368-413 factor + solve). For the config-4
+    stage shape (nu = 8, nx = 16, ny = 24) the assembly is fused into the
+    factorization's stage loads (the augmented Hessians never reach HBM);
+    other shapes run the assembly kernel first. CUDA torch tensors only."""
+    _check_opts(opts)
+    ctx = ctx or Context.default()
+    for a in [getattr(p, k) for k in OCP_FIELDS] + [D, Cm, sigma]:
+        if not _is_torch(a):
+            raise ValueError("solve_newton takes CUDA torch tensors")
+    sol = out if out is not None else _alloc_sol(p, True)
+    st = (_lib.CyqStatus * p.A.shape[0])()
+    rc = ctx.lib.cyq_solve_newton_batch(
+        ctx.h, C.byref(_dims(p, opts.P)), C.byref(_ocp_struct(p)), D.shape[2],
+        _ptr(D), _ptr(Cm), _ptr(sigma), float(gamma_inv),
+        C.byref(_lib.CyqSolBatch(*[_ptr(getattr(sol, k)) for k in SOL_FIELDS])), st)
+    if raise_on_error:
+        _raise_status(ctx, rc, st)
+    return sol if raise_on_error else (sol, rc, list(st))
+
+
+__all__ = ["augment_hessians", "solve_newton", "FactorOptions", "Factor", "FactorizeError", "CudaError", "Context", "factor",
            "solve", "solve_problem", "nu2", "EqOCPBatch", "EqRhsBatch", "EqSolutionBatch"]

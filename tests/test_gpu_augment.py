@@ -83,3 +83,66 @@ def test_twenty_iteration_loop_matches_oracle():
         ref, rc, _ = orc.solve_problem(seq[it], 16)
         assert rc == 0
         assert rel_error(host, ref).max() <= 1e-9
+
+
+def _host(sol):
+    return kkt.EqSolutionBatch(*[getattr(sol, k).cpu().numpy() for k in ("u", "x", "lam")])
+
+
+@pytest.mark.parametrize("gamma_inv", [0.0, 0.25])
+def test_fused_newton_matches_assembly_kernel_path(gamma_inv):
+    # kkt.solve_newton fuses the assembly into the stage-panel loads at the
+    # config-4 stage shape; it must agree with assembly kernel + solve_problem
+    base = synth.generate(4, seed=11, batch=3, N=32)
+    D, E, sig = synth.qpalm_data(base, seed=11, iters=2)
+    pd, Dd, Ed = _dev(base), _t(D), _t(E)
+    ctx = kkt.Context.default()
+    for it in range(2):
+        ctx.profile(True)
+        ctx.profile_read(reset=True)
+        fused = kkt.solve_newton(pd, Dd, Ed, _t(sig[it]), kkt.FactorOptions(P=16), gamma_inv=gamma_inv)
+        kern = ctx.profile_read(reset=True)
+        ctx.profile(False)
+        assert kern["augment"][1] == 0  # no separate assembly kernel ran
+        aug = kkt.augment_hessians(pd, Dd, Ed, _t(sig[it]), gamma_inv=gamma_inv)
+        two = kkt.solve_problem(aug, kkt.FactorOptions(P=16))
+        hf, h2 = _host(fused), _host(two)
+        assert rel_error(hf, h2).max() <= 1e-12
+        p_aug = EqOCPBatch(*[getattr(aug, k).cpu().numpy() for k in OCP_FIELDS])
+        rhs = EqRhsBatch.of_problem(p_aug)
+        res_f = kkt_residual(p_aug, rhs, hf).max(axis=1)
+        res_2 = kkt_residual(p_aug, rhs, h2).max(axis=1)
+        assert np.all(res_f <= np.maximum(1e-10, 4 * res_2))
+
+
+@pytest.mark.parametrize("it", [0, 1])
+def test_fused_newton_reproduces_reference(it):
+    p_ref, P, ref_sol, z = golden_util.load(f"cfg4_qpalm_N64_b2_P16_it{it}")
+    base = synth.generate(4, seed=0, batch=2, N=64)
+    D, E, sig = synth.qpalm_data(base, seed=0, iters=it + 1)
+    sol = kkt.solve_newton(_dev(base), _t(D), _t(E), _t(sig[it]), kkt.FactorOptions(P=P))
+    host = _host(sol)
+    assert rel_error(host, ref_sol).max() <= 1e-9
+    res = kkt_residual(p_ref, EqRhsBatch.of_problem(p_ref), host).max(axis=1)
+    assert np.all(res <= np.maximum(1e-10, 4 * z["residual"]))
+
+
+def test_newton_other_shape_uses_assembly_kernel():
+    # no fused variant for the config-1 stage shape: assembly kernel + pipeline
+    base = synth.generate(1, seed=5, batch=2, N=32)
+    D, E, sig = synth.qpalm_data(base, seed=5, iters=1, ny=12)
+    pd = _dev(base)
+    got = _host(kkt.solve_newton(pd, _t(D), _t(E), _t(sig[0]), kkt.FactorOptions(P=8)))
+    aug = kkt.augment_hessians(pd, _t(D), _t(E), _t(sig[0]))
+    ref = _host(kkt.solve_problem(aug, kkt.FactorOptions(P=8)))
+    for k in ("u", "x", "lam"):
+        assert np.array_equal(getattr(got, k), getattr(ref, k))
+
+
+def test_fused_newton_P_invariance():
+    base = synth.generate(4, seed=3, batch=2, N=64)
+    D, E, sig = synth.qpalm_data(base, seed=3, iters=1)
+    pd, Dd, Ed, sd = _dev(base), _t(D), _t(E), _t(sig[0])
+    a = _host(kkt.solve_newton(pd, Dd, Ed, sd, kkt.FactorOptions(P=16)))
+    b = _host(kkt.solve_newton(pd, Dd, Ed, sd, kkt.FactorOptions(P=4)))
+    assert rel_error(a, b).max() <= 1e-8
