@@ -29,7 +29,9 @@ template <int NU, int NX> struct BS {
     static constexpr int OFF_A = OFF_B + ((NX * NU + 1) & ~1);
     static constexpr int BUF = OFF_A + ((NX * NX + 1) & ~1);
     static constexpr int VEC = 64; // z (nux), lf/lb scratch
-    static constexpr int NBUF = 1; // single buffer: more resident warps hide the loads
+    // single buffer: more resident warps hide the loads (a double buffer
+    // was measured slower at both the config-1 and config-4 shapes)
+    static constexpr int NBUF = 1;
     static constexpr int PER_WARP = NBUF * BUF + VEC;
     // stored-tile offset of panel entry (r, col), r/col compile-time or not
     __host__ __device__ static constexpr int at(int r, int col) {

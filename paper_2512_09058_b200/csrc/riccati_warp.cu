@@ -114,6 +114,14 @@ template <int NU, int NX, int WPB, int NY>
 __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a) {
     using S = Shp<NU, NX>;
     using W = WS<NU, NX, NY>;
+    // "Pure" coupling tiles: trailing tiles whose rows and columns are all
+    // coupling rows (tile rows CT .. RT-1; tile row RT holds the rhs row).
+    // Their ALQ_s ALQ_s' terms cancel between stage s's trailing update and
+    // stage s+1's W W' (only LB LB' and the last stage's LA LA' remain in
+    // -Mfwd, kkt_factor.cpp:179-184), so both are skipped and LA LA' is
+    // subtracted once after the last stage.
+    constexpr int RT_ = S::RHS / 8;
+    auto pure = [](int ti, int tj) constexpr { return ti >= S::CT && tj >= S::CT && ti < RT_ && tj < RT_; };
     extern __shared__ __align__(16) double sm[];
     const Geo &g = a.g;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -290,7 +298,8 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
                     for (int ti = 0; ti < S::TT; ++ti)
 #pragma unroll
                         for (int tj = 0; tj <= ti; ++tj)
-                            dmma(P[S::T(ti, tj)], h ? w[ti].b : w[ti].a, h ? w[tj].b : w[tj].a);
+                            if (!pure(ti, tj)) // ALQ ALQ': cancels (see pure)
+                                dmma(P[S::T(ti, tj)], h ? w[ti].b : w[ti].a, h ? w[tj].b : w[tj].a);
                 }
             }
         }
@@ -384,7 +393,7 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
             // trailing update C(ti,tj) -= L(ti,kb) L(tj,kb)': the next diagonal
             // tile first (its factorization can start early), then both k
             // slices over all tiles so consecutive DMMAs are independent
-            if (kb + 1 < S::TT)
+            if (kb + 1 < S::CT) // a pivot diagonal tile (trailing ones: the loop below)
                 tile_gemm_nt_sub(P[S::T(kb + 1, kb + 1)], P[S::T(kb + 1, kb)], P[S::T(kb + 1, kb)]);
 #pragma unroll
             for (int h = 0; h < 2; ++h)
@@ -392,9 +401,14 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
                 for (int tj = kb + 1; tj < S::TT; ++tj)
 #pragma unroll
                     for (int ti = tj; ti < S::TT; ++ti)
-                        if (!(ti == kb + 1 && tj == kb + 1)) {
+                        if (!(ti == kb + 1 && tj == kb + 1 && kb + 1 < S::CT)) {
                             const Frag &li = P[S::T(ti, kb)], &lj = P[S::T(tj, kb)];
-                            dmma(P[S::T(ti, tj)], h ? -li.b : -li.a, h ? lj.b : lj.a);
+                            if (!pure(ti, tj) || 8 * kb + 7 < NU) {
+                                dmma(P[S::T(ti, tj)], h ? -li.b : -li.a, h ? lj.b : lj.a);
+                            } else if (8 * kb < NU) { // u columns only (LB LB')
+                                const double m = (h ? -li.b : -li.a);
+                                dmma(P[S::T(ti, tj)], (8 * kb + cq + h < NU) ? m : 0.0, h ? lj.b : lj.a);
+                            } // x columns: ALQ ALQ' cancels
                         }
         }
 
@@ -539,6 +553,21 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
     }
 
     if (ph) ph[n * 8] = clock64();
+    // -= LA LA' on the pure coupling tiles: the x columns of the last
+    // stage's coupling rows (the terms the stage loop skipped)
+#pragma unroll
+    for (int kb = 0; kb < S::CT; ++kb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int tj = S::CT; tj < RT_; ++tj)
+#pragma unroll
+                for (int ti = tj; ti < RT_; ++ti)
+                    if (8 * kb + 7 >= NU) {
+                        const Frag &li = P[S::T(ti, kb)], &lj = P[S::T(tj, kb)];
+                        const double m = (h ? -li.b : -li.a);
+                        dmma(P[S::T(ti, tj)], (8 * kb + cq + h >= NU) ? m : 0.0, h ? lj.b : lj.a);
+                    }
     // trailing tiles (coupling x coupling = -Mfwd, rhs x coupling = -fwd)
 #pragma unroll
     for (int u = 0; u < S::BT; ++u)

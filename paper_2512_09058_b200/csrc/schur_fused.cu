@@ -234,7 +234,7 @@ template <int XP> __host__ __device__ constexpr size_t sf_smem_doubles(int NW, i
 // others), and the solve vectors live in rank 0's shared memory, reached
 // through distributed shared memory.
 template <int NX, int NW, int CL>
-__global__ void __launch_bounds__(32 * NW, NW <= 4 ? 12 / NW : 1) schur_fused_kernel(SchurArgs a) {
+__global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_kernel(SchurArgs a) {
     using F = SF<NX>;
     constexpr int XT = F::XT, NL = F::NL, NF = F::NF, XP = F::XP;
     constexpr long long TL = 64LL * NL, TF = 64LL * NF;
