@@ -23,11 +23,19 @@ namespace {
 
 template <int NU, int NX> struct BS {
     using S = Shp<NU, NX>;
-    static constexpr int TILES = S::NPT * kTileElems;
+    // shared-memory strides chosen for conflict-free lane access: tiles at a
+    // 72-double stride (a row of consecutive tiles, 8 lanes each, lands on
+    // disjoint banks), B and A rows at odd strides (lane i walking row i)
+    // (measured: config 4 shape 8.47 -> 5.88 ms per step; at the config-1
+    // shape the padded layout was neutral-to-slower, so it keeps the dense one)
+    static constexpr bool PAD = NU * NX <= 128;
+    static constexpr int TS = PAD ? kTileElems + 8 : kTileElems;
+    static constexpr int BS_ = PAD ? (NU | 1) : NU, AS_ = PAD ? (NX | 1) : NX;
+    static constexpr int TILES = S::NPT * TS;
     static constexpr int OFF_Y = TILES, OFF_WL = OFF_Y + ((S::NUX + 1) & ~1);
     static constexpr int OFF_B = OFF_WL + ((NX + 1) & ~1);
-    static constexpr int OFF_A = OFF_B + ((NX * NU + 1) & ~1);
-    static constexpr int BUF = OFF_A + ((NX * NX + 1) & ~1);
+    static constexpr int OFF_A = OFF_B + ((NX * BS_ + 1) & ~1);
+    static constexpr int BUF = OFF_A + ((NX * AS_ + 1) & ~1);
     static constexpr int VEC = 64; // z (nux), lf/lb scratch
     // single buffer: more resident warps hide the loads (a double buffer
     // was measured slower at both the config-1 and config-4 shapes)
@@ -37,7 +45,7 @@ template <int NU, int NX> struct BS {
     __host__ __device__ static constexpr int at(int r, int col) {
         return ((r / 8) < S::CT ? S::T(r / 8, col / 8)
                                 : S::CT * (S::CT + 1) / 2 + (r / 8 - S::CT) * S::CT + col / 8) *
-                   kTileElems +
+                   TS +
                (r % 8) * 8 + col % 8;
     }
 };
@@ -49,16 +57,44 @@ __device__ __forceinline__ void bs_stage(const BacksubArgs &a, double *buf, size
     using L = BS<NU, NX>;
     const Geo &g = a.g;
     const int n = g.n, N = g.N;
-    wcopy<L::TILES, 0>(buf, a.fac + (chain * n + s) * S::NPT * kTileElems, lane);
+    {
+        const double *src = a.fac + (chain * n + s) * S::NPT * kTileElems;
+        if constexpr (!L::PAD) {
+            wcopy<L::TILES, 0>(buf, src, lane);
+        } else {
+#pragma unroll
+            for (int t = 0; t < S::NPT; ++t)
+                cp16(buf + t * L::TS + 2 * lane, src + t * kTileElems + 2 * lane);
+        }
+    }
     wcopy<S::NUX, 0>(buf + L::OFF_Y, a.y + (chain * n + s) * S::NUX, lane);
     if (s + 1 < n) {
         wcopy<NX, 0>(buf + L::OFF_WL, a.wl + (chain * n + s) * NX, lane);
         const int j1 = g.stage_of(c, s + 1);
         const bool in = j1 < N;
-        wcopy<NX * NU, 0>(buf + L::OFF_B, in ? a.p.B + ((size_t)b * N + j1) * NX * NU : nullptr,
-                          lane);
-        wcopy<NX * NX, 0>(buf + L::OFF_A,
-                          (in && j1 != 0) ? a.p.A + ((size_t)b * N + j1) * NX * NX : nullptr, lane);
+        const double *Bs = in ? a.p.B + ((size_t)b * N + j1) * NX * NU : nullptr;
+        const double *As = (in && j1 != 0) ? a.p.A + ((size_t)b * N + j1) * NX * NX : nullptr;
+        if constexpr (!L::PAD) {
+            wcopy<NX * NU, 0>(buf + L::OFF_B, Bs, lane);
+            wcopy<NX * NX, 0>(buf + L::OFF_A, As, lane);
+        } else {
+#pragma unroll
+            for (int e = lane; e < NX * NU; e += 32) {
+                double *d = buf + L::OFF_B + (e / NU) * L::BS_ + e % NU;
+                if (Bs)
+                    cp8(d, Bs + e);
+                else
+                    *d = 0.0;
+            }
+#pragma unroll
+            for (int e = lane; e < NX * NX; e += 32) {
+                double *d = buf + L::OFF_A + (e / NX) * L::AS_ + e % NX;
+                if (As)
+                    cp8(d, As + e);
+                else
+                    *d = 0.0;
+            }
+        }
     }
     cp_commit();
 }
@@ -103,7 +139,7 @@ __global__ void __launch_bounds__(32 * WPB) backsub_warp_kernel(BacksubArgs a) {
         double gk = 0.0;
 #pragma unroll
         for (int q = 0; q < NX; ++q)
-            gk += (k < NUX ? buf[L::at(TOP + q, 0) + (k / 8) * kTileElems + k % 8] : 0.0) * lf[q];
+            gk += (k < NUX ? buf[L::at(TOP + q, 0) + (k / 8) * L::TS + k % 8] : 0.0) * lf[q];
         double Y = (k < NUX) ? buf[L::OFF_Y + (k < NUX ? k : 0)] - gk : 0.0;
         const double idg = (k < NUX) ? 1.0 / buf[L::at(k < NUX ? k : 0, k < NUX ? k : 0)] : 0.0;
         if (s == n - 1) {
@@ -130,10 +166,10 @@ __global__ void __launch_bounds__(32 * WPB) backsub_warp_kernel(BacksubArgs a) {
             if (lane < NX) {
 #pragma unroll
                 for (int q = 0; q < NU; ++q)
-                    zn += buf[L::OFF_B + lane * NU + q] * z[q];
+                    zn += buf[L::OFF_B + lane * L::BS_ + q] * z[q];
 #pragma unroll
                 for (int q = 0; q < NX; ++q)
-                    zn += buf[L::OFF_A + lane * NX + q] * z[NU + q];
+                    zn += buf[L::OFF_A + lane * L::AS_ + q] * z[NU + q];
             }
             const double w = (lane < NX) ? -buf[L::OFF_WL + (lane < NX ? lane : 0)] - gx : 0.0;
             // t_i = w_i - sum_{k >= i} L_Q[k][i] zn_k
@@ -145,9 +181,12 @@ __global__ void __launch_bounds__(32 * WPB) backsub_warp_kernel(BacksubArgs a) {
                     t -= buf[L::at(NU + kk, NU + (lane < NX ? lane : 0))] * znk;
             }
             // lam^{j(s+1)}_i = -sum_{k <= i} L_Q[i][k] t_k
+            // (lane i walks its row from column i mod NX on: the per-lane
+            // skew makes the column reads of one step hit distinct banks)
             double lam = 0.0;
 #pragma unroll
-            for (int kk = 0; kk < NX; ++kk) {
+            for (int m = 0; m < NX; ++m) {
+                const int kk = L::PAD ? (lane + m) % NX : m;
                 const double tk = __shfl_sync(0xffffffffu, t, kk);
                 if (lane >= kk && lane < NX)
                     lam -= buf[L::at(NU + (lane < NX ? lane : 0), NU + kk)] * tk;
@@ -165,7 +204,7 @@ __global__ void __launch_bounds__(32 * WPB) backsub_warp_kernel(BacksubArgs a) {
             if (lane == r)
                 Y = zr;
             else if (lane < r)
-                Y -= buf[L::at(r, 0) + (lane / 8) * kTileElems + lane % 8] * zr;
+                Y -= buf[L::at(r, 0) + (lane / 8) * L::TS + lane % 8] * zr;
         }
         __syncwarp();
         if (L::NBUF == 1 && s > 0) { // buffer consumed: fetch stage s-1

@@ -8,12 +8,13 @@
 //
 // Execution model (one CTA of NW warps per partition column):
 //  * the extended panel (TT x TT lower tiles, 231 at config 3) lives in the
-//    warps' registers for the stage. Warp kb (< CT) owns the pivot diagonal
-//    tile (kb, kb) in a dedicated register tile; every other tile is on a
-//    LIST ordered by tile column descending (and tile row descending inside
-//    a column), dealt round-robin to the warps. So at block column kb the
-//    tiles a warp must update (tj > kb) are a PREFIX of its list and the
-//    update loop leaves through a warp-uniform branch: no predicated-off
+//    warps' registers for the stage. Warp kb+1 (kb < CT) owns the pivot
+//    diagonal tile (kb, kb) in a dedicated register tile; every other tile is
+//    on a per-warp LIST ordered by tile column descending, planned on the
+//    host (launch_c: a greedy over a cycle model, so that the look-ahead
+//    warp of each block column holds few tiles right of it). At block column
+//    kb the tiles a warp must update (tj > kb) are a PREFIX of its list and
+//    the update loop leaves through a warp-uniform branch: no predicated-off
 //    DMMA is ever issued (they occupy the DMMA pipe like real ones; the
 //    previous triangular-order ownership issued 58% of its DMMAs
 //    predicated off);
@@ -22,7 +23,7 @@
 //        at the end of the previous step, are solved in place there
 //        (X <- X L_kk^{-T} = X (L_kk^{-1})', two DMMAs) by any warp -- a
 //        runtime loop over the column, no register-array indexing;
-//    (B) warp kb+1 applies column kb to its diagonal tile and factors it
+//    (B) the owner of (kb+1, kb+1) applies column kb to it and factors it
 //        (identity tile carried through the pivot steps -> L^{-1} for free),
 //        while every warp takes its solved column-kb tiles back into
 //        registers, applies C -= L_i L_j' to its list prefix and publishes
