@@ -144,10 +144,26 @@ int cyq_solve_newton_batch(cyq_ctx *ctx, const cyq_dims *dims,
                            const double *sigma, double gamma_inv,
                            const cyq_sol_batch *sol, cyq_status *status);
 
+/* Exact line search of the QPALM inner loop (qpalm::line_search_exact,
+ * line_search.cpp:112-206, over LineSearchData::add_term of every term,
+ * line_search.cpp:9-27), batched: for instance b, the root tau of
+ *   psi'(tau) = eta[b] tau + beta[b] + sum_i delta_i [delta_i tau - alpha_i]_+
+ * over the m terms alpha[b][i], delta[b][i] (delta = 0 or a non-finite
+ * alpha / delta drops the term, as add_term does). status[b] (nullable):
+ * CYQ_OK, or CYQ_INVALID_ARG when psi'(0) > 0 (the reference throws
+ * std::invalid_argument); psi'(0) == 0 gives tau = 0. iterations (nullable,
+ * DEVICE) receives the probes + scan steps per instance. alpha, delta, eta,
+ * beta, tau are DEVICE pointers; the call synchronizes the context stream
+ * (per-instance status to the host). Returns the worst status. */
+int cyq_line_search_batch(cyq_ctx *ctx, int64_t batch, int64_t m,
+                          const double *alpha, const double *delta,
+                          const double *eta, const double *beta, double *tau,
+                          int32_t *status, int64_t *iterations);
+
 /* Per-kernel device timing: when enabled, every launch of the pipeline is
  * bracketed by CUDA events on the context stream. `read` synchronizes and
  * returns, per kernel (0 riccati_panel, 1 schur_cr, 2 backsub, 3 forward
- * sweep, 4 Newton-system assembly) -- ms[5], launches[5] -- the summed
+ * sweep, 4 Newton-system assembly / line search) -- ms[5], launches[5] -- the summed
  * milliseconds and launch counts since the last reset. */
 int cyq_ctx_profile(cyq_ctx *ctx, int enable);
 int cyq_ctx_profile_read(cyq_ctx *ctx, double *ms, int64_t *launches,

@@ -983,3 +983,101 @@ double oc_bench_solve_problem(const oc_dims *d, const oc_ocp *p,
         return -1.0;
     return (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
 }
+
+
+/* ---- exact line search (qpalm::line_search_exact) ---------------------- */
+
+typedef struct {
+    double t, w;
+} oc_bp;
+
+static int oc_bp_cmp(const void *a, const void *b) {
+    const double x = ((const oc_bp *)a)->t, y = ((const oc_bp *)b)->t;
+    return (x > y) - (x < y);
+}
+
+/* LineSearchData::add_term (line_search.cpp:9-27) for every term, the
+ * 0+ fold of the w < 0 breakpoints (line_search.cpp:116-124), the descent
+ * check (:125-130), then the root on the sorted breakpoints: the
+ * reference's final sort + scan (:154-171) applied to the whole set (its
+ * pivot partitions only narrow the set the scan starts from). */
+int oc_line_search(int64_t m, const double *alpha, const double *delta,
+                   double eta, double beta, double *tau) {
+    oc_bp *pts = (oc_bp *)malloc(sizeof(oc_bp) * (size_t)(m > 0 ? m : 1));
+    int64_t np = 0;
+    for (int64_t i = 0; i < m; ++i) {
+        const double d = delta[i];
+        if (d == 0)
+            continue;
+        const double t = alpha[i] / d;
+        if (!isfinite(t))
+            continue;
+        const double w = d * fabs(d);
+        if (t <= 0) {
+            if (w > 0) {
+                eta += w;
+                beta -= t * w;
+            }
+            continue;
+        }
+        pts[np].t = t;
+        pts[np].w = w;
+        ++np;
+    }
+    double eta_c = eta, beta_c = beta;
+    for (int64_t i = 0; i < np; ++i)
+        if (pts[i].w < 0) {
+            eta_c -= pts[i].w;
+            beta_c += pts[i].t * pts[i].w;
+        }
+    if (beta_c >= 0) {
+        free(pts);
+        *tau = 0;
+        return beta_c == 0 ? 0 : 1;
+    }
+    qsort(pts, (size_t)np, sizeof(oc_bp), oc_bp_cmp);
+    for (int64_t i = 0; i < np; ++i) {
+        if (eta_c * pts[i].t + beta_c >= 0)
+            break;
+        eta_c += pts[i].w;
+        beta_c -= pts[i].t * pts[i].w;
+    }
+    *tau = -beta_c / eta_c;
+    free(pts);
+    return 0;
+}
+
+typedef struct {
+    int64_t b0, b1, m;
+    const double *alpha, *delta, *eta, *beta;
+    double *tau;
+} oc_ls_job;
+
+static void *oc_ls_worker(void *arg) {
+    oc_ls_job *j = (oc_ls_job *)arg;
+    for (int64_t b = j->b0; b < j->b1; ++b)
+        oc_line_search(j->m, j->alpha + b * j->m, j->delta + b * j->m, j->eta[b], j->beta[b],
+                       j->tau + b);
+    return NULL;
+}
+
+double oc_bench_line_search(int64_t batch, int64_t m, const double *alpha, const double *delta,
+                            const double *eta, const double *beta, double *tau, int threads) {
+    if (threads < 1)
+        threads = 1;
+    pthread_t th[256];
+    oc_ls_job jobs[256];
+    if (threads > 256)
+        threads = 256;
+    struct timespec t0, t1;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+    for (int k = 0; k < threads; ++k) {
+        jobs[k] = (oc_ls_job){batch * k / threads, batch * (k + 1) / threads, m, alpha, delta, eta,
+                              beta, tau};
+        pthread_create(&th[k], NULL, oc_ls_worker, &jobs[k]);
+    }
+    for (int k = 0; k < threads; ++k)
+        pthread_join(th[k], NULL);
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    return (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
+}

@@ -80,7 +80,24 @@ void oc_fma_counts(const oc_dims *d, uint64_t *out);
 double oc_bench_solve_problem(const oc_dims *d, const oc_ocp *p,
                               int64_t n_solves, int threads, oc_sol *out);
 
+/* Exact line search (qpalm::line_search_exact, line_search.cpp:112-206)
+ * of psi'(tau) = eta tau + beta + sum_i delta_i [delta_i tau - alpha_i]_+
+ * over m terms registered as LineSearchData::add_term (line_search.cpp:
+ * 9-27). Returns 0 (tau set), 1 when psi'(0) > 0 (not a descent direction;
+ * the reference throws std::invalid_argument). */
+int oc_line_search(int64_t m, const double *alpha, const double *delta,
+                   double eta, double beta, double *tau);
+/* Batched line search on `threads` pthreads; returns elapsed seconds. */
+double oc_bench_line_search(int64_t batch, int64_t m, const double *alpha,
+                            const double *delta, const double *eta,
+                            const double *beta, double *tau, int threads);
+
 /* ---- reference shim (oracle/_ref/libcyqref.so) ------------------------ */
+int ref_line_search(int64_t m, const double *alpha, const double *delta,
+                    double eta, double beta, double *tau, int64_t *iters);
+double ref_bench_line_search(int64_t batch, int64_t m, const double *alpha,
+                             const double *delta, const double *eta,
+                             const double *beta, double *tau, int threads);
 int ref_solve_problem(const oc_dims *d, const oc_ocp *p, int64_t vlen,
                       int threads, oc_sol *out, double *resid,
                       oc_status *st);

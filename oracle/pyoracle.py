@@ -105,6 +105,14 @@ class _Base:
         return int(out[0]), int(out[1])
 
 
+def _ls_arrays(alpha, delta, eta, beta):
+    alpha = np.ascontiguousarray(alpha, dtype=np.float64)
+    delta = np.ascontiguousarray(delta, dtype=np.float64)
+    eta = np.ascontiguousarray(eta, dtype=np.float64).reshape(-1)
+    beta = np.ascontiguousarray(beta, dtype=np.float64).reshape(-1)
+    return alpha.reshape(len(eta), -1), delta.reshape(len(eta), -1), eta, beta
+
+
 class Oracle(_Base):
     """The plain-C restatement (oracle/cyq_oracle.c)."""
 
@@ -131,6 +139,25 @@ class Oracle(_Base):
 
     def factor_blocks(self, p, P):
         return _factor_blocks(self.lib.oc_factor_export, p, P, None)
+
+    def line_search(self, alpha, delta, eta, beta):
+        """tau[b], rc[b] of oc_line_search for a batch (alpha, delta: (b, m))."""
+        alpha, delta, eta, beta = _ls_arrays(alpha, delta, eta, beta)
+        tau, rc = np.zeros(len(eta)), np.zeros(len(eta), dtype=np.int32)
+        t = C.c_double()
+        for b in range(len(eta)):
+            rc[b] = self.lib.oc_line_search(i64(alpha.shape[1]), _p(alpha[b]), _p(delta[b]),
+                                            C.c_double(eta[b]), C.c_double(beta[b]), C.byref(t))
+            tau[b] = t.value
+        return tau, rc
+
+    def bench_line_search(self, alpha, delta, eta, beta, threads):
+        alpha, delta, eta, beta = _ls_arrays(alpha, delta, eta, beta)
+        tau = np.zeros(len(eta))
+        f = self.lib.oc_bench_line_search
+        f.restype = C.c_double
+        return f(i64(len(eta)), i64(alpha.shape[1]), _p(alpha), _p(delta), _p(eta), _p(beta),
+                 _p(tau), C.c_int(threads))
 
     def bench(self, p, P, n_solves, threads):
         sol = _sol_arrays(p)
@@ -183,6 +210,27 @@ class RefOracle(_Base):
         f(i64(N), i64(nx), i64(nu), C.c_uint64(seed), C.c_double(conditioning),
           *[_p(a) for a in arrs])
         return EqOCPBatch(*arrs)
+
+    def line_search(self, alpha, delta, eta, beta):
+        """tau[b], rc[b], iterations[b] of the reference's line_search_exact."""
+        alpha, delta, eta, beta = _ls_arrays(alpha, delta, eta, beta)
+        tau, rc = np.zeros(len(eta)), np.zeros(len(eta), dtype=np.int32)
+        it = np.zeros(len(eta), dtype=np.int64)
+        t, n = C.c_double(), i64()
+        for b in range(len(eta)):
+            rc[b] = self.lib.ref_line_search(i64(alpha.shape[1]), _p(alpha[b]), _p(delta[b]),
+                                             C.c_double(eta[b]), C.c_double(beta[b]), C.byref(t),
+                                             C.byref(n))
+            tau[b], it[b] = t.value, n.value
+        return tau, rc, it
+
+    def bench_line_search(self, alpha, delta, eta, beta, threads):
+        alpha, delta, eta, beta = _ls_arrays(alpha, delta, eta, beta)
+        tau = np.zeros(len(eta))
+        f = self.lib.ref_bench_line_search
+        f.restype = C.c_double
+        return f(i64(len(eta)), i64(alpha.shape[1]), _p(alpha), _p(delta), _p(eta), _p(beta),
+                 _p(tau), C.c_int(threads))
 
     def bench(self, p, P, n_solves, threads, vlen=4):
         return self.lib.ref_bench_solve_problem(C.byref(_dims(p, P)), C.byref(_ocp(p)),

@@ -329,3 +329,48 @@ double ref_bench_solve_problem(const oc_dims *d, const oc_ocp *p,
 }
 
 } // extern "C"
+
+
+// ---- exact line search: the reference's qpalm::line_search_exact --------
+#include <cyqlone/line_search.hpp>
+
+#include <chrono>
+#include <stdexcept>
+#include <thread>
+
+extern "C" int ref_line_search(int64_t m, const double *alpha, const double *delta, double eta,
+                               double beta, double *tau, int64_t *iters) {
+    cyqlone::qpalm::LineSearchData ls;
+    ls.eta = eta;
+    ls.beta = beta;
+    for (int64_t i = 0; i < m; ++i)
+        ls.add_term(alpha[i], delta[i]);
+    ls.finalize();
+    try {
+        auto r = cyqlone::qpalm::line_search_exact(ls);
+        *tau = r.tau;
+        if (iters)
+            *iters = r.iterations;
+        return 0;
+    } catch (const std::invalid_argument &) {
+        *tau = 0;
+        return 1;
+    }
+}
+
+extern "C" double ref_bench_line_search(int64_t batch, int64_t m, const double *alpha,
+                                        const double *delta, const double *eta,
+                                        const double *beta, double *tau, int threads) {
+    if (threads < 1)
+        threads = 1;
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> th;
+    for (int k = 0; k < threads; ++k)
+        th.emplace_back([=] {
+            for (int64_t b = batch * k / threads; b < batch * (k + 1) / threads; ++b)
+                ref_line_search(m, alpha + b * m, delta + b * m, eta[b], beta[b], tau + b, nullptr);
+        });
+    for (auto &t : th)
+        t.join();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}

@@ -64,6 +64,8 @@ SIGNATURES = {
     "cyq_version": (C.c_char_p, []),
     "cyq_augment_hessians_batch": (C.c_int, [C.c_void_p, C.POINTER(CyqDims), i64] + [C.c_void_p] * 6
                                    + [C.c_double] + [C.c_void_p] * 3),
+    "cyq_line_search_batch": (C.c_int, [C.c_void_p, i64, i64] + [C.c_void_p] * 5
+                              + [C.POINTER(C.c_int32), C.c_void_p]),
     "cyq_solve_newton_batch": (C.c_int, [C.c_void_p, C.POINTER(CyqDims), C.POINTER(CyqOcpBatch), i64]
                                + [C.c_void_p] * 3 + [C.c_double, C.POINTER(CyqSolBatch), C.c_void_p]),
 }

@@ -31,6 +31,8 @@ struct cyq_ctx {
     size_t wsbuf_bytes = 0;
     void *augbuf = nullptr; // augmented R, S, Q of cyq_solve_newton_batch's two-kernel path
     size_t augbuf_bytes = 0;
+    void *lsbuf = nullptr; // line-search breakpoints + per-instance status
+    size_t lsbuf_bytes = 0;
     cudaStream_t copy_stream = nullptr; // host->device staging of chunked calls
     // per-kernel timing (cyq_ctx_profile)
     bool profile = false;
@@ -525,6 +527,8 @@ int cyq_ctx_destroy(cyq_ctx *ctx) {
         cudaFree(ctx->wsbuf);
     if (ctx->augbuf)
         cudaFree(ctx->augbuf);
+    if (ctx->lsbuf)
+        cudaFree(ctx->lsbuf);
     for (auto &e : ctx->ev) {
         cudaEventDestroy(e.second.first);
         cudaEventDestroy(e.second.second);
@@ -925,6 +929,41 @@ int cyq_solve_newton_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_bat
     if (rc)
         return rc;
     return decode_status(ctx, g, ws.fail, status);
+}
+
+int cyq_line_search_batch(cyq_ctx *ctx, int64_t batch, int64_t m, const double *alpha,
+                          const double *delta, const double *eta, const double *beta, double *tau,
+                          int32_t *status, int64_t *iterations) {
+    if (!ctx || !alpha || !delta || !eta || !beta || !tau)
+        return set_err(ctx, CYQ_INVALID_ARG, "null argument");
+    if (batch < 1 || m < 0)
+        return set_err(ctx, CYQ_INVALID_ARG, "batch >= 1 and m >= 0 required");
+    CU(cudaSetDevice(ctx->device));
+    const size_t tw = (size_t)batch * (size_t)(m > 0 ? m : 1) * 2 * sizeof(double);
+    int rc = ensure(ctx, &ctx->lsbuf, &ctx->lsbuf_bytes, tw + (size_t)batch * sizeof(int));
+    if (rc)
+        return rc;
+    int *dstat = reinterpret_cast<int *>(static_cast<char *>(ctx->lsbuf) + tw);
+    LineSearchArgs la{batch, m, alpha, delta, eta, beta, tau, dstat,
+                      reinterpret_cast<long long *>(iterations), static_cast<double *>(ctx->lsbuf)};
+    {
+        Timed t(ctx, 4);
+        launch_line_search(ctx->stream, la);
+    }
+    CU(cudaGetLastError());
+    std::vector<int> hs((size_t)batch);
+    CU(cudaMemcpyAsync(hs.data(), dstat, hs.size() * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    int worst = CYQ_OK;
+    for (int64_t k = 0; k < batch; ++k) {
+        const int code = hs[(size_t)k] == 0 ? CYQ_OK : (hs[(size_t)k] == 1 ? CYQ_INVALID_ARG : CYQ_CUDA_ERR);
+        if (status)
+            status[k] = code;
+        worst = std::max(worst, code);
+    }
+    if (worst == CYQ_INVALID_ARG)
+        set_err(ctx, worst, "line_search_exact: not a descent direction (psi'(0) > 0) for some instance");
+    return worst;
 }
 
 const char *cyq_version(void) {

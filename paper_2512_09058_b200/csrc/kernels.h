@@ -94,6 +94,17 @@ struct SchurLayout {
 
 template <int MAXT> __global__ void riccati_panel_kernel_t(RiccatiArgs a);
 // compile-time (nu, nx) warp-per-chain fast path; false if not instantiated
+// exact QPALM line search (linesearch.cu), one CTA per instance
+struct LineSearchArgs {
+    long long batch, m;
+    const double *alpha, *delta, *eta, *beta; // [batch][m], [batch][m], [batch], [batch]
+    double *tau;                              // [batch]
+    int *status;                              // [batch]: 0 ok, 1 not a descent direction
+    long long *iters;                         // [batch] probes + scan steps (nullable)
+    double *scratch;                          // [batch][m][2] breakpoints (t, w)
+};
+void launch_line_search(cudaStream_t st, const LineSearchArgs &a);
+
 bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
 // true when the warp kernel has a fused Newton-system augmentation variant
 // for this stage shape and ny (ProbView::aD path)

@@ -1,0 +1,258 @@
+// Exact line search of the QPALM inner loop, batched:
+// the reference's qpalm::line_search_exact (/root/reference/proj/src/
+// line_search.cpp:112-206) over the terms registered by
+// LineSearchData::add_term (line_search.cpp:9-27), one instance per CTA.
+//
+// psi'(tau) = eta tau + beta + sum_i delta_i [delta_i tau - alpha_i]_+ is
+// piecewise linear and nondecreasing; each term with a finite positive
+// breakpoint t = alpha / delta contributes w = delta |delta| to the slope
+// once tau crosses t (w < 0 terms are active below t and are folded into
+// the coefficients at tau = 0+, line_search.cpp:116-124). The root lies on
+// one linear segment between consecutive breakpoints.
+//
+// GPU formulation (no global sort): the breakpoints of an instance stay in
+// an L2-resident scratch array; a bracket (lo, hi) around the root shrinks by
+// value bisection (geometric midpoints, after probing the largest and the
+// smallest breakpoint), each probe one block-wide pass that sums w and t w
+// over t < p and counts the breakpoints left in each half (fixed-order
+// reductions: deterministic). Once at most kLsSmall breakpoints remain in
+// the bracket they are gathered into shared memory, ranked (t, then index)
+// and scanned like the reference's final sort + scan
+// (line_search.cpp:154-171); tau = -beta_c / eta_c, clamped to the bracket
+// top (line_search.cpp:145-150, 168-170). The summation order differs from
+// the reference's partition order, so results agree to rounding.
+#include "kernels.h"
+
+#include <cmath>
+#include <cstdint>
+
+namespace cyqb {
+
+namespace {
+
+constexpr int kLsThreads = 256;
+constexpr int kLsWarps = kLsThreads / 32;
+constexpr int kLsSmall = 64;
+
+// block-wide sums of K doubles (fixed order: lane tree, then warps 0..7)
+template <int K> __device__ __forceinline__ void block_sum(double (&v)[K], double *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            red[k * kLsWarps + warp] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < kLsWarps; ++w)
+            s += red[k * kLsWarps + w];
+        v[k] = s;
+    }
+}
+
+// SMEM: the instance's breakpoints (t, w) in dynamic shared memory, else in
+// the global (L2-resident) scratch array -- the launcher uses the latter
+template <bool SMEM>
+__global__ void __launch_bounds__(kLsThreads) line_search_kernel(LineSearchArgs a) {
+    extern __shared__ double2 tw_sm[];
+    __shared__ double red[6 * kLsWarps];
+    __shared__ double st[kLsSmall], sw[kLsSmall];
+    __shared__ long long sidx[kLsSmall];
+    __shared__ double ot[kLsSmall], ow[kLsSmall];
+    __shared__ int ncomp;
+    const int tid = threadIdx.x;
+    const long long b = blockIdx.x, m = a.m;
+    const double *al = a.alpha + b * m, *de = a.delta + b * m;
+    double2 *tw = SMEM ? tw_sm : reinterpret_cast<double2 *>(a.scratch) + b * m;
+
+    // ---- add_term for every term (line_search.cpp:9-27) + fold at 0+ ----
+    double v[6] = {0, 0, 0, 0, 0, 0}; // d_eta, d_beta, d_eta_lo, d_beta_lo, count, -
+    double tmax = 0.0, tmin = INFINITY;
+    for (long long i = tid; i < m; i += kLsThreads) {
+        const double alpha = al[i], delta = de[i];
+        double t = INFINITY, w = 0.0;
+        if (delta != 0.0) {
+            const double tt = alpha / delta;
+            if (isfinite(tt)) {
+                const double ww = delta * fabs(delta);
+                if (tt <= 0.0) {
+                    if (ww > 0.0) { // active for all tau >= 0
+                        v[0] += ww;
+                        v[1] -= tt * ww;
+                    }
+                } else {
+                    t = tt;
+                    w = ww;
+                    if (ww < 0.0) { // active just above 0 (line_search.cpp:116-124)
+                        v[2] -= ww;
+                        v[3] += tt * ww;
+                    }
+                    v[4] += 1.0;
+                    tmax = fmax(tmax, tt);
+                    tmin = fmin(tmin, tt);
+                }
+            }
+        }
+        tw[i] = make_double2(t, w);
+    }
+    // max / min of the breakpoints ride in the sum reduction as extra passes
+    block_sum<6>(v, red);
+    {
+        double mx = tmax, mn = tmin;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        }
+        __syncthreads();
+        if ((tid & 31) == 0) {
+            red[tid >> 5] = mx;
+            red[kLsWarps + (tid >> 5)] = mn;
+        }
+        __syncthreads();
+        mx = 0.0;
+        mn = INFINITY;
+        for (int w = 0; w < kLsWarps; ++w) {
+            mx = fmax(mx, red[w]);
+            mn = fmin(mn, red[kLsWarps + w]);
+        }
+        tmax = mx;
+        tmin = mn;
+    }
+    const double eta0 = a.eta[b] + v[0], beta0 = a.beta[b] + v[1];
+    const double eta_lo = eta0 + v[2], beta_lo = beta0 + v[3];
+    long long cnt = (long long)v[4];
+    int iters = 0;
+    if (!(beta_lo < 0.0)) { // psi'(0+) >= 0 (line_search.cpp:125-130)
+        if (tid == 0) {
+            a.tau[b] = 0.0;
+            a.status[b] = beta_lo == 0.0 ? 0 : 1;
+            if (a.iters)
+                a.iters[b] = 0;
+        }
+        return;
+    }
+
+    // ---- bracket the root by probes: F(p) = psi'(p), breakpoints t < p crossed
+    double lo = 0.0, hi = INFINITY;
+    auto probe = [&](double p, long long &c_below, long long &c_above) -> double {
+        double s[6] = {0, 0, 0, 0, 0, 0}; // sum w, sum t w, #(lo, p), #(p, hi)
+        for (long long i = tid; i < m; i += kLsThreads) {
+            const double2 e = tw[i];
+            if (e.x < p) {
+                s[0] += e.y;
+                s[1] += e.x * e.y;
+            }
+            s[2] += (e.x > lo && e.x < p) ? 1.0 : 0.0;
+            s[3] += (e.x > p && e.x < hi) ? 1.0 : 0.0;
+        }
+        block_sum<6>(s, red);
+        c_below = (long long)s[2];
+        c_above = (long long)s[3];
+        ++iters;
+        return (eta_lo + s[0]) * p + (beta_lo - s[1]);
+    };
+    if (cnt > 0) {
+        long long cb, ca;
+        // largest breakpoint: beyond it psi' is linear
+        double F = probe(tmax, cb, ca);
+        if (F < 0.0) {
+            lo = tmax;
+            cnt = 0;
+        } else {
+            hi = tmax;
+            cnt = cb;
+        }
+        if (cnt > 0) { // smallest breakpoint: the bracket gets a positive lower end
+            F = probe(tmin, cb, ca);
+            if (F < 0.0) {
+                lo = tmin;
+                cnt = ca;
+            } else {
+                hi = tmin;
+                cnt = cb;
+            }
+        }
+        // value bisection (geometric midpoint) down to a small bracket
+        for (int guard = 0; cnt > kLsSmall && guard < 2048; ++guard) {
+            const double p = sqrt(lo) * sqrt(hi);
+            if (!(p > lo && p < hi))
+                break;
+            F = probe(p, cb, ca);
+            if (F < 0.0) {
+                lo = p;
+                cnt = ca;
+            } else {
+                hi = p;
+                cnt = cb;
+            }
+        }
+    }
+
+    // ---- gather the bracket's breakpoints, coefficients at lo+ -------------
+    if (tid == 0)
+        ncomp = 0;
+    __syncthreads();
+    double s2[6] = {0, 0, 0, 0, 0, 0};
+    for (long long i = tid; i < m; i += kLsThreads) {
+        const double2 e = tw[i];
+        if (e.x <= lo) {
+            s2[0] += e.y;
+            s2[1] += e.x * e.y;
+        } else if (e.x < hi) {
+            const int k = atomicAdd(&ncomp, 1);
+            if (k < kLsSmall) {
+                st[k] = e.x;
+                sw[k] = e.y;
+                sidx[k] = i;
+            }
+        }
+    }
+    block_sum<6>(s2, red); // (includes the __syncthreads that publishes st/sw)
+    const int nc = ncomp < kLsSmall ? ncomp : kLsSmall;
+    // rank by (t, original index): deterministic order for ties
+    if (tid < nc) {
+        int r = 0;
+        for (int j = 0; j < nc; ++j)
+            r += (st[j] < st[tid] || (st[j] == st[tid] && sidx[j] < sidx[tid])) ? 1 : 0;
+        ot[r] = st[tid];
+        ow[r] = sw[tid];
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double eta_c = eta_lo + s2[0], beta_c = beta_lo - s2[1];
+        for (int k = 0; k < nc; ++k) { // line_search.cpp:160-169
+            ++iters;
+            if (eta_c * ot[k] + beta_c >= 0.0)
+                break;
+            eta_c += ow[k];
+            beta_c -= ot[k] * ow[k];
+        }
+        double tau = -beta_c / eta_c;
+        if (isfinite(hi))
+            tau = fmin(tau, hi);
+        a.tau[b] = tau;
+        a.status[b] = ncomp <= kLsSmall ? 0 : 3; // 3: bracket overflow (not reached)
+        if (a.iters)
+            a.iters[b] = iters;
+    }
+}
+
+} // namespace
+
+void launch_line_search(cudaStream_t st, const LineSearchArgs &a) {
+    // breakpoints in the L2-resident scratch: measured 0.205 ms for 512 x
+    // 12336 terms vs 0.359 ms with them in shared memory (one 8-warp CTA
+    // per SM then, too little parallelism to hide the reduction latency)
+    line_search_kernel<false><<<(unsigned)a.batch, kLsThreads, 0, st>>>(a);
+}
+
+} // namespace cyqb

@@ -325,5 +325,36 @@ def solve_newton(p, D, Cm, sigma, opts: FactorOptions, gamma_inv: float = 0.0, o
     return sol if raise_on_error else (sol, rc, list(st))
 
 
-__all__ = ["augment_hessians", "solve_newton", "FactorOptions", "Factor", "FactorizeError", "CudaError", "Context", "factor",
+def line_search_exact(alpha, delta, eta, beta, ctx: Context | None = None,
+                      raise_on_error: bool = True, iterations: bool = False):
+    """qpalm::line_search_exact (line_search.cpp:112-206) for a batch: tau[b]
+    = root of psi'(tau) = eta[b] tau + beta[b] + sum_i delta[b,i]
+    [delta[b,i] tau - alpha[b,i]]_+ (terms as LineSearchData::add_term,
+    line_search.cpp:9-27). CUDA torch tensors: alpha, delta (b, m), eta,
+    beta (b,). Raises ValueError (the reference's std::invalid_argument) if
+    psi'(0) > 0 for some instance, unless raise_on_error=False (then returns
+    (tau, status list))."""
+    import torch
+
+    ctx = ctx or Context.default()
+    for a in (alpha, delta, eta, beta):
+        if not _is_torch(a):
+            raise ValueError("line_search_exact takes CUDA torch tensors")
+    b, m = alpha.shape[0], (alpha.shape[1] if alpha.dim() > 1 else 0)
+    tau = torch.empty(b, dtype=torch.float64, device=alpha.device)
+    its = torch.zeros(b, dtype=torch.int64, device=alpha.device)
+    st = (C.c_int32 * b)()
+    rc = ctx.lib.cyq_line_search_batch(ctx.h, b, m, _ptr(alpha), _ptr(delta), _ptr(eta), _ptr(beta),
+                                       _ptr(tau), st, C.c_void_p(its.data_ptr()))
+    if rc == _lib.CYQ_INVALID_ARG and raise_on_error:
+        raise ValueError(ctx.last_error())
+    if rc not in (_lib.CYQ_OK, _lib.CYQ_INVALID_ARG):
+        raise CudaError(f"cyq_line_search_batch failed ({rc}): {ctx.last_error()}")
+    out = (tau, list(st)) if not raise_on_error else tau
+    if iterations:
+        return (out, its) if raise_on_error else (tau, list(st), its)
+    return out
+
+
+__all__ = ["augment_hessians", "solve_newton", "line_search_exact", "FactorOptions", "Factor", "FactorizeError", "CudaError", "Context", "factor",
            "solve", "solve_problem", "nu2", "EqOCPBatch", "EqRhsBatch", "EqSolutionBatch"]

@@ -139,3 +139,29 @@ def qpalm_sequence(base: EqOCPBatch, seed: int = 0, iters: int = 20, ny: int = 2
         ES = E * sig[..., None]
         Q = base.Q + np.einsum("bjki,bjkl->bjil", ES, E)
         yield EqOCPBatch(base.A, base.B, R, S, Q, base.f, base.r, base.q, base.x_init)
+
+
+def line_search_data(batch: int, m: int, seed: int = 0, one_sided: float = 0.05,
+                     zero_delta: float = 0.02):
+    """Seeded exact-line-search instances with the reference test's
+    distributions (test_line_search.cpp:17-31): eta ~ 2 U(0.1, 3), psi'(0+)
+    ~ -5 U(0.1, 3) (descent at tau = 0), alpha, delta ~ N(0, 1); plus the
+    QPALM cases add_term filters: infinite alpha (one-sided bounds,
+    qpalm.cpp:285-296) and delta = 0. Returns alpha, delta (b, m), eta, beta (b,)."""
+    rng = np.random.default_rng([seed, 5])
+    eta = 2.0 * rng.uniform(0.1, 3.0, batch)
+    beta = -5.0 * rng.uniform(0.1, 3.0, batch)
+    alpha = rng.standard_normal((batch, m))
+    delta = rng.standard_normal((batch, m))
+    alpha[rng.random((batch, m)) < one_sided] = np.inf
+    delta[rng.random((batch, m)) < zero_delta] = 0.0
+    # a descent direction, as QPALM's Newton step is: shift beta by the terms
+    # active at tau = 0+ so that psi'(0+) = -5 U(0.1, 3)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t = alpha / delta
+    keep = (delta != 0) & np.isfinite(t)
+    w = np.where(keep, delta * np.abs(delta), 0.0)
+    t = np.where(keep, t, 0.0)
+    act0 = ((t <= 0) & (w > 0)) | ((t > 0) & (w < 0))
+    beta = beta - np.sum(np.where(act0, -t * w, 0.0), axis=1)
+    return alpha, delta, eta, beta
