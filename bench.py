@@ -68,23 +68,44 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        self.lines = []
+        self.proc = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
-            self.proc = None
+            return self
+
+        def reader():
+            for line in self.proc.stdout:
+                self.lines.append(line)
+
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+        # the timed region starts once the sampler is live (nvidia-smi can take
+        # a second to initialise; a short run would otherwise see no sample)
+        t0 = time.time()
+        while not self.lines and time.time() - t0 < 10 and self.proc.poll() is None:
+            time.sleep(0.01)
         return self
 
     def __exit__(self, *exc):
         self.rows = []
         if self.proc is None:
             return
-        time.sleep(0.25)
+        # at least two samples after the timed region ended
+        n0, t0 = len(self.lines), time.time()
+        while len(self.lines) < n0 + 2 and time.time() - t0 < 3 and self.proc.poll() is None:
+            time.sleep(0.01)
         self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
-        for line in out.strip().splitlines():
+        try:
+            self.proc.wait(timeout=10)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=5)
+        for line in self.lines:
             f = [x.strip() for x in line.split(",")]
             if len(f) >= 7:
                 self.rows.append(f)
