@@ -311,9 +311,16 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
         // kernel choice: compile-time-shape one-warp kernel (default), the
         // two-warp variant (CYQ_RICCATI=c) or the runtime-shape CTA kernel
         // (CYQ_RICCATI=g, and every shape without a specialisation)
-        static const char *sel = getenv("CYQ_RICCATI");
+        const char *sel = getenv("CYQ_RICCATI"); // read per call (tests switch it)
         const bool want_c2 = sel && sel[0] == 'c', want_gen = sel && sel[0] == 'g';
-        const bool want_pc = sel && sel[0] == 'p';
+        // latency-bound launches (at most ~2 chains per SM: a single long
+        // horizon, config 0 / 2) take the two-warp producer/consumer panel
+        // (measured 0.078 -> 0.074 ms at config 2); batches keep one warp
+        // per chain (CYQ_RICCATI=w forces it, =p forces the two-warp kernel)
+        static int sms = 0;
+        if (!sms)
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        const bool want_pc = (sel && sel[0] == 'p') || (!sel && (long long)g.batch * g.P <= 2LL * sms);
         bool done = false;
         if (p.aD) { // fused Newton-system augmentation: the warp kernel only
             if (!launch_riccati_warp(g, ctx->stream, ra))

@@ -127,3 +127,26 @@ def test_cluster_schur_single_long_horizon(P):
     f = kkt.factor(p, kkt.FactorOptions(P=P))
     s2 = kkt.solve(f, p, EqRhsBatch.of_problem(p))
     assert rel_error(s2, s_cl).max() <= 1e-13
+
+
+@pytest.fixture(params=["w", "p"])
+def riccati_mode(request):
+    old = os.environ.get("CYQ_RICCATI")
+    os.environ["CYQ_RICCATI"] = request.param
+    yield request.param
+    if old is None:
+        os.environ.pop("CYQ_RICCATI", None)
+    else:
+        os.environ["CYQ_RICCATI"] = old
+
+
+@pytest.mark.parametrize("name", ["cfg0_N64_b1_P4", "cfg2_N512_b1_P128", "cfg1_N40_b3_P16",
+                                  "cfg4_N64_b2_P16", "kat_n64_nx16_P4"])
+def test_both_warp_panels_match_reference(riccati_mode, name):
+    # single-warp panel (batches) and the two-warp producer/consumer panel
+    # (the default for latency-bound launches of <= 2 chains per SM)
+    p, P, ref_sol, z = golden_util.load(name)
+    sol = kkt.solve_problem(p, kkt.FactorOptions(P=P))
+    assert rel_error(sol, ref_sol).max() <= REL_TOL
+    res = kkt_residual(p, EqRhsBatch.of_problem(p), sol).max(axis=1)
+    assert np.all(res <= RES_TOL)
