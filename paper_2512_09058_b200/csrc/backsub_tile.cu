@@ -44,16 +44,24 @@ __device__ __forceinline__ void tmv_t(const double *tiles, int i0, int i1, int j
                                       double *out, double sgn, bool acc, bool lower, int lane) {
     using B = BT<NU, NX>;
     const int rq = lane >> 2, cq = 2 * (lane & 3);
+    constexpr int MI = 8; // tile rows per batch: all loads of a batch in flight at once
     for (int j = j0; j < j1; ++j) {
         double a0 = 0.0, a1 = 0.0;
-#pragma unroll 4
-        for (int i = i0; i < i1; ++i) {
-            if (lower && i < j)
-                continue;
-            const Frag f = ld_frag_g(tiles + B::tile(i, j) * kTileElems, lane);
-            const double vi = v[8 * (i - i0) + rq];
-            a0 = fma(f.a, vi, a0);
-            a1 = fma(f.b, vi, a1);
+        for (int ib = i0; ib < i1; ib += MI) {
+            Frag f[MI];
+#pragma unroll
+            for (int u = 0; u < MI; ++u) {
+                const int i = ib + u;
+                const bool on = i < i1 && !(lower && i < j);
+                f[u] = on ? ld_frag_g(tiles + B::tile(i, j) * kTileElems, lane) : Frag{0.0, 0.0};
+            }
+#pragma unroll
+            for (int u = 0; u < MI; ++u) {
+                const int i = ib + u;
+                const double vi = i < i1 ? v[8 * (i - i0) + rq] : 0.0;
+                a0 = fma(f[u].a, vi, a0);
+                a1 = fma(f[u].b, vi, a1);
+            }
         }
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) {
@@ -172,22 +180,44 @@ __global__ void __launch_bounds__(32 * WPB) backsub_tile_kernel(BacksubArgs a) {
                 Y[NU + k] += t[k];
         } else {
             const int j1 = g.stage_of(c, s + 1);
-            // zn = BA_{s+1} z_{s+1} (row-major B, A; lane per row, L1-cached)
+            // zn = BA_{s+1} z_{s+1}: coalesced row reads (lane = column pair
+            // of A / column of B), 32 row partials per lane, then a butterfly
+            // reduce-scatter leaves row r of the batch in lane r
             const bool in = j1 < N;
             const double *Bg = a.p.B + ((size_t)b * N + j1) * NX * NU;
             const double *Ag = a.p.A + ((size_t)b * N + j1) * NX * NX;
-            for (int i = lane; i < NX; i += 32) {
-                double s0 = 0.0;
-                if (in) {
-#pragma unroll 8
-                    for (int k = 0; k < NU; ++k)
-                        s0 = fma(__ldg(Bg + i * NU + k), z[k], s0);
-                    if (j1 != 0)
-#pragma unroll 8
-                        for (int k = 0; k < NX; ++k)
-                            s0 = fma(__ldg(Ag + i * NX + k), z[NU + k], s0);
+            static_assert(NX % 32 == 0 && NX <= 64 && NU <= 32, "zn layout");
+            const double za0 = z[NU + 2 * lane], za1 = z[NU + 2 * lane + 1];
+            const double zb = lane < NU ? z[lane] : 0.0;
+#pragma unroll
+            for (int r0 = 0; r0 < NX; r0 += 32) {
+                double pr[32];
+#pragma unroll
+                for (int r = 0; r < 32; ++r) {
+                    double acc = 0.0;
+                    if (in) {
+                        if (j1 != 0 && 2 * lane < NX) {
+                            const double2 av = __ldg(reinterpret_cast<const double2 *>(Ag + (r0 + r) * NX) + lane);
+                            acc = fma(av.x, za0, av.y * za1);
+                        }
+                        if (lane < NU)
+                            acc = fma(__ldg(Bg + (r0 + r) * NU + lane), zb, acc);
+                    }
+                    pr[r] = acc;
                 }
-                zn[i] = s0;
+                // reduce-scatter: after step h, lane keeps the rows whose bit
+                // h matches its own
+#pragma unroll
+                for (int h = 16; h >= 1; h >>= 1) {
+#pragma unroll
+                    for (int r = 0; r < h; ++r) {
+                        const bool up = (lane & h) != 0;
+                        const double send = up ? pr[r] : pr[r + h];
+                        const double keep = up ? pr[r + h] : pr[r];
+                        pr[r] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+                    }
+                }
+                zn[r0 + lane] = pr[0];
             }
             __syncwarp();
             // t = w - L_Q' zn
