@@ -39,12 +39,13 @@ using namespace cyqb::ric;
 
 namespace {
 
-template <int NU, int NX, int NY = 0> struct WS : PanelShape<NU, NX> {
+template <int NU, int NX, int NY = 0, bool TM = false> struct WS : PanelShape<NU, NX> {
     using P_ = PanelShape<NU, NX>;
     static constexpr int TT = P_::TT, NXC = P_::NXC, NXR = P_::NXR, NIMG = P_::NIMG, PW = P_::PW;
-    // per-warp shared memory (doubles); every offset is even (16-byte aligned)
+    // per-warp shared memory (doubles); every offset is even (16-byte aligned).
+    // TM: W lives in tensor memory instead (natural x-tile layout, no shared copy)
     static constexpr int O_W = 0;
-    static constexpr int O_LQ = O_W + TT * NXC * kTileElems;
+    static constexpr int O_LQ = O_W + (TM ? 0 : TT * NXC * kTileElems);
     static constexpr int O_IMG = O_LQ + NXR * NX;
     static constexpr int O_IMR = O_IMG + NIMG * kTileElems;
     static constexpr int O_S = O_IMR + PW;
@@ -110,24 +111,101 @@ __device__ __forceinline__ void stage_aug(const Geo &g, const ProbView &p, int b
 
 } // namespace
 
-template <int NU, int NX, int WPB, int NY>
-__global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a) {
+// ---- tensor memory as a per-lane store (TM variant) --------------------------
+// W = [V; ALQ; -wl] is the one panel-sized operand that lives across a stage
+// boundary; keeping it in TMEM (each warp owns its 32-lane sub-partition
+// slice, a tile fragment = 4 consecutive 32-bit columns of the lane) frees
+// 10.75 KB of shared memory per chain at config 1, enough for 12 resident
+// chains per SM instead of 8. tcgen05.ld results are valid only after
+// tcgen05.wait::ld, which therefore takes them as in/out operands.
+__device__ __forceinline__ void tm_st4(uint32_t addr, Frag f) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr),
+                 "r"(__double2loint(f.a)), "r"(__double2hiint(f.a)), "r"(__double2loint(f.b)),
+                 "r"(__double2hiint(f.b))
+                 : "memory");
+}
+template <int NTL> struct TmFrags {
+    uint32_t r[4 * NTL];
+};
+// NTL consecutive tile fragments (4 columns each) starting at addr
+template <int NTL> __device__ __forceinline__ void tm_ld(uint32_t addr, TmFrags<NTL> &t) {
+    static_assert(NTL == 8, "x32 load");
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+                 "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                 : "=r"(t.r[0]), "=r"(t.r[1]), "=r"(t.r[2]), "=r"(t.r[3]), "=r"(t.r[4]), "=r"(t.r[5]),
+                   "=r"(t.r[6]), "=r"(t.r[7]), "=r"(t.r[8]), "=r"(t.r[9]), "=r"(t.r[10]), "=r"(t.r[11]),
+                   "=r"(t.r[12]), "=r"(t.r[13]), "=r"(t.r[14]), "=r"(t.r[15]), "=r"(t.r[16]), "=r"(t.r[17]),
+                   "=r"(t.r[18]), "=r"(t.r[19]), "=r"(t.r[20]), "=r"(t.r[21]), "=r"(t.r[22]), "=r"(t.r[23]),
+                   "=r"(t.r[24]), "=r"(t.r[25]), "=r"(t.r[26]), "=r"(t.r[27]), "=r"(t.r[28]), "=r"(t.r[29]),
+                   "=r"(t.r[30]), "=r"(t.r[31])
+                 : "r"(addr)
+                 : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(t.r[0]), "+r"(t.r[1]), "+r"(t.r[2]), "+r"(t.r[3]), "+r"(t.r[4]), "+r"(t.r[5]),
+                   "+r"(t.r[6]), "+r"(t.r[7]), "+r"(t.r[8]), "+r"(t.r[9]), "+r"(t.r[10]), "+r"(t.r[11]),
+                   "+r"(t.r[12]), "+r"(t.r[13]), "+r"(t.r[14]), "+r"(t.r[15]), "+r"(t.r[16]), "+r"(t.r[17]),
+                   "+r"(t.r[18]), "+r"(t.r[19]), "+r"(t.r[20]), "+r"(t.r[21]), "+r"(t.r[22]), "+r"(t.r[23]),
+                   "+r"(t.r[24]), "+r"(t.r[25]), "+r"(t.r[26]), "+r"(t.r[27]), "+r"(t.r[28]), "+r"(t.r[29]),
+                   "+r"(t.r[30]), "+r"(t.r[31])
+                 :
+                 : "memory");
+}
+template <int NTL> __device__ __forceinline__ Frag tm_frag(const TmFrags<NTL> &t, int i) {
+    return Frag{__hiloint2double(t.r[4 * i + 1], t.r[4 * i]), __hiloint2double(t.r[4 * i + 3], t.r[4 * i + 2])};
+}
+
+template <int NU, int NX, int WPB, int NY, bool TM>
+__device__ __forceinline__ void riccati_warp_body(const RiccatiArgs &a, int chain, uint32_t tmw, double *sm);
+
+template <int NU, int NX, int WPB, int NY, bool TM>
+__global__ void __launch_bounds__(32 * WPB, TM ? 3 : 1) riccati_warp_kernel(RiccatiArgs a) {
     using S = Shp<NU, NX>;
-    using W = WS<NU, NX, NY>;
-    // "Pure" coupling tiles: trailing tiles whose rows and columns are all
-    // coupling rows (tile rows CT .. RT-1; tile row RT holds the rhs row).
-    // Their ALQ_s ALQ_s' terms cancel between stage s's trailing update and
-    // stage s+1's W W' (only LB LB' and the last stage's LA LA' remain in
-    // -Mfwd, kkt_factor.cpp:179-184), so both are skipped and LA LA' is
-    // subtracted once after the last stage.
-    constexpr int RT_ = S::RHS / 8;
-    auto pure = [](int ti, int tj) constexpr { return ti >= S::CT && tj >= S::CT && ti < RT_ && tj < RT_; };
+    static_assert(!TM || (WPB == 4 && S::TT <= 8 && S::NXT * S::TT * 4 <= 128), "TM layout");
     extern __shared__ __align__(16) double sm[];
     const Geo &g = a.g;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int wib = threadIdx.x >> 5;
     const int chain = blockIdx.x * WPB + wib;
-    if (chain >= g.batch * g.P)
-        return;
+    uint32_t tmw = 0; // TM: this warp's TMEM base (lane offset 32 wib, column 0)
+    __shared__ uint32_t s_taddr;
+    if constexpr (TM) {
+        if (wib == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                             static_cast<uint32_t>(__cvta_generic_to_shared(&s_taddr)))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        tmw = s_taddr + ((32u * (uint32_t)(wib & 3)) << 16);
+    }
+    if (chain < g.batch * g.P)
+        riccati_warp_body<NU, NX, WPB, NY, TM>(a, chain, tmw, sm);
+    if constexpr (TM) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (wib == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(s_taddr) : "memory");
+        }
+    }
+}
+
+// "Pure" coupling tiles: trailing tiles whose rows and columns are all
+// coupling rows (tile rows CT .. RT-1; tile row RT holds the rhs row).
+// Their ALQ_s ALQ_s' terms cancel between stage s's trailing update and
+// stage s+1's W W' (only LB LB' and the last stage's LA LA' remain in
+// -Mfwd, kkt_factor.cpp:179-184), so both are skipped and LA LA' is
+// subtracted once after the last stage.
+template <int NU, int NX, int WPB, int NY, bool TM>
+__device__ __forceinline__ void riccati_warp_body(const RiccatiArgs &a, int chain, uint32_t tmw, double *sm) {
+    (void)tmw;
+    using S = Shp<NU, NX>;
+    using W = WS<NU, NX, NY, TM>;
+    constexpr int RT_ = S::RHS / 8;
+    auto pure = [](int ti, int tj) constexpr { return ti >= S::CT && tj >= S::CT && ti < RT_ && tj < RT_; };
+    const Geo &g = a.g;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int b = chain / g.P, c = chain % g.P, n = g.n;
     const int rq = lane >> 2, cq = 2 * (lane & 3), q2 = lane & 3;
 
@@ -281,7 +359,40 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
                 }
             }
         }
-        if (s > 0) {
+        if (TM && s > 0) {
+            // += W W' from tensor memory: natural x-tile columns XT0 .. CT-1,
+            // one 32-column load per k-slice pair (all TT row tiles)
+#pragma unroll
+            for (int kt = 0; kt < S::NXT; ++kt) {
+                TmFrags<8> t;
+                tm_ld<8>(tmw + (uint32_t)(kt * S::TT * 4), t);
+                Frag w[S::TT];
+#pragma unroll
+                for (int i = 0; i < S::TT; ++i)
+                    w[i] = tm_frag(t, i);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    // skip k-slices without an x column (u columns are zero in W)
+                    constexpr int dummy = 0;
+                    (void)dummy;
+                    bool has_x = false;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int col = 8 * (S::XT0 + kt) + 2 * q + h;
+                        has_x = has_x || (col >= NU && col < S::NUX);
+                    }
+                    if (!has_x)
+                        continue;
+#pragma unroll
+                    for (int ti = 0; ti < S::TT; ++ti)
+#pragma unroll
+                        for (int tj = 0; tj <= ti; ++tj)
+                            if (!pure(ti, tj))
+                                dmma(P[S::T(ti, tj)], h ? w[ti].b : w[ti].a, h ? w[tj].b : w[tj].a);
+                }
+            }
+        }
+        if (!TM && s > 0) {
             // += W W' over the compact x-columns: k-slice outer, tiles inner
             // (consecutive DMMAs hit different accumulators)
 #pragma unroll
@@ -478,12 +589,32 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
                             wl[C - NU] = -mw[kt][e];
                     }
             }
+            if constexpr (TM) {
+                // W bottom rows in TMEM, natural x tiles: ALQ (x columns of the
+                // coupling rows), the rhs row -wl (mw), zero u / padding columns
+                // and rows past the rhs row
+#pragma unroll
+                for (int ti = S::CT; ti < S::TT; ++ti)
+#pragma unroll
+                    for (int kt = 0; kt < S::NXT; ++kt) {
+                        const int ct = S::XT0 + kt, r = 8 * ti + rq;
+                        Frag f = P[S::T(ti, ct)];
+                        const int C0 = 8 * ct + cq;
+                        f.a = (C0 >= NU && C0 < S::NUX) ? f.a : 0.0;
+                        f.b = (C0 + 1 >= NU && C0 + 1 < S::NUX) ? f.b : 0.0;
+                        if (r == S::RHS)
+                            f = Frag{mw[kt][0], mw[kt][1]};
+                        else if (r > S::RHS)
+                            f = Frag{0.0, 0.0};
+                        tm_st4(tmw + (uint32_t)((kt * S::TT + ti) * 4), f);
+                    }
+            }
             // W bottom rows: ALQ (x columns of the coupling rows) and the rhs
             // row -wl, scattered to the compact column positions; L_Q -> LQ
             {
             const int lv = lane_v(), rq = lv >> 2, cq = 2 * (lv & 3);
 #pragma unroll
-            for (int ti = S::CT; ti < S::TT; ++ti)
+            for (int ti = S::CT; ti < (TM ? S::CT : S::TT); ++ti)
 #pragma unroll
                 for (int kt = 0; kt < S::NXT; ++kt) {
                     const int ct = S::XT0 + kt, r = 8 * ti + rq;
@@ -515,7 +646,37 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
             __syncwarp();
             if (ph) ph[s * 8 + 4] = clock64();
             // V = BA_{s+1}' L_Q : rows 0..nux-1 of W (DMMA over x rows K)
-            {
+            if constexpr (TM) {
+                Frag vacc[S::CT * S::NXT];
+#pragma unroll
+                for (int v = 0; v < S::CT * S::NXT; ++v)
+                    vacc[v] = Frag{0.0, 0.0};
+#pragma unroll
+                for (int ks = 0; ks < W::KQ; ++ks) {
+                    const int K = 4 * ks + (lane & 3);
+                    double av[S::CT], bv[S::NXT];
+#pragma unroll
+                    for (int ti = 0; ti < S::CT; ++ti)
+                        av[ti] = BA[K * W::PW + 8 * ti + rq];
+#pragma unroll
+                    for (int kt = 0; kt < S::NXT; ++kt) { // natural x column of this lane's B column
+                        const int xc = 8 * (S::XT0 + kt) + rq - NU;
+                        bv[kt] = (xc >= 0 && xc < NX) ? LQ[K * NX + (xc >= 0 && xc < NX ? xc : 0)] : 0.0;
+                    }
+#pragma unroll
+                    for (int ti = 0; ti < S::CT; ++ti)
+#pragma unroll
+                        for (int kt = 0; kt < S::NXT; ++kt)
+                            if (4 * ks + 3 >= 8 * (S::XT0 + kt) - NU) // L_Q upper part is zero
+                                dmma(vacc[ti * S::NXT + kt], av[ti], bv[kt]);
+                }
+#pragma unroll
+                for (int ti = 0; ti < S::CT; ++ti)
+#pragma unroll
+                    for (int kt = 0; kt < S::NXT; ++kt)
+                        tm_st4(tmw + (uint32_t)((kt * S::TT + ti) * 4), vacc[ti * S::NXT + kt]);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            } else {
                 Frag vacc[S::CT * W::NXC];
 #pragma unroll
                 for (int v = 0; v < S::CT * W::NXC; ++v)
@@ -586,21 +747,22 @@ __global__ void __launch_bounds__(32 * WPB, 1) riccati_warp_kernel(RiccatiArgs a
 
 // ---- dispatch ----------------------------------------------------------------
 namespace {
-template <int NU, int NX, int WPB, int NY> bool launch_w(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
+template <int NU, int NX, int WPB, int NY, bool TM = false>
+bool launch_w(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
     if (g.nu != NU || g.nx != NX)
         return false;
     if ((NY > 0) != (ra.p.aD != nullptr) || (NY > 0 && ra.p.ny != NY))
         return false;
-    using W = WS<NU, NX, NY>;
+    using W = WS<NU, NX, NY, TM>;
     const size_t smem = (size_t)WPB * W::SMEM * sizeof(double);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(riccati_warp_kernel<NU, NX, WPB, NY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        cudaFuncSetAttribute(riccati_warp_kernel<NU, NX, WPB, NY, TM>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     const int chains = g.batch * g.P;
-    riccati_warp_kernel<NU, NX, WPB, NY><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ra);
+    riccati_warp_kernel<NU, NX, WPB, NY, TM><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ra);
     return true;
 }
 } // namespace
@@ -614,6 +776,12 @@ bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
         return false;
     if (ra.p.aD) // fused Newton-system augmentation (config 4 stage shape)
         return launch_w<8, 16, 1, 24>(g, st, ra);
+    // W in tensor memory (12 chains per SM at config 1): opt-in, CYQ_TMEM=1 --
+    // measured 1.52 vs 1.41 ms at config 1 (the natural x-tile layout costs a
+    // 6th W W' k-slice and 168 registers spill), see DESIGN.md §3.4
+    const char *tm = getenv("CYQ_TMEM");
+    if (tm && tm[0] == '1' && launch_w<10, 20, 4, 0, true>(g, st, ra))
+        return true;
     static const int wpb = getenv("CYQ_RICCATI_WPB") ? atoi(getenv("CYQ_RICCATI_WPB")) : 1;
     if (wpb == 2)
         return launch_w<10, 20, 2, 0>(g, st, ra) || launch_w<8, 16, 2, 0>(g, st, ra) ||

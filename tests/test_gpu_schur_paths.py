@@ -150,3 +150,23 @@ def test_both_warp_panels_match_reference(riccati_mode, name):
     assert rel_error(sol, ref_sol).max() <= REL_TOL
     res = kkt_residual(p, EqRhsBatch.of_problem(p), sol).max(axis=1)
     assert np.all(res <= RES_TOL)
+
+
+def test_tmem_panel_variant_matches_oracle():
+    # opt-in variant of the config-1 warp panel with W in tensor memory
+    # (tcgen05.st / tcgen05.ld, 4 chains per CTA); a batch large enough for
+    # the batched (non producer/consumer) path
+    old = os.environ.get("CYQ_TMEM")
+    os.environ["CYQ_TMEM"] = "1"
+    try:
+        p = synth.generate(1, seed=8, batch=24, N=128)
+        sol = kkt.solve_problem(p, kkt.FactorOptions(P=16))
+    finally:
+        if old is None:
+            os.environ.pop("CYQ_TMEM", None)
+        else:
+            os.environ["CYQ_TMEM"] = old
+    ref, rc, _ = Oracle().solve_problem(p, 16)
+    assert rc == 0
+    assert rel_error(sol, ref).max() <= REL_TOL
+    assert kkt_residual(p, EqRhsBatch.of_problem(p), sol).max() <= RES_TOL
