@@ -38,6 +38,7 @@
 #include "riccati_common.cuh"
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 namespace cyqb {
@@ -67,6 +68,15 @@ template <int NU, int NX, int NW> struct CS {
     static constexpr int XT0 = NU / 8, NXC = NX / 8; // x columns: tiles XT0 .. CT-1
     static constexpr int NPT = CT * (CT + 1) / 2 + BT * CT;
     static constexpr int MAXL = (NL + NW - 1) / NW;  // tiles per warp (the host plan meets it)
+    // "pure" coupling tiles (rows and columns all coupling rows: tile rows
+    // CT .. RT-1, tile row RT holds the rhs row): their ALQ_s ALQ_s' terms
+    // cancel between stage s's trailing update and stage s+1's W W' (only
+    // sum LB LB' + LA LA' stays in -Mfwd, kkt_factor.cpp:179-184). Every warp
+    // holds NPS of them at list slots 0 .. NPS-1 in "skip mode": W W' and the
+    // x-column (kb >= XT0) trailing updates of stages s < n-1 skip them
+    // (compile-time loop starts: no predicated-off DMMAs)
+    static constexpr int NPURE = (RT - CT) * (RT - CT + 1) / 2;
+    static constexpr int NPS = NPURE / NW;
     static_assert(MAXL <= kMaxL, "list table size");
     // [B A] and L_Q row strides, padded by 8 doubles: the V = BA' L_Q
     // operand loads (4 rows x 8 columns per warp) then need the minimum two
@@ -312,7 +322,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         // ---- += W W' (s > 0) --------------------------------------------
         if (s > 0) {
 #pragma unroll
-            for (int k = 0; k < MAXL; ++k) {
+            for (int k = C::NPS; k < MAXL; ++k) { // skip-mode pure tiles: no W W'
                 if (k >= mycnt)
                     break;
                 const int ti = LTI(k), tj = LTJ(k);
@@ -410,11 +420,14 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
             // completed column-(kb+1) tiles are published for step kb+1. The
             // next tile's operands are loaded one iteration ahead (a read of
             // a valid column slot even past the prefix)
-            {
-                int tj = LTJ(0);
-                Frag li = ld_frag(col + LTI(0) * kTileElems, lane), lj = ld_frag(col + tj * kTileElems, lane);
+            auto trail = [&](auto K0C) {
+                constexpr int K0 = decltype(K0C)::value;
+                if (cnt <= K0)
+                    return;
+                int tj = LTJ(K0);
+                Frag li = ld_frag(col + LTI(K0) * kTileElems, lane), lj = ld_frag(col + tj * kTileElems, lane);
 #pragma unroll
-                for (int k = 0; k < MAXL; ++k) {
+                for (int k = K0; k < MAXL; ++k) {
                     if (k >= cnt)
                         break;
                     Frag nli{0.0, 0.0}, nlj{0.0, 0.0};
@@ -431,7 +444,11 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                     lj = nlj;
                     tj = ntj;
                 }
-            }
+            };
+            if (kb >= C::XT0 && s + 1 < n)
+                trail(std::integral_constant<int, C::NPS>{}); // ALQ ALQ' cancels on pure tiles
+            else
+                trail(std::integral_constant<int, 0>{});
             __syncthreads(); // column kb consumed, column kb+1 / linv published
         }
         if (tid == 0)
@@ -589,9 +606,28 @@ template <int NU, int NX, int NW> bool launch_c(const Geo &g, cudaStream_t st, c
             }
             return t;
         };
+        // skip-mode pure tiles first: NPS per warp at slots 0 .. NPS-1 (they
+        // take trailing updates only from the u columns, kb < XT0)
+        auto is_pure = [&](int ti, int tj) { return ti >= C::CT && tj >= C::CT && ti < C::RT && tj < C::RT; };
+        bool skip_mode[64][64] = {};
+        {
+            int w = 0;
+            for (int tj = C::RT - 1; tj >= C::CT && C::NPS > 0; --tj)
+                for (int ti = C::RT - 1; ti >= tj; --ti) {
+                    if (w >= NW * C::NPS)
+                        break;
+                    const int ww = w % NW;
+                    h[ww * kMaxL + nown[ww]++] = (unsigned short)((ti << 8) | tj);
+                    for (int kb = 0; kb < C::XT0; ++kb)
+                        load[ww][kb] += kUpd;
+                    skip_mode[ti][tj] = true;
+                    ++w;
+                }
+        }
+        (void)is_pure;
         for (int tj = C::TT - 1; tj >= 0; --tj)
             for (int ti = C::TT - 1; ti >= tj; --ti) {
-                if (ti == tj && tj < C::CT)
+                if ((ti == tj && tj < C::CT) || skip_mode[ti][tj])
                     continue;
                 int best = -1;
                 double bc = 0;
