@@ -453,6 +453,8 @@ __device__ __forceinline__ void riccati_warp_body(const RiccatiArgs &a, int chai
             Frag idt{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0};
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
+                if (8 * kb + k >= S::NUX)
+                    break; // padding pivots: the identity tile stays as it is
                 constexpr unsigned FULL = 0xffffffffu;
                 const int src = k / 2;
                 const double vk = (k & 1) ? dg.b : dg.a;
