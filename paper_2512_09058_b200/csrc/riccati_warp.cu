@@ -451,6 +451,12 @@ __device__ __forceinline__ void riccati_warp_body(const RiccatiArgs &a, int chai
         for (int kb = 0; kb < S::CT; ++kb) {
             Frag &dg = P[S::T(kb, kb)];
             Frag idt{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0};
+            // The next pivot is computed in every lane from the values
+            // shuffled at this step (d = (k+1, k+1) and u = (k+1, k) before
+            // this step's update): pv' = d - (u iv)^2, exactly the owner
+            // lane's fma -- so the pivot chain is rsqrt -> mul -> fma, with
+            // no shuffle on it (bit-identical to shuffling the updated value)
+            double pvn = 0.0;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 if (8 * kb + k >= S::NUX)
@@ -458,16 +464,25 @@ __device__ __forceinline__ void riccati_warp_body(const RiccatiArgs &a, int chai
                 constexpr unsigned FULL = 0xffffffffu;
                 const int src = k / 2;
                 const double vk = (k & 1) ? dg.b : dg.a;
-                double pv = __shfl_sync(FULL, vk, 4 * k + src);
+                const double pv = k == 0 ? __shfl_sync(FULL, vk, 4 * k + src) : pvn;
                 const double urk = __shfl_sync(FULL, vk, 4 * rq + src);
                 const double uc0 = __shfl_sync(FULL, vk, 4 * cq + src);
                 const double uc1 = __shfl_sync(FULL, vk, 4 * (cq + 1) + src);
+                double dn = 0.0, un = 0.0;
+                if (k + 1 < 8 && 8 * kb + k + 1 < S::NUX) {
+                    dn = __shfl_sync(FULL, ((k + 1) & 1) ? dg.b : dg.a, 4 * (k + 1) + (k + 1) / 2);
+                    un = __shfl_sync(FULL, vk, 4 * (k + 1) + src);
+                }
                 if (8 * kb + k < S::NUX) { // potrf pivot check (off the critical path)
                     const bool first = !(pv > dfloor && isfinite(pv)) && fail_piv < 0;
                     fail_piv = first ? 8 * kb + k : fail_piv;
                     fail_stage = first ? s : fail_stage;
                 }
                 const double iv = rsqrt_nr(pv);
+                if (k + 1 < 8) {
+                    const double l = un * iv;
+                    pvn = fma(-l, l, dn);
+                }
                 const double lc0 = (cq > k) ? uc0 * iv : 0.0;
                 const double lc1 = (cq + 1 > k) ? uc1 * iv : 0.0;
                 const double lrk = urk * iv;
@@ -476,8 +491,8 @@ __device__ __forceinline__ void riccati_warp_body(const RiccatiArgs &a, int chai
                     dg.b = (q2 == src) ? nv : dg.b;
                 else
                     dg.a = (q2 == src) ? nv : dg.a;
-                dg.a -= lrk * lc0;
-                dg.b -= lrk * lc1;
+                dg.a = fma(-lrk, lc0, dg.a);
+                dg.b = fma(-lrk, lc1, dg.b);
                 const double vq = (k & 1) ? idt.b : idt.a;
                 const double xrq = __shfl_sync(FULL, vq, 4 * rq + src) * iv;
                 if (k & 1)
