@@ -231,11 +231,10 @@ template <int NU, int NX, int WPB> bool launch_b(const Geo &g, cudaStream_t st, 
     if (g.nu != NU || g.nx != NX)
         return false;
     const size_t smem = (size_t)WPB * BS<NU, NX>::PER_WARP * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(backsub_warp_kernel<NU, NX, WPB>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
     }
     const int chains = g.batch * g.P;
     backsub_warp_kernel<NU, NX, WPB><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ba);

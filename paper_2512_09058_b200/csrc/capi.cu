@@ -223,11 +223,10 @@ void riccati_shape(const Geo &g, int &nw, int &maxt) {
 }
 
 template <int M> void launch_riccati_t(const Geo &g, int nw, cudaStream_t st, const RiccatiArgs &ra) {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(riccati_panel_kernel_t<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              227 * 1024);
-        attr = true;
     }
     riccati_panel_kernel_t<M><<<g.batch * g.P, 32 * nw, riccati_smem_bytes(g), st>>>(ra);
 }
@@ -278,13 +277,12 @@ struct Timed {
 
 int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &ws,
                     const SolView *sol, bool do_solve) {
-    static bool attrs = false;
-    if (!attrs) {
+    static std::atomic<unsigned long long> attrs{0};
+    if (first_on_device(attrs)) {
         CU(cudaFuncSetAttribute(backsub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 227 * 1024));
         CU(cudaFuncSetAttribute(schur_cr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 227 * 1024));
-        attrs = true;
     }
     const int chains = g.batch * g.P;
     CU(cudaMemsetAsync(ws.fail, 0xFF, sizeof(unsigned long long) * g.batch, ctx->stream));
@@ -317,9 +315,8 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
         // horizon, config 0 / 2) take the two-warp producer/consumer panel
         // (measured 0.078 -> 0.074 ms at config 2); batches keep one warp
         // per chain (CYQ_RICCATI=w forces it, =p forces the two-warp kernel)
-        static int sms = 0;
-        if (!sms)
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
         const bool want_pc = (sel && sel[0] == 'p') || (!sel && (long long)g.batch * g.P <= 2LL * sms);
         bool done = false;
         if (p.aD) { // fused Newton-system augmentation: the warp kernel only
@@ -414,11 +411,10 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
 // solve, back substitution. `p` carries the explicit rhs.
 int launch_solve(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &ws,
                  const SolView &sol) {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) {
         CU(cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 227 * 1024));
-        attr = true;
     }
     const int chains = g.batch * g.P;
     BacksubArgs ba{g, p, ws.fac, ws.y, ws.wl, ws.lamc, sol};

@@ -1,6 +1,8 @@
 // Kernel argument blocks and launch helpers shared by the C ABI.
 #pragma once
 
+#include <atomic>
+
 #include "kkt_common.cuh"
 
 #include <cuda_runtime.h>
@@ -8,6 +10,17 @@
 struct cyq_ctx; // include/cyqlone_b200.h
 
 namespace cyqb {
+
+// One-time per-device launch setup (function attributes, constant-memory
+// tables are per device): true the first time the current device asks. A
+// context per GPU may live in one process (include/cyqlone_b200.h).
+inline bool first_on_device(std::atomic<unsigned long long> &mask) {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long bit = 1ull << (d & 63);
+    return !(mask.fetch_or(bit) & bit);
+}
+
 
 // Device workspace of one factorization of a batch (all chains).
 struct FactorWS {

@@ -580,8 +580,8 @@ template <int NU, int NX, int NW> bool launch_c(const Geo &g, cudaStream_t st, c
         return false;
     using C = CS<NU, NX, NW>;
     const size_t smem = (size_t)C::SMEM * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(riccati_cta_kernel<NU, NX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         // tile plan: every list tile (all but the pivot diagonals) goes,
@@ -657,7 +657,6 @@ template <int NU, int NX, int NW> bool launch_c(const Geo &g, cudaStream_t st, c
         }
         cudaMemcpyToSymbol(c_list, h, sizeof h);
         cudaMemcpyToSymbol(c_cnt, cnt, sizeof cnt);
-        attr = true;
     }
     riccati_cta_kernel<NU, NX, NW><<<g.batch * g.P, 32 * NW, smem, st>>>(ra);
     return true;

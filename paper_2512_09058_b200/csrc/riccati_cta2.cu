@@ -381,11 +381,10 @@ template <int NU, int NX> bool launch_c2(const Geo &g, cudaStream_t st, const Ri
     if (g.nu != NU || g.nx != NX)
         return false;
     const size_t smem = (size_t)C2<NU, NX>::SMEM * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(riccati_cta2_kernel<NU, NX>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
     }
     riccati_cta2_kernel<NU, NX><<<g.batch * g.P, 64, smem, st>>>(ra);
     return true;

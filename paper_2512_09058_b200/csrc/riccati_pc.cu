@@ -523,10 +523,9 @@ template <int NU, int NX> bool launch_p(const Geo &g, cudaStream_t st, const Ric
     if (g.nu != NU || g.nx != NX)
         return false;
     const size_t smem = (size_t)PCS<NU, NX>::SMEM * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(riccati_pc_kernel<NU, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
     }
     riccati_pc_kernel<NU, NX><<<g.batch * g.P, 64, smem, st>>>(ra);
     return true;

@@ -772,11 +772,10 @@ bool launch_w(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
         return false;
     using W = WS<NU, NX, NY, TM>;
     const size_t smem = (size_t)WPB * W::SMEM * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(riccati_warp_kernel<NU, NX, WPB, NY, TM>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
     }
     const int chains = g.batch * g.P;
     riccati_warp_kernel<NU, NX, WPB, NY, TM><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ra);

@@ -317,11 +317,10 @@ template <int NX> bool launch_sb(const Geo &g, cudaStream_t st, const SchurArgs 
                          2 * NX) * sizeof(double);
     if (smem > 200 * 1024)
         return false;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(schur_big_kernel<NX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              200 * 1024);
-        attr = true;
     }
     schur_big_kernel<NX, NW><<<g.batch, 32 * NW, smem, st>>>(sa);
     return true;

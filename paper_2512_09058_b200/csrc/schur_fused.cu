@@ -707,11 +707,10 @@ template <int NX, int NW, int CL> bool launch_sfw(const Geo &g, cudaStream_t st,
                          (CL > 1 ? (size_t)g.P * SF<NX>::XP : 0)) * sizeof(double);
     if (smem > 220 * 1024)
         return false;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(schur_fused_kernel<NX, NW, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              220 * 1024);
-        attr = true;
     }
     if (CL == 1) {
         schur_fused_kernel<NX, NW, CL><<<g.batch, 32 * NW, smem, st>>>(sa);
