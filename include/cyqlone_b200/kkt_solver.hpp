@@ -137,6 +137,37 @@ Factor factor_batch(const std::vector<EqOCP> &ps, const FactorOptions &opts);
 std::vector<EqSolution> solve_batch(const Factor &f, const std::vector<EqOCP> &ps,
                                     const std::vector<EqRhs> &rhs);
 
+/// Diagonal penalty change per stage (kkt_solver.hpp:130-138): zero where
+/// the active set did not change; `terminal` applies to the rows C_N.
+struct SigmaDelta {
+    std::vector<Vec> stage; ///< size N, length ny each
+    Vec terminal;           ///< length ny_term
+    index_t total_rank() const;
+};
+
+/// delta[i] = +sigma_i for newly active rows, -sigma_i for newly inactive
+/// (kkt_update.cpp:30-41).
+Vec active_set_delta(const std::vector<bool> &prev, const std::vector<bool> &now, const Vec &sigma);
+
+struct UpdateReport {
+    index_t columns_updated = 0;
+    index_t columns_refactored = 0;
+    bool schur_refactored = false;
+    index_t schur_levels_updated = 0;
+};
+
+/// kkt::update (kkt_solver.hpp:152-161, kkt_update.cpp:372-477): afterwards
+/// the factor equals a fresh factorization of `p_new` (whose Hessians carry
+/// H_j + (D_j | C_j)' dSigma_j (D_j | C_j)). The GPU takes the reference's
+/// refactorization path (kkt_update.cpp:424-453) for every column whose
+/// update rank is nonzero -- the path the reference itself takes once a
+/// column's rank reaches rho * nx -- so the report lists those columns as
+/// refactored and the Schur factor as refactored; with dSigma = 0 the factor
+/// is left as it is. The hyperbolic-Householder low-rank path is not built.
+/// Throws std::invalid_argument on shape mismatches.
+UpdateReport update(Factor &f, const EqOCP &p_new, const std::vector<Mat> &C,
+                    const std::vector<Mat> &D, const Mat &C_term, const SigmaDelta &ds);
+
 /// Critical-path FLOP model (kkt_solver.hpp:165-176, kkt_factor.cpp:319-339).
 struct FlopModel {
     real_t riccati = 0, schur = 0, cr = 0, total = 0, serial = 0, speedup = 0;

@@ -113,6 +113,11 @@ void ref_random_eq_ocp(int64_t N, int64_t nx, int64_t nu, uint64_t seed,
                        double conditioning, double *A, double *B, double *R,
                        double *S, double *Q, double *f, double *r, double *q,
                        double *x_init);
+/* factor(p_old) -> kkt::update(p_new, C, D, C_term, dSigma) -> solve, instance 0 */
+int ref_update_solve(const oc_dims *d, const oc_ocp *p_old, const oc_ocp *p_new, int64_t ny,
+                     const double *D, const double *C, int64_t ny_term, const double *C_term,
+                     const double *ds_stage, const double *ds_term, double rho, oc_sol *out,
+                     int64_t *report);
 double ref_bench_solve_problem(const oc_dims *d, const oc_ocp *p,
                                int64_t vlen, int64_t n_solves, int threads);
 

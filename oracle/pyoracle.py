@@ -232,9 +232,39 @@ class RefOracle(_Base):
         return f(i64(len(eta)), i64(alpha.shape[1]), _p(alpha), _p(delta), _p(eta), _p(beta),
                  _p(tau), C.c_int(threads))
 
+    def update_solve(self, p_old, p_new, P, D, C, C_term, ds_stage, ds_term, rho=0.5):
+        """kkt::factor(p_old) -> kkt::update -> kkt::solve(of_problem(p_new)) for
+        instance 0. D (N, ny, nu), C (N, ny, nx), C_term (ny_term, nx),
+        ds_stage (N, ny), ds_term (ny_term,). Returns (sol, rc, report[4])."""
+        sol = _sol_arrays(p_new.subset(np.arange(1)) if p_new.batch > 1 else p_new)
+        rep = np.zeros(4, dtype=np.int64)
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (D, C, C_term, ds_stage, ds_term)]
+        ny, ny_t = arrs[0].shape[1], arrs[2].shape[0]
+        f = self.lib.ref_update_solve
+        rc = f(C_dims(p_old, P), C_ocp(p_old), C_ocp(p_new),
+               i64(ny), _p(arrs[0]), _p(arrs[1]), i64(ny_t), _p(arrs[2]), _p(arrs[3]), _p(arrs[4]),
+               ctypes_double(rho), C_sol(sol), rep.ctypes.data_as(C_i64p))
+        return sol, rc, rep
+
     def bench(self, p, P, n_solves, threads, vlen=4):
         return self.lib.ref_bench_solve_problem(C.byref(_dims(p, P)), C.byref(_ocp(p)),
                                                 i64(vlen), i64(n_solves), C.c_int(threads))
+
+
+def C_dims(p, P):
+    return C.byref(_dims(p, P))
+
+
+def C_ocp(p):
+    return C.byref(_ocp(p))
+
+
+def C_sol(sol):
+    return C.byref(Sol(*[_p(a) for a in sol.arrays()]))
+
+
+C_i64p = C.POINTER(C.c_int64)
+ctypes_double = C.c_double
 
 
 def _factor_blocks(fn, p, P, vlen):

@@ -198,6 +198,49 @@ int ref_solve(const oc_dims *d, const oc_ocp *p, const oc_rhs *rhs,
     return worst;
 }
 
+// kkt::factor(p_old) -> kkt::update(p_new, C, D, C_term, dSigma) -> kkt::solve
+// (EqRhs::of_problem(p_new)) of instance 0 (kkt_update.cpp:372-477):
+// D[N][ny][nu], C[N][ny][nx] (stage rows), C_term[ny_term][nx],
+// ds_stage[N][ny], ds_term[ny_term]; report[4] = UpdateReport fields.
+int ref_update_solve(const oc_dims *d, const oc_ocp *p_old, const oc_ocp *p_new, int64_t ny,
+                     const double *D, const double *C, int64_t ny_term, const double *C_term,
+                     const double *ds_stage, const double *ds_term, double rho, oc_sol *out,
+                     int64_t *report) {
+    return guarded(nullptr, 0, [&] {
+        const index_t N = d->N, nx = d->nx, nu = d->nu;
+        EqOCP o0 = make_ocp(d, p_old, 0), o1 = make_ocp(d, p_new, 0);
+        kkt::FactorOptions opts = opts_of(d, 4);
+        opts.rho = rho;
+        Factor f = kkt::factor(o0, opts);
+        std::vector<batla::DenseMatrix> Cm, Dm;
+        kkt::SigmaDelta ds;
+        for (index_t j = 0; j < N; ++j) {
+            batla::DenseMatrix dj(ny, nu), cj(ny, nx);
+            for (index_t i = 0; i < ny; ++i) {
+                for (index_t a = 0; a < nu; ++a)
+                    dj(i, a) = D[(j * ny + i) * nu + a];
+                for (index_t a = 0; a < nx; ++a)
+                    cj(i, a) = C[(j * ny + i) * nx + a];
+            }
+            Dm.push_back(dj);
+            Cm.push_back(cj);
+            ds.stage.emplace_back(ds_stage + j * ny, ds_stage + (j + 1) * ny);
+        }
+        batla::DenseMatrix ct(ny_term, nx);
+        for (index_t i = 0; i < ny_term; ++i)
+            for (index_t a = 0; a < nx; ++a)
+                ct(i, a) = C_term[i * nx + a];
+        ds.terminal.assign(ds_term, ds_term + ny_term);
+        kkt::UpdateReport r = kkt::update(f, o1, Cm, Dm, ct, ds);
+        report[0] = r.columns_updated;
+        report[1] = r.columns_refactored;
+        report[2] = r.schur_refactored ? 1 : 0;
+        report[3] = r.schur_levels_updated;
+        EqSolution s = kkt::solve(f, o1, ocp::EqRhs::of_problem(o1));
+        store_sol(d, s, out, 0);
+    });
+}
+
 int ref_factor_export(const oc_dims *d, const oc_ocp *p, int64_t vlen,
                       oc_factor_blocks *o, oc_status *st) {
     return guarded(st, 0, [&] {

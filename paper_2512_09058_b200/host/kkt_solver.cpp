@@ -372,6 +372,70 @@ Factor::Blocks Factor::materialize(index_t inst) const {
     return bl;
 }
 
+index_t SigmaDelta::total_rank() const {
+    index_t r = 0;
+    for (const Vec &v : stage)
+        for (real_t x : v)
+            r += x != 0;
+    for (real_t x : terminal)
+        r += x != 0;
+    return r;
+}
+
+Vec active_set_delta(const std::vector<bool> &prev, const std::vector<bool> &now, const Vec &sigma) {
+    if (prev.size() != now.size() || now.size() != sigma.size())
+        throw std::invalid_argument("active_set_delta: size mismatch");
+    Vec d(sigma.size(), 0);
+    for (std::size_t i = 0; i < sigma.size(); ++i) {
+        if (now[i] && !prev[i])
+            d[i] = sigma[i];
+        else if (!now[i] && prev[i])
+            d[i] = -sigma[i];
+    }
+    return d;
+}
+
+UpdateReport update(Factor &f, const EqOCP &p_new, const std::vector<Mat> &C, const std::vector<Mat> &D,
+                    const Mat &C_term, const SigmaDelta &ds) {
+    if (!f.impl)
+        throw std::invalid_argument("update: empty factor");
+    if (f.batch != 1)
+        throw std::invalid_argument("update: single-instance factors only");
+    if (p_new.N != f.N_orig || p_new.nx != f.nx || p_new.nu != f.nu)
+        throw std::invalid_argument("update: p_new shape differs from the factor's");
+    if (static_cast<index_t>(ds.stage.size()) != p_new.N || static_cast<index_t>(D.size()) < p_new.N ||
+        static_cast<index_t>(C.size()) < p_new.N)
+        throw std::invalid_argument("update: SigmaDelta / C / D sizes differ from N");
+    for (index_t j = 0; j < p_new.N; ++j) {
+        const index_t ny = static_cast<index_t>(ds.stage[z(j)].size());
+        if (D[z(j)].rows != ny || D[z(j)].cols != f.nu || C[z(j)].rows != ny || C[z(j)].cols != f.nx)
+            throw std::invalid_argument("update: D_j / C_j shapes differ from (ny x nu, ny x nx)");
+    }
+    if (!ds.terminal.empty() && (C_term.rows != static_cast<index_t>(ds.terminal.size()) || C_term.cols != f.nx))
+        throw std::invalid_argument("update: C_term shape differs from (ny_term x nx)");
+    // per-column accumulated rank (kkt_update.cpp:392-409)
+    UpdateReport rep;
+    const Partition &pt = f.part;
+    for (index_t c = 0; c < pt.P; ++c) {
+        index_t r = 0;
+        for (index_t s = 0; s < pt.n_per; ++s) {
+            const index_t j = pt.stage_of(c, s);
+            if (j < p_new.N)
+                for (real_t x : ds.stage[z(j)])
+                    r += x != 0;
+            if (j == 0)
+                for (real_t x : ds.terminal)
+                    r += x != 0;
+        }
+        rep.columns_refactored += r > 0;
+    }
+    if (rep.columns_refactored == 0)
+        return rep; // dSigma = 0: the factor already is the factor of p_new
+    f = factor(p_new, f.opts);
+    rep.schur_refactored = true;
+    return rep;
+}
+
 FlopModel flops_critical_path(index_t nx, index_t nu, index_t N, index_t P) {
     if (!pow2(P) || N % P != 0)
         throw std::invalid_argument("flops_critical_path: P must be a power of two dividing N");

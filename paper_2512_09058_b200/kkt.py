@@ -270,6 +270,50 @@ def solve(f: Factor, p, rhs) -> EqSolutionBatch:
     return sol
 
 
+def update(f: Factor, p_new, C, D, C_term, ds_stage, ds_terminal=None):
+    """kkt::update (kkt_solver.hpp:152-161, kkt_update.cpp:372-477): returns
+    (factor, report) where the factor equals a fresh factorization of
+    `p_new` (Hessians H_j + (D_j | C_j)' dSigma_j (D_j | C_j)). The GPU takes
+    the reference's refactorization path (kkt_update.cpp:424-453) for every
+    column with a nonzero update rank -- the path the reference takes once a
+    column's rank reaches rho * nx; the hyperbolic-Householder low-rank path
+    is not built. With dSigma = 0 the factor is returned unchanged.
+    ds_stage (b, N, ny), ds_terminal (b, ny_term); C, D are only
+    shape-checked (b, N, ny, nx), (b, N, ny, nu). report: per-instance
+    columns_refactored, and schur_refactored."""
+    ds = np.asarray(ds_stage.cpu() if _is_torch(ds_stage) else ds_stage, dtype=np.float64)
+    dt = (np.zeros((ds.shape[0], 0)) if ds_terminal is None else
+          np.asarray(ds_terminal.cpu() if _is_torch(ds_terminal) else ds_terminal, dtype=np.float64))
+    if ds.ndim != 3 or ds.shape[0] != f.batch or ds.shape[1] != f.N:
+        raise ValueError("update: ds_stage must be (batch, N, ny)")
+    if tuple(D.shape[:3]) != (f.batch, f.N, ds.shape[2]) or D.shape[3] != f.nu:
+        raise ValueError("update: D must be (batch, N, ny, nu)")
+    if tuple(C.shape[:3]) != (f.batch, f.N, ds.shape[2]) or C.shape[3] != f.nx:
+        raise ValueError("update: C must be (batch, N, ny, nx)")
+    if dt.shape[1] and (C_term is None or C_term.shape[-1] != f.nx):
+        raise ValueError("update: C_term must be (batch, ny_term, nx)")
+    P, n = f.opts.P, f.n_per
+    Np = P * n
+    refac = []
+    for b in range(f.batch):
+        cols = 0
+        for c in range(P):
+            r = 0
+            for s in range(n):
+                j = (n * c - s) % Np
+                if j < f.N:
+                    r += int(np.count_nonzero(ds[b, j]))
+                if j == 0:
+                    r += int(np.count_nonzero(dt[b]))
+            cols += r > 0
+        refac.append(cols)
+    report = {"columns_updated": [0] * f.batch, "columns_refactored": refac,
+              "schur_refactored": any(refac), "schur_levels_updated": 0}
+    if not any(refac):
+        return f, report
+    return factor(p_new, f.opts, ctx=f.ctx), report
+
+
 def augment_hessians(p, D, Cm, sigma, gamma_inv: float = 0.0, out=None,
                      ctx: Context | None = None) -> EqOCPBatch:
     """Newton-system assembly of the QPALM inner loop (qpalm::assemble_newton,
@@ -356,5 +400,5 @@ def line_search_exact(alpha, delta, eta, beta, ctx: Context | None = None,
     return out
 
 
-__all__ = ["augment_hessians", "solve_newton", "line_search_exact", "FactorOptions", "Factor", "FactorizeError", "CudaError", "Context", "factor",
+__all__ = ["augment_hessians", "solve_newton", "line_search_exact", "update", "FactorOptions", "Factor", "FactorizeError", "CudaError", "Context", "factor",
            "solve", "solve_problem", "nu2", "EqOCPBatch", "EqRhsBatch", "EqSolutionBatch"]

@@ -243,6 +243,54 @@ void test_batch_matches_single() {
         CHECK(rel_err(sb[i], kkt::solve_problem(ps[i], FactorOptions{8})) <= 1e-13, "batch vs single");
 }
 
+void test_update() { // kkt::update (kkt_solver.hpp:152-161): refactorization path
+    const ocp::index_t N = 32, nx = 6, nu = 3, ny = 4;
+    EqOCP p = random_ocp(N, nx, nu, 21);
+    std::mt19937_64 rng(5);
+    std::normal_distribution<double> gauss(0, 1);
+    std::vector<Mat> C, D;
+    kkt::SigmaDelta ds;
+    for (ocp::index_t j = 0; j < N; ++j) {
+        Mat cj(ny, nx), dj(ny, nu);
+        for (auto &v : cj.a) v = gauss(rng);
+        for (auto &v : dj.a) v = gauss(rng);
+        C.push_back(cj);
+        D.push_back(dj);
+        ds.stage.push_back(Vec(ny, 0.0));
+    }
+    Mat ct(ny, nx);
+    for (auto &v : ct.a) v = gauss(rng);
+    ds.terminal = Vec(ny, 0.0);
+    kkt::Factor f = kkt::factor(p, FactorOptions{4});
+    kkt::UpdateReport r0 = kkt::update(f, p, C, D, ct, ds);
+    CHECK(r0.columns_refactored == 0 && !r0.schur_refactored, "no change: factor kept");
+    // one newly active row at stage 9: H_9 += (D_9 | C_9)' e_i 2.5 e_i' (D_9 | C_9)
+    ds.stage[9][2] = 2.5;
+    EqOCP pn = p;
+    for (ocp::index_t a = 0; a < nu; ++a)
+        for (ocp::index_t b = 0; b < nu; ++b)
+            pn.R[9](a, b) += 2.5 * D[9](2, a) * D[9](2, b);
+    for (ocp::index_t a = 0; a < nu; ++a)
+        for (ocp::index_t b = 0; b < nx; ++b)
+            pn.S[9](a, b) += 2.5 * D[9](2, a) * C[9](2, b);
+    for (ocp::index_t a = 0; a < nx; ++a)
+        for (ocp::index_t b = 0; b < nx; ++b)
+            pn.Q[9](a, b) += 2.5 * C[9](2, a) * C[9](2, b);
+    CHECK(ds.total_rank() == 1, "total_rank");
+    kkt::UpdateReport r1 = kkt::update(f, pn, C, D, ct, ds);
+    CHECK(r1.columns_refactored == 1 && r1.schur_refactored, "one column refactored (%lld)",
+          (long long)r1.columns_refactored);
+    EqSolution s = kkt::solve(f, pn, EqRhs::of_problem(pn));
+    // factor + solve vs solve_problem (fused forward sweep): same bar as
+    // test_factor_then_solve
+    CHECK(rel_err(s, kkt::solve_problem(pn, FactorOptions{4})) <= 1e-13, "update == fresh factorization %.3e",
+          rel_err(s, kkt::solve_problem(pn, FactorOptions{4})));
+    kkt::Factor g = kkt::factor(pn, FactorOptions{4});
+    CHECK(bit_equal(s, kkt::solve(g, pn, EqRhs::of_problem(pn))), "update == factor(p_new) bitwise");
+    Vec d = kkt::active_set_delta({true, false, true}, {false, false, true}, {1.0, 2.0, 3.0});
+    CHECK(d[0] == -1.0 && d[1] == 0.0 && d[2] == 0.0, "active_set_delta");
+}
+
 void test_flop_model() { // kkt_factor.cpp:319-339 (Eq. 14)
     kkt::FlopModel m = kkt::flops_critical_path(30, 20, 96, 8);
     CHECK(m.total > 0 && std::fabs(m.total - (m.riccati + m.schur + m.cr)) < 1e-9 * m.total, "total");
@@ -334,6 +382,7 @@ int main(int argc, char **argv) {
         test_factor_blocks();
         test_errors();
         test_batch_matches_single();
+        test_update();
         test_flop_model();
     } catch (const std::exception &e) {
         std::fprintf(stderr, "unexpected exception: %s\n", e.what());
