@@ -937,7 +937,7 @@ int cyq_solve_newton_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_bat
 int cyq_line_search_batch(cyq_ctx *ctx, int64_t batch, int64_t m, const double *alpha,
                           const double *delta, const double *eta, const double *beta, double *tau,
                           int32_t *status, int64_t *iterations) {
-    if (!ctx || !alpha || !delta || !eta || !beta || !tau)
+    if (!ctx || !eta || !beta || !tau || (m > 0 && (!alpha || !delta)))
         return set_err(ctx, CYQ_INVALID_ARG, "null argument");
     if (batch < 1 || m < 0)
         return set_err(ctx, CYQ_INVALID_ARG, "batch >= 1 and m >= 0 required");

@@ -147,3 +147,23 @@ def test_gpu_line_search_root_beyond_last_breakpoint_and_below_first():
     assert np.all(rc == 0)
     assert tau[0] > 1.0 and tau[1] < 0.1
     assert np.all(np.abs(tau - ref) <= 1e-12 * np.maximum(1.0, np.abs(ref)))
+
+
+@pytest.mark.gpu
+def test_gpu_line_search_without_terms_and_large_batch():
+    import torch
+    from paper_2512_09058_b200 import kkt
+
+    # m = 0: psi' is linear, tau = -beta / eta (line_search.cpp:140-146)
+    E = torch.tensor([2.0, 4.0], dtype=torch.float64, device="cuda")
+    B = torch.tensor([-2.0, -1.0], dtype=torch.float64, device="cuda")
+    Z = torch.zeros((2, 0), dtype=torch.float64, device="cuda")
+    tau = kkt.line_search_exact(Z, Z, E, B).cpu().numpy()
+    assert np.allclose(tau, [1.0, 0.25], rtol=0, atol=1e-15)
+    # a batch larger than the SM count, small m: every instance vs the oracle
+    alpha, delta, eta, beta = synth.line_search_data(700, 37, seed=21)
+    dev = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (alpha, delta, eta, beta)]
+    got = kkt.line_search_exact(*dev).cpu().numpy()
+    ref, rc = Oracle().line_search(alpha, delta, eta, beta)
+    assert np.all(rc == 0)
+    assert np.all(np.abs(got - ref) <= 1e-12 * np.maximum(1.0, np.abs(ref)))
