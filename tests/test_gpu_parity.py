@@ -14,7 +14,7 @@ import golden_util
 from pyoracle import Oracle
 
 from paper_2512_09058_b200 import kkt, synth
-from paper_2512_09058_b200.ocp import EqRhsBatch, kkt_residual, rel_error, residual_scale
+from paper_2512_09058_b200.ocp import OCP_FIELDS, EqOCPBatch, EqRhsBatch, kkt_residual, rel_error, residual_scale
 
 pytestmark = pytest.mark.gpu
 
@@ -144,3 +144,22 @@ def test_device_resident_inputs_match_host():
     sd = kkt.solve_problem(dev, kkt.FactorOptions(P=16))
     for k in ("u", "x", "lam"):
         assert np.array_equal(getattr(sd, k).cpu().numpy(), getattr(host, k))
+
+
+def test_split_device_batch_matches_unsplit():
+    # device batches >= 256 run as two halves on two streams (capi
+    # split_device_pipeline); CYQ_SPLIT=0 forces the single-stream path
+    import os
+    import torch
+    p = synth.generate(1, seed=13, batch=300, N=32)
+    dev = EqOCPBatch.__new__(EqOCPBatch)
+    for k in OCP_FIELDS:
+        setattr(dev, k, torch.from_numpy(getattr(p, k)).cuda())
+    a = kkt.solve_problem(dev, kkt.FactorOptions(P=8))
+    os.environ["CYQ_SPLIT"] = "0"
+    try:
+        b = kkt.solve_problem(dev, kkt.FactorOptions(P=8))
+    finally:
+        os.environ.pop("CYQ_SPLIT", None)
+    for k in ("u", "x", "lam"):
+        assert torch.equal(getattr(a, k), getattr(b, k))
