@@ -575,7 +575,7 @@ const char *cyq_ctx_last_error(cyq_ctx *ctx) {
     return ctx ? ctx->err.c_str() : g_last_err.c_str();
 }
 
-// Device-resident batch in K parts (CYQ_SPLIT, default 2), alternating
+// Device-resident batch in K parts (CYQ_SPLIT=K, opt-in), alternating
 // between the context stream and a side stream (joined back into the
 // context stream): the tail of each kernel of one part overlaps kernels of
 // the next (measured +2% at config 1 with K = 2).
@@ -660,8 +660,10 @@ int cyq_solve_problem_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_ba
     FactorWS ws = carve(ctx->wsbuf, wsz);
     if (mem == CYQ_MEM_DEVICE) {
         SolView sv{sol->u, sol->x, sol->lam};
+        // opt-in (CYQ_SPLIT=K): the overlapped launches make each kernel's
+        // own event-timed duration (the roofline's denominator) meaningless
         const char *sp = getenv("CYQ_SPLIT");
-        const int K = sp ? atoi(sp) : 2;
+        const int K = sp ? atoi(sp) : 1;
         if (g.batch >= 128 * K && K >= 2) {
             // K parts, each a full pipeline, on two alternating streams: the
             // kernels' tails (the Schur kernel's second wave above all)
