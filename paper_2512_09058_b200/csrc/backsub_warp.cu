@@ -31,12 +31,16 @@ template <int NU, int NX> struct BS {
     static constexpr bool PAD = NU * NX <= 128;
     static constexpr int TS = PAD ? kTileElems + 8 : kTileElems;
     static constexpr int BS_ = PAD ? (NU | 1) : NU, AS_ = PAD ? (NX | 1) : NX;
-    static constexpr int TILES = S::NPT * TS;
+    // GBA shapes stage only the pivot-block tiles; the coupling rows (read
+    // once, by y -= [LB ALQ]' lam_f) come straight from global memory
+    static constexpr bool GBA_ = !PAD && S::NUX <= 32 && NX <= 32;
+    static constexpr int NSTG = GBA_ ? S::CT * (S::CT + 1) / 2 : S::NPT;
+    static constexpr int TILES = NSTG * TS;
     static constexpr int OFF_Y = TILES, OFF_WL = OFF_Y + ((S::NUX + 1) & ~1);
     // GBA: [B A]_{s+1} read straight from global (coalesced rows, lane =
     // column, butterfly reduce-scatter) instead of staged: 4.8 KB less shared
     // memory per warp at the config-1 shape -> 16 instead of 12 resident warps
-    static constexpr bool GBA = !PAD && S::NUX <= 32 && NX <= 32;
+    static constexpr bool GBA = GBA_;
     static constexpr int OFF_B = OFF_WL + ((NX + 1) & ~1);
     static constexpr int OFF_A = OFF_B + (GBA ? 0 : ((NX * BS_ + 1) & ~1));
     static constexpr int BUF = OFF_A + (GBA ? 0 : ((NX * AS_ + 1) & ~1));
@@ -64,7 +68,7 @@ __device__ __forceinline__ void bs_stage(const BacksubArgs &a, double *buf, size
     {
         const double *src = a.fac + (chain * n + s) * S::NPT * kTileElems;
         if constexpr (!L::PAD) {
-            wcopy<L::TILES, 0>(buf, src, lane);
+            wcopy<L::TILES, 0>(buf, src, lane); // (GBA: the pivot-block tiles only)
         } else {
 #pragma unroll
             for (int t = 0; t < S::NPT; ++t)
@@ -133,6 +137,16 @@ __global__ void __launch_bounds__(32 * WPB) backsub_warp_kernel(BacksubArgs a) {
 
     for (int s = n - 1; s >= 0; --s) {
         const double *buf = bufs[(n - 1 - s) & 1];
+        const int k = lane; // this lane's entry of the nux-vector
+        // y_k -= ([LB ALQ]' lam_f)_k: GBA shapes read the coupling rows from
+        // global memory, issued before the wait for the staged pivot tiles
+        double gk = 0.0;
+        if constexpr (L::GBA) {
+            const double *gfac = a.fac + (chain * n + s) * S::NPT * kTileElems;
+#pragma unroll
+            for (int q = 0; q < NX; ++q)
+                gk += (k < NUX ? __ldg(gfac + L::at(TOP + q, 0) + (k / 8) * kTileElems + k % 8) : 0.0) * lf[q];
+        }
         if (L::NBUF > 1 && s > 0) {
             bs_stage<NU, NX>(a, bufs[(n - s) & 1], chain, b, c, s - 1, lane);
             cp_wait<1>();
@@ -141,12 +155,12 @@ __global__ void __launch_bounds__(32 * WPB) backsub_warp_kernel(BacksubArgs a) {
         }
         __syncwarp();
         const int j = g.stage_of(c, s), xi = g.x_index_of(c, s);
-        const int k = lane; // this lane's entry of the nux-vector
-        // y_k -= ([LB ALQ]' lam_f)_k ; idg_k = 1 / LH_kk
-        double gk = 0.0;
+        // idg_k = 1 / LH_kk
+        if constexpr (!L::GBA) {
 #pragma unroll
-        for (int q = 0; q < NX; ++q)
-            gk += (k < NUX ? buf[L::at(TOP + q, 0) + (k / 8) * L::TS + k % 8] : 0.0) * lf[q];
+            for (int q = 0; q < NX; ++q)
+                gk += (k < NUX ? buf[L::at(TOP + q, 0) + (k / 8) * L::TS + k % 8] : 0.0) * lf[q];
+        }
         double Y = (k < NUX) ? buf[L::OFF_Y + (k < NUX ? k : 0)] - gk : 0.0;
         const double idg = (k < NUX) ? 1.0 / buf[L::at(k < NUX ? k : 0, k < NUX ? k : 0)] : 0.0;
         if (s == n - 1) {
