@@ -33,7 +33,7 @@ template <int NU, int NX> struct BS {
     static constexpr int BS_ = PAD ? (NU | 1) : NU, AS_ = PAD ? (NX | 1) : NX;
     // GBA shapes stage only the pivot-block tiles; the coupling rows (read
     // once, by y -= [LB ALQ]' lam_f) come straight from global memory
-    static constexpr bool GBA_ = !PAD && S::NUX <= 32 && NX <= 32;
+    static constexpr bool GBA_ = !PAD && S::NUX <= 32 && NX <= 32; // measured slower for the small (PAD) shapes
     static constexpr int NSTG = GBA_ ? S::CT * (S::CT + 1) / 2 : S::NPT;
     static constexpr int TILES = NSTG * TS;
     static constexpr int OFF_Y = TILES, OFF_WL = OFF_Y + ((S::NUX + 1) & ~1);
@@ -50,6 +50,13 @@ template <int NU, int NX> struct BS {
     static constexpr int NBUF = 1;
     static constexpr int PER_WARP = NBUF * BUF + VEC;
     // stored-tile offset of panel entry (r, col), r/col compile-time or not
+    // the same entry in the global factor (dense 64-double tile stride)
+    __host__ __device__ static constexpr int gat(int r, int col) {
+        return ((r / 8) < S::CT ? S::T(r / 8, col / 8)
+                                : S::CT * (S::CT + 1) / 2 + (r / 8 - S::CT) * S::CT + col / 8) *
+                   kTileElems +
+               (r % 8) * 8 + col % 8;
+    }
     __host__ __device__ static constexpr int at(int r, int col) {
         return ((r / 8) < S::CT ? S::T(r / 8, col / 8)
                                 : S::CT * (S::CT + 1) / 2 + (r / 8 - S::CT) * S::CT + col / 8) *
@@ -71,7 +78,7 @@ __device__ __forceinline__ void bs_stage(const BacksubArgs &a, double *buf, size
             wcopy<L::TILES, 0>(buf, src, lane); // (GBA: the pivot-block tiles only)
         } else {
 #pragma unroll
-            for (int t = 0; t < S::NPT; ++t)
+            for (int t = 0; t < L::NSTG; ++t)
                 cp16(buf + t * L::TS + 2 * lane, src + t * kTileElems + 2 * lane);
         }
     }
@@ -145,7 +152,7 @@ __global__ void __launch_bounds__(32 * WPB) backsub_warp_kernel(BacksubArgs a) {
             const double *gfac = a.fac + (chain * n + s) * S::NPT * kTileElems;
 #pragma unroll
             for (int q = 0; q < NX; ++q)
-                gk += (k < NUX ? __ldg(gfac + L::at(TOP + q, 0) + (k / 8) * kTileElems + k % 8) : 0.0) * lf[q];
+                gk += (k < NUX ? __ldg(gfac + L::gat(TOP + q, 0) + (k / 8) * kTileElems + k % 8) : 0.0) * lf[q];
         }
         if (L::NBUF > 1 && s > 0) {
             bs_stage<NU, NX>(a, bufs[(n - s) & 1], chain, b, c, s - 1, lane);
