@@ -133,14 +133,16 @@ def fp64_peak():
 
 def ncu_traffic(kernel_tag, cfg_idx, batch):
     """DRAM bytes per launch of a kernel from the committed `ncu --set full`
-    summary (profiles/ncu_r01_<tag>.json, tools/ncu_summary.py) -- only for
-    the workload it was captured on (config 1, 1024 instances)."""
-    path = os.path.join(ROOT, "profiles", f"ncu_r01_{kernel_tag}.json")
-    if cfg_idx != 1 or batch != 1024 or not os.path.exists(path):
+    summary (profiles/ncu_r01_<tag>[_cfgK].json, tools/ncu_summary.py) -- only
+    for the workload it was captured on (config 1: 1024 instances, config 4:
+    512 instances, one Newton system)."""
+    name = {(1, 1024): kernel_tag, (4, 512): f"{kernel_tag}_cfg4"}.get((cfg_idx, batch))
+    path = os.path.join(ROOT, "profiles", f"ncu_r01_{name}.json")
+    if name is None or not os.path.exists(path):
         return None, None
     with open(path) as fh:
         d = json.load(fh)
-    return d.get("dram_bytes"), f"profiles/ncu_r01_{kernel_tag}.json ({d.get('report')})"
+    return d.get("dram_bytes"), f"profiles/ncu_r01_{name}.json ({d.get('report')})"
 
 
 def hbm_peak():

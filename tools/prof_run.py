@@ -1,5 +1,5 @@
 """Small driver for ncu captures: solve_problem on a reduced batch of a
-BASELINE config, device-resident inputs (python tools/prof_run.py CFG BATCH REPS)."""
+BASELINE config (config 4: one fused Newton system), device-resident inputs (python tools/prof_run.py CFG BATCH REPS)."""
 import os
 import sys
 
@@ -17,7 +17,13 @@ p = synth.generate(cfg, seed=0, batch=batch)
 dev = EqOCPBatch.__new__(EqOCPBatch)
 for k in OCP_FIELDS:
     setattr(dev, k, torch.from_numpy(getattr(p, k)).cuda())
-for _ in range(reps):
-    s = kkt.solve_problem(dev, kkt.FactorOptions(P=c.P))
+if cfg == 4:  # QPALM Newton system: assembly fused into the panel
+    D, E, sig = (torch.from_numpy(a).cuda()
+                 for a in synth.qpalm_data(p, seed=0, iters=1, ny=c.ny))
+    for _ in range(reps):
+        s = kkt.solve_newton(dev, D, E, sig[0], kkt.FactorOptions(P=c.P))
+else:
+    for _ in range(reps):
+        s = kkt.solve_problem(dev, kkt.FactorOptions(P=c.P))
 torch.cuda.synchronize()
 print("ok", float(s.u.abs().max()))
