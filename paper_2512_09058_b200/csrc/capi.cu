@@ -76,6 +76,17 @@ int set_err(cyq_ctx *ctx, int code, const std::string &msg) {
 
 bool pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 
+// The runtime-shape kernels keep a stage's blocks (back substitution, forward
+// sweep) or an instance's Schur rows in shared memory: shapes beyond it are
+// rejected like the too-large stage panel in make_geo, never launched.
+constexpr size_t kMaxDynSmem = 227 * 1024;
+int smem_too_large(cyq_ctx *ctx, const char *what, size_t bytes) {
+    char msg[160];
+    snprintf(msg, sizeof msg, "stage shape too large: %s needs %zu KB of shared memory (max %zu)", what,
+             bytes / 1024, kMaxDynSmem / 1024);
+    return set_err(ctx, CYQ_INVALID_ARG, msg);
+}
+
 int make_geo(cyq_ctx *ctx, const cyq_dims *d, Geo &g) {
     if (!d || d->N < 1 || d->nx < 1 || d->nu < 1 || d->batch < 1)
         return set_err(ctx, CYQ_INVALID_ARG, "dims: N, nx, nu, batch must be >= 1");
@@ -220,7 +231,9 @@ void riccati_shape(const Geo &g, int &nw, int &maxt) {
         nw = 8;
         per = (nt + nw - 1) / nw;
     }
-    maxt = per <= 4 ? 4 : per <= 8 ? 8 : per <= 16 ? 16 : 32;
+    // 8 warps only exist in the MAXT = 32 instantiation (launch bounds: 128
+    // threads below it)
+    maxt = nw == 8 ? 32 : per <= 4 ? 4 : per <= 8 ? 8 : per <= 16 ? 16 : 32;
 }
 
 template <int M> void launch_riccati_t(const Geo &g, int nw, cudaStream_t st, const RiccatiArgs &ra) {
@@ -350,9 +363,13 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
                 SchurArgs sv = sa;
                 sv.do_factor = 0;
                 const int nw = schur_warps_solve(g);
+                if (schur_smem_for(g, nw) > kMaxDynSmem)
+                    return smem_too_large(ctx, "Schur/CR solve (P x nx)", schur_smem_for(g, nw));
                 schur_cr_kernel<<<g.batch, 32 * nw, schur_smem_for(g, nw), ctx->stream>>>(sv);
             }
         } else {
+            if (schur_smem_bytes(g) > kMaxDynSmem)
+                return smem_too_large(ctx, "Schur/CR (P x nx)", schur_smem_bytes(g));
             schur_cr_kernel<<<g.batch, 32 * schur_warps(g), schur_smem_bytes(g), ctx->stream>>>(sa);
         }
     }
@@ -399,6 +416,8 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
             Timed t(ctx, 2);
             if (!launch_backsub_warp(g, ctx->stream, ba) && !launch_backsub_tile(g, ctx->stream, ba)) {
                 const int wpb = backsub_wpb(g);
+                if (backsub_smem_bytes(g) > kMaxDynSmem)
+                    return smem_too_large(ctx, "back substitution", backsub_smem_bytes(g));
                 backsub_kernel<<<(chains + wpb - 1) / wpb, 32 * wpb, backsub_smem_bytes(g),
                                  ctx->stream>>>(ba);
             }
@@ -422,6 +441,8 @@ int launch_solve(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &
     {
         Timed t(ctx, 3);
         const int wpb = 2 * forward_smem_per_warp(g) <= 200 * 1024 ? 2 : 1;
+        if ((size_t)wpb * forward_smem_per_warp(g) > kMaxDynSmem)
+            return smem_too_large(ctx, "forward sweep", forward_smem_per_warp(g));
         forward_kernel<<<(chains + wpb - 1) / wpb, 32 * wpb, wpb * forward_smem_per_warp(g),
                          ctx->stream>>>(ba, ws.y, ws.wl, ws.trail);
     }
@@ -431,6 +452,8 @@ int launch_solve(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &
         Timed t(ctx, 1);
         if (!launch_schur_fused(g, ctx->stream, sa) && !launch_schur_big(g, ctx->stream, sa)) {
             const int nw = schur_warps_solve(g);
+            if (schur_smem_for(g, nw) > kMaxDynSmem)
+                return smem_too_large(ctx, "Schur/CR solve (P x nx)", schur_smem_for(g, nw));
             schur_cr_kernel<<<g.batch, 32 * nw, schur_smem_for(g, nw), ctx->stream>>>(sa);
         }
     }
@@ -439,6 +462,8 @@ int launch_solve(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &
         Timed t(ctx, 2);
         if (!launch_backsub_warp(g, ctx->stream, ba) && !launch_backsub_tile(g, ctx->stream, ba)) {
             const int wpb = backsub_wpb(g);
+            if (backsub_smem_bytes(g) > kMaxDynSmem)
+                return smem_too_large(ctx, "back substitution", backsub_smem_bytes(g));
             backsub_kernel<<<(chains + wpb - 1) / wpb, 32 * wpb, backsub_smem_bytes(g),
                              ctx->stream>>>(ba);
         }
