@@ -75,3 +75,20 @@ def test_gpu_shape_beyond_envelope_is_rejected(N, nx, nu, P):
     p = _problem(N, nx, nu, P, 1)
     with pytest.raises(ValueError, match="too large"):
         kkt.solve_problem(p, kkt.FactorOptions(P=P))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,nx,nu,P,batch", SHAPES[::2] + [(16, 40, 8, 4, 1)])
+def test_gpu_factor_solve_new_rhs_shape_vs_oracle(oracle, N, nx, nu, P, batch):
+    """kkt::factor once, kkt::solve with an independent rhs (the forward
+    sweep kernel) -- kkt_solve.cpp:23-309 -- on the same shape sweep."""
+    p = _problem(N, nx, nu, P, batch)
+    f = kkt.factor(p, kkt.FactorOptions(P=P))
+    rng = np.random.default_rng(N * 100 + nx)
+    rhs = EqRhsBatch(rng.standard_normal((batch, N, nu)), rng.standard_normal((batch, N + 1, nx)),
+                     rng.standard_normal((batch, N, nx)))
+    sol = kkt.solve(f, p, rhs)
+    ref, rc, _ = oracle.solve(p, rhs, P)
+    assert rc == 0
+    assert rel_error(sol, ref).max() <= REL_TOL
+    assert kkt_residual(p, rhs, sol).max() <= RES_TOL
