@@ -15,6 +15,7 @@
 #include "kernels.h"
 #include "riccati_common.cuh" // cp8 / cp_commit / cp_wait
 
+#include <algorithm>
 #include <string>
 
 namespace cyqb {
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(32 * kAugWarps) augment_kernel(
     const int nx = CNX > 0 ? CNX : nx_, nu = CNU > 0 ? CNU : nu_, ny = CNY > 0 ? CNY : ny_;
     extern __shared__ __align__(16) double sm[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const long long task = (long long)blockIdx.x * kAugWarps + wib;
+    const long long task = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
     if (task >= (long long)batch * (N + 1))
         return;
     const int b = (int)(task / (N + 1)), j = (int)(task % (N + 1));
@@ -138,13 +139,20 @@ bool launch_augment(cudaStream_t st, int batch, int N, int nx, int nu, int ny, c
         return false;
     const int nux = nx + nu, ldc = 8 * ((nux + 7) / 8), ks = (ny + 3) / 4;
     const int per_warp = (4 * ks * ldc + 4 * ks + ldc * ldc + 1) & ~1;
+    // warps per CTA: as many (up to 8) as shared memory holds -- the largest
+    // shapes (nx + nu = 64, ny = 64: 66 KB per warp) run 3 per CTA
+    constexpr size_t kSmemCap = 200 * 1024;
+    const size_t per_warp_bytes = (size_t)per_warp * sizeof(double);
+    const int nw = (int)std::min<size_t>(kAugWarps, kSmemCap / per_warp_bytes);
+    if (nw < 1)
+        return false;
     const long long tasks = (long long)batch * (N + 1);
-    const int grid = (int)((tasks + kAugWarps - 1) / kAugWarps);
-    const size_t smem = (size_t)kAugWarps * per_warp * sizeof(double);
+    const int grid = (int)((tasks + nw - 1) / nw);
+    const size_t smem = (size_t)nw * per_warp_bytes;
     auto go = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        kern<<<grid, 32 * kAugWarps, smem, st>>>(batch, N, nx, nu, ny, R, S, Q, D, C, sigma, gamma_inv,
-                                                R_out, S_out, Q_out, per_warp);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
+        kern<<<grid, 32 * nw, smem, st>>>(batch, N, nx, nu, ny, R, S, Q, D, C, sigma, gamma_inv,
+                                         R_out, S_out, Q_out, per_warp);
     };
     if (nu == 8 && nx == 16 && ny == 24)
         go(augment_kernel<8, 16, 24>); // BASELINE config 4

@@ -81,6 +81,22 @@ class Context:
                             f"{self.lib.cyq_ctx_last_error(None).decode()}")
         self.h = h
         self.device = device
+        self._bound = False  # set_stream() called: keep the caller's stream
+        self._cur = None
+
+    def follow_torch(self, arrays):
+        """Stream ordering with torch: unless the caller bound a stream with
+        set_stream(), calls that take CUDA torch tensors run on torch's current
+        stream of this device, so inputs produced by earlier torch work are
+        complete and results are ordered before later torch work."""
+        if self._bound or not any(_is_torch(a) for a in arrays):
+            return
+        import torch
+
+        s = torch.cuda.current_stream(self.device).cuda_stream or 1  # 1 = cudaStreamLegacy
+        if s != self._cur:
+            self.lib.cyq_ctx_set_stream(self.h, C.c_void_p(s))
+            self._cur = s
 
     @classmethod
     def default(cls, device: int = 0) -> "Context":
@@ -92,7 +108,10 @@ class Context:
         return self.lib.cyq_ctx_last_error(self.h).decode()
 
     def set_stream(self, stream_ptr: int | None):
+        """Bind the context to a CUDA stream (None: a private non-blocking
+        stream); either way it stops following torch's current stream."""
         self.lib.cyq_ctx_set_stream(self.h, C.c_void_p(stream_ptr or 0))
+        self._bound, self._cur = True, stream_ptr
 
     def synchronize(self):
         self.lib.cyq_ctx_synchronize(self.h)
@@ -196,6 +215,7 @@ def solve_problem(p, opts: FactorOptions, ctx: Context | None = None, out=None,
     ctx = ctx or Context.default()
     arrs = [getattr(p, k) for k in OCP_FIELDS]
     mem = _mem(arrs)
+    ctx.follow_torch(arrs)
     sol = out if out is not None else _alloc_sol(p, mem == _lib.CYQ_MEM_DEVICE)
     st = (_lib.CyqStatus * p.A.shape[0])()
     rc = ctx.lib.cyq_solve_problem_batch(ctx.h, C.byref(_dims(p, opts.P)),
@@ -247,6 +267,7 @@ def factor(p, opts: FactorOptions, ctx: Context | None = None) -> Factor:
     _check_opts(opts)
     ctx = ctx or Context.default()
     mem = _mem([getattr(p, k) for k in OCP_FIELDS])
+    ctx.follow_torch([getattr(p, k) for k in OCP_FIELDS])
     h = C.c_void_p()
     st = (_lib.CyqStatus * p.A.shape[0])()
     rc = ctx.lib.cyq_factor_batch(ctx.h, C.byref(_dims(p, opts.P)), C.byref(_ocp_struct(p)),
@@ -261,6 +282,7 @@ def solve(f: Factor, p, rhs) -> EqSolutionBatch:
     ctx = f.ctx
     arrs = [getattr(rhs, k) for k in RHS_FIELDS]
     mem = _mem(arrs)
+    ctx.follow_torch(arrs + [getattr(p, k) for k in OCP_FIELDS])
     sol = _alloc_sol(p, mem == _lib.CYQ_MEM_DEVICE)
     rc = ctx.lib.cyq_solve_batch(ctx.h, f.h, C.byref(_ocp_struct(p)),
                                  C.byref(_lib.CyqRhsBatch(*[_ptr(a) for a in arrs])),
@@ -328,6 +350,7 @@ def augment_hessians(p, D, Cm, sigma, gamma_inv: float = 0.0, out=None,
     for a in (p.R, p.S, p.Q, D, Cm, sigma):
         if not _is_torch(a):
             raise ValueError("augment_hessians takes CUDA torch tensors")
+    ctx.follow_torch([D])
     b, N, nx, nu = p.A.shape[0], p.A.shape[1], p.A.shape[2], p.B.shape[3]
     ny = D.shape[2]
     if out is None:
@@ -358,6 +381,7 @@ def solve_newton(p, D, Cm, sigma, opts: FactorOptions, gamma_inv: float = 0.0, o
     for a in [getattr(p, k) for k in OCP_FIELDS] + [D, Cm, sigma]:
         if not _is_torch(a):
             raise ValueError("solve_newton takes CUDA torch tensors")
+    ctx.follow_torch([D])
     sol = out if out is not None else _alloc_sol(p, True)
     st = (_lib.CyqStatus * p.A.shape[0])()
     rc = ctx.lib.cyq_solve_newton_batch(
@@ -384,6 +408,7 @@ def line_search_exact(alpha, delta, eta, beta, ctx: Context | None = None,
     for a in (alpha, delta, eta, beta):
         if not _is_torch(a):
             raise ValueError("line_search_exact takes CUDA torch tensors")
+    ctx.follow_torch([alpha])
     b, m = alpha.shape[0], (alpha.shape[1] if alpha.dim() > 1 else 0)
     tau = torch.empty(b, dtype=torch.float64, device=alpha.device)
     its = torch.zeros(b, dtype=torch.int64, device=alpha.device)

@@ -92,3 +92,77 @@ def test_gpu_factor_solve_new_rhs_shape_vs_oracle(oracle, N, nx, nu, P, batch):
     assert rc == 0
     assert rel_error(sol, ref).max() <= REL_TOL
     assert kkt_residual(p, rhs, sol).max() <= RES_TOL
+
+
+# (N, nx, nu, ny, P): Newton-system assembly kernel (cyq_augment_hessians_batch)
+NEWTON_SHAPES = [(5, 3, 1, 1, 2), (6, 1, 1, 5, 1), (9, 17, 9, 33, 4), (7, 40, 24, 64, 2),
+                 (12, 8, 8, 8, 8), (10, 20, 10, 24, 4)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,nx,nu,ny,P", NEWTON_SHAPES)
+def test_gpu_newton_assembly_shapes(oracle, N, nx, nu, ny, P):
+    """qpalm::assemble_newton (qpalm.cpp:184-221) on the GPU for stage shapes
+    other than config 4's: Hessians vs the host construction, and the
+    Newton solve vs the oracle on the host-assembled system."""
+    import torch
+
+    base = _problem(N, nx, nu, P, 2)
+    D, E, sig = synth.qpalm_data(base, seed=3, iters=1, ny=ny)
+    ref_p = next(synth.qpalm_sequence(base, seed=3, iters=1, ny=ny))
+    dev = EqOCPBatch.__new__(EqOCPBatch)
+    for k in ("A", "B", "R", "S", "Q", "f", "r", "q", "x_init"):
+        setattr(dev, k, torch.from_numpy(np.ascontiguousarray(getattr(base, k))).cuda())
+    Dd, Ed, sd = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (D, E, sig[0]))
+    aug = kkt.augment_hessians(dev, Dd, Ed, sd)
+    for got, ref in ((aug.R, ref_p.R), (aug.S, ref_p.S), (aug.Q, ref_p.Q)):
+        assert np.abs(got.cpu().numpy() - ref).max() <= 1e-13 * np.abs(ref).max()
+    sol = kkt.solve_newton(dev, Dd, Ed, sd, kkt.FactorOptions(P=P))
+    ref, rc, _ = oracle.solve_problem(ref_p, P)
+    assert rc == 0
+    got = type(ref)(*[a.cpu().numpy() if hasattr(a, "cpu") else a for a in (sol.u, sol.x, sol.lam)])
+    assert rel_error(got, ref).max() <= REL_TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nx,nu,ny", [(8, 4, 65), (40, 25, 8)])
+def test_gpu_newton_assembly_beyond_envelope_is_rejected(nx, nu, ny):
+    import torch
+
+    base = _problem(4, nx, nu, 2, 1)
+    D, E, sig = synth.qpalm_data(base, seed=3, iters=1, ny=ny)
+    dev = EqOCPBatch.__new__(EqOCPBatch)
+    for k in ("A", "B", "R", "S", "Q", "f", "r", "q", "x_init"):
+        setattr(dev, k, torch.from_numpy(np.ascontiguousarray(getattr(base, k))).cuda())
+    Dd, Ed, sd = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (D, E, sig[0]))
+    with pytest.raises(ValueError):
+        kkt.augment_hessians(dev, Dd, Ed, sd)
+
+
+@pytest.mark.gpu
+def test_gpu_calls_follow_torch_current_stream():
+    """Calls with CUDA torch tensors run on torch's current stream: inputs
+    written by torch work still queued on that stream (behind a 20 ms sleep)
+    are complete when the assembly kernel reads them, and the result is
+    complete when torch reads it back on the same stream."""
+    import torch
+
+    base = _problem(6, 17, 9, 2, 2)
+    D, E, sig = synth.qpalm_data(base, seed=3, iters=1, ny=33)
+    ref_p = next(synth.qpalm_sequence(base, seed=3, iters=1, ny=33))
+    dev = EqOCPBatch.__new__(EqOCPBatch)
+    for k in ("A", "B", "R", "S", "Q", "f", "r", "q", "x_init"):
+        setattr(dev, k, torch.from_numpy(np.ascontiguousarray(getattr(base, k))).cuda())
+    src = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (D, E, sig[0])]
+    dst = [torch.zeros_like(a) for a in src]
+    kkt.augment_hessians(dev, *src)  # loads the kernel (a lazy module load synchronizes)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(40_000_000)  # ~20 ms of GPU time ahead of the copies
+        for d, a in zip(dst, src):
+            d.copy_(a, non_blocking=True)
+        aug = kkt.augment_hessians(dev, *dst)
+        R = aug.R.cpu()
+    assert np.abs(R.numpy() - ref_p.R).max() <= 1e-13 * np.abs(ref_p.R).max()
+    assert kkt.Context.default()._cur == s.cuda_stream
