@@ -301,7 +301,7 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
     const int chains = g.batch * g.P;
     CU(cudaMemsetAsync(ws.fail, 0xFF, sizeof(unsigned long long) * g.batch, ctx->stream));
     const bool staged = riccati_staged(g);
-    { // identity / zero constants for the direct-mode kernels
+    if (!staged) { // identity / zero constants for the direct-mode generic panel
         std::vector<double> h(riccati_consts_doubles(g), 0.0);
         for (int i = 0; i < g.nu; ++i)
             h[(size_t)i * g.nu + i] = 1.0;

@@ -135,16 +135,23 @@ class Context:
             pass
 
 
+_F64 = np.dtype(np.float64)
+
+
 def _is_torch(a) -> bool:
-    return type(a).__module__.startswith("torch")
+    return not isinstance(a, np.ndarray) and type(a).__module__.startswith("torch")
 
 
-def _ptr(a):
-    if _is_torch(a):
-        assert a.is_cuda and a.is_contiguous() and str(a.dtype) == "torch.float64"
-        return C.c_void_p(a.data_ptr())
-    assert isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous
-    return C.c_void_p(a.ctypes.data)
+def _ptr(a) -> int:
+    """Address of a contiguous float64 array (every ABI pointer parameter is
+    declared c_void_p in _lib.SIGNATURES, so a plain int converts)."""
+    if isinstance(a, np.ndarray):
+        assert a.dtype == _F64 and a.flags.c_contiguous
+        return a.ctypes.data
+    import torch
+
+    assert a.is_cuda and a.is_contiguous() and a.dtype == torch.float64
+    return a.data_ptr()
 
 
 def _mem(arrs) -> int:
