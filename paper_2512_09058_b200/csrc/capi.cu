@@ -33,6 +33,8 @@ struct cyq_ctx {
     size_t augbuf_bytes = 0;
     void *lsbuf = nullptr; // line-search breakpoints + per-instance status
     size_t lsbuf_bytes = 0;
+    unsigned long long *hfail = nullptr; // pinned per-instance failure keys (status readback)
+    size_t hfail_n = 0;
     cudaStream_t copy_stream = nullptr; // host->device staging of chunked calls
     cudaStream_t side_stream = nullptr; // second compute stream (split device batches)
     // per-kernel timing (cyq_ctx_profile)
@@ -474,9 +476,17 @@ int launch_solve(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &
 
 int decode_status(cyq_ctx *ctx, const Geo &g, const unsigned long long *dfail,
                   cyq_status *status) {
-    std::vector<unsigned long long> h(g.batch);
-    CU(cudaMemcpyAsync(h.data(), dfail, sizeof(unsigned long long) * g.batch,
-                       cudaMemcpyDeviceToHost, ctx->stream));
+    if (ctx->hfail_n < (size_t)g.batch) { // pinned: the readback is one DMA, no staging copy
+        if (ctx->hfail)
+            CU(cudaFreeHost(ctx->hfail));
+        ctx->hfail = nullptr;
+        ctx->hfail_n = 0;
+        CU(cudaMallocHost(reinterpret_cast<void **>(&ctx->hfail), sizeof(unsigned long long) * g.batch));
+        ctx->hfail_n = (size_t)g.batch;
+    }
+    unsigned long long *h = ctx->hfail;
+    CU(cudaMemcpyAsync(h, dfail, sizeof(unsigned long long) * g.batch, cudaMemcpyDeviceToHost,
+                       ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     int worst = CYQ_OK;
     for (int b = 0; b < g.batch; ++b) {
@@ -558,6 +568,8 @@ int cyq_ctx_destroy(cyq_ctx *ctx) {
         cudaFree(ctx->augbuf);
     if (ctx->lsbuf)
         cudaFree(ctx->lsbuf);
+    if (ctx->hfail)
+        cudaFreeHost(ctx->hfail);
     for (auto &e : ctx->ev) {
         cudaEventDestroy(e.second.first);
         cudaEventDestroy(e.second.second);
