@@ -387,7 +387,7 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
             for (int k = 0; k < 8; ++k)
                 fprintf(stderr, " %lld", h[s * 16 + k] ? h[s * 16 + k] - t0 : -1);
             fprintf(stderr, " | C:");
-            for (int k = 8; k < 15; ++k)
+            for (int k = 8; k < 16; ++k)
                 fprintf(stderr, " %lld", h[s * 16 + k] ? h[s * 16 + k] - t0 : -1);
             fprintf(stderr, "\n");
         }

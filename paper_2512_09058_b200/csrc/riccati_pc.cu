@@ -55,7 +55,8 @@ template <int NU, int NX> struct PCS : PanelShape<NU, NX> {
     static constexpr int O_RU0 = O_YX + ((NX + 1) & ~1);        // NU
     static constexpr int O_SCR = O_RU0 + ((NU + 1) & ~1);       // 64
     static constexpr int O_MB = O_SCR + kTileElems;             // mbarriers (8 bytes each)
-    static constexpr int SMEM = O_MB + 16;
+    static constexpr int O_TAB = O_MB + 16;                     // staging copy plan (int16)
+    static constexpr int SMEM = O_TAB + CopyPlan<NU, NX>::DOUBLES;
 };
 
 // Hand-off mbarriers (one arrival per phase, one phase per stage). P -> C:
@@ -64,12 +65,23 @@ template <int NU, int NX> struct PCS : PanelShape<NU, NX> {
 // targets the next phase of its barrier; the acknowledgements keep either
 // side from running two phases ahead (so parity waits are unambiguous).
 enum : int { kMbH = 0, kMbLQ = 1, kMbV = 2, kMbCInit = 3, kMbCWW = 4, kMbCChol = 5, kMbCMW = 6, kMbCol = 7 };
+// after the CT column barriers: P -> C "pivot-block image read" (C may stage
+// H_{s+1} into it), and H_{s+1} landed (32 arrivals: one per consumer lane,
+// each when that lane's copies complete -- cp.async.mbarrier.arrive.noinc)
+template <int CT> struct MbX {
+    static constexpr int kImgFree = kMbCol + CT, kHFill = kMbCol + CT + 1, kBAFill = kMbCol + CT + 2,
+                         kCount = kMbCol + CT + 3;
+};
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void mb_init(unsigned long long *mb) {
-    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(mb)) : "memory");
+__device__ __forceinline__ void mb_init(unsigned long long *mb, int count = 1) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+// this lane's arrival, triggered when its prior cp.async copies complete
+__device__ __forceinline__ void mb_arrive_on_copies(unsigned long long *mb) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(mb)) : "memory");
 }
 // all lanes' prior shared-memory writes, then one (release) arrival
 __device__ __forceinline__ void mb_signal(unsigned long long *mb, int lane) {
@@ -108,6 +120,7 @@ __global__ void __launch_bounds__(64, 6) riccati_pc_kernel(RiccatiArgs a) {
     double *imr = sm + W::O_IMR, *Sb = sm + W::O_S, *BA = sm + W::O_BA, *fbuf = sm + W::O_F;
     double *colb = sm + W::O_COL, *yx = sm + W::O_YX, *ru0 = sm + W::O_RU0, *tscr = sm + W::O_SCR;
     unsigned long long *mb = reinterpret_cast<unsigned long long *>(sm + W::O_MB);
+    short *ctab = reinterpret_cast<short *>(sm + W::O_TAB);
     constexpr int FST = (NX + 1) & ~1; // f slot stride
     const bool implicit_rhs = (a.p.ru == nullptr);
     const double sgn = implicit_rhs ? -1.0 : 1.0;
@@ -115,9 +128,13 @@ __global__ void __launch_bounds__(64, 6) riccati_pc_kernel(RiccatiArgs a) {
     for (int i = threadIdx.x; i < W::SMEM; i += 64)
         sm[i] = 0.0;
     __syncthreads();
-    if (threadIdx.x == 0)
-        for (int i = 0; i < kMbCol + CT; ++i)
-            mb_init(mb + i);
+    static_assert(MbX<CT>::kCount <= 16, "mbarrier slots");
+    if (role == 0)
+        CopyPlan<NU, NX>::build(ctab, lane);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < MbX<CT>::kCount; ++i)
+            mb_init(mb + i, (i == MbX<CT>::kHFill || i == MbX<CT>::kBAFill) ? 32 : 1);
+    }
     if (role == 0 && lane < W::PW - W::NUX) { // unit padding diagonal of the image
         const int r = W::NUX + lane;
         img[S::T(r / 8, r / 8) * kTileElems + (r % 8) * 9] = 1.0;
@@ -147,9 +164,9 @@ __global__ void __launch_bounds__(64, 6) riccati_pc_kernel(RiccatiArgs a) {
             const bool j0 = j == 0;
             if (ph) ph[s * 16 + 0] = clock64();
             if (s == 0)
-                cp_wait<0>();
+                cp_wait<0>(); // prologue: H_0, BA_0
             else
-                cp_wait<1>(); // H_s landed (BA_{s+1} may fly)
+                mb_wait(mb + MbX<CT>::kHFill, (s - 1) & 1); // H_s staged by C has landed
             if (s > 0)
                 mb_wait(mb + kMbCInit, (s - 1) & 1); // C has read [r; q]_{s-1}
             mb_signal(mb + kMbH, lane);
@@ -171,6 +188,7 @@ __global__ void __launch_bounds__(64, 6) riccati_pc_kernel(RiccatiArgs a) {
                     }
                     P[S::T(ti, tj)] = f;
                 }
+            mb_signal(mb + MbX<CT>::kImgFree, lane); // image and S' read: C stages H_{s+1}
             if (s > 0) {
 #pragma unroll
                 for (int kt = 0; kt < NXC; ++kt) {
@@ -190,15 +208,7 @@ __global__ void __launch_bounds__(64, 6) riccati_pc_kernel(RiccatiArgs a) {
                     }
                 }
             }
-            // ---- stage H_{s+1} ([r; q] into the other parity slot, read by C at
-            // stage s-1: acknowledged above) ------------------------------------
-            if (s + 1 < n) {
-                stage_H<NU, NX>(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), img,
-                                imr + ((s + 1) & 1) * W::PW, Sb);
-                if (s == 0)
-                    stage_BA<NU, NX>(g, a.p, b, g.stage_of(c, 1), BA, fbuf + FST);
-            }
-            cp_commit();
+            if (ph) ph[s * 16 + 15] = clock64();
             // ---- pivot floor --------------------------------------------------
             double dmax = 0.0;
 #pragma unroll
@@ -288,6 +298,11 @@ __global__ void __launch_bounds__(64, 6) riccati_pc_kernel(RiccatiArgs a) {
                 for (int t = 0; t < W::NP; ++t)
                     st_frag(dst + t * kTileElems, lane, P[t]);
             }
+            // (H_{s+1} is staged by the consumer warp, off the pivot chain)
+            if (s == 0 && n > 1) {
+                stage_BA<NU, NX>(g, a.p, b, g.stage_of(c, 1), BA, fbuf + FST);
+                cp_commit();
+            }
             if (s + 1 < n) {
                 // L_Q -> LQ once C has used the previous one
                 if (s > 0)
@@ -309,9 +324,9 @@ __global__ void __launch_bounds__(64, 6) riccati_pc_kernel(RiccatiArgs a) {
                         }
                 }
                 if (s == 0)
-                    cp_wait<0>();
+                    cp_wait<0>(); // BA_1, f_1 (the producer's own copies)
                 else
-                    cp_wait<1>(); // BA_{s+1}, f_{s+1} landed
+                    mb_wait(mb + MbX<CT>::kBAFill, (s - 1) & 1); // BA_{s+1}, f_{s+1} staged by C
                 mb_signal(mb + kMbLQ, lane);
                 // V_{s+1} = BA' L_Q -> W rows 0..CT-1, once C has read V_s
                 if (ph) ph[s * 16 + 5] = clock64();
@@ -348,9 +363,6 @@ __global__ void __launch_bounds__(64, 6) riccati_pc_kernel(RiccatiArgs a) {
                 mb_signal(mb + kMbV, lane);
                 if (ph) ph[s * 16 + 7] = clock64();
                 __syncwarp();
-                if (s + 2 < n) // f_{s+2} into the slot C used for f_s (acked by kCMW >= s)
-                    stage_BA<NU, NX>(g, a.p, b, g.stage_of(c, s + 2), BA, fbuf + ((s + 2) & 1) * FST);
-                cp_commit();
             }
         }
         unsigned long long my_fail =
@@ -399,6 +411,14 @@ __global__ void __launch_bounds__(64, 6) riccati_pc_kernel(RiccatiArgs a) {
             // ---- += W W' for my rows -----------------------------------------
             if (s > 0) {
                 mb_wait(mb + kMbV, (s - 1) & 1);
+                // V_s is computed: the BA buffer is free -- stage BA_{s+1} (and
+                // f_{s+1} into the slot of f_{s-1}) for the producer's V_{s+1}
+                if (s + 1 < n) {
+                    stage_BA_plan<NU, NX>(g, a.p, b, g.stage_of(c, s + 1), BA, fbuf + ((s + 1) & 1) * FST, ctab);
+                    __syncwarp();
+                    __threadfence_block();
+                    mb_arrive_on_copies(mb + MbX<CT>::kBAFill);
+                }
 #pragma unroll
                 for (int kt = 0; kt < NXC; ++kt) {
                     Frag w[TT];
@@ -419,6 +439,16 @@ __global__ void __launch_bounds__(64, 6) riccati_pc_kernel(RiccatiArgs a) {
                 }
             }
             mb_signal(mb + kMbCWW, lane);
+            // ---- stage H_{s+1} for the producer ([r; q] into the parity slot
+            // read at stage s-1), while the pivot chain runs -------------------
+            if (s + 1 < n) {
+                mb_wait(mb + MbX<CT>::kImgFree, s & 1);
+                stage_H_plan<NU, NX>(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), img,
+                                     imr + ((s + 1) & 1) * W::PW, Sb, ctab);
+                __syncwarp();
+                __threadfence_block(); // identity / zero fills of padding stages
+                mb_arrive_on_copies(mb + MbX<CT>::kHFill);
+            }
             if (ph) ph[s * 16 + 10] = clock64();
             // ---- my rows of each pivot column --------------------------------
 #pragma unroll

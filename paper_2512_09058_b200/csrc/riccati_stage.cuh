@@ -155,5 +155,98 @@ __device__ __forceinline__ void stage_BA(const Geo &g, const ProbView &p, int b,
     wcopy<NX, 0>(fb, in ? fs + ((size_t)b * N + j) * NX : nullptr, lane);
 }
 
+// Per-lane copy plan of the two scattered stagings -- R / Q into the tile
+// image (lower tiles only) and [B A] into padded rows -- built once per CTA
+// into shared memory: slot k of lane l holds the destination offset (in
+// doubles, -1 = none) of source element G (l + 32 k). Staging a stage is then
+// one 16-bit shared load and one cp.async per slot instead of the index
+// arithmetic of stage_H / stage_BA (~2k cycles per stage at config 0, issued
+// on the pivot chain's warp). G = 2 (16-byte copies) when every offset is
+// even, else 1.
+template <int NU, int NX> struct CopyPlan {
+    using S = Shp<NU, NX>;
+    using W = PanelShape<NU, NX>;
+    static constexpr int G = (NU % 2 == 0 && NX % 2 == 0) ? 2 : 1;
+    static constexpr int KR = (NU * NU / G + 31) / 32, KQ = (NX * NX / G + 31) / 32;
+    static constexpr int KB = (NX * NU / G + 31) / 32, KA = KQ;
+    static constexpr int OR = 0, OQ = KR, OB = OQ + KQ, OA = OB + KB, SLOTS = OA + KA;
+    static constexpr int DOUBLES = (SLOTS * 32 * 2 + 15) / 16 * 2; // footprint (even)
+    __device__ static int img_off(int r, int c) {
+        return S::T(r / 8, c / 8) * kTileElems + (r % 8) * 8 + c % 8;
+    }
+    __device__ static void build(short *tab, int lane) {
+        for (int k = 0; k < KR; ++k) {
+            const int e = G * (lane + 32 * k), r = e / NU, c = e % NU;
+            tab[(OR + k) * 32 + lane] = (short)((e < NU * NU && c / 8 <= r / 8) ? img_off(r, c) : -1);
+        }
+        for (int k = 0; k < KQ; ++k) {
+            const int e = G * (lane + 32 * k), r = NU + e / NX, c = NU + e % NX;
+            tab[(OQ + k) * 32 + lane] = (short)((e < NX * NX && c / 8 <= r / 8) ? img_off(r, c) : -1);
+        }
+        for (int k = 0; k < KB; ++k) {
+            const int e = G * (lane + 32 * k);
+            tab[(OB + k) * 32 + lane] = (short)(e < NX * NU ? (e / NU) * W::PW + e % NU : -1);
+        }
+        for (int k = 0; k < KA; ++k) {
+            const int e = G * (lane + 32 * k);
+            tab[(OA + k) * 32 + lane] = (short)(e < NX * NX ? (e / NX) * W::PW + NU + e % NX : -1);
+        }
+    }
+    template <int O, int K>
+    __device__ static void run(const short *tab, double *dst, const double *src, int lane) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int o = tab[(O + k) * 32 + lane];
+            if (o >= 0) {
+                if (G == 2)
+                    cp16(dst + o, src + 2 * (lane + 32 * k));
+                else
+                    cp8(dst + o, src + lane + 32 * k);
+            }
+        }
+    }
+};
+
+// stage_H / stage_BA through the plan; stages that need fills (padding, A at
+// j = 0) or unaligned sources take the general path
+template <int NU, int NX>
+__device__ __forceinline__ void stage_H_plan(const Geo &g, const ProbView &p, int b, int j, int xi,
+                                             double *img, double *imr, double *Sb, const short *tab) {
+    using CP = CopyPlan<NU, NX>;
+    const int N = g.N;
+    const double *Rs = j < N ? p.R + ((size_t)b * N + j) * NU * NU : nullptr;
+    const double *Qs = xi <= N ? p.Q + ((size_t)b * (N + 1) + xi) * NX * NX : nullptr;
+    if (!Rs || !Qs || (CP::G == 2 && !(aligned16(Rs) && aligned16(Qs)))) {
+        stage_H<NU, NX>(g, p, b, j, xi, img, imr, Sb);
+        return;
+    }
+    const int lane = lane_v();
+    CP::template run<CP::OR, CP::KR>(tab, img, Rs, lane);
+    CP::template run<CP::OQ, CP::KQ>(tab, img, Qs, lane);
+    wcopy<NU * NX, 0>(Sb, p.S + ((size_t)b * N + j) * NU * NX, lane);
+    const double *rs = p.ru ? p.ru : p.r;
+    const double *qs = p.qx ? p.qx : p.q;
+    wcopy<NU, 0>(imr, rs + ((size_t)b * N + j) * NU, lane);
+    wcopy<NX, 0>(imr + NU, qs + ((size_t)b * (N + 1) + xi) * NX, lane);
+}
+
+template <int NU, int NX>
+__device__ __forceinline__ void stage_BA_plan(const Geo &g, const ProbView &p, int b, int j, double *ba,
+                                              double *fb, const short *tab) {
+    using CP = CopyPlan<NU, NX>;
+    const int N = g.N;
+    const double *Bs = j < N ? p.B + ((size_t)b * N + j) * NX * NU : nullptr;
+    const double *As = (j < N && j != 0) ? p.A + ((size_t)b * N + j) * NX * NX : nullptr;
+    if (!Bs || !As || (CP::G == 2 && !(aligned16(Bs) && aligned16(As)))) {
+        stage_BA<NU, NX>(g, p, b, j, ba, fb);
+        return;
+    }
+    const int lane = lane_v();
+    CP::template run<CP::OB, CP::KB>(tab, ba, Bs, lane);
+    CP::template run<CP::OA, CP::KA>(tab, ba, As, lane);
+    const double *fs = p.fd ? p.fd : p.f;
+    wcopy<NX, 0>(fb, fs + ((size_t)b * N + j) * NX, lane);
+}
+
 } // namespace ric
 } // namespace cyqb
