@@ -171,10 +171,12 @@ template <int NU, int NX> struct CopyPlan {
     static constexpr int KB = (NX * NU / G + 31) / 32, KA = KQ;
     static constexpr int OR = 0, OQ = KR, OB = OQ + KQ, OA = OB + KB, SLOTS = OA + KA;
     static constexpr int DOUBLES = (SLOTS * 32 * 2 + 15) / 16 * 2; // footprint (even)
+    // the R / Q slots only (stage_H_plan), for kernels short of shared memory
+    static constexpr int DOUBLES_H = ((KR + KQ) * 32 * 2 + 15) / 16 * 2;
     __device__ static int img_off(int r, int c) {
         return S::T(r / 8, c / 8) * kTileElems + (r % 8) * 8 + c % 8;
     }
-    __device__ static void build(short *tab, int lane) {
+    __device__ static void build(short *tab, int lane, bool with_ba = true) {
         for (int k = 0; k < KR; ++k) {
             const int e = G * (lane + 32 * k), r = e / NU, c = e % NU;
             tab[(OR + k) * 32 + lane] = (short)((e < NU * NU && c / 8 <= r / 8) ? img_off(r, c) : -1);
@@ -183,6 +185,8 @@ template <int NU, int NX> struct CopyPlan {
             const int e = G * (lane + 32 * k), r = NU + e / NX, c = NU + e % NX;
             tab[(OQ + k) * 32 + lane] = (short)((e < NX * NX && c / 8 <= r / 8) ? img_off(r, c) : -1);
         }
+        if (!with_ba)
+            return;
         for (int k = 0; k < KB; ++k) {
             const int e = G * (lane + 32 * k);
             tab[(OB + k) * 32 + lane] = (short)(e < NX * NU ? (e / NU) * W::PW + e % NU : -1);

@@ -59,8 +59,13 @@ template <int NU, int NX, int NY = 0, bool TM = false> struct WS : PanelShape<NU
     static constexpr int O_X = O_SCR + kTileElems;
     static constexpr int O_SGU = O_X + ((NY * NUX_ + 1) & ~1);
     static constexpr int O_SGX = O_SGU + NYP;
-    static constexpr int SMEM = NY > 0 ? O_SGX + NYP : O_SCR + kTileElems;
-    static_assert((O_LQ | O_IMG | O_IMR | O_S | O_BA | O_F | O_RU0 | O_SCR | O_X | O_SGU | O_SGX | SMEM) % 2 == 0,
+    // per-lane copy plan: R / Q only (stage_H_plan; 576 B at config 1, inside
+    // the 8-chains-per-SM shared-memory budget), plus [B A] (stage_BA_plan)
+    // when the kernel is register-limited anyway (NY > 0)
+    static constexpr bool PLAN_BA = NY > 0;
+    static constexpr int O_TAB = NY > 0 ? O_SGX + NYP : O_SCR + kTileElems;
+    static constexpr int SMEM = O_TAB + (PLAN_BA ? CopyPlan<NU, NX>::DOUBLES : CopyPlan<NU, NX>::DOUBLES_H);
+    static_assert((O_LQ | O_IMG | O_IMR | O_S | O_BA | O_F | O_RU0 | O_SCR | O_X | O_SGU | O_SGX | O_TAB | SMEM) % 2 == 0,
                   "align");
 };
 
@@ -214,6 +219,7 @@ __device__ __forceinline__ void riccati_warp_body(const RiccatiArgs &a, int chai
     double *imr = base + W::O_IMR, *Sb = base + W::O_S, *BA = base + W::O_BA;
     double *fb = base + W::O_F, *ru0 = base + W::O_RU0, *tscr = base + W::O_SCR;
     double *Xa = base + W::O_X, *sgu = base + W::O_SGU, *sgx = base + W::O_SGX; // NY > 0 only
+    short *ctab = reinterpret_cast<short *>(base + W::O_TAB);
     const bool implicit_rhs = (a.p.ru == nullptr);
     const double sgn = implicit_rhs ? -1.0 : 1.0;
     int fail_piv = -1, fail_stage = 0;
@@ -227,6 +233,7 @@ __device__ __forceinline__ void riccati_warp_body(const RiccatiArgs &a, int chai
         const int r = W::NUX + lane;
         img[S::T(r / 8, r / 8) * kTileElems + (r % 8) * 9] = 1.0;
     }
+    CopyPlan<NU, NX>::build(ctab, lane, W::PLAN_BA);
     __syncwarp();
 
     // prologue: H_0, BA_0 and the x_init term of ru[0]
@@ -417,7 +424,7 @@ __device__ __forceinline__ void riccati_warp_body(const RiccatiArgs &a, int chai
         __syncwarp();
         // the H buffers are free: prefetch H_{s+1} (and BA_1 at s = 0)
         if (s + 1 < n) {
-            stage_H<NU, NX>(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), img, imr, Sb);
+            stage_H_plan<NU, NX>(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), img, imr, Sb, ctab);
             if constexpr (NY > 0)
                 stage_aug<NU, NX, NY>(g, a.p, b, g.stage_of(c, s + 1), g.x_index_of(c, s + 1), Xa, sgu, sgx);
             if (s == 0)
@@ -724,8 +731,12 @@ __device__ __forceinline__ void riccati_warp_body(const RiccatiArgs &a, int chai
                         st_frag(Wsm + (ti * W::NXC + kt) * kTileElems, lane, vacc[ti * W::NXC + kt]);
             }
             __syncwarp();
-            if (s + 2 < n)
-                stage_BA<NU, NX>(g, a.p, b, g.stage_of(c, s + 2), BA, fb);
+            if (s + 2 < n) {
+                if constexpr (W::PLAN_BA)
+                    stage_BA_plan<NU, NX>(g, a.p, b, g.stage_of(c, s + 2), BA, fb, ctab);
+                else
+                    stage_BA<NU, NX>(g, a.p, b, g.stage_of(c, s + 2), BA, fb);
+            }
             cp_commit();
         }
     }
