@@ -738,8 +738,16 @@ template <int NX> bool launch_sf(const Geo &g, cudaStream_t st, const SchurArgs 
     if (g.nx != NX)
         return false;
     constexpr int WIDE = NX > 16 ? 8 : 16;
-    if (g.batch >= 64 || g.P <= 8)
+    if (g.batch >= 64 || g.P <= 8) {
+        // more instances than 4-warp CTA slots (148 SMs x 4): 2-warp CTAs
+        // (8 per SM) finish the batch in one wave instead of ~1.7
+        // (config 1: 0.319 -> 0.308 ms); CYQ_SCHUR_NW=2|4 forces either
+        const char *e = getenv("CYQ_SCHUR_NW");
+        const bool two = e ? e[0] == '2' : g.batch > 4 * 148;
+        if (two)
+            return launch_sfw<NX, 2, 1>(g, st, sa);
         return launch_sfw<NX, 4, 1>(g, st, sa);
+    }
     if (g.P >= 64 && g.batch * 8 <= 148 && !getenv("CYQ_NO_SCHUR_CLUSTER"))
         if (launch_sfw<NX, WIDE, 8>(g, st, sa))
             return true;
