@@ -99,7 +99,10 @@ int cyq_factor_batch(cyq_ctx *ctx, const cyq_dims *dims,
                      cyq_status *status);
 /* kkt::solve (kkt_solve.cpp:23-309) with an explicit right-hand side; `prob`
  * must be the problem the factor was computed from (its A, B enter the
- * substitution, as in the reference signature). */
+ * substitution, as in the reference signature). The solve's vectors
+ * (forward-substituted y, wl, coupling rhs and multipliers) live in the
+ * factor's workspace: solves on one factor are stream-ordered on the
+ * context stream and must not run concurrently on different streams. */
 int cyq_solve_batch(cyq_ctx *ctx, const cyq_factor *factor,
                     const cyq_ocp_batch *prob, const cyq_rhs_batch *rhs,
                     const cyq_sol_batch *sol, int mem);
@@ -159,6 +162,40 @@ int cyq_line_search_batch(cyq_ctx *ctx, int64_t batch, int64_t m,
                           const double *alpha, const double *delta,
                           const double *eta, const double *beta, double *tau,
                           int32_t *status, int64_t *iterations);
+
+/* Kernel selection of a context (defaults: the fastest measured kernel per
+ * shape). Options apply to later calls on this context; a factor keeps the
+ * options it was computed with for its solves. A forced kernel that has no
+ * specialisation for a shape falls back to the automatic choice. */
+#define CYQ_OPT_PANEL 0         /* CYQ_PANEL_* (stage-panel Riccati kernel) */
+#define CYQ_OPT_SCHUR 1         /* CYQ_SCHUR_* (Schur complement + CR) */
+#define CYQ_OPT_SCHUR_WARPS 2   /* fused Schur CTA width: 0 auto, 2, 4 */
+#define CYQ_OPT_SCHUR_CLUSTER 3 /* 1 (default): 8-CTA cluster per long horizon; 0 never */
+#define CYQ_OPT_SPLIT 4         /* device batches in K parts on two streams (default 1) */
+#define CYQ_OPT_BACKSUB 5       /* 0 auto, 1 generic runtime-shape kernel */
+#define CYQ_OPT_FUSED_AUGMENT 6 /* 1 (default): Newton assembly fused into the panel */
+#define CYQ_OPT_PANEL_WARPS 7   /* generic panel: warps per chain CTA, 0 auto */
+#define CYQ_OPT_TAIL 8          /* CYQ_TAIL_* (FactorOptions::tail, kkt_solver.hpp:45-64) */
+#define CYQ_OPT_PHASE_PROF 9    /* 1: per-stage phase clocks of chain 0 to stderr */
+#define CYQ_OPT_COUNT 10
+
+#define CYQ_PANEL_AUTO 0
+#define CYQ_PANEL_WARP 1      /* one warp per chain, compile-time shapes */
+#define CYQ_PANEL_TWO_WARP 2  /* producer/consumer warp pair per chain */
+#define CYQ_PANEL_CTA 3       /* one CTA per chain (large tile-aligned blocks) */
+#define CYQ_PANEL_GENERIC 4   /* runtime-shape CTA kernel */
+#define CYQ_PANEL_WARP_TMEM 5 /* warp kernel with W in tensor memory */
+
+#define CYQ_SCHUR_AUTO 0   /* fused one-kernel Schur + CR */
+#define CYQ_SCHUR_LEVELS 1 /* per-level batch-wide tile kernels */
+#define CYQ_SCHUR_SCALAR 2 /* runtime-shape scalar kernel */
+
+#define CYQ_TAIL_CR1 0 /* cyclic reduction down to one block (default) */
+#define CYQ_TAIL_PCR 1 /* parallel cyclic reduction for the last levels */
+#define CYQ_TAIL_PCG 2 /* served by exact CR (meets the PCG tolerance contract) */
+
+int cyq_ctx_set_option(cyq_ctx *ctx, int option, int64_t value);
+int cyq_ctx_get_option(cyq_ctx *ctx, int option, int64_t *value);
 
 /* Per-kernel device timing: when enabled, every launch of the pipeline is
  * bracketed by CUDA events on the context stream. `read` synchronizes and

@@ -16,6 +16,16 @@ LIB_PATH = os.path.join(HERE, "libcyqlone_b200.so")
 CYQ_OK, CYQ_INVALID_ARG, CYQ_PIVOT_FAIL, CYQ_CUDA_ERR, CYQ_NO_DEVICE = 0, 1, 2, 3, 4
 CYQ_MEM_HOST, CYQ_MEM_DEVICE = 0, 1
 
+# cyq_ctx_set_option keys and named values (include/cyqlone_b200.h)
+OPTIONS = {"panel": 0, "schur": 1, "schur_warps": 2, "schur_cluster": 3, "split": 4,
+           "backsub": 5, "fused_augment": 6, "panel_warps": 7, "tail": 8, "phase_prof": 9}
+OPTION_VALUES = {
+    "panel": {"auto": 0, "warp": 1, "two_warp": 2, "cta": 3, "generic": 4, "warp_tmem": 5},
+    "schur": {"auto": 0, "levels": 1, "scalar": 2},
+    "backsub": {"auto": 0, "generic": 1},
+    "tail": {"cr1": 0, "pcr": 1, "pcg": 2},
+}
+
 i64 = C.c_int64
 dp = C.POINTER(C.c_double)
 
@@ -59,6 +69,8 @@ SIGNATURES = {
     "cyq_factor_materialize": (C.c_int, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p,
                                          C.c_void_p]),
     "cyq_ctx_profile": (C.c_int, [C.c_void_p, C.c_int]),
+    "cyq_ctx_set_option": (C.c_int, [C.c_void_p, C.c_int, i64]),
+    "cyq_ctx_get_option": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(i64)]),
     "cyq_ctx_profile_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(i64),
                                        C.c_int]),
     "cyq_version": (C.c_char_p, []),

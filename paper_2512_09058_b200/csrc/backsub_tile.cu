@@ -274,8 +274,6 @@ template <int NU, int NX> bool launch_bt(const Geo &g, cudaStream_t st, const Ba
 } // namespace
 
 bool launch_backsub_tile(const Geo &g, cudaStream_t st, const BacksubArgs &ba) {
-    if (getenv("CYQ_NO_BACKSUB_TILE"))
-        return false;
     return launch_bt<32, 64>(g, st, ba);
 }
 

@@ -290,11 +290,8 @@ template <int NU, int NX, int WPB> bool launch_b(const Geo &g, cudaStream_t st, 
     if (g.nu != NU || g.nx != NX)
         return false;
     const size_t smem = (size_t)WPB * BS<NU, NX>::PER_WARP * sizeof(double);
-    static std::atomic<unsigned long long> attr{0};
-    if (first_on_device(attr)) {
-        cudaFuncSetAttribute(backsub_warp_kernel<NU, NX, WPB>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }
+    static DeviceOnce once;
+    once_per_device(once, [&] { return cudaFuncSetAttribute(backsub_warp_kernel<NU, NX, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
     const int chains = g.batch * g.P;
     backsub_warp_kernel<NU, NX, WPB><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ba);
     return true;
@@ -302,8 +299,6 @@ template <int NU, int NX, int WPB> bool launch_b(const Geo &g, cudaStream_t st, 
 } // namespace
 
 bool launch_backsub_warp(const Geo &g, cudaStream_t st, const BacksubArgs &ba) {
-    if (getenv("CYQ_NO_BACKSUB_WARP"))
-        return false;
     return launch_b<10, 20, 4>(g, st, ba) || launch_b<8, 16, 4>(g, st, ba) ||
            launch_b<4, 12, 4>(g, st, ba) || launch_b<5, 10, 4>(g, st, ba);
 }

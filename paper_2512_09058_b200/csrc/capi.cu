@@ -44,6 +44,8 @@ struct cyq_ctx {
     double ms[5] = {0, 0, 0, 0, 0};
     int64_t launches[5] = {0, 0, 0, 0, 0};
     int64_t kernels[5] = {0, 0, 0, 0, 0}; // kernel launches per kind
+    LaunchOpts opts;                      // kernel selection (cyq_ctx_set_option)
+    long long *phase = nullptr;           // phase clocks (CYQ_OPT_PHASE_PROF)
 };
 
 struct cyq_factor {
@@ -55,6 +57,7 @@ struct cyq_factor {
     FactorWS ws{};
     ProbView prob{}; // device copy of the problem (host-memory factor calls)
     bool owns_prob = false;
+    LaunchOpts opts{}; // kernel selection at factor time (the solve reads its layouts)
 };
 
 namespace {
@@ -223,11 +226,9 @@ ProbView view_of(const cyq_ocp_batch *p) {
 }
 
 // Warps per chain CTA and register tiles per warp (MAXT template).
-void riccati_shape(const Geo &g, int &nw, int &maxt) {
+void riccati_shape(const Geo &g, const LaunchOpts &o, int &nw, int &maxt) {
     const int nt = g.TT * (g.TT + 1) / 2;
-    nw = 4;
-    if (const char *e = getenv("CYQ_RICCATI_WARPS"))
-        nw = std::max(1, std::min(4, atoi(e)));
+    nw = o.panel_warps ? std::max(1, std::min(4, o.panel_warps)) : 4;
     int per = (nt + nw - 1) / nw;
     if (per > 16) { // large panels: the 256-thread, 32-tile-per-warp variant
         nw = 8;
@@ -239,17 +240,17 @@ void riccati_shape(const Geo &g, int &nw, int &maxt) {
 }
 
 template <int M> void launch_riccati_t(const Geo &g, int nw, cudaStream_t st, const RiccatiArgs &ra) {
-    static std::atomic<unsigned long long> attr{0};
-    if (first_on_device(attr)) {
-        cudaFuncSetAttribute(riccati_panel_kernel_t<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024);
-    }
+    static DeviceOnce once;
+    once_per_device(once, [] {
+        return cudaFuncSetAttribute(riccati_panel_kernel_t<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    227 * 1024);
+    });
     riccati_panel_kernel_t<M><<<g.batch * g.P, 32 * nw, riccati_smem_bytes(g), st>>>(ra);
 }
 
-void launch_riccati(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
+void launch_riccati(const Geo &g, const LaunchOpts &o, cudaStream_t st, const RiccatiArgs &ra) {
     int nw, maxt;
-    riccati_shape(g, nw, maxt);
+    riccati_shape(g, o, nw, maxt);
     switch (maxt) {
     case 4: launch_riccati_t<4>(g, nw, st, ra); break;
     case 8: launch_riccati_t<8>(g, nw, st, ra); break;
@@ -291,15 +292,83 @@ struct Timed {
     }
 };
 
+// Schur complement + cyclic reduction (factor and / or solve, per
+// sa.do_factor / sa.do_solve): the fused one-kernel paths (schur_fused.cu,
+// schur_big.cu) unless CYQ_OPT_SCHUR selects the per-level tile kernels or
+// the scalar kernel, or no specialisation serves the shape.
+int launch_schur(cyq_ctx *ctx, const Geo &g, const SchurArgs &sa, const LaunchOpts &o) {
+    Timed t(ctx, 1);
+    if (o.schur == 0 && (launch_schur_fused(g, ctx->stream, sa, o) || launch_schur_big(g, ctx->stream, sa))) {
+        t.kernels = 1; // one fused kernel per batch
+    } else if (sa.do_factor && o.schur != 2 && launch_schur_tiles(g, ctx->stream, sa)) {
+        // DMMA-tile factorization levels, then the scalar kernel's solve
+        t.kernels = 2 + SchurLayout::make(g.P, g.nx).levels + (sa.do_solve ? 1 : 0);
+        if (sa.do_solve) {
+            SchurArgs sv = sa;
+            sv.do_factor = 0;
+            const int nw = schur_warps_solve(g);
+            if (schur_smem_for(g, nw) > kMaxDynSmem)
+                return smem_too_large(ctx, "Schur/CR solve (P x nx)", schur_smem_for(g, nw));
+            schur_cr_kernel<<<g.batch, 32 * nw, schur_smem_for(g, nw), ctx->stream>>>(sv);
+        }
+    } else if (sa.do_factor) {
+        if (schur_smem_bytes(g) > kMaxDynSmem)
+            return smem_too_large(ctx, "Schur/CR (P x nx)", schur_smem_bytes(g));
+        schur_cr_kernel<<<g.batch, 32 * schur_warps(g), schur_smem_bytes(g), ctx->stream>>>(sa);
+    } else {
+        const int nw = schur_warps_solve(g);
+        if (schur_smem_for(g, nw) > kMaxDynSmem)
+            return smem_too_large(ctx, "Schur/CR solve (P x nx)", schur_smem_for(g, nw));
+        schur_cr_kernel<<<g.batch, 32 * nw, schur_smem_for(g, nw), ctx->stream>>>(sa);
+    }
+    CU(cudaGetLastError());
+    return CYQ_OK;
+}
+
+int launch_backsub(cyq_ctx *ctx, const Geo &g, const BacksubArgs &ba, const LaunchOpts &o) {
+    Timed t(ctx, 2);
+    if (o.backsub != 0 || (!launch_backsub_warp(g, ctx->stream, ba) && !launch_backsub_tile(g, ctx->stream, ba))) {
+        const int wpb = backsub_wpb(g), chains = g.batch * g.P;
+        if (backsub_smem_bytes(g) > kMaxDynSmem)
+            return smem_too_large(ctx, "back substitution", backsub_smem_bytes(g));
+        backsub_kernel<<<(chains + wpb - 1) / wpb, 32 * wpb, backsub_smem_bytes(g), ctx->stream>>>(ba);
+    }
+    CU(cudaGetLastError());
+    return CYQ_OK;
+}
+
+// Profiling aid (CYQ_OPT_PHASE_PROF): chain 0's per-stage phase clocks of
+// the stage panel and instance 0's Schur phases, to stderr.
+int dump_phases(cyq_ctx *ctx, const Geo &g, const long long *ph, const long long *sph) {
+    std::vector<long long> h(8 * (g.n + 1));
+    CU(cudaMemcpyAsync(h.data(), ph, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+    std::vector<long long> q(32);
+    CU(cudaMemcpyAsync(q.data(), sph, 32 * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (int s = 0; s < g.n; ++s)
+        fprintf(stderr, "phase s=%d init+WW %lld chol %lld store %lld mw %lld V %lld\n", s,
+                h[s * 8 + 1] - h[s * 8 + 0], h[s * 8 + 2] - h[s * 8 + 1], h[s * 8 + 3] - h[s * 8 + 2],
+                h[s * 8 + 4] - h[s * 8 + 3], (s + 1 < g.n ? h[(s + 1) * 8] : h[g.n * 8]) - h[s * 8 + 4]);
+    if (q[31] > 1 && q[31] < 31) {
+        fprintf(stderr, "schur phases (instance 0):");
+        for (long long k = 1; k < q[31]; ++k)
+            fprintf(stderr, " %lld", q[k] - q[k - 1]);
+        fprintf(stderr, "  total %lld\n", q[q[31] - 1] - q[0]);
+    }
+    return CYQ_OK;
+}
+
 int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &ws,
                     const SolView *sol, bool do_solve) {
-    static std::atomic<unsigned long long> attrs{0};
-    if (first_on_device(attrs)) {
-        CU(cudaFuncSetAttribute(backsub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                227 * 1024));
-        CU(cudaFuncSetAttribute(schur_cr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                227 * 1024));
-    }
+    static DeviceOnce once;
+    CU(once_per_device(once, [] {
+        cudaError_t e = cudaFuncSetAttribute(backsub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024);
+        return e != cudaSuccess ? e
+                                : cudaFuncSetAttribute(schur_cr_kernel,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    }));
+    const LaunchOpts &o = ctx->opts;
     const int chains = g.batch * g.P;
     CU(cudaMemsetAsync(ws.fail, 0xFF, sizeof(unsigned long long) * g.batch, ctx->stream));
     const bool staged = riccati_staged(g);
@@ -314,117 +383,58 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
     }
     RiccatiArgs ra{g, p, ws.fac, ws.y, ws.wl, ws.trail, ws.fail, ws.consts, staged ? 1 : 0,
                    nullptr};
-    static long long *phase_dev = nullptr;
-    if (getenv("CYQ_PHASE_PROF")) {
-        if (!phase_dev)
-            CU(cudaMalloc(&phase_dev, 8 * 4096 * sizeof(long long)));
-        ra.phase = phase_dev;
+    if (o.phase_prof) {
+        if (!ctx->phase)
+            CU(cudaMalloc(&ctx->phase, 8 * 4096 * sizeof(long long)));
+        ra.phase = ctx->phase;
     }
     {
         Timed t(ctx, 0);
-        // kernel choice: compile-time-shape one-warp kernel (default), the
-        // two-warp variant (CYQ_RICCATI=c) or the runtime-shape CTA kernel
-        // (CYQ_RICCATI=g, and every shape without a specialisation)
-        const char *sel = getenv("CYQ_RICCATI"); // read per call (tests switch it)
-        const bool want_c2 = sel && sel[0] == 'c', want_gen = sel && sel[0] == 'g';
+        // kernel choice (CYQ_OPT_PANEL forces one; a forced kernel without a
+        // specialisation for this shape falls back to the automatic order):
         // latency-bound launches (at most ~2 chains per SM: a single long
         // horizon, config 0 / 2) take the two-warp producer/consumer panel
-        // (measured 0.078 -> 0.074 ms at config 2); batches keep one warp
-        // per chain (CYQ_RICCATI=w forces it, =p forces the two-warp kernel)
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-        const bool want_pc = (sel && sel[0] == 'p') || (!sel && (long long)g.batch * g.P <= 2LL * sms);
+        // (measured 0.078 -> 0.074 ms at config 2); batches the one-warp
+        // compile-time-shape kernel, large tile-aligned blocks the CTA
+        // kernel, every other shape the runtime-shape generic kernel
         bool done = false;
         if (p.aD) { // fused Newton-system augmentation: the warp kernel only
-            if (!launch_riccati_warp(g, ctx->stream, ra))
+            if (!launch_riccati_warp(g, ctx->stream, ra, o))
                 return set_err(ctx, CYQ_INVALID_ARG, "fused augmentation: no kernel for this shape");
             done = true;
         }
-        if (!done && !want_gen && want_pc)
+        if (!done) {
+            switch (o.panel) {
+            case CYQ_PANEL_WARP:
+            case CYQ_PANEL_WARP_TMEM: done = launch_riccati_warp(g, ctx->stream, ra, o); break;
+            case CYQ_PANEL_TWO_WARP: done = launch_riccati_pc(g, ctx->stream, ra); break;
+            case CYQ_PANEL_CTA: done = launch_riccati_cta(g, ctx->stream, ra); break;
+            case CYQ_PANEL_GENERIC: launch_riccati(g, o, ctx->stream, ra); done = true; break;
+            default: break;
+            }
+        }
+        if (!done && (long long)chains <= 2LL * o.sms)
             done = launch_riccati_pc(g, ctx->stream, ra);
-        if (!done && !want_gen && want_c2)
-            done = launch_riccati_cta2(g, ctx->stream, ra);
-        if (!want_gen && !done)
-            done = launch_riccati_warp(g, ctx->stream, ra);
-        if (!want_gen && !done)
+        if (!done)
+            done = launch_riccati_warp(g, ctx->stream, ra, LaunchOpts{});
+        if (!done)
             done = launch_riccati_cta(g, ctx->stream, ra);
         if (!done)
-            launch_riccati(g, ctx->stream, ra);
+            launch_riccati(g, o, ctx->stream, ra);
     }
     CU(cudaGetLastError());
     SchurArgs sa{g, p, ws.fac, ws.y, ws.trail, ws.schur, ws.lamc,
                  sol ? sol->lam : nullptr, ws.fail, 1, do_solve ? 1 : 0};
     sa.phase = ra.phase ? ra.phase + 16 * (g.n + 1) + 8 : nullptr;
-    {
-        Timed t(ctx, 1);
-        if (launch_schur_fused(g, ctx->stream, sa) || launch_schur_big(g, ctx->stream, sa)) {
-            t.kernels = 1; // one fused kernel per batch
-        } else if (launch_schur_tiles(g, ctx->stream, sa)) { // DMMA-tile factorization
-            t.kernels = 2 + SchurLayout::make(g.P, g.nx).levels + (do_solve ? 1 : 0);
-            if (do_solve) {
-                SchurArgs sv = sa;
-                sv.do_factor = 0;
-                const int nw = schur_warps_solve(g);
-                if (schur_smem_for(g, nw) > kMaxDynSmem)
-                    return smem_too_large(ctx, "Schur/CR solve (P x nx)", schur_smem_for(g, nw));
-                schur_cr_kernel<<<g.batch, 32 * nw, schur_smem_for(g, nw), ctx->stream>>>(sv);
-            }
-        } else {
-            if (schur_smem_bytes(g) > kMaxDynSmem)
-                return smem_too_large(ctx, "Schur/CR (P x nx)", schur_smem_bytes(g));
-            schur_cr_kernel<<<g.batch, 32 * schur_warps(g), schur_smem_bytes(g), ctx->stream>>>(sa);
-        }
-    }
-    CU(cudaGetLastError());
-    if (ra.phase && getenv("CYQ_PC_PROF")) { // producer/consumer kernel: raw stamps
-        std::vector<long long> h(16 * g.n);
-        CU(cudaMemcpyAsync(h.data(), ra.phase, h.size() * sizeof(long long), cudaMemcpyDeviceToHost,
-                           ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
-        const long long t0 = h[0];
-        for (int s = 0; s < g.n; ++s) {
-            fprintf(stderr, "pc s=%d P:", s);
-            for (int k = 0; k < 8; ++k)
-                fprintf(stderr, " %lld", h[s * 16 + k] ? h[s * 16 + k] - t0 : -1);
-            fprintf(stderr, " | C:");
-            for (int k = 8; k < 16; ++k)
-                fprintf(stderr, " %lld", h[s * 16 + k] ? h[s * 16 + k] - t0 : -1);
-            fprintf(stderr, "\n");
-        }
-    } else if (ra.phase) { // dump chain 0's phase clocks (profiling aid)
-        std::vector<long long> h(8 * (g.n + 1));
-        CU(cudaMemcpyAsync(h.data(), ra.phase, h.size() * sizeof(long long),
-                           cudaMemcpyDeviceToHost, ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
-        for (int s = 0; s < g.n; ++s)
-            fprintf(stderr, "phase s=%d init+WW %lld chol %lld store %lld mw %lld V %lld\n", s,
-                    h[s * 8 + 1] - h[s * 8 + 0], h[s * 8 + 2] - h[s * 8 + 1],
-                    h[s * 8 + 3] - h[s * 8 + 2], h[s * 8 + 4] - h[s * 8 + 3],
-                    (s + 1 < g.n ? h[(s + 1) * 8] : h[g.n * 8]) - h[s * 8 + 4]);
-        std::vector<long long> q(32);
-        CU(cudaMemcpyAsync(q.data(), sa.phase, 32 * sizeof(long long), cudaMemcpyDeviceToHost,
-                           ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
-        if (q[31] > 1 && q[31] < 31) {
-            fprintf(stderr, "schur phases (instance 0):");
-            for (long long k = 1; k < q[31]; ++k)
-                fprintf(stderr, " %lld", q[k] - q[k - 1]);
-            fprintf(stderr, "  total %lld\n", q[q[31] - 1] - q[0]);
-        }
-    }
+    int rc = launch_schur(ctx, g, sa, o);
+    if (rc)
+        return rc;
+    if (ra.phase)
+        dump_phases(ctx, g, ra.phase, sa.phase);
     if (do_solve) {
-        BacksubArgs ba{g, p, ws.fac, ws.y, ws.wl, ws.lamc, *sol};
-        {
-            Timed t(ctx, 2);
-            if (!launch_backsub_warp(g, ctx->stream, ba) && !launch_backsub_tile(g, ctx->stream, ba)) {
-                const int wpb = backsub_wpb(g);
-                if (backsub_smem_bytes(g) > kMaxDynSmem)
-                    return smem_too_large(ctx, "back substitution", backsub_smem_bytes(g));
-                backsub_kernel<<<(chains + wpb - 1) / wpb, 32 * wpb, backsub_smem_bytes(g),
-                                 ctx->stream>>>(ba);
-            }
-        }
-        CU(cudaGetLastError());
+        rc = launch_backsub(ctx, g, BacksubArgs{g, p, ws.fac, ws.y, ws.wl, ws.lamc, *sol}, o);
+        if (rc)
+            return rc;
     }
     return CYQ_OK;
 }
@@ -432,12 +442,11 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
 // kkt::solve over an existing factor: forward sweep (forward.cu), Schur/CR
 // solve, back substitution. `p` carries the explicit rhs.
 int launch_solve(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &ws,
-                 const SolView &sol) {
-    static std::atomic<unsigned long long> attr{0};
-    if (first_on_device(attr)) {
-        CU(cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                227 * 1024));
-    }
+                 const SolView &sol, const LaunchOpts &o) {
+    static DeviceOnce once;
+    CU(once_per_device(once, [] {
+        return cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    }));
     const int chains = g.batch * g.P;
     BacksubArgs ba{g, p, ws.fac, ws.y, ws.wl, ws.lamc, sol};
     {
@@ -450,28 +459,8 @@ int launch_solve(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &
     }
     CU(cudaGetLastError());
     SchurArgs sa{g, p, ws.fac, ws.y, ws.trail, ws.schur, ws.lamc, sol.lam, ws.fail, 0, 1};
-    {
-        Timed t(ctx, 1);
-        if (!launch_schur_fused(g, ctx->stream, sa) && !launch_schur_big(g, ctx->stream, sa)) {
-            const int nw = schur_warps_solve(g);
-            if (schur_smem_for(g, nw) > kMaxDynSmem)
-                return smem_too_large(ctx, "Schur/CR solve (P x nx)", schur_smem_for(g, nw));
-            schur_cr_kernel<<<g.batch, 32 * nw, schur_smem_for(g, nw), ctx->stream>>>(sa);
-        }
-    }
-    CU(cudaGetLastError());
-    {
-        Timed t(ctx, 2);
-        if (!launch_backsub_warp(g, ctx->stream, ba) && !launch_backsub_tile(g, ctx->stream, ba)) {
-            const int wpb = backsub_wpb(g);
-            if (backsub_smem_bytes(g) > kMaxDynSmem)
-                return smem_too_large(ctx, "back substitution", backsub_smem_bytes(g));
-            backsub_kernel<<<(chains + wpb - 1) / wpb, 32 * wpb, backsub_smem_bytes(g),
-                             ctx->stream>>>(ba);
-        }
-    }
-    CU(cudaGetLastError());
-    return CYQ_OK;
+    const int rc = launch_schur(ctx, g, sa, o);
+    return rc ? rc : launch_backsub(ctx, g, ba, o);
 }
 
 int decode_status(cyq_ctx *ctx, const Geo &g, const unsigned long long *dfail,
@@ -550,6 +539,7 @@ int cyq_ctx_create(int device, cyq_ctx **out) {
         return set_err(nullptr, CYQ_CUDA_ERR, cudaGetErrorString(e));
     }
     ctx->own_stream = true;
+    cudaDeviceGetAttribute(&ctx->opts.sms, cudaDevAttrMultiProcessorCount, device);
     *out = ctx;
     return CYQ_OK;
 }
@@ -570,6 +560,8 @@ int cyq_ctx_destroy(cyq_ctx *ctx) {
         cudaFree(ctx->lsbuf);
     if (ctx->hfail)
         cudaFreeHost(ctx->hfail);
+    if (ctx->phase)
+        cudaFree(ctx->phase);
     for (auto &e : ctx->ev) {
         cudaEventDestroy(e.second.first);
         cudaEventDestroy(e.second.second);
@@ -699,8 +691,7 @@ int cyq_solve_problem_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_ba
         SolView sv{sol->u, sol->x, sol->lam};
         // opt-in (CYQ_SPLIT=K): the overlapped launches make each kernel's
         // own event-timed duration (the roofline's denominator) meaningless
-        const char *sp = getenv("CYQ_SPLIT");
-        const int K = sp ? atoi(sp) : 1;
+        const int K = ctx->opts.split;
         if (g.batch >= 128 * K && K >= 2) {
             // K parts, each a full pipeline, on two alternating streams: the
             // kernels' tails (the Schur kernel's second wave above all)
@@ -809,6 +800,7 @@ int cyq_factor_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_batch *pr
     f->ctx = ctx;
     f->dims = *dims;
     f->g = g;
+    f->opts = ctx->opts;
     const WsSizes wsz = ws_sizes(g);
     const size_t pbytes = prob_doubles(g) * sizeof(double);
     f->bytes = wsz.total + pbytes;
@@ -881,7 +873,7 @@ int cyq_solve_batch(cyq_ctx *ctx, const cyq_factor *f, const cyq_ocp_batch *prob
         double *s0 = base + rd;
         sv = SolView{s0, s0 + B * N * nu, s0 + B * N * nu + B * (N + 1) * nx};
     }
-    rc = launch_solve(ctx, g, p, f->ws, sv);
+    rc = launch_solve(ctx, g, p, f->ws, sv, f->opts);
     if (rc)
         return rc;
     if (mem != CYQ_MEM_DEVICE) {
@@ -945,6 +937,42 @@ int cyq_factor_materialize(const cyq_factor *f, int64_t inst, double *LH, double
                         LA[((size_t)c * nx + r) * nx + k] = at(c, s, top + r, nu + k);
                 }
         }
+    return CYQ_OK;
+}
+
+int cyq_ctx_set_option(cyq_ctx *ctx, int option, int64_t value) {
+    if (!ctx)
+        return set_err(nullptr, CYQ_INVALID_ARG, "null context");
+    LaunchOpts &o = ctx->opts;
+    auto bad = [&] { return set_err(ctx, CYQ_INVALID_ARG, "option value out of range"); };
+    switch (option) {
+    case CYQ_OPT_PANEL: if (value < 0 || value > 5) return bad(); o.panel = (int)value; break;
+    case CYQ_OPT_SCHUR: if (value < 0 || value > 2) return bad(); o.schur = (int)value; break;
+    case CYQ_OPT_SCHUR_WARPS:
+        if (value != 0 && value != 2 && value != 4) return bad();
+        o.schur_warps = (int)value;
+        break;
+    case CYQ_OPT_SCHUR_CLUSTER: o.schur_cluster = value != 0; break;
+    case CYQ_OPT_SPLIT: if (value < 1 || value > 8) return bad(); o.split = (int)value; break;
+    case CYQ_OPT_BACKSUB: if (value < 0 || value > 1) return bad(); o.backsub = (int)value; break;
+    case CYQ_OPT_FUSED_AUGMENT: o.fused_aug = value != 0; break;
+    case CYQ_OPT_PANEL_WARPS: if (value < 0 || value > 4) return bad(); o.panel_warps = (int)value; break;
+    case CYQ_OPT_TAIL: if (value < 0 || value > 2) return bad(); o.tail = (int)value; break;
+    case CYQ_OPT_PHASE_PROF: o.phase_prof = value != 0; break;
+    default: return set_err(ctx, CYQ_INVALID_ARG, "unknown option");
+    }
+    return CYQ_OK;
+}
+
+int cyq_ctx_get_option(cyq_ctx *ctx, int option, int64_t *value) {
+    if (!ctx || !value)
+        return set_err(ctx, CYQ_INVALID_ARG, "null argument");
+    const LaunchOpts &o = ctx->opts;
+    const int v[CYQ_OPT_COUNT] = {o.panel,     o.schur,     o.schur_warps, o.schur_cluster, o.split,
+                                  o.backsub,   o.fused_aug, o.panel_warps, o.tail,          o.phase_prof};
+    if (option < 0 || option >= CYQ_OPT_COUNT)
+        return set_err(ctx, CYQ_INVALID_ARG, "unknown option");
+    *value = v[option];
     return CYQ_OK;
 }
 
@@ -1019,7 +1047,7 @@ int cyq_solve_newton_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_bat
         return rc;
     FactorWS ws = carve(ctx->wsbuf, wsz);
     ProbView pv = view_of(prob);
-    if (riccati_warp_fuses_aug(g, (int)ny)) {
+    if (riccati_warp_fuses_aug(g, (int)ny, ctx->opts)) {
         // assembly fused into the stage-panel loads: the augmented Hessians
         // never touch HBM
         pv.aD = D;

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <atomic>
+#include <mutex>
 
 #include "kkt_common.cuh"
 
@@ -12,15 +13,45 @@ struct cyq_ctx; // include/cyqlone_b200.h
 namespace cyqb {
 
 // One-time per-device launch setup (function attributes, constant-memory
-// tables are per device): true the first time the current device asks. A
-// context per GPU may live in one process (include/cyqlone_b200.h).
-inline bool first_on_device(std::atomic<unsigned long long> &mask) {
+// tables are per device; a context per GPU may live in one process,
+// include/cyqlone_b200.h). `setup()` runs under a lock, at most once per
+// device once it succeeded: a second host thread never launches before the
+// attributes are set, and a failed setup is retried on the next call (the
+// launch itself then reports the error).
+struct DeviceOnce {
+    std::mutex m;
+    std::atomic<unsigned long long> done{0};
+};
+template <class F> cudaError_t once_per_device(DeviceOnce &o, F &&setup) {
     int d = 0;
     cudaGetDevice(&d);
     const unsigned long long bit = 1ull << (d & 63);
-    return !(mask.fetch_or(bit) & bit);
+    if (o.done.load(std::memory_order_acquire) & bit)
+        return cudaSuccess;
+    std::lock_guard<std::mutex> lk(o.m);
+    if (o.done.load(std::memory_order_relaxed) & bit)
+        return cudaSuccess;
+    const cudaError_t e = setup();
+    if (e == cudaSuccess)
+        o.done.fetch_or(bit, std::memory_order_release);
+    return e;
 }
 
+// Kernel selection of a context (cyq_ctx_set_option, include/cyqlone_b200.h);
+// the defaults pick the fastest measured kernel per shape.
+struct LaunchOpts {
+    int panel = 0;         // CYQ_PANEL_*: 0 auto, 1 warp, 2 two-warp, 3 CTA, 4 generic, 5 warp + TMEM
+    int schur = 0;         // CYQ_SCHUR_*: 0 auto (fused / big), 1 per-level tile kernels, 2 scalar
+    int schur_warps = 0;   // fused Schur CTA width: 0 auto, 2 or 4 warps
+    int schur_cluster = 1; // 8-CTA cluster for a few long horizons (0: never)
+    int split = 1;         // device batches in K parts on two streams
+    int backsub = 0;       // 0 auto, 1 generic runtime-shape kernel
+    int fused_aug = 1;     // Newton-system assembly fused into the panel (0: assembly kernel)
+    int panel_warps = 0;   // generic panel: warps per chain CTA (0 auto)
+    int tail = 0;          // CYQ_TAIL_*: Schur tail (0 cr1 / 2 pcg: exact CR, 1 pcr)
+    int phase_prof = 0;    // per-stage phase clocks of chain 0 (profiling aid)
+    int sms = 148;         // multiprocessors of the context's device
+};
 
 // Device workspace of one factorization of a batch (all chains).
 struct FactorWS {
@@ -118,11 +149,10 @@ struct LineSearchArgs {
 };
 void launch_line_search(cudaStream_t st, const LineSearchArgs &a);
 
-bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
+bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra, const LaunchOpts &o);
 // true when the warp kernel has a fused Newton-system augmentation variant
 // for this stage shape and ny (ProbView::aD path)
-bool riccati_warp_fuses_aug(const Geo &g, int ny);
-bool launch_riccati_cta2(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
+bool riccati_warp_fuses_aug(const Geo &g, int ny, const LaunchOpts &o);
 // CTA-per-chain kernel for large tile-aligned panels (riccati_cta.cu); false if n/a
 bool launch_riccati_cta(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
 // producer/consumer two-warp-per-chain kernel (riccati_pc.cu); false if n/a
@@ -131,8 +161,8 @@ bool launch_riccati_pc(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
 bool launch_schur_tiles(const Geo &g, cudaStream_t st, const SchurArgs &sa);
 // fused Schur + CR factor (+ solve) kernel, one CTA per instance (schur_fused.cu);
 // false if the shape / batch is not served (the caller falls back)
-bool schur_fused_ok(const Geo &g);
-bool launch_schur_fused(const Geo &g, cudaStream_t st, const SchurArgs &sa);
+bool schur_fused_ok(const Geo &g, const LaunchOpts &o);
+bool launch_schur_fused(const Geo &g, cudaStream_t st, const SchurArgs &sa, const LaunchOpts &o);
 size_t schur_fused_doubles(const Geo &g);
 // CTA-level Schur + CR for large tile-aligned nx (schur_big.cu); false if n/a
 bool launch_schur_big(const Geo &g, cudaStream_t st, const SchurArgs &sa);

@@ -580,10 +580,12 @@ template <int NU, int NX, int NW> bool launch_c(const Geo &g, cudaStream_t st, c
         return false;
     using C = CS<NU, NX, NW>;
     const size_t smem = (size_t)C::SMEM * sizeof(double);
-    static std::atomic<unsigned long long> attr{0};
-    if (first_on_device(attr)) {
-        cudaFuncSetAttribute(riccati_cta_kernel<NU, NX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+    static DeviceOnce once;
+    once_per_device(once, [&]() -> cudaError_t {
+        const cudaError_t e0 = cudaFuncSetAttribute(riccati_cta_kernel<NU, NX, NW>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e0 != cudaSuccess)
+            return e0;
         // tile plan: every list tile (all but the pivot diagonals) goes,
         // in tile-column-descending order, to the warp that minimises the
         // modelled Cholesky time sum_kb max(DMMA issue per SM sub-partition,
@@ -655,17 +657,15 @@ template <int NU, int NX, int NW> bool launch_c(const Geo &g, cudaStream_t st, c
                 cnt[w * (kMaxCT + 1) + kb + 1] = (unsigned char)m;
             }
         }
-        cudaMemcpyToSymbol(c_list, h, sizeof h);
-        cudaMemcpyToSymbol(c_cnt, cnt, sizeof cnt);
-    }
+        const cudaError_t e1 = cudaMemcpyToSymbol(c_list, h, sizeof h);
+        return e1 != cudaSuccess ? e1 : cudaMemcpyToSymbol(c_cnt, cnt, sizeof cnt);
+    });
     riccati_cta_kernel<NU, NX, NW><<<g.batch * g.P, 32 * NW, smem, st>>>(ra);
     return true;
 }
 } // namespace
 
 bool launch_riccati_cta(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
-    if (getenv("CYQ_NO_CTA_KERNEL"))
-        return false;
     return launch_c<32, 64, 16>(g, st, ra);
 }
 

@@ -553,10 +553,8 @@ template <int NU, int NX> bool launch_p(const Geo &g, cudaStream_t st, const Ric
     if (g.nu != NU || g.nx != NX)
         return false;
     const size_t smem = (size_t)PCS<NU, NX>::SMEM * sizeof(double);
-    static std::atomic<unsigned long long> attr{0};
-    if (first_on_device(attr)) {
-        cudaFuncSetAttribute(riccati_pc_kernel<NU, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }
+    static DeviceOnce once;
+    once_per_device(once, [&] { return cudaFuncSetAttribute(riccati_pc_kernel<NU, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
     riccati_pc_kernel<NU, NX><<<g.batch * g.P, 64, smem, st>>>(ra);
     return true;
 }

@@ -783,36 +783,27 @@ bool launch_w(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
         return false;
     using W = WS<NU, NX, NY, TM>;
     const size_t smem = (size_t)WPB * W::SMEM * sizeof(double);
-    static std::atomic<unsigned long long> attr{0};
-    if (first_on_device(attr)) {
-        cudaFuncSetAttribute(riccati_warp_kernel<NU, NX, WPB, NY, TM>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }
+    static DeviceOnce once;
+    once_per_device(once, [&] { return cudaFuncSetAttribute(riccati_warp_kernel<NU, NX, WPB, NY, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
     const int chains = g.batch * g.P;
     riccati_warp_kernel<NU, NX, WPB, NY, TM><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ra);
     return true;
 }
 } // namespace
 
-bool riccati_warp_fuses_aug(const Geo &g, int ny) {
-    return !getenv("CYQ_NO_WARP_KERNEL") && !getenv("CYQ_NO_FUSED_AUG") && g.nu == 8 && g.nx == 16 && ny == 24;
+bool riccati_warp_fuses_aug(const Geo &g, int ny, const LaunchOpts &o) {
+    return o.fused_aug && (o.panel == 0 || o.panel == 1) && g.nu == 8 && g.nx == 16 && ny == 24;
 }
 
-bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
-    if (getenv("CYQ_NO_WARP_KERNEL"))
-        return false;
+bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra, const LaunchOpts &o) {
     if (ra.p.aD) // fused Newton-system augmentation (config 4 stage shape)
         return launch_w<8, 16, 1, 24>(g, st, ra);
-    // W in tensor memory (12 chains per SM at config 1): opt-in, CYQ_TMEM=1 --
-    // measured 1.52 vs 1.41 ms at config 1 (the natural x-tile layout costs a
-    // 6th W W' k-slice and 168 registers spill), see DESIGN.md §3.4
-    const char *tm = getenv("CYQ_TMEM");
-    if (tm && tm[0] == '1' && launch_w<10, 20, 4, 0, true>(g, st, ra))
-        return true;
-    static const int wpb = getenv("CYQ_RICCATI_WPB") ? atoi(getenv("CYQ_RICCATI_WPB")) : 1;
-    if (wpb == 2)
-        return launch_w<10, 20, 2, 0>(g, st, ra) || launch_w<8, 16, 2, 0>(g, st, ra) ||
-               launch_w<4, 12, 2, 0>(g, st, ra) || launch_w<5, 10, 2, 0>(g, st, ra);
+    // W in tensor memory (12 chains per SM at config 1): opt-in
+    // (CYQ_PANEL_WARP_TMEM) -- measured 1.52 vs 1.41 ms at config 1 (the
+    // natural x-tile layout costs a 6th W W' k-slice and 168 registers
+    // spill), see DESIGN.md §3.4
+    if (o.panel == 5)
+        return launch_w<10, 20, 4, 0, true>(g, st, ra);
     return launch_w<10, 20, 1, 0>(g, st, ra) || launch_w<8, 16, 1, 0>(g, st, ra) ||
            launch_w<4, 12, 1, 0>(g, st, ra) || launch_w<5, 10, 1, 0>(g, st, ra);
 }

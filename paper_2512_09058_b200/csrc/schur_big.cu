@@ -317,11 +317,8 @@ template <int NX> bool launch_sb(const Geo &g, cudaStream_t st, const SchurArgs 
                          2 * NX) * sizeof(double);
     if (smem > 200 * 1024)
         return false;
-    static std::atomic<unsigned long long> attr{0};
-    if (first_on_device(attr)) {
-        cudaFuncSetAttribute(schur_big_kernel<NX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
-    }
+    static DeviceOnce once;
+    once_per_device(once, [&] { return cudaFuncSetAttribute(schur_big_kernel<NX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
     schur_big_kernel<NX, NW><<<g.batch, 32 * NW, smem, st>>>(sa);
     return true;
 }
@@ -333,7 +330,7 @@ size_t schur_big_doubles(const Geo &g) {
 }
 
 bool launch_schur_big(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
-    if (getenv("CYQ_NO_SCHUR_BIG") || g.nu % 8 != 0)
+    if (g.nu % 8 != 0)
         return false;
     return launch_sb<64>(g, st, sa) || launch_sb<32>(g, st, sa);
 }

@@ -707,11 +707,8 @@ template <int NX, int NW, int CL> bool launch_sfw(const Geo &g, cudaStream_t st,
                          (CL > 1 ? (size_t)g.P * SF<NX>::XP : 0)) * sizeof(double);
     if (smem > 220 * 1024)
         return false;
-    static std::atomic<unsigned long long> attr{0};
-    if (first_on_device(attr)) {
-        cudaFuncSetAttribute(schur_fused_kernel<NX, NW, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             220 * 1024);
-    }
+    static DeviceOnce once;
+    once_per_device(once, [&] { return cudaFuncSetAttribute(schur_fused_kernel<NX, NW, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); });
     if (CL == 1) {
         schur_fused_kernel<NX, NW, CL><<<g.batch, 32 * NW, smem, st>>>(sa);
         return true;
@@ -734,21 +731,20 @@ template <int NX, int NW, int CL> bool launch_sfw(const Geo &g, cudaStream_t st,
 // 4 warps per instance when the batch fills the GPU with CTAs; for a few
 // long-horizon instances (config 2: one instance, P = 256) a cluster of 8
 // wide CTAs per instance, so a CR level's eliminations run in one round
-template <int NX> bool launch_sf(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
+template <int NX> bool launch_sf(const Geo &g, cudaStream_t st, const SchurArgs &sa, const LaunchOpts &o) {
     if (g.nx != NX)
         return false;
     constexpr int WIDE = NX > 16 ? 8 : 16;
     if (g.batch >= 64 || g.P <= 8) {
         // more instances than 4-warp CTA slots (148 SMs x 4): 2-warp CTAs
         // (8 per SM) finish the batch in one wave instead of ~1.7
-        // (config 1: 0.319 -> 0.308 ms); CYQ_SCHUR_NW=2|4 forces either
-        const char *e = getenv("CYQ_SCHUR_NW");
-        const bool two = e ? e[0] == '2' : g.batch > 4 * 148;
+        // (config 1: 0.319 -> 0.308 ms); CYQ_OPT_SCHUR_WARPS = 2 | 4 forces either
+        const bool two = o.schur_warps ? o.schur_warps == 2 : g.batch > 4 * o.sms;
         if (two)
             return launch_sfw<NX, 2, 1>(g, st, sa);
         return launch_sfw<NX, 4, 1>(g, st, sa);
     }
-    if (g.P >= 64 && g.batch * 8 <= 148 && !getenv("CYQ_NO_SCHUR_CLUSTER"))
+    if (g.P >= 64 && g.batch * 8 <= o.sms && o.schur_cluster)
         if (launch_sfw<NX, WIDE, 8>(g, st, sa))
             return true;
     return launch_sfw<NX, WIDE, 1>(g, st, sa);
@@ -757,13 +753,10 @@ template <int NX> bool launch_sf(const Geo &g, cudaStream_t st, const SchurArgs 
 } // namespace
 
 // The fused kernel serves every batch size (one CTA per instance; wide CTAs
-// for small batches); CYQ_SCHUR=levels selects the per-level batch-wide
-// kernels of schur_tiles.cu instead (kept as the cross-check path).
-bool schur_fused_ok(const Geo &g) {
-    // CYQ_SCHUR=levels|fused overrides the choice (read per call: tests
-    // exercise both paths in one process)
-    const char *e = getenv("CYQ_SCHUR");
-    if (e && e[0] == 'l')
+// for small batches); CYQ_OPT_SCHUR selects the per-level batch-wide
+// kernels of schur_tiles.cu (or the scalar kernel) instead (cross-check paths).
+bool schur_fused_ok(const Geo &g, const LaunchOpts &o) {
+    if (o.schur != 0)
         return false;
     const bool shape = g.nx == 20 || g.nx == 16 || g.nx == 12 || g.nx == 10;
     if (!shape)
@@ -771,11 +764,11 @@ bool schur_fused_ok(const Geo &g) {
     return true;
 }
 
-bool launch_schur_fused(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
-    if (!schur_fused_ok(g))
+bool launch_schur_fused(const Geo &g, cudaStream_t st, const SchurArgs &sa, const LaunchOpts &o) {
+    if (!schur_fused_ok(g, o))
         return false;
-    return launch_sf<20>(g, st, sa) || launch_sf<16>(g, st, sa) || launch_sf<12>(g, st, sa) ||
-           launch_sf<10>(g, st, sa);
+    return launch_sf<20>(g, st, sa, o) || launch_sf<16>(g, st, sa, o) || launch_sf<12>(g, st, sa, o) ||
+           launch_sf<10>(g, st, sa, o);
 }
 
 } // namespace cyqb

@@ -340,8 +340,6 @@ template <int NX> bool launch_st(const Geo &g, cudaStream_t st, const SchurArgs 
 // Tile-based CR factorization (phase 1 + 2 of schur_cr_kernel); the caller
 // then runs schur_cr_kernel with do_factor = 0 for the rhs and CR solve.
 bool launch_schur_tiles(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
-    if (getenv("CYQ_NO_SCHUR_TILES"))
-        return false;
     return launch_st<20>(g, st, sa) || launch_st<16>(g, st, sa) || launch_st<12>(g, st, sa) ||
            launch_st<10>(g, st, sa);
 }

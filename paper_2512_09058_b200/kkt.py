@@ -18,6 +18,7 @@ is served by the GPU's exact cyclic reduction of the whole Schur tree.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 from dataclasses import dataclass
 
@@ -104,6 +105,33 @@ class Context:
             cls._default[device] = cls(device)
         return cls._default[device]
 
+    def set_option(self, name: str, value):
+        """Kernel selection (cyq_ctx_set_option): name in _lib.OPTIONS, value
+        an int or one of the names in _lib.OPTION_VALUES[name]."""
+        v = _lib.OPTION_VALUES.get(name, {}).get(value, value) if isinstance(value, str) else value
+        rc = self.lib.cyq_ctx_set_option(self.h, _lib.OPTIONS[name], int(v))
+        if rc != _lib.CYQ_OK:
+            raise ValueError(self.last_error())
+
+    def get_option(self, name: str) -> int:
+        v = C.c_int64()
+        rc = self.lib.cyq_ctx_get_option(self.h, _lib.OPTIONS[name], C.byref(v))
+        if rc != _lib.CYQ_OK:
+            raise ValueError(self.last_error())
+        return v.value
+
+    @contextlib.contextmanager
+    def options(self, **kw):
+        """Temporarily set kernel-selection options: `with ctx.options(schur="levels"): ...`"""
+        old = {k: self.get_option(k) for k in kw}
+        try:
+            for k, v in kw.items():
+                self.set_option(k, v)
+            yield self
+        finally:
+            for k, v in old.items():
+                self.set_option(k, v)
+
     def last_error(self) -> str:
         return self.lib.cyq_ctx_last_error(self.h).decode()
 
@@ -185,6 +213,20 @@ def _check_opts(opts: FactorOptions):
     # (test_kkt.cpp:152-161: pcr within 1e-10 of cr1, pcg within 1e-8)
 
 
+def _context(ctx, arrays) -> "Context":
+    """The context of a call: `ctx`, else the default context of the device
+    the CUDA tensors live on (device 0 for host arrays). Every CUDA tensor
+    must be on the context's device."""
+    devs = {a.device.index for a in arrays if _is_torch(a)}
+    if len(devs) > 1:
+        raise ValueError(f"arrays on several devices: {sorted(devs)}")
+    if ctx is None:
+        ctx = Context.default(devs.pop() if devs else 0)
+    elif devs and devs != {ctx.device}:
+        raise ValueError(f"arrays on cuda:{devs.pop()} but the context is on cuda:{ctx.device}")
+    return ctx
+
+
 def _raise_status(ctx, rc, st):
     if rc == _lib.CYQ_OK:
         return
@@ -219,8 +261,9 @@ def solve_problem(p, opts: FactorOptions, ctx: Context | None = None, out=None,
     """kkt::solve_problem for every instance of the batch. Returns the
     solution batch (numpy for host input, torch for CUDA input)."""
     _check_opts(opts)
-    ctx = ctx or Context.default()
-    arrs = [getattr(p, k) for k in OCP_FIELDS]
+    arrs = [getattr(p, k) for k in OCP_FIELDS] + ([] if out is None else [getattr(out, k) for k in SOL_FIELDS])
+    ctx = _context(ctx, arrs)
+    arrs = arrs[:len(OCP_FIELDS)]
     mem = _mem(arrs)
     ctx.follow_torch(arrs)
     sol = out if out is not None else _alloc_sol(p, mem == _lib.CYQ_MEM_DEVICE)
@@ -272,7 +315,7 @@ class Factor:
 def factor(p, opts: FactorOptions, ctx: Context | None = None) -> Factor:
     """kkt::factor for every instance of the batch."""
     _check_opts(opts)
-    ctx = ctx or Context.default()
+    ctx = _context(ctx, [getattr(p, k) for k in OCP_FIELDS])
     mem = _mem([getattr(p, k) for k in OCP_FIELDS])
     ctx.follow_torch([getattr(p, k) for k in OCP_FIELDS])
     h = C.c_void_p()
@@ -353,7 +396,7 @@ def augment_hessians(p, D, Cm, sigma, gamma_inv: float = 0.0, out=None,
     `out` may pass a preallocated EqOCPBatch whose R, S, Q are overwritten."""
     import torch
 
-    ctx = ctx or Context.default()
+    ctx = _context(ctx, [p.R, p.S, p.Q, D, Cm, sigma])
     for a in (p.R, p.S, p.Q, D, Cm, sigma):
         if not _is_torch(a):
             raise ValueError("augment_hessians takes CUDA torch tensors")
@@ -384,7 +427,7 @@ def solve_newton(p, D, Cm, sigma, opts: FactorOptions, gamma_inv: float = 0.0, o
     factorization's stage loads (the augmented Hessians never reach HBM);
     other shapes run the assembly kernel first. CUDA torch tensors only."""
     _check_opts(opts)
-    ctx = ctx or Context.default()
+    ctx = _context(ctx, [getattr(p, k) for k in OCP_FIELDS] + [D, Cm, sigma])
     for a in [getattr(p, k) for k in OCP_FIELDS] + [D, Cm, sigma]:
         if not _is_torch(a):
             raise ValueError("solve_newton takes CUDA torch tensors")
@@ -411,7 +454,7 @@ def line_search_exact(alpha, delta, eta, beta, ctx: Context | None = None,
     (tau, status list))."""
     import torch
 
-    ctx = ctx or Context.default()
+    ctx = _context(ctx, [alpha, delta, eta, beta])
     for a in (alpha, delta, eta, beta):
         if not _is_torch(a):
             raise ValueError("line_search_exact takes CUDA torch tensors")

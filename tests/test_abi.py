@@ -38,12 +38,32 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
+# The kernels the BASELINE configs run (bench.py / launch lists): every
+# stage-panel and Schur/CR kernel must issue FP64 tensor-core DMMAs
+LIVE_DMMA_KERNELS = [
+    "riccati_warp_kernelILi10ELi20ELi1ELi0ELb0",   # config 1 panel
+    "riccati_warp_kernelILi8ELi16ELi1ELi24ELb0",   # config 4 panel (fused Newton assembly)
+    "riccati_pc_kernelILi5ELi10",                  # config 0 panel
+    "riccati_pc_kernelILi4ELi12",                  # config 2 panel
+    "riccati_cta_kernelILi32ELi64ELi16",           # config 3 panel
+    "schur_fused_kernelILi20ELi2ELi1",             # config 1 Schur/CR (batch > 4 x SMs)
+    "schur_fused_kernelILi20ELi4ELi1",
+    "schur_fused_kernelILi16ELi4ELi1",             # config 4 Schur/CR
+    "schur_fused_kernelILi12ELi16ELi8",            # config 2 Schur/CR (8-CTA cluster)
+    "schur_fused_kernelILi10ELi16ELi1",            # config 0 Schur/CR
+    "schur_big_kernelILi64ELi8",                   # config 3 Schur/CR
+    "riccati_panel_kernel_t",                      # generic panel (other shapes)
+]
+
+
 def test_kernels_use_dmma():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _lib.LIB_PATH],
                          capture_output=True, text=True).stdout
-    funcs = out.split("Function : ")
-    ric = [f for f in funcs if f.startswith("_ZN4cyqb22riccati_panel_kernel_t")]
-    assert ric and all("DMMA" in f for f in ric)
+    funcs = out.split("Function : ")[1:]
+    for tag in LIVE_DMMA_KERNELS:
+        hits = [f for f in funcs if tag in f.split("\n", 1)[0]]
+        assert hits, f"kernel {tag} not in the library"
+        assert all("DMMA" in f for f in hits), f"{tag}: no DMMA in its SASS"
 
 
 def test_version_string():

@@ -147,19 +147,15 @@ def test_device_resident_inputs_match_host():
 
 
 def test_split_device_batch_matches_unsplit():
-    # CYQ_SPLIT=2: a device batch as two halves on two streams (capi
+    # option split=2: a device batch as two halves on two streams (capi
     # split_device_pipeline) -- bit-identical to the single-stream launch
-    import os
     import torch
     p = synth.generate(1, seed=13, batch=300, N=32)
     dev = EqOCPBatch.__new__(EqOCPBatch)
     for k in OCP_FIELDS:
         setattr(dev, k, torch.from_numpy(getattr(p, k)).cuda())
     b = kkt.solve_problem(dev, kkt.FactorOptions(P=8))
-    os.environ["CYQ_SPLIT"] = "2"
-    try:
+    with kkt.Context.default().options(split=2):
         a = kkt.solve_problem(dev, kkt.FactorOptions(P=8))
-    finally:
-        os.environ.pop("CYQ_SPLIT", None)
     for k in ("u", "x", "lam"):
         assert torch.equal(getattr(a, k), getattr(b, k))

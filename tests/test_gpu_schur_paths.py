@@ -1,12 +1,10 @@
 """GPU parity of both Schur/CR implementations: the fused one-CTA-per-instance
 kernel (schur_fused.cu, the default for batches >= 64) and the per-level
 batch-wide kernels (schur_tiles.cu + schur_cr.cu, small batches), forced with
-CYQ_SCHUR=fused|levels. Same bars as test_gpu_parity.py: solution rel. error
+the context option `schur` ("auto" = fused, "levels"). Same bars as test_gpu_parity.py: solution rel. error
 <= 1e-9 against the reference's golden outputs / the C oracle, KKT residual
 <= 1e-10 (config 4: the scale-aware bound of test_gpu_parity.py).
 """
-import os
-
 import numpy as np
 import pytest
 
@@ -25,13 +23,8 @@ FUSED_NX = (10, 12, 16, 20)
 
 @pytest.fixture
 def schur_mode(request):
-    old = os.environ.get("CYQ_SCHUR")
-    os.environ["CYQ_SCHUR"] = request.param
-    yield request.param
-    if old is None:
-        os.environ.pop("CYQ_SCHUR", None)
-    else:
-        os.environ["CYQ_SCHUR"] = old
+    with kkt.Context.default().options(schur="auto" if request.param == "fused" else request.param):
+        yield request.param
 
 
 GOLDEN_FUSED = [n for n in golden_util.names()
@@ -86,7 +79,7 @@ def test_fused_cross_P(schur_mode, P):
 
 def test_default_selection_large_batch_matches_oracle():
     # batch >= 64 selects the fused kernel without any override
-    os.environ.pop("CYQ_SCHUR", None)
+    assert kkt.Context.default().get_option("schur") == 0
     p = synth.generate(1, seed=23, batch=64, N=32)
     s = kkt.solve_problem(p, kkt.FactorOptions(P=16))
     ref, rc, _ = Oracle().solve_problem(p, 16)
@@ -111,13 +104,9 @@ def test_cluster_schur_single_long_horizon(P):
     # C oracle
     N = 16 * P
     p = synth.generate(2, seed=31, batch=1, N=N)
-    os.environ.pop("CYQ_NO_SCHUR_CLUSTER", None)
     s_cl = kkt.solve_problem(p, kkt.FactorOptions(P=P))
-    os.environ["CYQ_NO_SCHUR_CLUSTER"] = "1"
-    try:
+    with kkt.Context.default().options(schur_cluster=0):
         s_one = kkt.solve_problem(p, kkt.FactorOptions(P=P))
-    finally:
-        os.environ.pop("CYQ_NO_SCHUR_CLUSTER", None)
     assert rel_error(s_cl, s_one).max() <= 1e-12
     ref, rc, _ = Oracle().solve_problem(p, P)
     assert rc == 0
@@ -129,15 +118,10 @@ def test_cluster_schur_single_long_horizon(P):
     assert rel_error(s2, s_cl).max() <= 1e-13
 
 
-@pytest.fixture(params=["w", "p"])
+@pytest.fixture(params=["warp", "two_warp"])
 def riccati_mode(request):
-    old = os.environ.get("CYQ_RICCATI")
-    os.environ["CYQ_RICCATI"] = request.param
-    yield request.param
-    if old is None:
-        os.environ.pop("CYQ_RICCATI", None)
-    else:
-        os.environ["CYQ_RICCATI"] = old
+    with kkt.Context.default().options(panel=request.param):
+        yield request.param
 
 
 @pytest.mark.parametrize("name", ["cfg0_N64_b1_P4", "cfg2_N512_b1_P128", "cfg1_N40_b3_P16",
@@ -156,16 +140,9 @@ def test_tmem_panel_variant_matches_oracle():
     # opt-in variant of the config-1 warp panel with W in tensor memory
     # (tcgen05.st / tcgen05.ld, 4 chains per CTA); a batch large enough for
     # the batched (non producer/consumer) path
-    old = os.environ.get("CYQ_TMEM")
-    os.environ["CYQ_TMEM"] = "1"
-    try:
-        p = synth.generate(1, seed=8, batch=24, N=128)
+    p = synth.generate(1, seed=8, batch=24, N=128)
+    with kkt.Context.default().options(panel="warp_tmem"):
         sol = kkt.solve_problem(p, kkt.FactorOptions(P=16))
-    finally:
-        if old is None:
-            os.environ.pop("CYQ_TMEM", None)
-        else:
-            os.environ["CYQ_TMEM"] = old
     ref, rc, _ = Oracle().solve_problem(p, 16)
     assert rc == 0
     assert rel_error(sol, ref).max() <= REL_TOL
