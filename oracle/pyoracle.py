@@ -246,6 +246,13 @@ class RefOracle(_Base):
                ctypes_double(rho), C_sol(sol), rep.ctypes.data_as(C_i64p))
         return sol, rc, rep
 
+    def bench_latency(self, p, P, vlen, workers, reps):
+        """Best single-instance factor+solve time (s) of instance 0 with
+        FactorOptions{P, vlen, workers} over `reps` repetitions."""
+        f = self.lib.ref_bench_latency
+        f.restype = C.c_double
+        return f(C.byref(_dims(p, P)), C.byref(_ocp(p)), i64(vlen), i64(workers), i64(reps))
+
     def bench(self, p, P, n_solves, threads, vlen=4):
         return self.lib.ref_bench_solve_problem(C.byref(_dims(p, P)), C.byref(_ocp(p)),
                                                 i64(vlen), i64(n_solves), C.c_int(threads))

@@ -371,6 +371,33 @@ double ref_bench_solve_problem(const oc_dims *d, const oc_ocp *p,
     return std::chrono::duration<double>(t1 - t0).count();
 }
 
+// Single-instance latency: kkt::factor +
+// kkt::solve of instance 0 with FactorOptions{P, vlen, workers}, repeated
+// `reps` times after one warm-up; returns the best time per solve (s).
+double ref_bench_latency(const oc_dims *d, const oc_ocp *p, int64_t vlen, int64_t workers,
+                         int64_t reps) {
+    EqOCP prob = make_ocp(d, p, 0);
+    EqRhs rhs  = EqRhs::of_problem(prob);
+    FactorOptions o = opts_of(d, vlen);
+    o.workers       = std::max<int64_t>(1, workers);
+    double best     = 1e300;
+    try {
+        for (int64_t r = 0; r <= reps; ++r) {
+            auto t0      = std::chrono::steady_clock::now();
+            Factor f     = kkt::factor(prob, o);
+            EqSolution s = kkt::solve(f, prob, rhs);
+            auto t1      = std::chrono::steady_clock::now();
+            if (s.u.empty())
+                return -1.0;
+            if (r > 0)
+                best = std::min(best, std::chrono::duration<double>(t1 - t0).count());
+        }
+    } catch (...) {
+        return -1.0;
+    }
+    return best;
+}
+
 } // extern "C"
 
 

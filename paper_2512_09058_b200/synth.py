@@ -20,6 +20,7 @@ reproducible on its own (parity tests use small subsets of the full batch).
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -88,8 +89,19 @@ def generate(cfg_idx: int, seed: int = 0, batch: int | None = None,
     batch = cfg.batch if batch is None else batch
     N = cfg.N if N is None else N
     cols = [[] for _ in range(9)]
-    for i in range(start, start + batch):
-        vals = _instance(cfg, N, seed, i)[:9]
+    # instances are independent streams: drawn on a thread pool (LAPACK's
+    # eigvals for the spectral-radius scaling dominates and releases the
+    # GIL), one BLAS thread each; the values do not depend on the pool
+    workers = min(batch, os.cpu_count() or 1) if batch * N * cfg.nx ** 3 > 1 << 24 else 1
+    if workers > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(1), ThreadPoolExecutor(workers) as ex:
+            insts = list(ex.map(lambda i: _instance(cfg, N, seed, i)[:9], range(start, start + batch)))
+    else:
+        insts = [_instance(cfg, N, seed, i)[:9] for i in range(start, start + batch)]
+    for vals in insts:
         for c, v in zip(cols, vals):
             c.append(v)
     return EqOCPBatch(*[np.stack(c) for c in cols])
