@@ -177,7 +177,11 @@ int cyq_line_search_batch(cyq_ctx *ctx, int64_t batch, int64_t m,
 #define CYQ_OPT_PANEL_WARPS 7   /* generic panel: warps per chain CTA, 0 auto */
 #define CYQ_OPT_TAIL 8          /* CYQ_TAIL_* (FactorOptions::tail, kkt_solver.hpp:45-64) */
 #define CYQ_OPT_PHASE_PROF 9    /* 1: per-stage phase clocks of chain 0 to stderr */
-#define CYQ_OPT_COUNT 10
+#define CYQ_OPT_ASYNC_STATUS 10 /* 1: device-memory calls return without a host sync;
+                                   cyq_ctx_wait_status reports the last call */
+#define CYQ_OPT_GRAPHS 11       /* 1 (default): a device-memory call repeated with the same
+                                   shape and pointers replays a captured CUDA graph */
+#define CYQ_OPT_COUNT 12
 
 #define CYQ_PANEL_AUTO 0
 #define CYQ_PANEL_WARP 1      /* one warp per chain, compile-time shapes */
@@ -196,6 +200,12 @@ int cyq_line_search_batch(cyq_ctx *ctx, int64_t batch, int64_t m,
 
 int cyq_ctx_set_option(cyq_ctx *ctx, int option, int64_t value);
 int cyq_ctx_get_option(cyq_ctx *ctx, int option, int64_t *value);
+/* With CYQ_OPT_ASYNC_STATUS, device-memory factor / solve_problem / Newton
+ * calls enqueue their work and the per-instance failure keys' readback and
+ * return CYQ_OK (argument errors are still reported at once). This waits
+ * for the context stream and decodes the most recent such call's status
+ * into `status` (n entries, may be NULL); returns its worst code. */
+int cyq_ctx_wait_status(cyq_ctx *ctx, cyq_status *status, int64_t n);
 
 /* Per-kernel device timing: when enabled, every launch of the pipeline is
  * bracketed by CUDA events on the context stream. `read` synchronizes and

@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(32 * WPB) backsub_tile_kernel(BacksubArgs a) {
     const Geo &g = a.g;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const size_t chain = (size_t)blockIdx.x * WPB + wib;
+    griddep_wait(); // the Schur kernel's multipliers
     if (chain >= (size_t)g.batch * g.P)
         return;
     const int b = (int)(chain / g.P), c = (int)(chain % g.P), n = g.n, N = g.N;
@@ -268,7 +269,7 @@ template <int NU, int NX> bool launch_bt(const Geo &g, cudaStream_t st, const Ba
     constexpr int WPB = 4;
     const size_t smem = (size_t)WPB * BT<NU, NX>::PER_WARP * sizeof(double);
     const int chains = g.batch * g.P;
-    backsub_tile_kernel<NU, NX, WPB><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ba);
+    launch_pdl(backsub_tile_kernel<NU, NX, WPB>, dim3((chains + WPB - 1) / WPB), dim3(32 * WPB), smem, st, 1, ba);
     return true;
 }
 } // namespace

@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(32 * WPB) backsub_warp_kernel(BacksubArgs a) {
     const Geo &g = a.g;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const size_t chain = (size_t)blockIdx.x * WPB + wib;
+    griddep_wait(); // the Schur kernel's multipliers
     if (chain >= (size_t)g.batch * g.P)
         return;
     const int b = (int)(chain / g.P), c = (int)(chain % g.P), n = g.n;
@@ -293,7 +294,7 @@ template <int NU, int NX, int WPB> bool launch_b(const Geo &g, cudaStream_t st, 
     static DeviceOnce once;
     once_per_device(once, [&] { return cudaFuncSetAttribute(backsub_warp_kernel<NU, NX, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
     const int chains = g.batch * g.P;
-    backsub_warp_kernel<NU, NX, WPB><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ba);
+    launch_pdl(backsub_warp_kernel<NU, NX, WPB>, dim3((chains + WPB - 1) / WPB), dim3(32 * WPB), smem, st, 1, ba);
     return true;
 }
 } // namespace

@@ -46,6 +46,14 @@ struct cyq_ctx {
     int64_t kernels[5] = {0, 0, 0, 0, 0}; // kernel launches per kind
     LaunchOpts opts;                      // kernel selection (cyq_ctx_set_option)
     long long *phase = nullptr;           // phase clocks (CYQ_OPT_PHASE_PROF)
+    // asynchronous status (CYQ_OPT_ASYNC_STATUS): pinned keys of the last call
+    unsigned long long *hpend = nullptr;
+    size_t hpend_n = 0;
+    int64_t pend_batch = -1;
+    // CUDA graph of the last repeated device pipeline (CYQ_OPT_GRAPHS)
+    std::vector<unsigned long long> gkey_seen, gkey;
+    cudaGraphExec_t gexec = nullptr;
+    cudaStream_t cap_stream = nullptr;
 };
 
 struct cyq_factor {
@@ -497,6 +505,95 @@ int decode_status(cyq_ctx *ctx, const Geo &g, const unsigned long long *dfail,
     return worst;
 }
 
+// Status of a device-memory call: decoded now (host sync), or with
+// CYQ_OPT_ASYNC_STATUS copied into pinned memory stream-ordered and decoded
+// by cyq_ctx_wait_status.
+int finish_status(cyq_ctx *ctx, const Geo &g, const unsigned long long *dfail, cyq_status *status) {
+    if (!ctx->opts.async_status)
+        return decode_status(ctx, g, dfail, status);
+    if (ctx->hpend_n < (size_t)g.batch) {
+        if (ctx->hpend)
+            CU(cudaFreeHost(ctx->hpend));
+        ctx->hpend = nullptr;
+        ctx->hpend_n = 0;
+        CU(cudaMallocHost(reinterpret_cast<void **>(&ctx->hpend), sizeof(unsigned long long) * g.batch));
+        ctx->hpend_n = (size_t)g.batch;
+    }
+    CU(cudaMemcpyAsync(ctx->hpend, dfail, sizeof(unsigned long long) * g.batch, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    ctx->pend_batch = g.batch;
+    return CYQ_OK;
+}
+
+int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &ws,
+                    const SolView *sol, bool do_solve);
+
+// launch_pipeline through a CUDA graph when the same device call (shape,
+// pointers, options, solve or factor only) repeats: the first occurrence
+// launches directly, the second is captured (on a private stream) and
+// launched, later ones replay it -- one graph launch instead of a memset
+// and three kernel launches per call. Not used while per-kernel profiling
+// (events between the kernels) is on.
+int run_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorWS &ws, const SolView *sol,
+                 bool do_solve) {
+    const LaunchOpts &o = ctx->opts;
+    if (ctx->profile || !o.graphs || o.phase_prof || !riccati_staged(g))
+        return launch_pipeline(ctx, g, p, ws, sol, do_solve);
+    std::vector<unsigned long long> key;
+    auto put = [&](const void *q, size_t bytes) {
+        const unsigned char *c = static_cast<const unsigned char *>(q);
+        for (size_t i = 0; i < bytes; i += 8) {
+            unsigned long long v = 0;
+            memcpy(&v, c + i, std::min<size_t>(8, bytes - i));
+            key.push_back(v);
+        }
+    };
+    put(&g, sizeof g);
+    put(&p, sizeof p);
+    put(&ws, sizeof ws);
+    if (sol)
+        put(sol, sizeof *sol);
+    put(&o, sizeof o);
+    key.push_back(do_solve);
+    key.push_back(reinterpret_cast<unsigned long long>(ctx->stream));
+    if (ctx->gexec && key == ctx->gkey) {
+        CU(cudaGraphLaunch(ctx->gexec, ctx->stream));
+        return CYQ_OK;
+    }
+    if (key != ctx->gkey_seen) { // first occurrence: direct launches
+        ctx->gkey_seen = key;
+        return launch_pipeline(ctx, g, p, ws, sol, do_solve);
+    }
+    if (!ctx->cap_stream)
+        CU(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    const cudaStream_t user = ctx->stream;
+    ctx->stream = ctx->cap_stream;
+    CU(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    int rc = launch_pipeline(ctx, g, p, ws, sol, do_solve);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(ctx->cap_stream, &graph);
+    ctx->stream = user;
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t ei = cudaErrorUnknown;
+    if (rc == CYQ_OK && ec == cudaSuccess && graph)
+        ei = cudaGraphInstantiate(&exec, graph, 0);
+    if (graph)
+        cudaGraphDestroy(graph);
+    if (rc != CYQ_OK)
+        return rc;
+    if (ei != cudaSuccess) { // not capturable: launch directly from now on
+        cudaGetLastError();
+        ctx->gkey_seen.clear();
+        return launch_pipeline(ctx, g, p, ws, sol, do_solve);
+    }
+    if (ctx->gexec)
+        cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = exec;
+    ctx->gkey = key;
+    CU(cudaGraphLaunch(ctx->gexec, ctx->stream));
+    return CYQ_OK;
+}
+
 int ensure(cyq_ctx *ctx, void **buf, size_t *have, size_t need) {
     if (*have >= need)
         return CYQ_OK;
@@ -562,6 +659,12 @@ int cyq_ctx_destroy(cyq_ctx *ctx) {
         cudaFreeHost(ctx->hfail);
     if (ctx->phase)
         cudaFree(ctx->phase);
+    if (ctx->hpend)
+        cudaFreeHost(ctx->hpend);
+    if (ctx->gexec)
+        cudaGraphExecDestroy(ctx->gexec);
+    if (ctx->cap_stream)
+        cudaStreamDestroy(ctx->cap_stream);
     for (auto &e : ctx->ev) {
         cudaEventDestroy(e.second.first);
         cudaEventDestroy(e.second.second);
@@ -698,10 +801,10 @@ int cyq_solve_problem_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_ba
             // overlap the next part's kernels
             return split_device_pipeline(ctx, g, view_of(prob), sv, status, K);
         }
-        rc = launch_pipeline(ctx, g, view_of(prob), ws, &sv, true);
+        rc = run_pipeline(ctx, g, view_of(prob), ws, &sv, true);
         if (rc)
             return rc;
-        return decode_status(ctx, g, ws.fail, status);
+        return finish_status(ctx, g, ws.fail, status);
     }
     // host memory: the batch is split into chunks whose host->device copies
     // (copy stream) overlap the previous chunk's kernels (compute stream);
@@ -959,17 +1062,47 @@ int cyq_ctx_set_option(cyq_ctx *ctx, int option, int64_t value) {
     case CYQ_OPT_PANEL_WARPS: if (value < 0 || value > 4) return bad(); o.panel_warps = (int)value; break;
     case CYQ_OPT_TAIL: if (value < 0 || value > 2) return bad(); o.tail = (int)value; break;
     case CYQ_OPT_PHASE_PROF: o.phase_prof = value != 0; break;
+    case CYQ_OPT_ASYNC_STATUS: o.async_status = value != 0; break;
+    case CYQ_OPT_GRAPHS: o.graphs = value != 0; break;
     default: return set_err(ctx, CYQ_INVALID_ARG, "unknown option");
     }
     return CYQ_OK;
+}
+
+int cyq_ctx_wait_status(cyq_ctx *ctx, cyq_status *status, int64_t n) {
+    if (!ctx)
+        return set_err(nullptr, CYQ_INVALID_ARG, "null context");
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (ctx->pend_batch < 0)
+        return CYQ_OK;
+    int worst = CYQ_OK;
+    for (int64_t b = 0; b < ctx->pend_batch; ++b) {
+        const unsigned long long k = ctx->hpend[b];
+        cyq_status st{};
+        st.instance = b;
+        if (k != ~0ull) {
+            st.code = CYQ_PIVOT_FAIL;
+            st.kind = (int)(k >> 60);
+            st.column_or_level = (int64_t)((k >> 40) & 0xFFFFF);
+            st.stage = (int64_t)((k >> 20) & 0xFFFFF);
+            st.pivot = (int64_t)(k & 0xFFFFF);
+            worst = CYQ_PIVOT_FAIL;
+        }
+        if (status && b < n)
+            status[b] = st;
+    }
+    if (worst != CYQ_OK)
+        set_err(ctx, worst, "factorization pivot failure (see status)");
+    return worst;
 }
 
 int cyq_ctx_get_option(cyq_ctx *ctx, int option, int64_t *value) {
     if (!ctx || !value)
         return set_err(ctx, CYQ_INVALID_ARG, "null argument");
     const LaunchOpts &o = ctx->opts;
-    const int v[CYQ_OPT_COUNT] = {o.panel,     o.schur,     o.schur_warps, o.schur_cluster, o.split,
-                                  o.backsub,   o.fused_aug, o.panel_warps, o.tail,          o.phase_prof};
+    const int v[CYQ_OPT_COUNT] = {o.panel,       o.schur,        o.schur_warps, o.schur_cluster,
+                                  o.split,       o.backsub,      o.fused_aug,   o.panel_warps,
+                                  o.tail,        o.phase_prof,   o.async_status, o.graphs};
     if (option < 0 || option >= CYQ_OPT_COUNT)
         return set_err(ctx, CYQ_INVALID_ARG, "unknown option");
     *value = v[option];
@@ -1075,10 +1208,10 @@ int cyq_solve_newton_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_bat
         pv.Q = Qo;
     }
     SolView sv{sol->u, sol->x, sol->lam};
-    rc = launch_pipeline(ctx, g, pv, ws, &sv, true);
+    rc = run_pipeline(ctx, g, pv, ws, &sv, true);
     if (rc)
         return rc;
-    return decode_status(ctx, g, ws.fail, status);
+    return finish_status(ctx, g, ws.fail, status);
 }
 
 int cyq_line_search_batch(cyq_ctx *ctx, int64_t batch, int64_t m, const double *alpha,

@@ -3,6 +3,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <utility>
 
 #include "kkt_common.cuh"
 
@@ -37,6 +38,32 @@ template <class F> cudaError_t once_per_device(DeviceOnce &o, F &&setup) {
     return e;
 }
 
+// Launch with programmatic stream serialization (PDL, see griddep_wait in
+// kkt_common.cuh); `cluster` > 1 adds a thread-block cluster dimension.
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,
+                       Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    int na = 1;
+    if (cluster > 1) {
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = cluster;
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
+        na = 2;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 // Kernel selection of a context (cyq_ctx_set_option, include/cyqlone_b200.h);
 // the defaults pick the fastest measured kernel per shape.
 struct LaunchOpts {
@@ -50,6 +77,8 @@ struct LaunchOpts {
     int panel_warps = 0;   // generic panel: warps per chain CTA (0 auto)
     int tail = 0;          // CYQ_TAIL_*: Schur tail (0 cr1 / 2 pcg: exact CR, 1 pcr)
     int phase_prof = 0;    // per-stage phase clocks of chain 0 (profiling aid)
+    int async_status = 0;  // device calls return without a host sync (cyq_ctx_wait_status)
+    int graphs = 1;        // repeated identical device calls replay a captured CUDA graph
     int sms = 148;         // multiprocessors of the context's device
 };
 

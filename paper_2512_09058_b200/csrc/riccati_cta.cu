@@ -208,6 +208,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
     const Geo &g = a.g;
     const int chain = blockIdx.x;
     const int b = chain / g.P, c = chain % g.P, n = g.n, N = g.N;
+    griddep_launch();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rq = lane >> 2, cq = 2 * (lane & 3), q2 = lane & 3;
     double *Wsm = sm + C::O_W, *colb = sm + C::O_COL, *linvb = sm + C::O_LINV, *BA = sm + C::O_BA;

@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(64, 6) riccati_pc_kernel(RiccatiArgs a) {
     const Geo &g = a.g;
     const int lane = threadIdx.x & 31, role = threadIdx.x >> 5; // 0 producer, 1 consumer
     const int chain = blockIdx.x;
+    griddep_launch();
     if (chain >= g.batch * g.P)
         return;
     const int b = chain / g.P, c = chain % g.P, n = g.n;

@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(32 * WPB, TM ? 3 : 1) riccati_warp_kernel(Ricc
     const Geo &g = a.g;
     const int wib = threadIdx.x >> 5;
     const int chain = blockIdx.x * WPB + wib;
+    griddep_launch();
     uint32_t tmw = 0; // TM: this warp's TMEM base (lane offset 32 wib, column 0)
     __shared__ uint32_t s_taddr;
     if constexpr (TM) {

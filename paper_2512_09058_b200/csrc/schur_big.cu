@@ -82,6 +82,8 @@ __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
     const Geo &g = a.g;
     const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int P = g.P, nu = g.nu, n = g.n, CT = g.CT;
+    griddep_launch();
+    griddep_wait(); // the stage panel's factor tiles
     const SBLayout Lo = SBLayout::make(P, NX);
     double *ws = a.schur + (size_t)b * Lo.total;
     double *Tt = ws + Lo.Tt, *D = ws + Lo.D, *Mb = ws + Lo.Mb, *K = ws + Lo.K, *S1 = ws + Lo.S1,
@@ -319,7 +321,7 @@ template <int NX> bool launch_sb(const Geo &g, cudaStream_t st, const SchurArgs 
         return false;
     static DeviceOnce once;
     once_per_device(once, [&] { return cudaFuncSetAttribute(schur_big_kernel<NX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
-    schur_big_kernel<NX, NW><<<g.batch, 32 * NW, smem, st>>>(sa);
+    launch_pdl(schur_big_kernel<NX, NW>, dim3(g.batch), dim3(32 * NW), smem, st, 1, sa);
     return true;
 }
 

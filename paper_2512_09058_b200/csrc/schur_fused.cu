@@ -244,6 +244,8 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
     const int crank = CL > 1 ? (int)cg::this_cluster().block_rank() : 0;
     const int b = blockIdx.x / CL, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int vwarp = crank * NW + warp, vtid = crank * 32 * NW + threadIdx.x;
+    griddep_launch();
+    griddep_wait(); // the stage panel's factor tiles
     constexpr int VNW = CL * NW, VNTH = CL * 32 * NW;
     auto csync = [&]() {
         if (CL > 1)
@@ -709,23 +711,11 @@ template <int NX, int NW, int CL> bool launch_sfw(const Geo &g, cudaStream_t st,
         return false;
     static DeviceOnce once;
     once_per_device(once, [&] { return cudaFuncSetAttribute(schur_fused_kernel<NX, NW, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); });
-    if (CL == 1) {
-        schur_fused_kernel<NX, NW, CL><<<g.batch, 32 * NW, smem, st>>>(sa);
+    if (launch_pdl(schur_fused_kernel<NX, NW, CL>, dim3(g.batch * CL), dim3(32 * NW), smem, st, CL, sa) ==
+        cudaSuccess)
         return true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(g.batch * CL);
-    cfg.blockDim = dim3(32 * NW);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = CL;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, schur_fused_kernel<NX, NW, CL>, sa) == cudaSuccess;
+    cudaGetLastError(); // e.g. a cluster that cannot be co-scheduled: the caller falls back
+    return false;
 }
 
 // 4 warps per instance when the batch fills the GPU with CTAs; for a few

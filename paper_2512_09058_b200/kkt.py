@@ -132,6 +132,18 @@ class Context:
             for k, v in old.items():
                 self.set_option(k, v)
 
+    def wait_status(self, batch: int, raise_on_error: bool = True):
+        """With the `async_status` option: wait for the context stream and
+        decode the most recent device call's per-instance status (raises
+        FactorizeError like a synchronous call unless raise_on_error=False;
+        then returns (rc, status list))."""
+        st = (_lib.CyqStatus * batch)()
+        rc = self.lib.cyq_ctx_wait_status(self.h, st, batch)
+        if raise_on_error:
+            _raise_status(self, rc, st)
+            return None
+        return rc, list(st)
+
     def last_error(self) -> str:
         return self.lib.cyq_ctx_last_error(self.h).decode()
 

@@ -87,10 +87,16 @@ def main():
     ap.add_argument("--algo-flops", type=float, default=None)
     ap.add_argument("--algo-bytes", type=float, default=None)
     ap.add_argument("--note", default="")
+    ap.add_argument("--batch", type=int, default=None, help="instances of the captured launch")
+    ap.add_argument("--config", type=int, default=None, help="BASELINE config of the capture")
     a = ap.parse_args()
     res = raw_metrics(a.report, a.kernel)
     res["report"] = a.report.split("/")[-1]
     res["note"] = a.note
+    if a.batch is not None:
+        res["batch"] = a.batch
+    if a.config is not None:
+        res["config"] = a.config
     if a.algo_flops and res.get("duration_ns"):
         res["algo_flops"] = a.algo_flops
         res["algo_tflops_under_ncu"] = a.algo_flops / res["duration_ns"] / 1e3
