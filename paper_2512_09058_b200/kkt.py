@@ -148,10 +148,13 @@ class Context:
         return self.lib.cyq_ctx_last_error(self.h).decode()
 
     def set_stream(self, stream_ptr: int | None):
-        """Bind the context to a CUDA stream (None: a private non-blocking
-        stream); either way it stops following torch's current stream."""
-        self.lib.cyq_ctx_set_stream(self.h, C.c_void_p(stream_ptr or 0))
-        self._bound, self._cur = True, stream_ptr
+        """Bind the context to a CUDA stream handle (0, as torch reports its
+        default stream: the legacy default stream) or None (a private
+        non-blocking stream); either way it stops following torch's current
+        stream."""
+        h = None if stream_ptr is None else (stream_ptr or 1)  # 1 = cudaStreamLegacy
+        self.lib.cyq_ctx_set_stream(self.h, C.c_void_p(h))
+        self._bound, self._cur = True, h
 
     def synchronize(self):
         self.lib.cyq_ctx_synchronize(self.h)
@@ -188,10 +191,13 @@ def _ptr(a) -> int:
     if isinstance(a, np.ndarray):
         assert a.dtype == _F64 and a.flags.c_contiguous
         return a.ctypes.data
-    import torch
-
-    assert a.is_cuda and a.is_contiguous() and a.dtype == torch.float64
+    assert a.is_cuda and a.is_contiguous() and a.dtype == _torch().float64
     return a.data_ptr()
+
+
+def _torch():
+    import torch
+    return torch
 
 
 def _mem(arrs) -> int:
@@ -430,6 +436,68 @@ def augment_hessians(p, D, Cm, sigma, gamma_inv: float = 0.0, out=None,
     return out
 
 
+class Prepared:
+    """A prepared device-resident call over fixed arrays -- kkt::solve_problem
+    (`Prepared.solve_problem`) or the QPALM Newton system
+    (`Prepared.solve_newton`): the argument blocks are validated and built
+    once, each call is one C-ABI call. For loops that rewrite the device
+    arrays in place between calls (MPC, the QPALM inner loop); with the
+    context's `async_status` option the calls do not synchronize the host
+    (check `ctx.wait_status(batch)` afterwards)."""
+
+    def __init__(self, ctx, fn, args, batch, out):
+        self.ctx, self.fn, self.args, self.batch, self.out = ctx, fn, args, batch, out
+        self.st = (_lib.CyqStatus * batch)()
+        self._keep = []
+
+    @classmethod
+    def solve_problem(cls, p, opts: FactorOptions, out=None, ctx: Context | None = None):
+        _check_opts(opts)
+        arrs = [getattr(p, k) for k in OCP_FIELDS]
+        if not all(_is_torch(a) for a in arrs):
+            raise ValueError("Prepared calls take CUDA torch tensors")
+        ctx = _context(ctx, arrs + ([] if out is None else [getattr(out, k) for k in SOL_FIELDS]))
+        ctx.follow_torch(arrs)
+        sol = out if out is not None else _alloc_sol(p, True)
+        dims, ocp = _dims(p, opts.P), _ocp_struct(p)
+        solb = _lib.CyqSolBatch(*[_ptr(getattr(sol, k)) for k in SOL_FIELDS])
+        self = cls(ctx, ctx.lib.cyq_solve_problem_batch, None, p.A.shape[0], sol)
+        self._keep = [dims, ocp, solb]
+        self.args = (ctx.h, C.byref(dims), C.byref(ocp), C.byref(solb), self.st, _lib.CYQ_MEM_DEVICE)
+        return self
+
+    @classmethod
+    def solve_newton(cls, p, D, Cm, opts: FactorOptions, gamma_inv: float = 0.0, out=None,
+                     ctx: Context | None = None):
+        """Call with the Σ of each Newton system: `plan(sigma)`."""
+        _check_opts(opts)
+        arrs = [getattr(p, k) for k in OCP_FIELDS] + [D, Cm]
+        if not all(_is_torch(a) for a in arrs):
+            raise ValueError("Prepared calls take CUDA torch tensors")
+        ctx = _context(ctx, arrs)
+        ctx.follow_torch(arrs)
+        sol = out if out is not None else _alloc_sol(p, True)
+        dims, ocp = _dims(p, opts.P), _ocp_struct(p)
+        solb = _lib.CyqSolBatch(*[_ptr(getattr(sol, k)) for k in SOL_FIELDS])
+        self = cls(ctx, ctx.lib.cyq_solve_newton_batch, None, p.A.shape[0], sol)
+        self._keep = [dims, ocp, solb]
+        self.args = (ctx.h, C.byref(dims), C.byref(ocp), D.shape[2], _ptr(D), _ptr(Cm))
+        self.tail = (float(gamma_inv), C.byref(solb), self.st)
+        self.sig_shape = (p.A.shape[0], p.A.shape[1] + 1, D.shape[2])
+        return self
+
+    def __call__(self, sigma=None, raise_on_error: bool = True):
+        if sigma is None:
+            rc = self.fn(*self.args)
+        else:
+            if tuple(sigma.shape) != self.sig_shape:
+                raise ValueError(f"sigma must be {self.sig_shape}")
+            rc = self.fn(*self.args, _ptr(sigma), *self.tail)
+        if rc != _lib.CYQ_OK and raise_on_error:
+            _raise_status(self.ctx, rc, self.st)
+        return self.out
+
+
 def solve_newton(p, D, Cm, sigma, opts: FactorOptions, gamma_inv: float = 0.0, out=None,
                  ctx: Context | None = None, raise_on_error: bool = True):
     """One Newton system of the QPALM inner loop per instance: assembly as in
@@ -487,5 +555,5 @@ def line_search_exact(alpha, delta, eta, beta, ctx: Context | None = None,
     return out
 
 
-__all__ = ["augment_hessians", "solve_newton", "line_search_exact", "update", "FactorOptions", "Factor", "FactorizeError", "CudaError", "Context", "factor",
+__all__ = ["Prepared", "augment_hessians", "solve_newton", "line_search_exact", "update", "FactorOptions", "Factor", "FactorizeError", "CudaError", "Context", "factor",
            "solve", "solve_problem", "nu2", "EqOCPBatch", "EqRhsBatch", "EqSolutionBatch"]
