@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcyqlone_b200.so")
+# CYQ_LIB selects another build of the same library (tools/build_debug.sh)
+LIB_PATH = os.environ.get("CYQ_LIB") or os.path.join(HERE, "libcyqlone_b200.so")
 
 CYQ_OK, CYQ_INVALID_ARG, CYQ_PIVOT_FAIL, CYQ_CUDA_ERR, CYQ_NO_DEVICE = 0, 1, 2, 3, 4
 CYQ_MEM_HOST, CYQ_MEM_DEVICE = 0, 1

@@ -1,5 +1,5 @@
 // Shared compile-time-shape helpers of the Riccati stage-panel kernels
-// (riccati_warp.cu, riccati_cta2.cu): tile geometry, cp.async staging of the
+// (riccati_warp.cu, riccati_pc.cu, riccati_cta.cu): tile geometry, cp.async staging of the
 // stage data (R, S, Q, r, q / B, A, f) and the panel initialisation.
 #pragma once
 
@@ -7,6 +7,7 @@
 #include "kernels.h"
 
 #include <cstdint>
+#include <cstdio>
 
 namespace cyqb {
 namespace ric {
@@ -45,6 +46,50 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int K> __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory");
 }
+
+// ---- shared-memory mbarriers (hand-offs between warps of one CTA) ----------
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mb_init(unsigned long long *mb, int count = 1) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+// this lane's arrival, triggered when its prior cp.async copies complete
+__device__ __forceinline__ void mb_arrive_on_copies(unsigned long long *mb) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(mb)) : "memory");
+}
+// all lanes' prior shared-memory writes, then one (release) arrival
+__device__ __forceinline__ void mb_signal(unsigned long long *mb, int lane) {
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0)
+        asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(mb)) : "memory");
+    __syncwarp();
+}
+// suspend until the phase with parity `par` has completed (acquire)
+#ifdef CYQ_MB_WATCHDOG // debug builds: a wait that never completes reports and traps
+__device__ __forceinline__ void mb_wait(unsigned long long *mb, int par) {
+    unsigned ok = 0;
+    for (long long it = 0; !ok; ++it) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok) : "r"(smem_u32(mb)), "r"(par) : "memory");
+        if (!ok && it == (1LL << 22) && (threadIdx.x & 31) == 0 && blockIdx.x < 2) {
+            printf("mb_wait stuck: block %d warp %d barrier smem+%u parity %d\n", blockIdx.x, threadIdx.x >> 5,
+                   smem_u32(mb), par);
+            __trap();
+        }
+    }
+}
+#else
+__device__ __forceinline__ void mb_wait(unsigned long long *mb, int par) {
+    asm volatile("{\n .reg .pred p;\n"
+                 "MB_WAIT_%=:\n"
+                 " mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+                 " @!p bra MB_WAIT_%=;\n}" ::"r"(smem_u32(mb)),
+                 "r"(par)
+                 : "memory");
+}
+#endif
 
 // async copy of cnt doubles (16-byte granules when both ends are aligned),
 // or an identity / zero fill when src == nullptr

@@ -73,34 +73,6 @@ template <int CT> struct MbX {
                          kCount = kMbCol + CT + 3;
 };
 
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mb_init(unsigned long long *mb, int count = 1) {
-    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
-}
-// this lane's arrival, triggered when its prior cp.async copies complete
-__device__ __forceinline__ void mb_arrive_on_copies(unsigned long long *mb) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(mb)) : "memory");
-}
-// all lanes' prior shared-memory writes, then one (release) arrival
-__device__ __forceinline__ void mb_signal(unsigned long long *mb, int lane) {
-    __syncwarp();
-    __threadfence_block();
-    if (lane == 0)
-        asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(mb)) : "memory");
-    __syncwarp();
-}
-// suspend until the phase with parity `par` has completed (acquire)
-__device__ __forceinline__ void mb_wait(unsigned long long *mb, int par) {
-    asm volatile("{\n .reg .pred p;\n"
-                 "MB_WAIT_%=:\n"
-                 " mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
-                 " @!p bra MB_WAIT_%=;\n}" ::"r"(smem_u32(mb)),
-                 "r"(par)
-                 : "memory");
-}
-
 } // namespace
 
 template <int NU, int NX>
