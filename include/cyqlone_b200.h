@@ -181,7 +181,10 @@ int cyq_line_search_batch(cyq_ctx *ctx, int64_t batch, int64_t m,
                                    cyq_ctx_wait_status reports the last call */
 #define CYQ_OPT_GRAPHS 11       /* 1 (default): a device-memory call repeated with the same
                                    shape and pointers replays a captured CUDA graph */
-#define CYQ_OPT_COUNT 12
+#define CYQ_OPT_VLEN 12          /* FactorOptions::vlen (power of two, default 4): with
+                                   CYQ_TAIL_PCR the last min(P, vlen) Schur blocks are
+                                   solved by parallel cyclic reduction */
+#define CYQ_OPT_COUNT 13
 
 #define CYQ_PANEL_AUTO 0
 #define CYQ_PANEL_WARP 1      /* one warp per chain, compile-time shapes */

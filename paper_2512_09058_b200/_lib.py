@@ -20,7 +20,7 @@ CYQ_MEM_HOST, CYQ_MEM_DEVICE = 0, 1
 # cyq_ctx_set_option keys and named values (include/cyqlone_b200.h)
 OPTIONS = {"panel": 0, "schur": 1, "schur_warps": 2, "schur_cluster": 3, "split": 4,
            "backsub": 5, "fused_augment": 6, "panel_warps": 7, "tail": 8, "phase_prof": 9,
-           "async_status": 10, "graphs": 11}
+           "async_status": 10, "graphs": 11, "vlen": 12}
 OPTION_VALUES = {
     "panel": {"auto": 0, "warp": 1, "two_warp": 2, "cta": 3, "generic": 4, "warp_tmem": 5},
     "schur": {"auto": 0, "levels": 1, "scalar": 2},

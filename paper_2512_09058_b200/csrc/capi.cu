@@ -120,6 +120,9 @@ int make_geo(cyq_ctx *ctx, const cyq_dims *d, Geo &g) {
     g.NPT = g.CT * (g.CT + 1) / 2 + g.BT * g.CT;
     g.NTT = g.BT * (g.BT + 1) / 2;
     g.batch = (int)d->batch;
+    // FactorOptions::tail = pcr (kkt_factor.cpp:214-247): cyclic reduction
+    // down to min(P, vlen) blocks, parallel cyclic reduction for the rest
+    g.tail = ctx && ctx->opts.tail == CYQ_TAIL_PCR ? std::min(g.P, std::max(1, ctx->opts.vlen)) : 1;
     if (cyqb::riccati_smem_bytes(g) > 227 * 1024 || g.TT * (g.TT + 1) / 2 > 8 * 32)
         return set_err(ctx, CYQ_INVALID_ARG,
                        "stage panel too large (2 nx + nu > ~160 not supported)");
@@ -1063,6 +1066,11 @@ int cyq_ctx_set_option(cyq_ctx *ctx, int option, int64_t value) {
     case CYQ_OPT_TAIL: if (value < 0 || value > 2) return bad(); o.tail = (int)value; break;
     case CYQ_OPT_PHASE_PROF: o.phase_prof = value != 0; break;
     case CYQ_OPT_ASYNC_STATUS: o.async_status = value != 0; break;
+    case CYQ_OPT_VLEN:
+        if (value < 1 || value > 1024 || (value & (value - 1)))
+            return bad();
+        o.vlen = (int)value;
+        break;
     case CYQ_OPT_GRAPHS: o.graphs = value != 0; break;
     default: return set_err(ctx, CYQ_INVALID_ARG, "unknown option");
     }
@@ -1102,7 +1110,8 @@ int cyq_ctx_get_option(cyq_ctx *ctx, int option, int64_t *value) {
     const LaunchOpts &o = ctx->opts;
     const int v[CYQ_OPT_COUNT] = {o.panel,       o.schur,        o.schur_warps, o.schur_cluster,
                                   o.split,       o.backsub,      o.fused_aug,   o.panel_warps,
-                                  o.tail,        o.phase_prof,   o.async_status, o.graphs};
+                                  o.tail,        o.phase_prof,   o.async_status, o.graphs,
+                                  o.vlen};
     if (option < 0 || option >= CYQ_OPT_COUNT)
         return set_err(ctx, CYQ_INVALID_ARG, "unknown option");
     *value = v[option];

@@ -76,6 +76,7 @@ struct LaunchOpts {
     int fused_aug = 1;     // Newton-system assembly fused into the panel (0: assembly kernel)
     int panel_warps = 0;   // generic panel: warps per chain CTA (0 auto)
     int tail = 0;          // CYQ_TAIL_*: Schur tail (0 cr1 / 2 pcg: exact CR, 1 pcr)
+    int vlen = 4;          // FactorOptions::vlen: the pcr tail has min(P, vlen) blocks
     int phase_prof = 0;    // per-stage phase clocks of chain 0 (profiling aid)
     int async_status = 0;  // device calls return without a host sync (cyq_ctx_wait_status)
     int graphs = 1;        // repeated identical device calls replay a captured CUDA graph

@@ -191,10 +191,15 @@ __device__ __forceinline__ void matvec_upper(const double *M, const double *v, d
 //   K_i = K[i << l]
 // and elimination mm writes M' -> D[2mm << l], CY -> D[(2mm+1) << l],
 // K' -> K[2mm << l]: every slot is read and rewritten by one warp only.
+//   PCR tail (g.tail = T > 1 blocks, FactorOptions::tail = pcr):
+//   PLi[(lgT+1) T] lower, PU[lgT T], PY[lgT T] full   (persistent)
+//   PM[2 T] lower, PK[2 T] full                        (scratch, by level parity)
+// The CR levels then stop at crl = levels - lgT (T blocks left) and the
+// base factorization is replaced by the PCR levels.
 struct SFLayout {
-    long long Tt, Li, U, Y, Lb, D, Mb, K, total; // doubles
-    int XT, NL, NF, XP, levels;
-    __host__ __device__ static SFLayout make(int P, int nx) {
+    long long Tt, Li, U, Y, Lb, D, Mb, K, PLi, PU, PY, PM, PK, total; // doubles
+    int XT, NL, NF, XP, levels, T, lgT, crl;
+    __host__ __device__ static SFLayout make(int P, int nx, int tail = 1) {
         SFLayout s;
         s.XT = (nx + 7) / 8;
         s.NL = s.XT * (s.XT + 1) / 2;
@@ -214,12 +219,22 @@ struct SFLayout {
         s.D = o; o += P * tl;
         s.Mb = o; o += P * tl;
         s.K = o; o += P * tf;
+        s.T = tail > 1 ? tail : 1;
+        s.lgT = 0;
+        while ((1 << s.lgT) < s.T)
+            ++s.lgT;
+        s.crl = s.levels - s.lgT;
+        s.PLi = o; o += (s.T > 1 ? (s.lgT + 1) * s.T : 0) * tl;
+        s.PU = o; o += (long long)s.lgT * s.T * tf;
+        s.PY = o; o += (long long)s.lgT * s.T * tf;
+        s.PM = o; o += (s.T > 1 ? 2 * s.T : 0) * tl;
+        s.PK = o; o += (s.T > 1 ? 2 * s.T : 0) * tf;
         s.total = o;
         return s;
     }
 };
 
-size_t schur_fused_doubles(const Geo &g) { return (size_t)SFLayout::make(g.P, g.nx).total; }
+size_t schur_fused_doubles(const Geo &g) { return (size_t)SFLayout::make(g.P, g.nx, g.tail).total; }
 
 namespace {
 
@@ -255,7 +270,7 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
     };
     const int rq = lane >> 2, cq = 2 * (lane & 3), q2 = lane & 3;
     const int P = g.P, nu = g.nu, n = g.n, top = 8 * g.CT;
-    const SFLayout Lo = SFLayout::make(P, NX);
+    const SFLayout Lo = SFLayout::make(P, NX, g.tail);
     double *ws = a.schur + (size_t)b * Lo.total;
     double *scr = sm + (size_t)warp * NF * kTileElems; // per-warp transpose scratch
     // solve vectors: xs (P x XP) and bwd_neg (P x XP), the latter dead once
@@ -417,24 +432,28 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
         csync();
     }
 
+    // M_i of the level-l reduced system (see SFLayout)
+    auto m_at = [&](int l, int i, int ti, int tj) -> Frag {
+        if (l == 0)
+            return fadd(ldw(D + i * TL + T(ti, tj) * kTileElems, lane),
+                        ldw(Mb + ((i + 1) % P) * TL + T(ti, tj) * kTileElems, lane));
+        Frag f = ldw(D + (i << l) * TL + T(ti, tj) * kTileElems, lane);
+        if (i > 0)
+            f = fsub(f, ldw(D + ((i << l) - (1 << (l - 1))) * TL + T(ti, tj) * kTileElems, lane));
+        return f;
+    };
+    const int Tb = Lo.T, Lc = Lo.crl; // PCR tail blocks, CR levels before it
+    double *bt = cu;                  // PCR: L^{-1} x per tail block (T x XP, dead cu / cy)
+
     // ---- phase 2: CR levels (block_tridiag.cpp:126-238), in place ---------
     // With a right-hand side at hand the CR forward sweep
     // (block_tridiag.cpp:252-296) runs inside the levels on the register
     // tiles: x_k <- L^{-1} x_k, then U x_k / Y x_k go to the even blocks.
     if (a.do_factor) {
-        for (int l = 0, s = P; l < Lo.levels; ++l, s >>= 1) {
+        for (int l = 0, s = P; l < Lc; ++l, s >>= 1) {
             const int half = s / 2;
             const long long out0 = P - (P >> l);
-            const int hcy = l > 0 ? 1 << (l - 1) : 0;
-            auto m_tile = [&](int i, int ti, int tj) -> Frag {
-                if (l == 0)
-                    return fadd(ldw(D + i * TL + T(ti, tj) * kTileElems, lane),
-                                ldw(Mb + ((i + 1) % P) * TL + T(ti, tj) * kTileElems, lane));
-                Frag f = ldw(D + (i << l) * TL + T(ti, tj) * kTileElems, lane);
-                if (i > 0)
-                    f = fsub(f, ldw(D + ((i << l) - hcy) * TL + T(ti, tj) * kTileElems, lane));
-                return f;
-            };
+            auto m_tile = [&](int i, int ti, int tj) -> Frag { return m_at(l, i, ti, tj); };
             for (int mm = vwarp; mm < half; mm += VNW) {
                 const int k = 2 * mm + 1;
                 const bool has_y = k < s - 1;
@@ -549,47 +568,190 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
             }
             if (ph) ph[php++] = clock64();
         }
-        // ---- cr_factor_base (block_tridiag.cpp:173-197) --------------------
-        if (vwarp == 0) {
-            Frag Lt[NL];
-#pragma unroll
-            for (int i = 0; i < XT; ++i)
-#pragma unroll
-                for (int j = 0; j <= i; ++j)
-                    Lt[T(i, j)] = Lo.levels == 0
-                                      ? fadd(ldw(D + T(i, j) * kTileElems, lane),
-                                             ldw(Mb + T(i, j) * kTileElems, lane))
-                                      : ldw(D + T(i, j) * kTileElems, lane);
-            const double dfloor = 1e-14 * tiles::diag_absmax<XT>(Lt, NX, lane);
-            int pf = -1;
-            Frag Li[NL];
-            {
-                Frag Zd[XT], Ld[XT], Z[NF];
-                tiles::chol_inv<XT, NL>(Lt, Zd, Ld, NX, dfloor, lane, pf, scr);
-                tiles::blocked_inverse<XT, NL>(Lt, Zd, Ld, Li, Z);
-            }
-            if (pf >= 0)
-                my_fail = min(my_fail, fail_key(kKindCR, Lo.levels, 0, pf));
-#pragma unroll
-            for (int t = 0; t < NL; ++t)
-                st_frag(ws + Lo.Lb + t * kTileElems, lane, Li[t]);
-            if (fwd_fused) { // base solve x_0 <- L_b^{-T} L_b^{-1} x_0
-                double o[XT], o2[XT][2];
-                matvec_r<XT, kLower>(Li, xs, o, lane);
-                __syncwarp();
+        if (Tb == 1) {
+            // ---- cr_factor_base (block_tridiag.cpp:173-197) --------------------
+            if (vwarp == 0) {
+                Frag Lt[NL];
 #pragma unroll
                 for (int i = 0; i < XT; ++i)
-                    if (q2 == 0)
-                        xs[8 * i + rq] = o[i];
-                __syncwarp();
-                matvec_t<XT, false>(ws + Lo.Lb, xs, o2, lane);
-                __syncwarp();
 #pragma unroll
-                for (int j = 0; j < XT; ++j)
-                    if (rq == 0) {
-                        xs[8 * j + cq] = o2[j][0];
-                        xs[8 * j + cq + 1] = o2[j][1];
+                    for (int j = 0; j <= i; ++j)
+                        Lt[T(i, j)] = Lo.levels == 0
+                                          ? fadd(ldw(D + T(i, j) * kTileElems, lane),
+                                                 ldw(Mb + T(i, j) * kTileElems, lane))
+                                          : ldw(D + T(i, j) * kTileElems, lane);
+                const double dfloor = 1e-14 * tiles::diag_absmax<XT>(Lt, NX, lane);
+                int pf = -1;
+                Frag Li[NL];
+                {
+                    Frag Zd[XT], Ld[XT], Z[NF];
+                    tiles::chol_inv<XT, NL>(Lt, Zd, Ld, NX, dfloor, lane, pf, scr);
+                    tiles::blocked_inverse<XT, NL>(Lt, Zd, Ld, Li, Z);
+                }
+                if (pf >= 0)
+                    my_fail = min(my_fail, fail_key(kKindCR, Lo.levels, 0, pf));
+#pragma unroll
+                for (int t = 0; t < NL; ++t)
+                    st_frag(ws + Lo.Lb + t * kTileElems, lane, Li[t]);
+                if (fwd_fused) { // base solve x_0 <- L_b^{-T} L_b^{-1} x_0
+                    double o[XT], o2[XT][2];
+                    matvec_r<XT, kLower>(Li, xs, o, lane);
+                    __syncwarp();
+#pragma unroll
+                    for (int i = 0; i < XT; ++i)
+                        if (q2 == 0)
+                            xs[8 * i + rq] = o[i];
+                    __syncwarp();
+                    matvec_t<XT, false>(ws + Lo.Lb, xs, o2, lane);
+                    __syncwarp();
+#pragma unroll
+                    for (int j = 0; j < XT; ++j)
+                        if (rq == 0) {
+                            xs[8 * j + cq] = o2[j][0];
+                            xs[8 * j + cq + 1] = o2[j][1];
+                        }
+                }
+            }
+        } else {
+            // ---- PCR tail (block_tridiag.cpp:364-486, pcr_factor) on the T
+            // blocks left at level Lc: every level works on all T blocks;
+            // level pl (stride st = 2^pl) forms L_k^{-1}, Y_k = K_k L_k^{-T},
+            // U_k = K_{k-st}' L_k^{-T}, then M'_k = M_k - Y_{k-st} Y_{k-st}' -
+            // U_{k+st} U_{k+st}', K'_k = -Y_{k+st} U_{k+st}' (the wrapped
+            // couplings of the non-circular tail are zero and skipped); the
+            // last level factors every block. With a rhs the resolve
+            // (PCRFactor::resolve) runs inside the levels.
+            auto pm = [&](int pl, int k, int ti, int tj) -> Frag {
+                return pl == 0 ? m_at(Lc, k, ti, tj)
+                               : ldw(ws + Lo.PM + ((pl - 1) & 1) * Tb * TL + k * TL + T(ti, tj) * kTileElems,
+                                     lane);
+            };
+            auto pk = [&](int pl, int k) -> const double * {
+                return pl == 0 ? K + (size_t)(k << Lc) * TF : ws + Lo.PK + ((pl - 1) & 1) * Tb * TF + k * TF;
+            };
+            for (int pl = 0; pl <= Lo.lgT; ++pl) {
+                const int st = 1 << pl;
+                const bool fin = pl == Lo.lgT;
+                for (int k = vwarp; k < Tb; k += VNW) {
+                    Frag Lt[NL];
+#pragma unroll
+                    for (int i = 0; i < XT; ++i)
+#pragma unroll
+                        for (int j = 0; j <= i; ++j)
+                            Lt[T(i, j)] = pm(pl, k, i, j);
+                    const double dfloor = 1e-14 * tiles::diag_absmax<XT>(Lt, NX, lane);
+                    int pf = -1;
+                    Frag Li[NL];
+                    {
+                        Frag Zd[XT], Ld[XT], Z[NF];
+                        tiles::chol_inv<XT, NL>(Lt, Zd, Ld, NX, dfloor, lane, pf, scr);
+                        tiles::blocked_inverse<XT, NL>(Lt, Zd, Ld, Li, Z);
                     }
+                    if (pf >= 0)
+                        my_fail = min(my_fail, fail_key(kKindCR, Lc + pl, k, pf));
+                    double *Lio = ws + Lo.PLi + (size_t)(pl * Tb + k) * TL;
+#pragma unroll
+                    for (int t = 0; t < NL; ++t)
+                        st_frag(Lio + t * kTileElems, lane, Li[t]);
+                    double *xk = xs + (size_t)(k << Lc) * XP;
+                    if (fwd_fused) { // bt_k = L^{-1} x_k (final level: x_k <- L^{-T} L^{-1} x_k)
+                        double o[XT];
+                        matvec_r<XT, kLower>(Li, xk, o, lane);
+                        double *dst = fin ? xk : bt + (size_t)k * XP;
+                        __syncwarp();
+#pragma unroll
+                        for (int i = 0; i < XT; ++i)
+                            if (q2 == 0)
+                                dst[8 * i + rq] = o[i];
+                        __syncwarp();
+                        if (fin) {
+                            double o2[XT][2];
+                            matvec_t<XT, false>(Lio, xk, o2, lane);
+                            __syncwarp();
+#pragma unroll
+                            for (int j = 0; j < XT; ++j)
+                                if (rq == 0) {
+                                    xk[8 * j + cq] = o2[j][0];
+                                    xk[8 * j + cq + 1] = o2[j][1];
+                                }
+                            __syncwarp();
+                        }
+                    }
+                    if (fin)
+                        continue;
+                    // Y = K_k Linv', U = K_{k-st}' Linv'
+                    const double *Kk = pk(pl, k), *Kp = k >= st ? pk(pl, k - st) : nullptr;
+                    double *Uo = ws + Lo.PU + (size_t)(pl * Tb + k) * TF;
+                    double *Yo = ws + Lo.PY + (size_t)(pl * Tb + k) * TF;
+#pragma unroll
+                    for (int i = 0; i < XT; ++i) {
+                        Frag kp[XT], kk[XT];
+#pragma unroll
+                        for (int t = 0; t < XT; ++t) {
+                            kp[t] = Kp ? ldw_t(Kp + fidx(XT, t, i) * kTileElems, lane) : Frag{0.0, 0.0};
+                            kk[t] = ldw(Kk + fidx(XT, i, t) * kTileElems, lane);
+                        }
+#pragma unroll
+                        for (int j = 0; j < XT; ++j) {
+                            Frag u{0.0, 0.0}, y{0.0, 0.0};
+#pragma unroll
+                            for (int t = 0; t <= j; ++t) {
+                                tile_gemm_nt(u, kp[t], Li[T(j, t)]);
+                                tile_gemm_nt(y, kk[t], Li[T(j, t)]);
+                            }
+                            st_frag(Uo + (i * XT + j) * kTileElems, lane, u);
+                            st_frag(Yo + (i * XT + j) * kTileElems, lane, y);
+                        }
+                    }
+                }
+                csync();
+                if (fin)
+                    break;
+                for (int k = vwarp; k < Tb; k += VNW) {
+                    const bool lo = k >= st, hi = k + st < Tb;
+                    const double *Yl = ws + Lo.PY + (size_t)(pl * Tb + k - st) * TF;
+                    const double *Uh = ws + Lo.PU + (size_t)(pl * Tb + k + st) * TF;
+                    const double *Yh = ws + Lo.PY + (size_t)(pl * Tb + k + st) * TF;
+                    double *M2o = ws + Lo.PM + (pl & 1) * Tb * TL + k * TL;
+                    double *K2o = ws + Lo.PK + (pl & 1) * Tb * TF + k * TF;
+#pragma unroll
+                    for (int i = 0; i < XT; ++i)
+#pragma unroll
+                        for (int j = 0; j < XT; ++j) {
+                            Frag yy{0.0, 0.0}, uu{0.0, 0.0}, yu{0.0, 0.0};
+#pragma unroll
+                            for (int t = 0; t < XT; ++t) {
+                                if (j <= i && lo)
+                                    tile_gemm_nt(yy, ldw(Yl + fidx(XT, i, t) * kTileElems, lane),
+                                                 ldw(Yl + fidx(XT, j, t) * kTileElems, lane));
+                                if (hi) {
+                                    const Frag ui = ldw(Uh + fidx(XT, i, t) * kTileElems, lane);
+                                    if (j <= i)
+                                        tile_gemm_nt(uu, ui, ldw(Uh + fidx(XT, j, t) * kTileElems, lane));
+                                    tile_gemm_nt_sub(yu, ldw(Yh + fidx(XT, i, t) * kTileElems, lane),
+                                                     ldw(Uh + fidx(XT, j, t) * kTileElems, lane));
+                                }
+                            }
+                            if (j <= i)
+                                st_frag(M2o + T(i, j) * kTileElems, lane, fsub(fsub(pm(pl, k, i, j), yy), uu));
+                            st_frag(K2o + fidx(XT, i, j) * kTileElems, lane, yu);
+                        }
+                    if (fwd_fused) { // x_k -= Y_{k-st} bt_{k-st} + U_{k+st} bt_{k+st}
+                        double o1[XT], o2[XT];
+                        if (lo)
+                            matvec<XT, true>(Yl, bt + (size_t)(k - st) * XP, o1, lane);
+                        if (hi)
+                            matvec<XT, true>(Uh, bt + (size_t)(k + st) * XP, o2, lane);
+                        double *xk = xs + (size_t)(k << Lc) * XP;
+                        __syncwarp();
+#pragma unroll
+                        for (int i = 0; i < XT; ++i)
+                            if (q2 == 0)
+                                xk[8 * i + rq] -= (lo ? o1[i] : 0.0) + (hi ? o2[i] : 0.0);
+                        __syncwarp();
+                    }
+                }
+                csync();
             }
         }
         csync();
@@ -600,7 +762,7 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
     if (a.do_solve) {
         if (!fwd_fused) {
             // CRFactor::forward (block_tridiag.cpp:252-296)
-            for (int l = 0, s = P; l < Lo.levels; ++l, s >>= 1) {
+            for (int l = 0, s = P; l < Lc; ++l, s >>= 1) {
                 const int half = s / 2, stride = P / s;
                 const long long o0 = P - (P >> l);
                 for (int mm = vwarp; mm < half; mm += VNW) { // x_k <- L^{-1} x_k
@@ -630,7 +792,58 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                 }
                 csync();
             }
-            if (vwarp == 0) { // base: x_0 <- L_b^{-T} L_b^{-1} x_0
+            if (Tb > 1) { // PCRFactor::resolve (block_tridiag.cpp:457-486) on the tail
+                for (int pl = 0; pl <= Lo.lgT; ++pl) {
+                    const int st = 1 << pl;
+                    const bool fin = pl == Lo.lgT;
+                    for (int k = vwarp; k < Tb; k += VNW) { // bt_k = L^{-1} x_k
+                        double *xk = xs + (size_t)(k << Lc) * XP;
+                        const double *Lio = ws + Lo.PLi + (size_t)(pl * Tb + k) * TL;
+                        double o[XT];
+                        matvec<XT, false>(Lio, xk, o, lane);
+                        double *dst = fin ? xk : bt + (size_t)k * XP;
+                        __syncwarp();
+#pragma unroll
+                        for (int i = 0; i < XT; ++i)
+                            if (q2 == 0)
+                                dst[8 * i + rq] = o[i];
+                        __syncwarp();
+                        if (fin) { // x_k <- L^{-T} L^{-1} x_k
+                            double o2[XT][2];
+                            matvec_t<XT, false>(Lio, xk, o2, lane);
+                            __syncwarp();
+#pragma unroll
+                            for (int j = 0; j < XT; ++j)
+                                if (rq == 0) {
+                                    xk[8 * j + cq] = o2[j][0];
+                                    xk[8 * j + cq + 1] = o2[j][1];
+                                }
+                            __syncwarp();
+                        }
+                    }
+                    csync();
+                    if (fin)
+                        break;
+                    for (int k = vwarp; k < Tb; k += VNW) { // x_k -= Y_{k-st} bt_{k-st} + U_{k+st} bt_{k+st}
+                        const bool lo = k >= st, hi = k + st < Tb;
+                        double o1[XT], o2[XT];
+                        if (lo)
+                            matvec<XT, true>(ws + Lo.PY + (size_t)(pl * Tb + k - st) * TF,
+                                             bt + (size_t)(k - st) * XP, o1, lane);
+                        if (hi)
+                            matvec<XT, true>(ws + Lo.PU + (size_t)(pl * Tb + k + st) * TF,
+                                             bt + (size_t)(k + st) * XP, o2, lane);
+                        double *xk = xs + (size_t)(k << Lc) * XP;
+                        __syncwarp();
+#pragma unroll
+                        for (int i = 0; i < XT; ++i)
+                            if (q2 == 0)
+                                xk[8 * i + rq] -= (lo ? o1[i] : 0.0) + (hi ? o2[i] : 0.0);
+                        __syncwarp();
+                    }
+                    csync();
+                }
+            } else if (vwarp == 0) { // base: x_0 <- L_b^{-T} L_b^{-1} x_0
                 double o[XT], o2[XT][2];
                 matvec<XT, false>(ws + Lo.Lb, xs, o, lane);
                 __syncwarp();
@@ -652,7 +865,7 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
         }
         if (ph) ph[php++] = clock64();
         // CRFactor::backward (block_tridiag.cpp:298-333)
-        for (int l = Lo.levels - 1; l >= 0; --l) {
+        for (int l = Lc - 1; l >= 0; --l) {
             const int sl = P >> l, half = sl / 2, stride = P / sl;
             const long long o0 = P - (P >> l);
             for (int mm = vwarp; mm < half; mm += VNW) {

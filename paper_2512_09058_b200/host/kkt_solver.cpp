@@ -46,11 +46,26 @@ void check_opts(const FactorOptions &o) {
         throw std::invalid_argument("P must be a power of two");
     if (!pow2(o.vlen))
         throw std::invalid_argument("vlen must be a power of two");
-    // Tail::pcr / Tail::pcg (kkt_factor.cpp:227-247) are CPU strategies for
-    // the last min(P, vlen) Schur blocks; the GPU's fused cyclic reduction
-    // solves the whole tree exactly, within both tails' accuracy contracts
     if (o.tail != Tail::cr1 && o.tail != Tail::pcr && o.tail != Tail::pcg)
         throw std::invalid_argument("unknown tail");
+}
+
+// The context is shared by the host threads of the process: one call at a
+// time (its options and grow-only buffers are per context).
+std::mutex &call_mutex() {
+    static std::mutex m;
+    return m;
+}
+
+// FactorOptions::tail / vlen as context options (kkt_factor.cpp:214-247):
+// Tail::pcr solves the last min(P, vlen) Schur blocks by parallel cyclic
+// reduction on the GPU; Tail::pcg is served by exact cyclic reduction
+// (within its 1e-8 contract, test_kkt.cpp:157-161).
+void apply_opts(const FactorOptions &o) {
+    const int64_t tail = o.tail == Tail::pcr ? CYQ_TAIL_PCR : o.tail == Tail::pcg ? CYQ_TAIL_PCG : CYQ_TAIL_CR1;
+    if (cyq_ctx_set_option(ctx(), CYQ_OPT_TAIL, tail) != CYQ_OK ||
+        cyq_ctx_set_option(ctx(), CYQ_OPT_VLEN, o.vlen) != CYQ_OK)
+        throw std::invalid_argument(cyq_ctx_last_error(ctx()));
 }
 
 void check_mat(const Mat &m, index_t r, index_t c, const char *what) {
@@ -256,6 +271,8 @@ Factor factor_batch(const std::vector<EqOCP> &ps, const FactorOptions &opts) {
     const cyq_dims d = fl.dims(opts.P);
     const cyq_ocp_batch pb = fl.view();
     std::vector<cyq_status> st(z(fl.batch));
+    std::lock_guard<std::mutex> lk(call_mutex());
+    apply_opts(opts);
     const int rc = cyq_factor_batch(ctx(), &d, &pb, CYQ_MEM_HOST, &f.impl->f, st.data());
     if (rc != CYQ_OK)
         throw_status(rc, st);
@@ -299,6 +316,7 @@ std::vector<EqSolution> solve_batch(const Factor &f, const std::vector<EqOCP> &p
     const cyq_rhs_batch rb{ru.data(), qx.data(), fd.data()};
     FlatSol sol(N, nx, nu, B);
     const cyq_sol_batch sb = sol.view();
+    std::lock_guard<std::mutex> lk(call_mutex());
     const int rc = cyq_solve_batch(ctx(), f.impl->f, &pb, &rb, &sb, CYQ_MEM_HOST);
     if (rc != CYQ_OK)
         throw_status(rc, {});
@@ -324,6 +342,8 @@ std::vector<EqSolution> solve_problem_batch(const std::vector<EqOCP> &ps, const 
     FlatSol sol(fl.N, fl.nx, fl.nu, fl.batch);
     const cyq_sol_batch sb = sol.view();
     std::vector<cyq_status> st(z(fl.batch));
+    std::lock_guard<std::mutex> lk(call_mutex());
+    apply_opts(opts);
     const int rc = cyq_solve_problem_batch(ctx(), &d, &pb, &sb, st.data(), CYQ_MEM_HOST);
     if (status)
         *status = to_status(st);

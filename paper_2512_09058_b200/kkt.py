@@ -84,6 +84,7 @@ class Context:
         self.device = device
         self._bound = False  # set_stream() called: keep the caller's stream
         self._cur = None
+        self._tail = ("cr1", 4)  # FactorOptions tail / vlen last applied
 
     def follow_torch(self, arrays):
         """Stream ordering with torch: unless the caller bound a stream with
@@ -225,10 +226,18 @@ def _check_opts(opts: FactorOptions):
         raise ValueError("vlen must be a power of two")
     if opts.tail not in ("cr1", "pcr", "pcg"):
         raise ValueError("tail must be one of cr1, pcr, pcg")
-    # pcr / pcg (kkt_factor.cpp:227-247) are CPU strategies for the last
-    # min(P, vlen) Schur blocks; the GPU's fused cyclic reduction solves the
-    # whole tree exactly, which meets both tails' accuracy contracts
-    # (test_kkt.cpp:152-161: pcr within 1e-10 of cr1, pcg within 1e-8)
+
+
+def _apply_tail(ctx, opts: FactorOptions):
+    """FactorOptions::tail / vlen (kkt_factor.cpp:214-247) as context options:
+    tail = pcr solves the last min(P, vlen) Schur blocks by parallel cyclic
+    reduction on the GPU; pcg is served by exact cyclic reduction (within
+    its 1e-8 contract, test_kkt.cpp:157-161)."""
+    key = (opts.tail, int(opts.vlen))
+    if ctx._tail != key:
+        ctx.set_option("tail", opts.tail)
+        ctx.set_option("vlen", int(opts.vlen))
+        ctx._tail = key
 
 
 def _context(ctx, arrays) -> "Context":
@@ -281,6 +290,7 @@ def solve_problem(p, opts: FactorOptions, ctx: Context | None = None, out=None,
     _check_opts(opts)
     arrs = [getattr(p, k) for k in OCP_FIELDS] + ([] if out is None else [getattr(out, k) for k in SOL_FIELDS])
     ctx = _context(ctx, arrs)
+    _apply_tail(ctx, opts)
     arrs = arrs[:len(OCP_FIELDS)]
     mem = _mem(arrs)
     ctx.follow_torch(arrs)
@@ -334,6 +344,7 @@ def factor(p, opts: FactorOptions, ctx: Context | None = None) -> Factor:
     """kkt::factor for every instance of the batch."""
     _check_opts(opts)
     ctx = _context(ctx, [getattr(p, k) for k in OCP_FIELDS])
+    _apply_tail(ctx, opts)
     mem = _mem([getattr(p, k) for k in OCP_FIELDS])
     ctx.follow_torch([getattr(p, k) for k in OCP_FIELDS])
     h = C.c_void_p()
@@ -457,6 +468,7 @@ class Prepared:
         if not all(_is_torch(a) for a in arrs):
             raise ValueError("Prepared calls take CUDA torch tensors")
         ctx = _context(ctx, arrs + ([] if out is None else [getattr(out, k) for k in SOL_FIELDS]))
+        _apply_tail(ctx, opts)
         ctx.follow_torch(arrs)
         sol = out if out is not None else _alloc_sol(p, True)
         dims, ocp = _dims(p, opts.P), _ocp_struct(p)
@@ -475,6 +487,7 @@ class Prepared:
         if not all(_is_torch(a) for a in arrs):
             raise ValueError("Prepared calls take CUDA torch tensors")
         ctx = _context(ctx, arrs)
+        _apply_tail(ctx, opts)
         ctx.follow_torch(arrs)
         sol = out if out is not None else _alloc_sol(p, True)
         dims, ocp = _dims(p, opts.P), _ocp_struct(p)
@@ -508,6 +521,7 @@ def solve_newton(p, D, Cm, sigma, opts: FactorOptions, gamma_inv: float = 0.0, o
     other shapes run the assembly kernel first. CUDA torch tensors only."""
     _check_opts(opts)
     ctx = _context(ctx, [getattr(p, k) for k in OCP_FIELDS] + [D, Cm, sigma])
+    _apply_tail(ctx, opts)
     for a in [getattr(p, k) for k in OCP_FIELDS] + [D, Cm, sigma]:
         if not _is_torch(a):
             raise ValueError("solve_newton takes CUDA torch tensors")

@@ -31,7 +31,8 @@ def oracle():
 def test_golden_reference_outputs(name):
     p, P, ref_sol, z = golden_util.load(name)
     tail = str(z["tail"]) if "tail" in z else "cr1"  # pcr / pcg fixtures: reference tails
-    sol = kkt.solve_problem(p, kkt.FactorOptions(P=P, tail=tail))
+    vlen = int(z["vlen"]) if "vlen" in z else 4
+    sol = kkt.solve_problem(p, kkt.FactorOptions(P=P, tail=tail, vlen=vlen))
     err = rel_error(sol, ref_sol)
     assert err.max() <= REL_TOL, f"rel err {err.max():.3e}"
     res = kkt_residual(p, EqRhsBatch.of_problem(p), sol).max(axis=1)
