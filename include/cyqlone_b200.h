@@ -115,6 +115,23 @@ int cyq_factor_destroy(cyq_factor *factor);
 int cyq_factor_materialize(const cyq_factor *factor, int64_t inst, double *LH,
                            double *LB, double *Acl, double *LA);
 
+/* The Schur-side factor blocks of instance `inst` in the reference's Factor
+ * member shapes (kkt_solver.hpp:84-97), dense row-major per column / block:
+ * T[P][nx][nx] (= L_Q^{-T} of the column's last stage, upper), Mfwd, Mbwd,
+ * W (= T LA') [P][nx][nx] (sc_Mfwd / sc_Mbwd / sc_W), the assembled Schur
+ * complement schur_diag[P][nx][nx], schur_sub[P][nx][nx] (block (k+1, k);
+ * the circular [P-1] is zero), and the CR factor (blocktri::CRFactor,
+ * block_tridiag.hpp:56-79): level l, slot mm at index P - (P >> l) + mm of
+ * cr_L / cr_U / cr_Y [P-1][nx][nx] (L = chol of the eliminated block,
+ * U = K_{k-1}' L^{-T}, Y = K_k L^{-T}), cr_Lbase[nx][nx]. Any pointer may
+ * be NULL. CYQ_INVALID_ARG for factors whose Schur path (the per-level /
+ * scalar kernels of unusual shapes) keeps no persistent blocks. */
+int cyq_factor_materialize_schur(const cyq_factor *factor, int64_t inst, double *T,
+                                 double *Mfwd, double *Mbwd, double *W,
+                                 double *schur_diag, double *schur_sub,
+                                 double *cr_L, double *cr_U, double *cr_Y,
+                                 double *cr_Lbase);
+
 /* Newton-system assembly of the QPALM inner loop (qpalm::assemble_newton,
  * qpalm.cpp:167-225, equality part; BASELINE config 4): for every instance
  * and stage j

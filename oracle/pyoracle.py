@@ -197,8 +197,18 @@ class RefOracle(_Base):
                                 C.byref(Sol(*[_p(a) for a in sol.arrays()])), st)
         return sol, rc, list(st)
 
-    def factor_blocks(self, p, P, vlen=4):
-        return _factor_blocks(self.lib.ref_factor_export, p, P, vlen)
+    def factor_blocks(self, p, P, vlen=4, cr=False):
+        out, rc, st = _factor_blocks(self.lib.ref_factor_export, p, P, vlen)
+        if cr and rc == 0:  # Factor::schur_cr (instance 0)
+            nx = p.nx
+            for k in ("cr_L", "cr_U", "cr_Y"):
+                out[k] = np.zeros((max(P - 1, 0), nx, nx))
+            out["cr_Lbase"] = np.zeros((nx, nx))
+            st2 = Status()
+            rc = self.lib.ref_factor_export_cr(C.byref(_dims(p, P)), C.byref(_ocp(p)), i64(vlen),
+                                               *[_p(out[k]) for k in ("cr_L", "cr_U", "cr_Y", "cr_Lbase")],
+                                               C.byref(st2))
+        return out, rc, st
 
     def random_eq_ocp(self, N, nx, nu, seed, conditioning=10.0):
         from paper_2512_09058_b200.ocp import EqOCPBatch

@@ -280,6 +280,38 @@ int ref_factor_export(const oc_dims *d, const oc_ocp *p, int64_t vlen,
     });
 }
 
+// The CR factor of the Schur complement (Factor::schur_cr,
+// block_tridiag.hpp:56-79) of instance 0: level l, slot mm at index
+// P - (P >> l) + mm of L / U / Y [P-1][nx][nx] (dense row-major), L_base.
+int ref_factor_export_cr(const oc_dims *d, const oc_ocp *p, int64_t vlen, double *L, double *U,
+                         double *Y, double *Lbase, oc_status *st) {
+    return guarded(st, 0, [&] {
+        EqOCP pr = make_ocp(d, p, 0);
+        Factor f = kkt::factor(pr, opts_of(d, vlen));
+        const index_t nx = d->nx, P = d->P;
+        const auto &cr = f.schur_cr;
+        for (index_t l = 0; l + 1 < cr.n_levels; ++l) {
+            const index_t half = (P >> l) / 2, o0 = P - (P >> l);
+            for (index_t mm = 0; mm < half; ++mm) {
+                const auto lu = static_cast<std::size_t>(l);
+                double *lo = L + (o0 + mm) * nx * nx;
+                dense_of(cr.L[lu], mm, lo);
+                for (index_t r = 0; r < nx; ++r)
+                    for (index_t k = r + 1; k < nx; ++k)
+                        lo[r * nx + k] = 0;
+                dense_of(cr.U[lu], mm, U + (o0 + mm) * nx * nx);
+                dense_of(cr.Y[lu], mm, Y + (o0 + mm) * nx * nx);
+            }
+        }
+        if (cr.L_base.batch() > 0) {
+            dense_of(cr.L_base, 0, Lbase);
+            for (index_t r = 0; r < nx; ++r)
+                for (index_t k = r + 1; k < nx; ++k)
+                    Lbase[r * nx + k] = 0;
+        }
+    });
+}
+
 void ref_kkt_residual(const oc_dims *d, const oc_ocp *p, const oc_rhs *rhs,
                       const oc_sol *s, double *out) {
     for (index_t b = 0; b < d->batch; ++b) {

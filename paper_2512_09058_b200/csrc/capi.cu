@@ -54,6 +54,7 @@ struct cyq_ctx {
     std::vector<unsigned long long> gkey_seen, gkey;
     cudaGraphExec_t gexec = nullptr;
     cudaStream_t cap_stream = nullptr;
+    int schur_path = -1; // Schur kernel of the last pipeline (see cyq_factor)
 };
 
 struct cyq_factor {
@@ -66,6 +67,7 @@ struct cyq_factor {
     ProbView prob{}; // device copy of the problem (host-memory factor calls)
     bool owns_prob = false;
     LaunchOpts opts{}; // kernel selection at factor time (the solve reads its layouts)
+    int schur_path = -1; // Schur kernel that factored it: 0 fused, 1 big, 2 per-level tiles, 3 scalar
 };
 
 namespace {
@@ -309,9 +311,14 @@ struct Timed {
 // the scalar kernel, or no specialisation serves the shape.
 int launch_schur(cyq_ctx *ctx, const Geo &g, const SchurArgs &sa, const LaunchOpts &o) {
     Timed t(ctx, 1);
-    if (o.schur == 0 && (launch_schur_fused(g, ctx->stream, sa, o) || launch_schur_big(g, ctx->stream, sa))) {
+    if (o.schur == 0 && launch_schur_fused(g, ctx->stream, sa, o)) {
         t.kernels = 1; // one fused kernel per batch
+        ctx->schur_path = 0;
+    } else if (o.schur == 0 && launch_schur_big(g, ctx->stream, sa)) {
+        t.kernels = 1;
+        ctx->schur_path = 1;
     } else if (sa.do_factor && o.schur != 2 && launch_schur_tiles(g, ctx->stream, sa)) {
+        ctx->schur_path = 2;
         // DMMA-tile factorization levels, then the scalar kernel's solve
         t.kernels = 2 + SchurLayout::make(g.P, g.nx).levels + (sa.do_solve ? 1 : 0);
         if (sa.do_solve) {
@@ -323,6 +330,7 @@ int launch_schur(cyq_ctx *ctx, const Geo &g, const SchurArgs &sa, const LaunchOp
             schur_cr_kernel<<<g.batch, 32 * nw, schur_smem_for(g, nw), ctx->stream>>>(sv);
         }
     } else if (sa.do_factor) {
+        ctx->schur_path = 3;
         if (schur_smem_bytes(g) > kMaxDynSmem)
             return smem_too_large(ctx, "Schur/CR (P x nx)", schur_smem_bytes(g));
         schur_cr_kernel<<<g.batch, 32 * schur_warps(g), schur_smem_bytes(g), ctx->stream>>>(sa);
@@ -940,6 +948,7 @@ int cyq_factor_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_batch *pr
         }
     }
     rc = launch_pipeline(ctx, g, f->prob, f->ws, nullptr, false);
+    f->schur_path = ctx->schur_path;
     if (rc == CYQ_OK)
         rc = decode_status(ctx, g, f->ws.fail, status);
     *out = f;
@@ -1115,6 +1124,132 @@ int cyq_ctx_get_option(cyq_ctx *ctx, int option, int64_t *value) {
     if (option < 0 || option >= CYQ_OPT_COUNT)
         return set_err(ctx, CYQ_INVALID_ARG, "unknown option");
     *value = v[option];
+    return CYQ_OK;
+}
+
+int cyq_factor_materialize_schur(const cyq_factor *f, int64_t inst, double *T, double *Mfwd, double *Mbwd,
+                                 double *W, double *schur_diag, double *schur_sub, double *cr_L,
+                                 double *cr_U, double *cr_Y, double *cr_Lbase) {
+    if (!f || inst < 0 || inst >= f->g.batch)
+        return set_err(nullptr, CYQ_INVALID_ARG, "bad factor / instance");
+    cyq_ctx *ctx = f->ctx;
+    const Geo &g = f->g;
+    SchurBlocks L{};
+    const bool ok = f->schur_path == 0 ? schur_fused_blocks(g, L) : f->schur_path == 1 && schur_big_blocks(g, L);
+    if (!ok)
+        return set_err(ctx, CYQ_INVALID_ARG,
+                       "materialize_schur: the factor's Schur path (per-level / scalar kernels) keeps no "
+                       "persistent Schur blocks");
+    const int P = g.P, nx = g.nx, XT = (nx + 7) / 8, n = g.n, nu = g.nu, top = 8 * g.CT;
+    const size_t NF = (size_t)XT * XT, NL = (size_t)XT * (XT + 1) / 2;
+    const size_t TF = 64 * NF, TLb = 64 * (L.full ? NF : NL);
+    CU(cudaSetDevice(ctx->device));
+    std::vector<double> ws((size_t)L.total), tr((size_t)P * g.NTT * kTileElems),
+        fac((size_t)P * g.NPT * kTileElems);
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaMemcpy(ws.data(), f->ws.schur + (size_t)inst * L.total, ws.size() * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(tr.data(), f->ws.trail + (size_t)inst * P * g.NTT * kTileElems, tr.size() * 8,
+                  cudaMemcpyDeviceToHost));
+    for (int c = 0; c < P; ++c) // the last stage's pivot tiles of every column (L_Q, LA)
+        CU(cudaMemcpy(fac.data() + (size_t)c * g.NPT * kTileElems,
+                      f->ws.fac + (((size_t)inst * P + c) * n + (n - 1)) * g.NPT * kTileElems,
+                      (size_t)g.NPT * kTileElems * 8, cudaMemcpyDeviceToHost));
+    // element (r, k) of a tile-ordered block at `base`
+    auto lower = [&](const double *base, int r, int k) {
+        if (L.full)
+            return base[((r / 8) * XT + k / 8) * 64 + (r % 8) * 8 + k % 8];
+        return k <= r ? base[(tri_index(r / 8, k / 8)) * 64 + (r % 8) * 8 + k % 8] : 0.0;
+    };
+    auto full = [&](const double *base, int r, int k) { return base[((r / 8) * XT + k / 8) * 64 + (r % 8) * 8 + k % 8]; };
+    auto sym = [&](const double *base, int r, int k) { return L.full ? full(base, r, k) : lower(base, std::max(r, k), std::min(r, k)); };
+    auto Tel = [&](int c, int r, int k) { // T_c = L_Q^{-T} (upper)
+        const double *b = ws.data() + L.Tt + c * TLb;
+        if (L.tt_is_inverse)
+            return full(b, k, r);
+        return k >= r ? b[(tri_index(k / 8, r / 8)) * 64 + (r % 8) * 8 + k % 8] : 0.0;
+    };
+    auto LAel = [&](int c, int r, int k) { // LA_c = ALQ of the last stage
+        const int ti = (top + r) / 8, tj = (nu + k) / 8;
+        const int t = g.CT * (g.CT + 1) / 2 + (ti - g.CT) * g.CT + tj;
+        return fac[(size_t)c * g.NPT * kTileElems + t * 64 + ((top + r) % 8) * 8 + (nu + k) % 8];
+    };
+    auto Mfel = [&](int c, int r, int k) { // Mfwd_c = -(trailing coupling block)
+        const int rr = std::max(r, k), kk = std::min(r, k);
+        return -tr[((size_t)c * g.NTT + tri_index(rr / 8, kk / 8)) * 64 + (rr % 8) * 8 + kk % 8];
+    };
+    const size_t nn = (size_t)nx * nx;
+    std::vector<double> Wv((size_t)P * nn), Mf((size_t)P * nn), Mb((size_t)P * nn);
+    for (int c = 0; c < P; ++c)
+        for (int r = 0; r < nx; ++r)
+            for (int k = 0; k < nx; ++k) {
+                double w = 0; // W_c = T_c LA_c'
+                for (int m = 0; m < nx; ++m)
+                    w += Tel(c, r, m) * LAel(c, k, m);
+                Wv[c * nn + r * nx + k] = w;
+                Mf[c * nn + r * nx + k] = Mfel(c, r, k);
+                Mb[c * nn + r * nx + k] = sym(ws.data() + L.Mb + c * TLb, r, k);
+                if (T)
+                    T[c * nn + r * nx + k] = Tel(c, r, k);
+            }
+    if (W)
+        memcpy(W, Wv.data(), Wv.size() * 8);
+    if (Mfwd)
+        memcpy(Mfwd, Mf.data(), Mf.size() * 8);
+    if (Mbwd)
+        memcpy(Mbwd, Mb.data(), Mb.size() * 8);
+    // assemble_schur (kkt_factor.cpp:194-212): diag[c] = Mfwd_c + Mbwd_{c+1},
+    // subdiag[c-1] = -W_c' (block (c, c-1)), subdiag[P-1] = 0
+    for (int c = 0; c < P; ++c)
+        for (size_t e = 0; e < nn; ++e) {
+            if (schur_diag)
+                schur_diag[c * nn + e] = Mf[c * nn + e] + Mb[((c + 1) % P) * nn + e];
+            if (schur_sub) {
+                const int r = (int)(e / nx), k = (int)(e % nx);
+                schur_sub[c * nn + e] = c + 1 < P ? -Wv[(c + 1) * nn + k * nx + r] : 0.0;
+            }
+        }
+    // CR levels: L (from the stored L^{-1}), U, Y per level slot; L_base
+    auto inv_lower = [&](const double *Li, double *out) { // out = (Li)^{-1}, Li lower nx x nx
+        for (int j = 0; j < nx; ++j)
+            for (int i = 0; i < nx; ++i) {
+                if (i < j) {
+                    out[i * nx + j] = 0.0;
+                    continue;
+                }
+                double s = i == j ? 1.0 : 0.0;
+                for (int m = j; m < i; ++m)
+                    s -= Li[i * nx + m] * out[m * nx + j];
+                out[i * nx + j] = s / Li[i * nx + i];
+            }
+    };
+    std::vector<double> tmp(nn);
+    for (int l = 0; l < L.cr_levels; ++l) {
+        const int half = (P >> l) / 2;
+        const long long o0 = P - (P >> l);
+        for (int mm = 0; mm < half; ++mm) {
+            const size_t slot = (size_t)(o0 + mm);
+            for (int r = 0; r < nx; ++r)
+                for (int k = 0; k < nx; ++k) {
+                    tmp[r * nx + k] = lower(ws.data() + L.Li + slot * TLb, r, k);
+                    if (cr_U)
+                        cr_U[slot * nn + r * nx + k] = full(ws.data() + L.U + slot * TF, r, k);
+                    if (cr_Y)
+                        cr_Y[slot * nn + r * nx + k] = full(ws.data() + L.Y + slot * TF, r, k);
+                }
+            if (cr_L)
+                inv_lower(tmp.data(), cr_L + slot * nn);
+        }
+    }
+    if (cr_Lbase) {
+        if (g.tail <= 1) {
+            for (int r = 0; r < nx; ++r)
+                for (int k = 0; k < nx; ++k)
+                    tmp[r * nx + k] = lower(ws.data() + L.Lb, r, k);
+            inv_lower(tmp.data(), cr_Lbase);
+        } else {
+            memset(cr_Lbase, 0, nn * 8); // PCR tail: no single base block
+        }
+    }
     return CYQ_OK;
 }
 

@@ -207,6 +207,19 @@ __host__ __device__ size_t forward_smem_per_warp(const Geo &g);
 __global__ void schur_cr_kernel(SchurArgs a);
 __global__ void backsub_kernel(BacksubArgs a);
 
+// Where the Schur-side factor blocks of one instance live in its workspace
+// slice (doubles), for cyq_factor_materialize_schur: 8x8-tile-ordered
+// blocks, `full` = XT x XT tiles (else lower tiles i(i+1)/2 + j, and T_c as
+// upper tiles at slot T(j, i)); tt_is_inverse: the slot holds L_Q^{-1}
+// (T = its transpose) instead of T. Li / Lb are L^{-1} of the CR pivots.
+struct SchurBlocks {
+    long long Tt, Li, U, Y, Lb, Mb, total;
+    bool full, tt_is_inverse;
+    int cr_levels; // CR levels stored (below a PCR tail)
+};
+bool schur_fused_blocks(const Geo &g, SchurBlocks &out);
+bool schur_big_blocks(const Geo &g, SchurBlocks &out);
+
 size_t riccati_smem_bytes(const Geo &g);
 // context helpers for entry points outside capi.cu: selects the context's
 // device, returns its stream

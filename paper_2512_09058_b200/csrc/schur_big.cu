@@ -327,6 +327,14 @@ template <int NX> bool launch_sb(const Geo &g, cudaStream_t st, const SchurArgs 
 
 } // namespace
 
+bool schur_big_blocks(const Geo &g, SchurBlocks &out) {
+    if (g.nx % 8 != 0)
+        return false;
+    const SBLayout L = SBLayout::make(g.P, g.nx);
+    out = SchurBlocks{L.Tt, L.Li, L.U, L.Y, L.Lb, L.Mb, L.total, true, true, L.levels};
+    return true;
+}
+
 size_t schur_big_doubles(const Geo &g) {
     return (g.nx % 8 == 0) ? (size_t)SBLayout::make(g.P, g.nx).total : 0;
 }

@@ -236,6 +236,12 @@ struct SFLayout {
 
 size_t schur_fused_doubles(const Geo &g) { return (size_t)SFLayout::make(g.P, g.nx, g.tail).total; }
 
+bool schur_fused_blocks(const Geo &g, SchurBlocks &out) {
+    const SFLayout L = SFLayout::make(g.P, g.nx, g.tail);
+    out = SchurBlocks{L.Tt, L.Li, L.U, L.Y, L.Lb, L.Mb, L.total, false, false, L.crl};
+    return true;
+}
+
 namespace {
 
 template <int XP> __host__ __device__ constexpr size_t sf_smem_doubles(int NW, int NF, int P) {

@@ -318,7 +318,12 @@ class Factor:
         P = opts.P
         self.n_per = (P * ((self.N + P - 1) // P)) // P
 
-    def materialize(self, inst: int = 0):
+    def materialize(self, inst: int = 0, schur: bool = True):
+        """Host copies of the reference's public Factor members for instance
+        `inst` (kkt_solver.hpp:76-97): LH, LB, Acl (n, P, ...), LA, T, Mfwd,
+        Mbwd, W (P, nx, nx), schur_diag / schur_sub (the assembled block
+        tridiagonal Schur complement) and the CR factor cr_L / cr_U / cr_Y
+        (P-1, nx, nx; level l, slot mm at P - (P >> l) + mm) and cr_Lbase."""
         P, n, nx, nu = self.opts.P, self.n_per, self.nx, self.nu
         nux = nx + nu
         LH = np.zeros((n, P, nux, nux))
@@ -329,7 +334,20 @@ class Factor:
                                                                  for a in (LH, LB, Acl, LA)])
         if rc:
             raise CudaError(self.ctx.last_error())
-        return {"LH": LH, "LB": LB, "Acl": Acl, "LA": LA}
+        out = {"LH": LH, "LB": LB, "Acl": Acl, "LA": LA}
+        if schur:
+            names = ("T", "Mfwd", "Mbwd", "W", "schur_diag", "schur_sub", "cr_L", "cr_U", "cr_Y")
+            arr = {k: np.zeros((P if i < 6 else max(P - 1, 0), nx, nx)) for i, k in enumerate(names)}
+            arr["cr_Lbase"] = np.zeros((nx, nx))
+            rc = self.ctx.lib.cyq_factor_materialize_schur(
+                self.h, inst, *[C.c_void_p(arr[k].ctypes.data if arr[k].size else None)
+                                for k in names + ("cr_Lbase",)])
+            if rc == _lib.CYQ_INVALID_ARG:
+                raise ValueError(self.ctx.last_error())
+            if rc:
+                raise CudaError(self.ctx.last_error())
+            out.update(arr)
+        return out
 
     def __del__(self):
         try:
