@@ -1161,7 +1161,9 @@ int cyq_factor_materialize_schur(const cyq_factor *f, int64_t inst, double *T, d
         return k <= r ? base[(tri_index(r / 8, k / 8)) * 64 + (r % 8) * 8 + k % 8] : 0.0;
     };
     auto full = [&](const double *base, int r, int k) { return base[((r / 8) * XT + k / 8) * 64 + (r % 8) * 8 + k % 8]; };
-    auto sym = [&](const double *base, int r, int k) { return L.full ? full(base, r, k) : lower(base, std::max(r, k), std::min(r, k)); };
+    // symmetric blocks keep their lower triangle (the upper tiles of a full
+    // layout are not written)
+    auto sym = [&](const double *base, int r, int k) { return lower(base, std::max(r, k), std::min(r, k)); };
     auto Tel = [&](int c, int r, int k) { // T_c = L_Q^{-T} (upper)
         const double *b = ws.data() + L.Tt + c * TLb;
         if (L.tt_is_inverse)
