@@ -164,6 +164,27 @@ int cyq_solve_newton_batch(cyq_ctx *ctx, const cyq_dims *dims,
                            const double *sigma, double gamma_inv,
                            const cyq_sol_batch *sol, cyq_status *status);
 
+/* Augmented-Lagrangian gradients of the QPALM inner loop
+ * (qpalm::eval_al_gradients, qpalm.cpp:106-165), batched, for every
+ * instance and stage j: with g = C_j x_j + D_j u_j (j = N: C_N x_N),
+ *   yhat_j = y_j + sigma_j (g - clamp(g + y_j / sigma_j, bl_j, bu_j))
+ *   ru_j   = r_j + R_j u_j + S_j x_j + D_j' yhat_j + gamma_inv (u_j - ubar_j)  j < N
+ *   cres_j = f_j + A_j x_j + B_j u_j - x_{j+1}                                j < N
+ *   qx_j   = q_j + Q_j x_j + S_j' u_j + C_j' yhat_j + gamma_inv (x_j - xbar_j) j >= 1
+ *            (no S term at j = N; qx_0 is written as 0, unused)
+ * Layouts: prob in the problem layout (R, S, Q, A, B, f, r, q read), D[b][N][ny][nu],
+ * C[b][N+1][ny][nx] (C[N] = the terminal rows, ny_term = ny), bl, bu, y,
+ * sigma, yhat [b][N+1][ny], u, ubar [b][N][nu], x, xbar, qx [b][N+1][nx],
+ * ru [b][N][nu], cres [b][N][nx]. The Newton step's rhs is
+ * (-ru, -qx, -cres) (qpalm.cpp:391-405). DEVICE pointers; stream-ordered. */
+int cyq_al_gradients_batch(cyq_ctx *ctx, const cyq_dims *dims, int64_t ny,
+                           const cyq_ocp_batch *prob, const double *D,
+                           const double *C, const double *bl, const double *bu,
+                           const double *u, const double *x, const double *y,
+                           const double *sigma, const double *ubar,
+                           const double *xbar, double gamma_inv, double *ru,
+                           double *qx, double *yhat, double *cres);
+
 /* Exact line search of the QPALM inner loop (qpalm::line_search_exact,
  * line_search.cpp:112-206, over LineSearchData::add_term of every term,
  * line_search.cpp:9-27), batched: for instance b, the root tau of

@@ -256,6 +256,20 @@ class RefOracle(_Base):
                ctypes_double(rho), C_sol(sol), rep.ctypes.data_as(C_i64p))
         return sol, rc, rep
 
+    def al_gradients(self, p, D, Cm, bl, bu, u, x, y, sigma, ubar, xbar, gamma_inv):
+        """The reference's qpalm::eval_al_gradients (qpalm.cpp:106-165) per
+        instance; arrays in the C ABI layout (see cyq_al_gradients_batch)."""
+        b, N, nx, nu, ny = p.batch, p.N, p.nx, p.nu, D.shape[2]
+        out = {"ru": np.zeros((b, N, nu)), "qx": np.zeros((b, N + 1, nx)),
+               "yhat": np.zeros((b, N + 1, ny)), "cres": np.zeros((b, N, nx))}
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (D, Cm, bl, bu, u, x, y, sigma, ubar, xbar)]
+        rc = self.lib.ref_al_gradients(C.byref(_dims(p, 1)), C.byref(_ocp(p)), i64(ny),
+                                       *[_p(a) for a in arrs], C.c_double(gamma_inv),
+                                       *[_p(out[k]) for k in ("ru", "qx", "yhat", "cres")])
+        if rc != 0:
+            raise RuntimeError("reference eval_al_gradients failed")
+        return out
+
     def bench_latency(self, p, P, vlen, workers, reps):
         """Best single-instance factor+solve time (s) of instance 0 with
         FactorOptions{P, vlen, workers} over `reps` repetitions."""

@@ -13,6 +13,7 @@
 #include "oracle.h"
 
 #include <cyqlone/kkt_solver.hpp>
+#include <cyqlone/qpalm.hpp>
 
 #include <algorithm>
 #include <atomic>
@@ -401,6 +402,63 @@ double ref_bench_solve_problem(const oc_dims *d, const oc_ocp *p,
     if (failed)
         return -1.0;
     return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// qpalm::eval_al_gradients (qpalm.cpp:106-165) of every instance: the
+// reference's own code on an OCPProblem built from the ABI layout (D
+// [b][N][ny][nu], C [b][N+1][ny][nx] with C[N] = C_term, bl / bu / y /
+// sigma [b][N+1][ny], u [b][N][nu], x [b][N+1][nx], ubar, xbar alike),
+// QPALMSettings::gamma = 1 / gamma_inv. Outputs ru [b][N][nu],
+// qx [b][N+1][nx] (qx[0] = 0, unused), yhat [b][N+1][ny], cres [b][N][nx].
+int ref_al_gradients(const oc_dims *d, const oc_ocp *p, int64_t ny, const double *D, const double *C,
+                     const double *bl, const double *bu, const double *u, const double *x,
+                     const double *y, const double *sigma, const double *ubar, const double *xbar,
+                     double gamma_inv, double *ru, double *qx, double *yhat, double *cres) {
+    const index_t N = d->N, nx = d->nx, nu = d->nu;
+    try {
+        for (index_t b = 0; b < d->batch; ++b) {
+            EqOCP e = make_ocp(d, p, b);
+            ocp::OCPProblem pr;
+            pr.N = N, pr.nx = nx, pr.nu = nu, pr.ny = ny, pr.ny_term = ny;
+            pr.A = e.A, pr.B = e.B, pr.f = e.f, pr.R = e.R, pr.S = e.S, pr.Q = e.Q, pr.q = e.q, pr.r = e.r;
+            pr.x_init = e.x_init;
+            qpalm::ALMState st;
+            for (index_t j = 0; j < N; ++j) {
+                pr.D.push_back(mat_from(D + (b * N + j) * ny * nu, ny, nu));
+                pr.C.push_back(mat_from(C + (b * (N + 1) + j) * ny * nx, ny, nx));
+                st.u.push_back(vec_from(u + (b * N + j) * nu, nu));
+                st.ubar.push_back(vec_from(ubar + (b * N + j) * nu, nu));
+            }
+            pr.C_term = mat_from(C + (b * (N + 1) + N) * ny * nx, ny, nx);
+            for (index_t j = 0; j <= N; ++j) {
+                const index_t o = (b * (N + 1) + j) * ny;
+                pr.bl.push_back(vec_from(bl + o, ny));
+                pr.bu.push_back(vec_from(bu + o, ny));
+                st.y.push_back(vec_from(y + o, ny));
+                st.sigma.push_back(vec_from(sigma + o, ny));
+                st.x.push_back(vec_from(x + (b * (N + 1) + j) * nx, nx));
+                st.xbar.push_back(vec_from(xbar + (b * (N + 1) + j) * nx, nx));
+            }
+            qpalm::QPALMSettings s;
+            s.gamma = 1.0 / gamma_inv;
+            const qpalm::AlGradients g = qpalm::eval_al_gradients(pr, st, s);
+            for (index_t j = 0; j <= N; ++j) {
+                const auto ju = static_cast<std::size_t>(j);
+                std::copy_n(g.yhat[ju].data(), ny, yhat + (b * (N + 1) + j) * ny);
+                if (j >= 1)
+                    std::copy_n(g.qx[ju].data(), nx, qx + (b * (N + 1) + j) * nx);
+                else
+                    std::fill_n(qx + b * (N + 1) * nx, nx, 0.0);
+                if (j < N) {
+                    std::copy_n(g.ru[ju].data(), nu, ru + (b * N + j) * nu);
+                    std::copy_n(g.cres[ju].data(), nx, cres + (b * N + j) * nx);
+                }
+            }
+        }
+    } catch (...) {
+        return 1;
+    }
+    return 0;
 }
 
 // Single-instance latency: kkt::factor +

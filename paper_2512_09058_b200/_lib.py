@@ -75,6 +75,8 @@ SIGNATURES = {
     "cyq_ctx_get_option": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(i64)]),
     "cyq_ctx_wait_status": (C.c_int, [C.c_void_p, C.c_void_p, i64]),
     "cyq_factor_materialize_schur": (C.c_int, [C.c_void_p, i64] + [C.c_void_p] * 10),
+    "cyq_al_gradients_batch": (C.c_int, [C.c_void_p, C.c_void_p, i64, C.c_void_p] + [C.c_void_p] * 10
+                               + [C.c_double] + [C.c_void_p] * 4),
     "cyq_ctx_profile_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(i64),
                                        C.c_int]),
     "cyq_version": (C.c_char_p, []),

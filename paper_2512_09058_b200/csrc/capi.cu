@@ -1360,6 +1360,29 @@ int cyq_solve_newton_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_bat
     return finish_status(ctx, g, ws.fail, status);
 }
 
+int cyq_al_gradients_batch(cyq_ctx *ctx, const cyq_dims *dims, int64_t ny, const cyq_ocp_batch *prob,
+                           const double *D, const double *C, const double *bl, const double *bu,
+                           const double *u, const double *x, const double *y, const double *sigma,
+                           const double *ubar, const double *xbar, double gamma_inv, double *ru,
+                           double *qx, double *yhat, double *cres) {
+    if (!ctx || !dims || !prob || !D || !C || !bl || !bu || !u || !x || !y || !sigma || !ubar || !xbar ||
+        !ru || !qx || !yhat || !cres)
+        return set_err(ctx, CYQ_INVALID_ARG, "null argument");
+    if (dims->N < 1 || dims->nx < 1 || dims->nu < 1 || dims->batch < 1 || ny < 1)
+        return set_err(ctx, CYQ_INVALID_ARG, "dims: N, nx, nu, batch, ny must be >= 1");
+    CU(cudaSetDevice(ctx->device));
+    GradArgs ga{(int)dims->batch, (int)dims->N, (int)dims->nx, (int)dims->nu, (int)ny,
+                prob->R, prob->S, prob->Q, prob->A, prob->B, prob->f, prob->r, prob->q,
+                D, C, bl, bu, u, x, y, sigma, ubar, xbar, gamma_inv, ru, qx, yhat, cres};
+    {
+        Timed t(ctx, 4);
+        if (!launch_al_gradients(ctx->stream, ga))
+            return set_err(ctx, CYQ_INVALID_ARG, "al_gradients: nx + nu + ny too large");
+    }
+    CU(cudaGetLastError());
+    return CYQ_OK;
+}
+
 int cyq_line_search_batch(cyq_ctx *ctx, int64_t batch, int64_t m, const double *alpha,
                           const double *delta, const double *eta, const double *beta, double *tau,
                           int32_t *status, int64_t *iterations) {

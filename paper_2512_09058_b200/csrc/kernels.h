@@ -178,6 +178,15 @@ struct LineSearchArgs {
     double *scratch;                          // [batch][m][2] breakpoints (t, w)
 };
 void launch_line_search(cudaStream_t st, const LineSearchArgs &a);
+// augmented-Lagrangian gradients of the QPALM inner loop (gradients.cu)
+struct GradArgs {
+    int batch, N, nx, nu, ny;
+    const double *R, *S, *Q, *A, *B, *f, *r, *q;                 // problem (ABI layout)
+    const double *D, *C, *bl, *bu, *u, *x, *y, *sigma, *ubar, *xbar; // QPALM data and state
+    double gamma_inv;
+    double *ru, *qx, *yhat, *cres;                               // outputs
+};
+bool launch_al_gradients(cudaStream_t st, const GradArgs &a);
 
 bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra, const LaunchOpts &o);
 // true when the warp kernel has a fused Newton-system augmentation variant

@@ -555,6 +555,49 @@ def solve_newton(p, D, Cm, sigma, opts: FactorOptions, gamma_inv: float = 0.0, o
     return sol if raise_on_error else (sol, rc, list(st))
 
 
+def al_gradients(p, D, Cm, bl, bu, u, x, y, sigma, ubar, xbar, gamma_inv: float,
+                 ctx: Context | None = None, out=None):
+    """qpalm::eval_al_gradients (qpalm.cpp:106-165) on the GPU for every
+    instance: returns dict(ru (b, N, nu), qx (b, N+1, nx; qx[:, 0] = 0),
+    yhat (b, N+1, ny), cres (b, N, nx)) as CUDA tensors. Inputs are CUDA
+    torch tensors: the problem batch `p`, D (b, N, ny, nu), Cm (b, N+1, ny,
+    nx; Cm[:, N] the terminal rows), bl, bu, y, sigma (b, N+1, ny), u, ubar
+    (b, N, nu), x, xbar (b, N+1, nx). The Newton step's rhs is
+    EqRhsBatch(-ru, -qx, -cres) (qpalm.cpp:391-405, `newton_rhs`)."""
+    import torch
+
+    arrs = [p.R, p.S, p.Q, p.A, p.B, p.f, p.r, p.q, D, Cm, bl, bu, u, x, y, sigma, ubar, xbar]
+    for a_ in arrs:
+        if not _is_torch(a_):
+            raise ValueError("al_gradients takes CUDA torch tensors")
+    ctx = _context(ctx, arrs)
+    ctx.follow_torch(arrs)
+    b, N, nx, nu = p.A.shape[0], p.A.shape[1], p.A.shape[2], p.B.shape[3]
+    ny = D.shape[2]
+    if tuple(Cm.shape) != (b, N + 1, ny, nx) or tuple(y.shape) != (b, N + 1, ny):
+        raise ValueError("al_gradients: Cm must be (b, N+1, ny, nx), y / sigma / bl / bu (b, N+1, ny)")
+    f64 = dict(dtype=torch.float64, device=p.A.device)
+    if out is None:
+        out = {"ru": torch.empty((b, N, nu), **f64), "qx": torch.empty((b, N + 1, nx), **f64),
+               "yhat": torch.empty((b, N + 1, ny), **f64), "cres": torch.empty((b, N, nx), **f64)}
+    rc = ctx.lib.cyq_al_gradients_batch(
+        ctx.h, C.byref(_lib.CyqDims(N, nx, nu, 1, b)), ny, C.byref(_ocp_struct(p)),
+        *[_ptr(a_) for a_ in (D, Cm, bl, bu, u, x, y, sigma, ubar, xbar)], float(gamma_inv),
+        *[_ptr(out[k]) for k in ("ru", "qx", "yhat", "cres")])
+    if rc != _lib.CYQ_OK:
+        raise (ValueError if rc == _lib.CYQ_INVALID_ARG else CudaError)(
+            f"cyq_al_gradients_batch failed ({rc}): {ctx.last_error()}")
+    return out
+
+
+def newton_rhs(grads) -> EqRhsBatch:
+    """The Newton step's right-hand side from al_gradients: ru = -ru,
+    qx = -qx (qx[0] unused), fd = -cres (qpalm.cpp:391-405)."""
+    rhs = EqRhsBatch.__new__(EqRhsBatch)  # device tensors as they are
+    rhs.ru, rhs.qx, rhs.fd = -grads["ru"], -grads["qx"], -grads["cres"]
+    return rhs
+
+
 def line_search_exact(alpha, delta, eta, beta, ctx: Context | None = None,
                       raise_on_error: bool = True, iterations: bool = False):
     """qpalm::line_search_exact (line_search.cpp:112-206) for a batch: tau[b]
@@ -587,5 +630,5 @@ def line_search_exact(alpha, delta, eta, beta, ctx: Context | None = None,
     return out
 
 
-__all__ = ["Prepared", "augment_hessians", "solve_newton", "line_search_exact", "update", "FactorOptions", "Factor", "FactorizeError", "CudaError", "Context", "factor",
+__all__ = ["Prepared", "al_gradients", "newton_rhs", "augment_hessians", "solve_newton", "line_search_exact", "update", "FactorOptions", "Factor", "FactorizeError", "CudaError", "Context", "factor",
            "solve", "solve_problem", "nu2", "EqOCPBatch", "EqRhsBatch", "EqSolutionBatch"]
