@@ -132,6 +132,30 @@ int cyq_factor_materialize_schur(const cyq_factor *factor, int64_t inst, double 
                                  double *cr_L, double *cr_U, double *cr_Y,
                                  double *cr_Lbase);
 
+/* kkt::update (kkt_solver.hpp:152-161, kkt_update.cpp:372-477) of every
+ * instance of a factor, in place: afterwards the factor is (up to roundoff)
+ * the factor of p_new, whose stage Hessians are H_j + (D_j | C_j)' dSigma_j
+ * (D_j | C_j) (terminal: C_term' dSigma_term C_term). Per partition column
+ * the accumulated update rank r (nonzeros of dSigma over its stages,
+ * kkt_update.cpp:392-409) selects the path: r = 0 untouched; r < rho nx
+ * the low-rank hyperbolic-Householder column update on the GPU; r >= rho nx
+ * (or a hyperbolic breakdown) a refactorization of the column. The Schur
+ * complement and its CR factor are then re-formed from the updated columns
+ * (instances with any nonzero rank). Layouts: C[b][N][ny][nx],
+ * D[b][N][ny][nu], ds_stage[b][N][ny], C_term[b][ny_term][nx],
+ * ds_term[b][ny_term] (ny_term may be 0); `mem` says where p_new, C, D,
+ * C_term and the dSigma arrays live. report[batch] (nullable) mirrors
+ * UpdateReport per instance. Returns CYQ_PIVOT_FAIL when a refactorized
+ * column or the CR factor breaks down. */
+typedef struct {
+    int64_t columns_updated, columns_refactored, schur_refactored, schur_levels_updated;
+} cyq_update_report;
+int cyq_factor_update_batch(cyq_ctx *ctx, cyq_factor *factor, const cyq_ocp_batch *p_new,
+                            int64_t ny, const double *C, const double *D,
+                            const double *ds_stage, int64_t ny_term,
+                            const double *C_term, const double *ds_term,
+                            double rho, int mem, cyq_update_report *report);
+
 /* Newton-system assembly of the QPALM inner loop (qpalm::assemble_newton,
  * qpalm.cpp:167-225, equality part; BASELINE config 4): for every instance
  * and stage j

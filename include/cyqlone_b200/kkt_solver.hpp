@@ -157,13 +157,14 @@ struct UpdateReport {
 };
 
 /// kkt::update (kkt_solver.hpp:152-161, kkt_update.cpp:372-477): afterwards
-/// the factor equals a fresh factorization of `p_new` (whose Hessians carry
-/// H_j + (D_j | C_j)' dSigma_j (D_j | C_j)). The GPU takes the reference's
-/// refactorization path (kkt_update.cpp:424-453) for every column whose
-/// update rank is nonzero -- the path the reference itself takes once a
-/// column's rank reaches rho * nx -- so the report lists those columns as
-/// refactored and the Schur factor as refactored; with dSigma = 0 the factor
-/// is left as it is. The hyperbolic-Householder low-rank path is not built.
+/// the factor equals (up to roundoff) a fresh factorization of `p_new`
+/// (whose Hessians carry H_j + (D_j | C_j)' dSigma_j (D_j | C_j)). Per
+/// partition column the accumulated update rank r selects the path, as in
+/// the reference: r < rho nx the hyperbolic-Householder low-rank column
+/// update (on the GPU), r >= rho nx (or a hyperbolic breakdown) a column
+/// refactorization; the Schur complement and its CR factor are then
+/// re-formed from the updated columns (schur_refactored = true,
+/// schur_levels_updated = 0). With dSigma = 0 the factor is left as it is.
 /// Throws std::invalid_argument on shape mismatches.
 UpdateReport update(Factor &f, const EqOCP &p_new, const std::vector<Mat> &C,
                     const std::vector<Mat> &D, const Mat &C_term, const SigmaDelta &ds);

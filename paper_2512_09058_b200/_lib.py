@@ -48,6 +48,11 @@ class CyqSolBatch(C.Structure):
     _fields_ = [(k, C.c_void_p) for k in ("u", "x", "lam")]
 
 
+class CyqUpdateReport(C.Structure):
+    _fields_ = [("columns_updated", i64), ("columns_refactored", i64), ("schur_refactored", i64),
+                ("schur_levels_updated", i64)]
+
+
 class CyqStatus(C.Structure):
     _fields_ = [("code", C.c_int32), ("kind", C.c_int32), ("instance", i64),
                 ("column_or_level", i64), ("stage", i64), ("pivot", i64)]
@@ -75,6 +80,9 @@ SIGNATURES = {
     "cyq_ctx_get_option": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(i64)]),
     "cyq_ctx_wait_status": (C.c_int, [C.c_void_p, C.c_void_p, i64]),
     "cyq_factor_materialize_schur": (C.c_int, [C.c_void_p, i64] + [C.c_void_p] * 10),
+    "cyq_factor_update_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, i64, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
+                                          C.c_void_p]),
     "cyq_al_gradients_batch": (C.c_int, [C.c_void_p, C.c_void_p, i64, C.c_void_p] + [C.c_void_p] * 10
                                + [C.c_double] + [C.c_void_p] * 4),
     "cyq_ctx_profile_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(i64),

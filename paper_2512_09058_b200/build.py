@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libcyqlone_b200.so")
-SOURCES = ["riccati.cu", "riccati_warp.cu", "riccati_cta.cu", "riccati_pc.cu", "schur_cr.cu", "schur_tiles.cu", "schur_fused.cu", "schur_big.cu", "backsub.cu", "backsub_warp.cu", "backsub_tile.cu", "forward.cu", "augment.cu", "linesearch.cu", "gradients.cu",
+SOURCES = ["riccati.cu", "riccati_warp.cu", "riccati_cta.cu", "riccati_pc.cu", "schur_cr.cu", "schur_tiles.cu", "schur_fused.cu", "schur_big.cu", "backsub.cu", "backsub_warp.cu", "backsub_tile.cu", "forward.cu", "augment.cu", "linesearch.cu", "gradients.cu", "update.cu",
            "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -258,7 +258,7 @@ template <int M> void launch_riccati_t(const Geo &g, int nw, cudaStream_t st, co
         return cudaFuncSetAttribute(riccati_panel_kernel_t<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     227 * 1024);
     });
-    riccati_panel_kernel_t<M><<<g.batch * g.P, 32 * nw, riccati_smem_bytes(g), st>>>(ra);
+    riccati_panel_kernel_t<M><<<ra.grid_chains(), 32 * nw, riccati_smem_bytes(g), st>>>(ra);
 }
 
 void launch_riccati(const Geo &g, const LaunchOpts &o, cudaStream_t st, const RiccatiArgs &ra) {
@@ -1000,6 +1000,163 @@ int cyq_solve_batch(cyq_ctx *ctx, const cyq_factor *f, const cyq_ocp_batch *prob
     }
     CU(cudaStreamSynchronize(ctx->stream));
     return CYQ_OK;
+}
+
+int cyq_factor_update_batch(cyq_ctx *ctx, cyq_factor *f, const cyq_ocp_batch *p_new, int64_t ny,
+                            const double *C, const double *D, const double *ds_stage, int64_t ny_term,
+                            const double *C_term, const double *ds_term, double rho, int mem,
+                            cyq_update_report *report) {
+    if (!ctx || !f || !p_new || ny < 0 || ny_term < 0 || (ny > 0 && (!C || !D || !ds_stage)) ||
+        (ny_term > 0 && (!C_term || !ds_term)))
+        return set_err(ctx, CYQ_INVALID_ARG, "null argument");
+    const Geo g = f->g;
+    const size_t B = g.batch, N = g.N, nx = g.nx, nu = g.nu, P = g.P;
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaStreamSynchronize(ctx->stream));
+    // ---- dSigma on the host: per-column ranks (kkt_update.cpp:392-409) -----
+    std::vector<double> hds(B * N * (size_t)ny), hdt(B * (size_t)ny_term);
+    if (mem == CYQ_MEM_DEVICE) {
+        if (!hds.empty())
+            CU(cudaMemcpy(hds.data(), ds_stage, hds.size() * 8, cudaMemcpyDeviceToHost));
+        if (!hdt.empty())
+            CU(cudaMemcpy(hdt.data(), ds_term, hdt.size() * 8, cudaMemcpyDeviceToHost));
+    } else {
+        std::copy(ds_stage, ds_stage + hds.size(), hds.begin());
+        std::copy(ds_term, ds_term + hdt.size(), hdt.begin());
+    }
+    std::vector<int> upd, refac;
+    std::vector<int64_t> rank(B * P, 0);
+    int cap = 1;
+    for (size_t b = 0; b < B; ++b)
+        for (size_t c = 0; c < P; ++c) {
+            int64_t r = 0;
+            for (int s = 0; s < g.n; ++s) {
+                const int j = g.stage_of((int)c, s);
+                if (j < (int)N)
+                    for (int64_t i = 0; i < ny; ++i)
+                        r += hds[(b * N + j) * ny + i] != 0.0;
+                if (j == 0)
+                    for (int64_t i = 0; i < ny_term; ++i)
+                        r += hdt[b * ny_term + i] != 0.0;
+            }
+            rank[b * P + c] = r;
+            if (r == 0)
+                continue;
+            if ((double)r >= rho * (double)nx) {
+                refac.push_back((int)(b * P + c));
+            } else {
+                upd.push_back((int)(b * P + c));
+                cap = std::max<int>(cap, (int)r);
+            }
+        }
+    if (report)
+        for (size_t b = 0; b < B; ++b)
+            report[b] = cyq_update_report{0, 0, 0, 0};
+    if (upd.empty() && refac.empty())
+        return CYQ_OK; // dSigma = 0: the factor already is the factor of p_new
+    if (!upd.empty() && update_smem_bytes(g.nx, g.nu, cap) > 227 * 1024) { // too wide: refactorize
+        refac.insert(refac.end(), upd.begin(), upd.end());
+        upd.clear();
+    }
+    // ---- device copies: p_new -> the factor's problem, update data --------
+    const size_t nC = B * N * ny * nx, nD = B * N * ny * nu, nds = B * N * ny, nCt = B * ny_term * nx,
+                 nt = B * ny_term;
+    const size_t scratch = (nC + nD + nds + nCt + nt) * 8 + (upd.size() + refac.size()) * 4 + upd.size() * 4 + 256;
+    int rc = ensure(ctx, &ctx->augbuf, &ctx->augbuf_bytes, scratch);
+    if (rc)
+        return rc;
+    double *dC = static_cast<double *>(ctx->augbuf), *dD = dC + nC, *dds = dD + nD, *dCt = dds + nds,
+           *ddt = dCt + nCt;
+    int *dlist = reinterpret_cast<int *>(ddt + nt), *dbreak = dlist + upd.size() + refac.size();
+    const cudaMemcpyKind kind = mem == CYQ_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    {
+        const ProbView src = view_of(p_new);
+        const std::pair<const double *, const double *> parts[] = {
+            {src.A, f->prob.A}, {src.B, f->prob.B}, {src.R, f->prob.R}, {src.S, f->prob.S},
+            {src.Q, f->prob.Q}, {src.f, f->prob.f}, {src.r, f->prob.r}, {src.q, f->prob.q},
+            {src.x_init, f->prob.x_init}};
+        const size_t cnt[] = {B * N * nx * nx, B * N * nx * nu, B * N * nu * nu, B * N * nu * nx,
+                              B * (N + 1) * nx * nx, B * N * nx, B * N * nu, B * (N + 1) * nx, B * nx};
+        for (int i = 0; i < 9; ++i) {
+            if (!parts[i].first)
+                return set_err(ctx, CYQ_INVALID_ARG, "null problem array");
+            CU(cudaMemcpyAsync(const_cast<double *>(parts[i].second), parts[i].first, cnt[i] * 8, kind,
+                               ctx->stream));
+        }
+    }
+    if (nC) {
+        CU(cudaMemcpyAsync(dC, C, nC * 8, kind, ctx->stream));
+        CU(cudaMemcpyAsync(dD, D, nD * 8, kind, ctx->stream));
+        CU(cudaMemcpyAsync(dds, hds.data(), nds * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    if (nCt) {
+        CU(cudaMemcpyAsync(dCt, C_term, nCt * 8, kind, ctx->stream));
+        CU(cudaMemcpyAsync(ddt, hdt.data(), nt * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    CU(cudaMemsetAsync(f->ws.fail, 0xFF, sizeof(unsigned long long) * B, ctx->stream));
+    // ---- low-rank column updates (update.cu) --------------------------------
+    std::vector<int> broke;
+    if (!upd.empty()) {
+        CU(cudaMemcpyAsync(dlist, upd.data(), upd.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemsetAsync(dbreak, 0, upd.size() * 4, ctx->stream));
+        UpdateArgs ua{g, f->prob, f->ws.fac, f->ws.trail, dlist, (int)upd.size(), dD, dC, dCt, dds, ddt,
+                      (int)ny, (int)ny_term, cap, dbreak};
+        {
+            Timed t(ctx, 0);
+            if (!launch_update_columns(ctx->stream, ua))
+                return set_err(ctx, CYQ_INVALID_ARG, "update: stage shape too large");
+        }
+        CU(cudaGetLastError());
+        std::vector<int> hb(upd.size());
+        CU(cudaMemcpyAsync(hb.data(), dbreak, hb.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        std::vector<int> kept;
+        for (size_t i = 0; i < upd.size(); ++i)
+            (hb[i] ? refac : kept).push_back(upd[i]);
+        upd.swap(kept);
+    }
+    // ---- refactorized columns: the panel kernels over the listed chains ----
+    if (!refac.empty()) {
+        int *dref = dlist + 0; // reuse the list slot (the update kernel is done reading it)
+        CU(cudaMemcpyAsync(dref, refac.data(), refac.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+        RiccatiArgs ra{g, f->prob, f->ws.fac, f->ws.y, f->ws.wl, f->ws.trail, f->ws.fail, f->ws.consts, 1,
+                       nullptr};
+        ra.chain_list = dref;
+        ra.n_list = (int)refac.size();
+        if (!riccati_staged(g))
+            return set_err(ctx, CYQ_INVALID_ARG, "update: refactorization needs the staged panel kernels");
+        Timed t(ctx, 0);
+        bool done = false;
+        if ((long long)refac.size() <= 2LL * ctx->opts.sms)
+            done = launch_riccati_pc(g, ctx->stream, ra);
+        if (!done)
+            done = launch_riccati_warp(g, ctx->stream, ra, LaunchOpts{});
+        if (!done)
+            done = launch_riccati_cta(g, ctx->stream, ra);
+        if (!done)
+            launch_riccati(g, ctx->opts, ctx->stream, ra);
+    }
+    CU(cudaGetLastError());
+    // ---- Schur complement + CR factor re-formed from the updated columns ---
+    SchurArgs sa{g, f->prob, f->ws.fac, f->ws.y, f->ws.trail, f->ws.schur, f->ws.lamc, nullptr,
+                 f->ws.fail, 1, 0};
+    rc = launch_schur(ctx, g, sa, f->opts);
+    if (rc)
+        return rc;
+    f->schur_path = ctx->schur_path;
+    if (report) {
+        for (int ch : upd)
+            ++report[ch / P].columns_updated;
+        for (int ch : refac)
+            ++report[ch / P].columns_refactored;
+        for (size_t b = 0; b < B; ++b) {
+            bool any = false;
+            for (size_t c = 0; c < P; ++c)
+                any = any || rank[b * P + c] > 0;
+            report[b].schur_refactored = any;
+        }
+    }
+    return decode_status(ctx, g, f->ws.fail, nullptr);
 }
 
 int cyq_factor_destroy(cyq_factor *f) {

@@ -103,6 +103,13 @@ struct RiccatiArgs {
     const double *consts; // I_nu | I_nx | zeros (direct-mode generic kernel)
     int staged;           // generic kernel: stage data staged in smem
     long long *phase;     // optional per-stage phase clocks of chain 0 (profiling)
+    // optional: factor only the listed chains (instance * P + column), n_list
+    // of them, one per grid slot (kkt::update's refactorized columns)
+    const int *chain_list = nullptr;
+    int n_list = 0;
+    // number of chains the grid covers
+    __host__ __device__ int grid_chains() const { return chain_list ? n_list : g.batch * g.P; }
+    __device__ int chain_of(int slot) const { return chain_list ? chain_list[slot] : slot; }
 };
 
 struct SchurArgs {
@@ -187,6 +194,21 @@ struct GradArgs {
     double *ru, *qx, *yhat, *cres;                               // outputs
 };
 bool launch_al_gradients(cudaStream_t st, const GradArgs &a);
+// kkt::update's column path (update.cu): listed chains, in place
+struct UpdateArgs {
+    Geo g;
+    ProbView p;           // the updated problem ([B A] for the propagation)
+    double *fac, *trail;  // factor tiles and -Mfwd, updated in place
+    const int *chains;    // chains to update (instance * P + column)
+    int n;
+    const double *D, *C;  // [b][N][ny][nu], [b][N][ny][nx]
+    const double *C_term; // [b][ny_term][nx]
+    const double *ds, *ds_term; // [b][N][ny], [b][ny_term]
+    int ny, ny_term, cap; // cap: max update columns of a listed chain
+    int *breakdown;       // [n]: 1 = hyperbolic breakdown / over cap -> refactorize
+};
+bool launch_update_columns(cudaStream_t st, const UpdateArgs &a);
+size_t update_smem_bytes(int nx, int nu, int cap);
 
 bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra, const LaunchOpts &o);
 // true when the warp kernel has a fused Newton-system augmentation variant

@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(MAXT == 32 ? 256 : 128, (MAXT <= 8 ? 4 : 1))
 riccati_panel_kernel_t(RiccatiArgs a) {
     extern __shared__ __align__(16) double sm[];
     const Geo &g = a.g;
-    const int chain = blockIdx.x;
+    const int chain = a.chain_of(blockIdx.x);
     const int b = chain / g.P, c = chain % g.P;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NW = blockDim.x >> 5, NTH = blockDim.x;

@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
     constexpr int NTH = 32 * NW, MAXL = C::MAXL, CT = C::CT, TT = C::TT;
     extern __shared__ __align__(16) double sm[];
     const Geo &g = a.g;
-    const int chain = blockIdx.x;
+    const int chain = a.chain_of(blockIdx.x);
     const int b = chain / g.P, c = chain % g.P, n = g.n, N = g.N;
     griddep_launch();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -661,7 +661,7 @@ template <int NU, int NX, int NW> bool launch_c(const Geo &g, cudaStream_t st, c
         const cudaError_t e1 = cudaMemcpyToSymbol(c_list, h, sizeof h);
         return e1 != cudaSuccess ? e1 : cudaMemcpyToSymbol(c_cnt, cnt, sizeof cnt);
     });
-    riccati_cta_kernel<NU, NX, NW><<<g.batch * g.P, 32 * NW, smem, st>>>(ra);
+    riccati_cta_kernel<NU, NX, NW><<<ra.grid_chains(), 32 * NW, smem, st>>>(ra);
     return true;
 }
 } // namespace

@@ -83,10 +83,10 @@ __global__ void __launch_bounds__(64, 6) riccati_pc_kernel(RiccatiArgs a) {
     extern __shared__ __align__(16) double sm[];
     const Geo &g = a.g;
     const int lane = threadIdx.x & 31, role = threadIdx.x >> 5; // 0 producer, 1 consumer
-    const int chain = blockIdx.x;
     griddep_launch();
-    if (chain >= g.batch * g.P)
+    if ((int)blockIdx.x >= a.grid_chains())
         return;
+    const int chain = a.chain_of(blockIdx.x);
     const int b = chain / g.P, c = chain % g.P, n = g.n;
     const int rq = lane >> 2, cq = 2 * (lane & 3), q2 = lane & 3;
     double *Wv = sm + W::O_WV, *Wc = sm + W::O_WC, *LQ = sm + W::O_LQ, *img = sm + W::O_IMG;
@@ -528,7 +528,7 @@ template <int NU, int NX> bool launch_p(const Geo &g, cudaStream_t st, const Ric
     const size_t smem = (size_t)PCS<NU, NX>::SMEM * sizeof(double);
     static DeviceOnce once;
     once_per_device(once, [&] { return cudaFuncSetAttribute(riccati_pc_kernel<NU, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
-    riccati_pc_kernel<NU, NX><<<g.batch * g.P, 64, smem, st>>>(ra);
+    riccati_pc_kernel<NU, NX><<<ra.grid_chains(), 64, smem, st>>>(ra);
     return true;
 }
 } // namespace

@@ -185,8 +185,8 @@ __global__ void __launch_bounds__(32 * WPB, TM ? 3 : 1) riccati_warp_kernel(Ricc
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         tmw = s_taddr + ((32u * (uint32_t)(wib & 3)) << 16);
     }
-    if (chain < g.batch * g.P)
-        riccati_warp_body<NU, NX, WPB, NY, TM>(a, chain, tmw, sm);
+    if (chain < a.grid_chains())
+        riccati_warp_body<NU, NX, WPB, NY, TM>(a, a.chain_of(chain), tmw, sm);
     if constexpr (TM) {
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
@@ -786,7 +786,7 @@ bool launch_w(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
     const size_t smem = (size_t)WPB * W::SMEM * sizeof(double);
     static DeviceOnce once;
     once_per_device(once, [&] { return cudaFuncSetAttribute(riccati_warp_kernel<NU, NX, WPB, NY, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
-    const int chains = g.batch * g.P;
+    const int chains = ra.grid_chains();
     riccati_warp_kernel<NU, NX, WPB, NY, TM><<<(chains + WPB - 1) / WPB, 32 * WPB, smem, st>>>(ra);
     return true;
 }

@@ -433,26 +433,36 @@ UpdateReport update(Factor &f, const EqOCP &p_new, const std::vector<Mat> &C, co
     }
     if (!ds.terminal.empty() && (C_term.rows != static_cast<index_t>(ds.terminal.size()) || C_term.cols != f.nx))
         throw std::invalid_argument("update: C_term shape differs from (ny_term x nx)");
-    // per-column accumulated rank (kkt_update.cpp:392-409)
-    UpdateReport rep;
-    const Partition &pt = f.part;
-    for (index_t c = 0; c < pt.P; ++c) {
-        index_t r = 0;
-        for (index_t s = 0; s < pt.n_per; ++s) {
-            const index_t j = pt.stage_of(c, s);
-            if (j < p_new.N)
-                for (real_t x : ds.stage[z(j)])
-                    r += x != 0;
-            if (j == 0)
-                for (real_t x : ds.terminal)
-                    r += x != 0;
-        }
-        rep.columns_refactored += r > 0;
+    // flat instance-major arrays of the ABI (batch of one)
+    const index_t N = p_new.N, nx = f.nx, nu = f.nu;
+    const index_t ny = N > 0 ? static_cast<index_t>(ds.stage[0].size()) : 0;
+    const index_t nyt = static_cast<index_t>(ds.terminal.size());
+    std::vector<double> Cf, Df, dsf, Ctf, dtf(ds.terminal.begin(), ds.terminal.end());
+    for (index_t j = 0; j < N; ++j) {
+        if (static_cast<index_t>(ds.stage[z(j)].size()) != ny)
+            throw std::invalid_argument("update: dSigma stages differ in length");
+        FlatOCP::append(Cf, C[z(j)].a);
+        FlatOCP::append(Df, D[z(j)].a);
+        FlatOCP::append(dsf, ds.stage[z(j)]);
     }
-    if (rep.columns_refactored == 0)
-        return rep; // dSigma = 0: the factor already is the factor of p_new
-    f = factor(p_new, f.opts);
-    rep.schur_refactored = true;
+    if (nyt > 0)
+        Ctf = C_term.a;
+    FlatOCP fl(std::vector<const EqOCP *>{&p_new});
+    const cyq_ocp_batch pb = fl.view();
+    cyq_update_report r{};
+    std::lock_guard<std::mutex> lk(call_mutex());
+    const int rc = cyq_factor_update_batch(ctx(), f.impl->f, &pb, ny, Cf.data(), Df.data(), dsf.data(), nyt,
+                                           nyt ? Ctf.data() : nullptr, nyt ? dtf.data() : nullptr, f.opts.rho,
+                                           CYQ_MEM_HOST, &r);
+    if (rc != CYQ_OK)
+        throw_status(rc, {});
+    UpdateReport rep;
+    rep.columns_updated = r.columns_updated;
+    rep.columns_refactored = r.columns_refactored;
+    rep.schur_refactored = r.schur_refactored != 0;
+    rep.schur_levels_updated = r.schur_levels_updated;
+    (void)nu;
+    (void)nx;
     return rep;
 }
 

@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import contextlib
 import ctypes as C
+from ctypes import byref as _byref
 from dataclasses import dataclass
 
 import numpy as np
@@ -390,47 +391,52 @@ def solve(f: Factor, p, rhs) -> EqSolutionBatch:
 
 
 def update(f: Factor, p_new, C, D, C_term, ds_stage, ds_terminal=None):
-    """kkt::update (kkt_solver.hpp:152-161, kkt_update.cpp:372-477): returns
-    (factor, report) where the factor equals a fresh factorization of
-    `p_new` (Hessians H_j + (D_j | C_j)' dSigma_j (D_j | C_j)). The GPU takes
-    the reference's refactorization path (kkt_update.cpp:424-453) for every
-    column with a nonzero update rank -- the path the reference takes once a
-    column's rank reaches rho * nx; the hyperbolic-Householder low-rank path
-    is not built. With dSigma = 0 the factor is returned unchanged.
-    ds_stage (b, N, ny), ds_terminal (b, ny_term); C, D are only
-    shape-checked (b, N, ny, nx), (b, N, ny, nu). report: per-instance
-    columns_refactored, and schur_refactored."""
-    ds = np.asarray(ds_stage.cpu() if _is_torch(ds_stage) else ds_stage, dtype=np.float64)
-    dt = (np.zeros((ds.shape[0], 0)) if ds_terminal is None else
-          np.asarray(ds_terminal.cpu() if _is_torch(ds_terminal) else ds_terminal, dtype=np.float64))
-    if ds.ndim != 3 or ds.shape[0] != f.batch or ds.shape[1] != f.N:
+    """kkt::update (kkt_solver.hpp:152-161, kkt_update.cpp:372-477) of every
+    instance of `f`, in place on the GPU: afterwards `f` is (up to roundoff)
+    the factor of `p_new` (stage Hessians H_j + (D_j | C_j)' dSigma_j
+    (D_j | C_j)). Per partition column the update rank r selects the path:
+    0 untouched, r < rho nx the hyperbolic-Householder column update
+    (update.cu), r >= rho nx or a breakdown a refactorization of the column;
+    the Schur complement and its CR factor are then re-formed. Arrays: C
+    (b, N, ny, nx), D (b, N, ny, nu), C_term (b, ny_term, nx), ds_stage
+    (b, N, ny), ds_terminal (b, ny_term) -- all host numpy or all CUDA
+    tensors, like p_new. Returns (f, report) with per-instance lists
+    columns_updated / columns_refactored / schur_refactored."""
+    ctx = f.ctx
+    dev = _is_torch(ds_stage)
+    b, N, nx, nu = f.batch, f.N, f.nx, f.nu
+    if ds_terminal is None:
+        ds_terminal = (_torch().zeros((b, 0), dtype=_torch().float64, device=ds_stage.device) if dev
+                       else np.zeros((b, 0)))
+    if C_term is None:
+        C_term = (_torch().zeros((b, 0, nx), dtype=_torch().float64, device=ds_stage.device) if dev
+                  else np.zeros((b, 0, nx)))
+    if not dev:
+        ds_stage, ds_terminal, C, D, C_term = (np.ascontiguousarray(a, dtype=np.float64)
+                                               for a in (ds_stage, ds_terminal, C, D, C_term))
+    ny, nyt = ds_stage.shape[2], ds_terminal.shape[1]
+    if tuple(ds_stage.shape) != (b, N, ny):
         raise ValueError("update: ds_stage must be (batch, N, ny)")
-    if tuple(D.shape[:3]) != (f.batch, f.N, ds.shape[2]) or D.shape[3] != f.nu:
+    if tuple(D.shape) != (b, N, ny, nu):
         raise ValueError("update: D must be (batch, N, ny, nu)")
-    if tuple(C.shape[:3]) != (f.batch, f.N, ds.shape[2]) or C.shape[3] != f.nx:
+    if tuple(C.shape) != (b, N, ny, nx):
         raise ValueError("update: C must be (batch, N, ny, nx)")
-    if dt.shape[1] and (C_term is None or C_term.shape[-1] != f.nx):
+    if tuple(C_term.shape) != (b, nyt, nx):
         raise ValueError("update: C_term must be (batch, ny_term, nx)")
-    P, n = f.opts.P, f.n_per
-    Np = P * n
-    refac = []
-    for b in range(f.batch):
-        cols = 0
-        for c in range(P):
-            r = 0
-            for s in range(n):
-                j = (n * c - s) % Np
-                if j < f.N:
-                    r += int(np.count_nonzero(ds[b, j]))
-                if j == 0:
-                    r += int(np.count_nonzero(dt[b]))
-            cols += r > 0
-        refac.append(cols)
-    report = {"columns_updated": [0] * f.batch, "columns_refactored": refac,
-              "schur_refactored": any(refac), "schur_levels_updated": 0}
-    if not any(refac):
-        return f, report
-    return factor(p_new, f.opts, ctx=f.ctx), report
+    arrs = [getattr(p_new, k) for k in OCP_FIELDS] + [C, D, ds_stage, C_term, ds_terminal]
+    mem = _mem(arrs)
+    ctx.follow_torch(arrs)
+    rep = (_lib.CyqUpdateReport * b)()
+    # (the parameter C shadows the ctypes module here: _byref)
+    rc = ctx.lib.cyq_factor_update_batch(ctx.h, f.h, _byref(_ocp_struct(p_new)), ny, _ptr(C), _ptr(D), _ptr(ds_stage),
+                                         nyt, _ptr(C_term) if nyt else None,
+                                         _ptr(ds_terminal) if nyt else None, float(f.opts.rho), mem, rep)
+    _raise_status(ctx, rc, [])
+    report = {"columns_updated": [r.columns_updated for r in rep],
+              "columns_refactored": [r.columns_refactored for r in rep],
+              "schur_refactored": [bool(r.schur_refactored) for r in rep],
+              "schur_levels_updated": [r.schur_levels_updated for r in rep]}
+    return f, report
 
 
 def augment_hessians(p, D, Cm, sigma, gamma_inv: float = 0.0, out=None,

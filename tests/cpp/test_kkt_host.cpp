@@ -243,7 +243,7 @@ void test_batch_matches_single() {
         CHECK(rel_err(sb[i], kkt::solve_problem(ps[i], FactorOptions{8})) <= 1e-13, "batch vs single");
 }
 
-void test_update() { // kkt::update (kkt_solver.hpp:152-161): refactorization path
+void test_update() { // kkt::update (kkt_solver.hpp:152-161): low-rank path for rank 1 < rho nx
     const ocp::index_t N = 32, nx = 6, nu = 3, ny = 4;
     EqOCP p = random_ocp(N, nx, nu, 21);
     std::mt19937_64 rng(5);
@@ -278,15 +278,33 @@ void test_update() { // kkt::update (kkt_solver.hpp:152-161): refactorization pa
             pn.Q[9](a, b) += 2.5 * C[9](2, a) * C[9](2, b);
     CHECK(ds.total_rank() == 1, "total_rank");
     kkt::UpdateReport r1 = kkt::update(f, pn, C, D, ct, ds);
-    CHECK(r1.columns_refactored == 1 && r1.schur_refactored, "one column refactored (%lld)",
-          (long long)r1.columns_refactored);
+    CHECK(r1.columns_updated == 1 && r1.columns_refactored == 0 && r1.schur_refactored,
+          "one column updated (%lld / %lld)", (long long)r1.columns_updated, (long long)r1.columns_refactored);
     EqSolution s = kkt::solve(f, pn, EqRhs::of_problem(pn));
-    // factor + solve vs solve_problem (fused forward sweep): same bar as
-    // test_factor_then_solve
-    CHECK(rel_err(s, kkt::solve_problem(pn, FactorOptions{4})) <= 1e-13, "update == fresh factorization %.3e",
+    // the reference's update-vs-refactor bar (test_kkt_update.cpp:127-241)
+    CHECK(rel_err(s, kkt::solve_problem(pn, FactorOptions{4})) <= 1e-8, "update == fresh factorization %.3e",
           rel_err(s, kkt::solve_problem(pn, FactorOptions{4})));
-    kkt::Factor g = kkt::factor(pn, FactorOptions{4});
-    CHECK(bit_equal(s, kkt::solve(g, pn, EqRhs::of_problem(pn))), "update == factor(p_new) bitwise");
+    // rank >= rho nx in one column: the refactorization path
+    for (ocp::index_t i = 0; i < ny; ++i)
+        ds.stage[9][i] = 0.0;
+    ds.stage[9][0] = ds.stage[9][1] = ds.stage[9][3] = 1.5;
+    EqOCP pn2 = pn;
+    for (ocp::index_t i : {0, 1, 3}) {
+        for (ocp::index_t a = 0; a < nu; ++a)
+            for (ocp::index_t b = 0; b < nu; ++b)
+                pn2.R[9](a, b) += 1.5 * D[9](i, a) * D[9](i, b);
+        for (ocp::index_t a = 0; a < nu; ++a)
+            for (ocp::index_t b = 0; b < nx; ++b)
+                pn2.S[9](a, b) += 1.5 * D[9](i, a) * C[9](i, b);
+        for (ocp::index_t a = 0; a < nx; ++a)
+            for (ocp::index_t b = 0; b < nx; ++b)
+                pn2.Q[9](a, b) += 1.5 * C[9](i, a) * C[9](i, b);
+    }
+    kkt::UpdateReport r2 = kkt::update(f, pn2, C, D, ct, ds);
+    CHECK(r2.columns_refactored == 1 && r2.columns_updated == 0, "rank 3 >= rho nx: refactored");
+    EqSolution s2 = kkt::solve(f, pn2, EqRhs::of_problem(pn2));
+    CHECK(rel_err(s2, kkt::solve_problem(pn2, FactorOptions{4})) <= 1e-8, "refactor path %.3e",
+          rel_err(s2, kkt::solve_problem(pn2, FactorOptions{4})));
     Vec d = kkt::active_set_delta({true, false, true}, {false, false, true}, {1.0, 2.0, 3.0});
     CHECK(d[0] == -1.0 && d[1] == 0.0 && d[2] == 0.0, "active_set_delta");
 }
