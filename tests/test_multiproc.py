@@ -81,3 +81,61 @@ def test_shard_bounds_cover_exactly():
                 assert s == pos
                 pos += c
             assert max(c for _, c in got) - min(c for _, c in got) <= 1
+
+
+def _gpu_worker(rank, world, port, out_dir):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_09058_b200 import kkt, shard
+
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    p, start = shard.generate_shard(1, 7, rank, world, total=9, N=32)
+    sol = kkt.solve_problem(p, kkt.FactorOptions(P=16), ctx=kkt.Context(rank))
+    full = shard.gather_solutions(sol)
+    if rank == 0:
+        with open(os.path.join(out_dir, "gpu.pkl"), "wb") as fh:
+            pickle.dump({"u": full.u, "x": full.x, "lam": full.lam}, fh)
+    dist.destroy_process_group()
+
+
+def _gpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_gpus() < 2, reason="needs 2 GPUs")
+def test_two_gpu_ranks_match_single_gpu(tmp_path):
+    # one process per GPU, each solving its strong-scaling shard on its own
+    # context (kkt.Context(local_rank)); the gathered batch equals the
+    # single-GPU solve of the whole batch bit for bit
+    mp.spawn(_gpu_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    with open(tmp_path / "gpu.pkl", "rb") as fh:
+        r = pickle.load(fh)
+    from paper_2512_09058_b200 import kkt, synth
+    whole = synth.generate(1, seed=7, batch=9, N=32)
+    ref = kkt.solve_problem(whole, kkt.FactorOptions(P=16))
+    for k in ("u", "x", "lam"):
+        assert np.array_equal(r[k], getattr(ref, k)), k
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_gpus() < 2, reason="needs 2 GPUs")
+def test_bench_two_ranks_strong_scaling():
+    import json
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--config", "1", "--extra", "none", "--steps", "2", "--warmup", "3", "--no-cpu"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900).stdout
+    line = json.loads([ln for ln in out.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["config"]["batch"] == 1024 and line["config"]["batch_per_gpu"] == 512
+    assert line["parity"]["ok"]
