@@ -256,20 +256,34 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
     // the owner factors its diagonal tile dg (L_kk, upper zeroed) and
     // publishes L_kk^{-1} -> linv[kb & 1] (identity tile carried through the
     // pivot steps gives L^{-T}; transposed through shared memory)
+    // The next pivot is computed in every lane from values shuffled one step
+    // early (d = (k+1, k+1), u = (k+1, k) before this step's update):
+    // pv' = d - (u iv)^2, the owner lane's exact fma -- no shuffle on the
+    // rsqrt -> mul -> fma pivot chain (as riccati_warp.cu; bit-identical)
     auto factor_diag = [&](int kb, double dfloor, int s) {
         Frag idt{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0};
+        double pvn = 0.0;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
             const int src = kk / 2;
             const double vk = (kk & 1) ? dg.b : dg.a;
-            const double pv = __shfl_sync(0xffffffffu, vk, 4 * kk + src);
+            const double pv = kk == 0 ? __shfl_sync(0xffffffffu, vk, 4 * kk + src) : pvn;
             const double urk = __shfl_sync(0xffffffffu, vk, 4 * rq + src);
             const double uc0 = __shfl_sync(0xffffffffu, vk, 4 * cq + src);
             const double uc1 = __shfl_sync(0xffffffffu, vk, 4 * (cq + 1) + src);
+            double dn = 0.0, un = 0.0;
+            if (kk + 1 < 8) {
+                dn = __shfl_sync(0xffffffffu, ((kk + 1) & 1) ? dg.b : dg.a, 4 * (kk + 1) + (kk + 1) / 2);
+                un = __shfl_sync(0xffffffffu, vk, 4 * (kk + 1) + src);
+            }
             const bool first = !(pv > dfloor && isfinite(pv)) && fail_piv < 0;
             fail_piv = first ? 8 * kb + kk : fail_piv;
             fail_stage = first ? s : fail_stage;
             const double iv = rsqrt_nr(pv);
+            if (kk + 1 < 8) {
+                const double l = un * iv;
+                pvn = fma(-l, l, dn);
+            }
             const double lc0 = (cq > kk) ? uc0 * iv : 0.0;
             const double lc1 = (cq + 1 > kk) ? uc1 * iv : 0.0;
             const double lrk = urk * iv;
@@ -278,8 +292,8 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                 dg.b = (q2 == src) ? nv : dg.b;
             else
                 dg.a = (q2 == src) ? nv : dg.a;
-            dg.a -= lrk * lc0;
-            dg.b -= lrk * lc1;
+            dg.a = fma(-lrk, lc0, dg.a);
+            dg.b = fma(-lrk, lc1, dg.b);
             const double vq = (kk & 1) ? idt.b : idt.a;
             const double xrq = __shfl_sync(0xffffffffu, vq, 4 * rq + src) * iv;
             if (kk & 1)
