@@ -132,7 +132,11 @@ __device__ __forceinline__ void tile_solve(const double *L, double *r, double *s
 } // namespace
 
 template <int NU, int NX, int WPB>
+#ifdef CYQ_BT_MINB
+__global__ void __launch_bounds__(32 * WPB, CYQ_BT_MINB) backsub_tile_kernel(BacksubArgs a) {
+#else
 __global__ void __launch_bounds__(32 * WPB) backsub_tile_kernel(BacksubArgs a) {
+#endif
     using B = BT<NU, NX>;
     constexpr int NUX = B::NUX, CT = B::CT, XT = B::XT, XT0 = B::XT0;
     extern __shared__ __align__(16) double sm[];
@@ -187,14 +191,18 @@ __global__ void __launch_bounds__(32 * WPB) backsub_tile_kernel(BacksubArgs a) {
             const bool in = j1 < N;
             const double *Bg = a.p.B + ((size_t)b * N + j1) * NX * NU;
             const double *Ag = a.p.A + ((size_t)b * N + j1) * NX * NX;
-            static_assert(NX % 32 == 0 && NX <= 64 && NU <= 32, "zn layout");
+            static_assert(NX % 16 == 0 && NX <= 64 && NU <= 32, "zn layout");
             const double za0 = z[NU + 2 * lane], za1 = z[NU + 2 * lane + 1];
             const double zb = lane < NU ? z[lane] : 0.0;
+            // 16 rows per pass (16 partials per lane: 64 registers, no
+            // spills): a 4-step butterfly leaves row r0 + (lane & 15) in
+            // lanes l and l ^ 16 (each half of the columns), one more xor
+            // adds the halves
 #pragma unroll
-            for (int r0 = 0; r0 < NX; r0 += 32) {
-                double pr[32];
+            for (int r0 = 0; r0 < NX; r0 += 16) {
+                double pr[16];
 #pragma unroll
-                for (int r = 0; r < 32; ++r) {
+                for (int r = 0; r < 16; ++r) {
                     double acc = 0.0;
                     if (in) {
                         if (j1 != 0 && 2 * lane < NX) {
@@ -209,7 +217,7 @@ __global__ void __launch_bounds__(32 * WPB) backsub_tile_kernel(BacksubArgs a) {
                 // reduce-scatter: after step h, lane keeps the rows whose bit
                 // h matches its own
 #pragma unroll
-                for (int h = 16; h >= 1; h >>= 1) {
+                for (int h = 8; h >= 1; h >>= 1) {
 #pragma unroll
                     for (int r = 0; r < h; ++r) {
                         const bool up = (lane & h) != 0;
@@ -218,7 +226,9 @@ __global__ void __launch_bounds__(32 * WPB) backsub_tile_kernel(BacksubArgs a) {
                         pr[r] = keep + __shfl_xor_sync(0xffffffffu, send, h);
                     }
                 }
-                zn[r0 + lane] = pr[0];
+                const double row = pr[0] + __shfl_xor_sync(0xffffffffu, pr[0], 16);
+                if (lane < 16)
+                    zn[r0 + lane] = row;
             }
             __syncwarp();
             // t = w - L_Q' zn

@@ -19,7 +19,10 @@ p = synth.generate(cfg, seed=0, batch=batch)
 dev = EqOCPBatch.__new__(EqOCPBatch)
 for k in OCP_FIELDS:
     setattr(dev, k, torch.from_numpy(getattr(p, k)).cuda())
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)
 ctx = kkt.Context(0)
+ctx.set_stream(stream.cuda_stream)
 opts = kkt.FactorOptions(P=c.P)
 sol = kkt.solve_problem(dev, opts, ctx=ctx)
 ctx.profile(True)
