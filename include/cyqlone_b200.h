@@ -254,6 +254,7 @@ int cyq_line_search_batch(cyq_ctx *ctx, int64_t batch, int64_t m,
 #define CYQ_PANEL_CTA 3       /* one CTA per chain (large tile-aligned blocks) */
 #define CYQ_PANEL_GENERIC 4   /* runtime-shape CTA kernel */
 #define CYQ_PANEL_WARP_TMEM 5 /* warp kernel with W in tensor memory */
+#define CYQ_PANEL_CTA_TMA 6   /* CTA kernel staging [B A] with TMA bulk copies */
 
 #define CYQ_SCHUR_AUTO 0   /* fused one-kernel Schur + CR */
 #define CYQ_SCHUR_LEVELS 1 /* per-level batch-wide tile kernels */

@@ -22,7 +22,7 @@ OPTIONS = {"panel": 0, "schur": 1, "schur_warps": 2, "schur_cluster": 3, "split"
            "backsub": 5, "fused_augment": 6, "panel_warps": 7, "tail": 8, "phase_prof": 9,
            "async_status": 10, "graphs": 11, "vlen": 12}
 OPTION_VALUES = {
-    "panel": {"auto": 0, "warp": 1, "two_warp": 2, "cta": 3, "generic": 4, "warp_tmem": 5},
+    "panel": {"auto": 0, "warp": 1, "two_warp": 2, "cta": 3, "generic": 4, "warp_tmem": 5, "cta_tma": 6},
     "schur": {"auto": 0, "levels": 1, "scalar": 2},
     "backsub": {"auto": 0, "generic": 1},
     "tail": {"cr1": 0, "pcr": 1, "pcg": 2},

@@ -428,6 +428,7 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
             case CYQ_PANEL_WARP_TMEM: done = launch_riccati_warp(g, ctx->stream, ra, o); break;
             case CYQ_PANEL_TWO_WARP: done = launch_riccati_pc(g, ctx->stream, ra); break;
             case CYQ_PANEL_CTA: done = launch_riccati_cta(g, ctx->stream, ra); break;
+            case CYQ_PANEL_CTA_TMA: done = launch_riccati_cta(g, ctx->stream, ra, true); break;
             case CYQ_PANEL_GENERIC: launch_riccati(g, o, ctx->stream, ra); done = true; break;
             default: break;
             }
@@ -1218,7 +1219,7 @@ int cyq_ctx_set_option(cyq_ctx *ctx, int option, int64_t value) {
     LaunchOpts &o = ctx->opts;
     auto bad = [&] { return set_err(ctx, CYQ_INVALID_ARG, "option value out of range"); };
     switch (option) {
-    case CYQ_OPT_PANEL: if (value < 0 || value > 5) return bad(); o.panel = (int)value; break;
+    case CYQ_OPT_PANEL: if (value < 0 || value > 6) return bad(); o.panel = (int)value; break;
     case CYQ_OPT_SCHUR: if (value < 0 || value > 2) return bad(); o.schur = (int)value; break;
     case CYQ_OPT_SCHUR_WARPS:
         if (value != 0 && value != 2 && value != 4) return bad();

@@ -67,7 +67,7 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
 // Kernel selection of a context (cyq_ctx_set_option, include/cyqlone_b200.h);
 // the defaults pick the fastest measured kernel per shape.
 struct LaunchOpts {
-    int panel = 0;         // CYQ_PANEL_*: 0 auto, 1 warp, 2 two-warp, 3 CTA, 4 generic, 5 warp + TMEM
+    int panel = 0;         // CYQ_PANEL_*: 0 auto, 1 warp, 2 two-warp, 3 CTA, 4 generic, 5 warp + TMEM, 6 CTA + TMA
     int schur = 0;         // CYQ_SCHUR_*: 0 auto (fused / big), 1 per-level tile kernels, 2 scalar
     int schur_warps = 0;   // fused Schur CTA width: 0 auto, 2 or 4 warps
     int schur_cluster = 1; // 8-CTA cluster for a few long horizons (0: never)
@@ -215,7 +215,7 @@ bool launch_riccati_warp(const Geo &g, cudaStream_t st, const RiccatiArgs &ra, c
 // for this stage shape and ny (ProbView::aD path)
 bool riccati_warp_fuses_aug(const Geo &g, int ny, const LaunchOpts &o);
 // CTA-per-chain kernel for large tile-aligned panels (riccati_cta.cu); false if n/a
-bool launch_riccati_cta(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
+bool launch_riccati_cta(const Geo &g, cudaStream_t st, const RiccatiArgs &ra, bool tma = false);
 // producer/consumer two-warp-per-chain kernel (riccati_pc.cu); false if n/a
 bool launch_riccati_pc(const Geo &g, cudaStream_t st, const RiccatiArgs &ra);
 // tile-based Schur assembly + CR factorization (compile-time nx); false if n/a

@@ -94,7 +94,8 @@ template <int NU, int NX, int NW> struct CS {
     static constexpr int O_RU0 = O_MW + NX;                        // NU
     static constexpr int O_RED = O_RU0 + NU;                       // 32 (pivot floor)
     static constexpr int O_SCR = O_RED + 32;                       // 64 (transpose)
-    static constexpr int SMEM = O_SCR + kTileElems;
+    static constexpr int O_MB = O_SCR + kTileElems;                // 1 mbarrier ([B A] staging)
+    static constexpr int SMEM = O_MB + 2;
     __host__ __device__ static constexpr int T(int i, int j) { return i * (i + 1) / 2 + j; }
     // stored-factor tile index of panel tile (i, j), j < CT
     __host__ __device__ static constexpr int PI(int i, int j) {
@@ -107,10 +108,16 @@ __device__ __forceinline__ void pf_lines(const double *p, int bytes, int tid, in
         asm volatile("prefetch.global.L2 [%0];\n" ::"l"(reinterpret_cast<const char *>(p) + o));
 }
 
-// [B A]_j -> BA rows (A omitted for j = 0, zero for padding stages), f_j
-template <int NU, int NX, int NW>
+// [B A]_j -> BA rows (A omitted for j = 0, zero for padding stages), f_j.
+// TMA bulk copies (cp.async.bulk, one issuing thread, one copy per row into
+// the padded row layout, completion counted in bytes on `mbar`); omitted /
+// padding blocks zero-filled by all threads; per-thread cp.async when a
+// source is not 16-byte aligned (then `mbar` gets a plain arrival and the
+// waiter's cp.async.wait_group covers the copies). Every call is matched by
+// one wait_BA.
+template <int NU, int NX, int NW, bool TMA>
 __device__ __forceinline__ void stage_BA_cta(const Geo &g, const ProbView &p, int b, int j, double *sm,
-                                             int tid) {
+                                             int tid, unsigned long long *mbar) {
     using C = CS<NU, NX, NW>;
     constexpr int NTH = 32 * NW;
     const int N = g.N;
@@ -118,12 +125,47 @@ __device__ __forceinline__ void stage_BA_cta(const Geo &g, const ProbView &p, in
     const bool in = j < N;
     const double *Bs = in ? p.B + ((size_t)b * N + j) * NX * NU : nullptr;
     const double *As = (in && j != 0) ? p.A + ((size_t)b * N + j) * NX * NX : nullptr;
-    const bool al = ((reinterpret_cast<uintptr_t>(Bs) | reinterpret_cast<uintptr_t>(As)) & 15) == 0;
+    const double *fs = in ? (p.fd ? p.fd : p.f) + ((size_t)b * N + j) * NX : nullptr;
+    const bool al = ((reinterpret_cast<uintptr_t>(Bs) | reinterpret_cast<uintptr_t>(As) |
+                      reinterpret_cast<uintptr_t>(fs)) & 15) == 0 && (NU * 8) % 16 == 0 && (NX * 8) % 16 == 0;
+    if (TMA && al) {
+        // the last warp issues: one lane announces the bytes, then every
+        // lane issues its share of the row copies
+        if (tid >= NTH - 32) {
+            const int l = tid - (NTH - 32);
+            if (l == 0) {
+                const unsigned bytes = (Bs ? NX * NU * 8 : 0) + (As ? NX * NX * 8 : 0) + (fs ? NX * 8 : 0);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)),
+                             "r"(bytes)
+                             : "memory");
+            }
+            __syncwarp();
+            auto bulk = [&](double *dst, const double *src, unsigned nbytes) {
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                 smem_u32(dst)),
+                             "l"(src), "r"(nbytes), "r"(smem_u32(mbar))
+                             : "memory");
+            };
+            for (int r = l; Bs && r < NX; r += 32)
+                bulk(ba + r * C::PW, Bs + r * NU, NU * 8);
+            for (int r = l; As && r < NX; r += 32)
+                bulk(ba + r * C::PW + NU, As + r * NX, NX * 8);
+            if (fs && l == 0)
+                bulk(sm + C::O_F, fs, NX * 8);
+        }
+        for (int e = tid; !Bs && e < NX * NU; e += NTH)
+            ba[(e / NU) * C::PW + e % NU] = 0.0;
+        for (int e = tid; !As && e < NX * NX; e += NTH)
+            ba[(e / NX) * C::PW + NU + e % NX] = 0.0;
+        for (int e = tid; !fs && e < NX; e += NTH)
+            sm[C::O_F + e] = 0.0;
+        return;
+    }
     for (int e = 2 * tid; e < NX * NU; e += 2 * NTH) {
         double *d = ba + (e / NU) * C::PW + e % NU;
-        if (Bs && al)
+        if (Bs && al) {
             cp16(d, Bs + e);
-        else if (Bs) {
+        } else if (Bs) {
             cp8(d, Bs + e);
             cp8(d + 1, Bs + e + 1);
         } else
@@ -131,21 +173,31 @@ __device__ __forceinline__ void stage_BA_cta(const Geo &g, const ProbView &p, in
     }
     for (int e = 2 * tid; e < NX * NX; e += 2 * NTH) {
         double *d = ba + (e / NX) * C::PW + NU + e % NX;
-        if (As && al)
+        if (As && al) {
             cp16(d, As + e);
-        else if (As) {
+        } else if (As) {
             cp8(d, As + e);
             cp8(d + 1, As + e + 1);
         } else
             d[0] = d[1] = 0.0;
     }
-    const double *fs = (p.fd ? p.fd : p.f);
     for (int e = tid; e < NX; e += NTH) {
-        if (in)
-            cp8(sm + C::O_F + e, fs + ((size_t)b * N + j) * NX + e);
+        if (fs)
+            cp8(sm + C::O_F + e, fs + e);
         else
             sm[C::O_F + e] = 0.0;
     }
+    cp_commit();
+    if (tid == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar)) : "memory");
+}
+
+// completion of the matching stage_BA_cta (phase `ph`, then advanced); the
+// caller's __syncthreads makes the zero fills visible
+__device__ __forceinline__ void wait_BA(unsigned long long *mbar, int &ph) {
+    cp_wait<0>();
+    mb_wait(mbar, ph & 1);
+    ++ph;
 }
 
 // initial value of panel tile (ti, tj), tj < CT: H_s (top), [B A]_0 rows at
@@ -200,7 +252,7 @@ __device__ __forceinline__ Frag init_tile(int ti, int tj, int rq, int cq, int s,
 
 } // namespace
 
-template <int NU, int NX, int NW>
+template <int NU, int NX, int NW, bool TMA>
 __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) {
     using C = CS<NU, NX, NW>;
     constexpr int NTH = 32 * NW, MAXL = C::MAXL, CT = C::CT, TT = C::TT;
@@ -229,12 +281,17 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
 #define LTJ(k) ((int)(c_list[warp * kMaxL + (k)] & 255))
     for (int i = tid; i < C::SMEM; i += NTH)
         sm[i] = 0.0;
+    unsigned long long *bamb = reinterpret_cast<unsigned long long *>(sm + C::O_MB);
+    int baph = 0; // completed [B A] stagings (mbarrier phases)
+    if (tid == 0) {
+        mb_init(bamb, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
     // prologue: BA_0, S_0 x_init (ru[0] term)
     {
         const int j0 = g.stage_of(c, 0);
-        stage_BA_cta<NU, NX, NW>(g, a.p, b, j0, sm, tid);
-        cp_commit();
+        stage_BA_cta<NU, NX, NW, TMA>(g, a.p, b, j0, sm, tid, bamb);
         if (implicit_rhs && c == 0)
             for (int i = tid; i < NU; i += NTH) {
                 double s0 = 0;
@@ -243,7 +300,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                           __ldg(a.p.x_init + (size_t)b * NX + k);
                 ru0[i] = s0;
             }
-        cp_wait<0>();
+        wait_BA(bamb, baph);
     }
     __syncthreads();
 
@@ -387,8 +444,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         }
         __syncthreads(); // W and BA_0 reads done, pivot floor, column 0 published
         if (s == 0 && n > 1)
-            stage_BA_cta<NU, NX, NW>(g, a.p, b, g.stage_of(c, 1), sm, tid);
-        cp_commit();
+            stage_BA_cta<NU, NX, NW, TMA>(g, a.p, b, g.stage_of(c, 1), sm, tid, bamb);
         const double dfloor = 1e-14 * __longlong_as_double((long long)red[0]);
         if (dkb == 0)
             factor_diag(0, dfloor, s);
@@ -518,7 +574,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                 LQ[r * C::LQS + c0] = dg.a;
                 LQ[r * C::LQS + c0 + 1] = dg.b;
             }
-            cp_wait<0>(); // BA_{s+1}, f_{s+1}
+            wait_BA(bamb, baph); // BA_{s+1}, f_{s+1}
             __syncthreads();
             if (ph) ph[s * 8 + 4] = clock64();
             // -wl_new = L_Q' (sgn f) + x'   (kkt_solve.cpp:85-90): 8 lanes per
@@ -561,8 +617,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
             for (int t = tid; t < NX; t += NTH)
                 Wsm[(C::RT * C::NXC + t / 8) * kTileElems + C::RR * 8 + t % 8] = mw[t];
             if (s + 2 < n)
-                stage_BA_cta<NU, NX, NW>(g, a.p, b, g.stage_of(c, s + 2), sm, tid);
-            cp_commit();
+                stage_BA_cta<NU, NX, NW, TMA>(g, a.p, b, g.stage_of(c, s + 2), sm, tid, bamb);
             __syncthreads();
         }
     }
@@ -590,14 +645,14 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
 }
 
 namespace {
-template <int NU, int NX, int NW> bool launch_c(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
+template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
     if (g.nu != NU || g.nx != NX)
         return false;
     using C = CS<NU, NX, NW>;
     const size_t smem = (size_t)C::SMEM * sizeof(double);
     static DeviceOnce once;
     once_per_device(once, [&]() -> cudaError_t {
-        const cudaError_t e0 = cudaFuncSetAttribute(riccati_cta_kernel<NU, NX, NW>,
+        const cudaError_t e0 = cudaFuncSetAttribute(riccati_cta_kernel<NU, NX, NW, TMA>,
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e0 != cudaSuccess)
             return e0;
@@ -681,13 +736,15 @@ template <int NU, int NX, int NW> bool launch_c(const Geo &g, cudaStream_t st, c
         const cudaError_t e1 = cudaMemcpyToSymbol(c_list, h, sizeof h);
         return e1 != cudaSuccess ? e1 : cudaMemcpyToSymbol(c_cnt, cnt, sizeof cnt);
     });
-    riccati_cta_kernel<NU, NX, NW><<<ra.grid_chains(), 32 * NW, smem, st>>>(ra);
+    riccati_cta_kernel<NU, NX, NW, TMA><<<ra.grid_chains(), 32 * NW, smem, st>>>(ra);
     return true;
 }
 } // namespace
 
-bool launch_riccati_cta(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
-    return launch_c<32, 64, 16>(g, st, ra);
+// tma: stage [B A] with TMA bulk copies instead of cp.async (opt-in,
+// CYQ_PANEL_CTA_TMA: measured 35.2 vs 32.3 ms at config 3)
+bool launch_riccati_cta(const Geo &g, cudaStream_t st, const RiccatiArgs &ra, bool tma) {
+    return tma ? launch_c<32, 64, 16, true>(g, st, ra) : launch_c<32, 64, 16, false>(g, st, ra);
 }
 
 } // namespace cyqb

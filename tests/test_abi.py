@@ -45,7 +45,8 @@ LIVE_DMMA_KERNELS = [
     "riccati_warp_kernelILi8ELi16ELi1ELi24ELb0",   # config 4 panel (fused Newton assembly)
     "riccati_pc_kernelILi5ELi10",                  # config 0 panel
     "riccati_pc_kernelILi4ELi12",                  # config 2 panel
-    "riccati_cta_kernelILi32ELi64ELi16",           # config 3 panel
+    "riccati_cta_kernelILi32ELi64ELi16ELb0",       # config 3 panel
+    "riccati_cta_kernelILi32ELi64ELi16ELb1",       # config 3 panel, TMA-staged variant
     "schur_fused_kernelILi20ELi2ELi1",             # config 1 Schur/CR (batch > 4 x SMs)
     "schur_fused_kernelILi20ELi4ELi1",
     "schur_fused_kernelILi16ELi4ELi1",             # config 4 Schur/CR
@@ -88,3 +89,12 @@ def test_no_device_fails_loudly():
     p = synth.generate(0, seed=0, batch=1, N=8)
     with pytest.raises(kkt.CudaError):
         kkt.solve_problem(p, kkt.FactorOptions(P=4))
+
+
+def test_tma_variant_issues_bulk_copies():
+    # the TMA-staged CTA panel carries UBLKCP (cp.async.bulk) in its SASS
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    funcs = {f.split("\n", 1)[0]: f for f in out.split("Function : ")[1:]}
+    tma = [f for k, f in funcs.items() if "riccati_cta_kernelILi32ELi64ELi16ELb1" in k]
+    assert tma and "UBLKCP" in tma[0]

@@ -153,3 +153,18 @@ def test_config4_fused_newton_full_batch_vs_unfused():
     with ctx.options(fused_augment=0):
         two = _host(kkt.solve_newton(*args, ctx=ctx))
     assert rel_error(fused, two).max() <= 1e-10
+
+
+def test_config3_tma_staging_variant_matches_oracle(oracle):
+    # opt-in CTA panel staging [B A] with TMA bulk copies (cp.async.bulk,
+    # mbarrier complete_tx): same results as the cp.async default
+    p = synth.generate(3, seed=25, batch=2)
+    ctx = kkt.Context.default()
+    with ctx.options(panel="cta_tma"):
+        sol = kkt.solve_problem(p, kkt.FactorOptions(P=32))
+    ref, rc, _ = oracle.solve_problem(p, 32)
+    assert rc == 0
+    assert rel_error(sol, ref).max() <= REL_TOL
+    base = kkt.solve_problem(p, kkt.FactorOptions(P=32))
+    for k in ("u", "x", "lam"):
+        assert np.array_equal(getattr(sol, k), getattr(base, k))
