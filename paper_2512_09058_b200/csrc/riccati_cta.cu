@@ -744,6 +744,8 @@ template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStre
 // tma: stage [B A] with TMA bulk copies instead of cp.async (opt-in,
 // CYQ_PANEL_CTA_TMA: measured 35.2 vs 32.3 ms at config 3)
 bool launch_riccati_cta(const Geo &g, cudaStream_t st, const RiccatiArgs &ra, bool tma) {
+    // 16 warps per chain CTA: 13 / 14 / 20 / 24 warps measured 38.6 / 36.3
+    // / 37.9 / 38.9 ms vs 32.3 ms at config 3
     return tma ? launch_c<32, 64, 16, true>(g, st, ra) : launch_c<32, 64, 16, false>(g, st, ra);
 }
 
