@@ -55,14 +55,19 @@ __device__ __forceinline__ Frag ld_frag_t(const double *tile, int lane) {
     return {tile[cq * 8 + rq], tile[(cq + 1) * 8 + rq]};
 }
 
-// workspace loads bypass L1 (ld.global.cg): blocks are rewritten in place by
-// other warps -- and, in the cluster variant, by other SMs -- between phases
-__device__ __forceinline__ Frag ldw(const double *tile, int lane) {
-    const double2 v = __ldcg(reinterpret_cast<const double2 *>(tile) + lane);
+// workspace loads: ld.global.cg (L2) when the blocks are rewritten by other
+// SMs (the cluster variant), ld.global.ca (L1 + L2) when one CTA owns the
+// instance -- the CTA's own global stores invalidate its L1 lines, and the
+// __syncthreads between phases orders them (config 0 Schur: 25 -> 21 us)
+template <bool L1> __device__ __forceinline__ Frag ldw(const double *tile, int lane) {
+    const double2 v = L1 ? __ldca(reinterpret_cast<const double2 *>(tile) + lane)
+                         : __ldcg(reinterpret_cast<const double2 *>(tile) + lane);
     return {v.x, v.y};
 }
-__device__ __forceinline__ Frag ldw_t(const double *tile, int lane) {
+template <bool L1> __device__ __forceinline__ Frag ldw_t(const double *tile, int lane) {
     const int rq = lane >> 2, cq = 2 * (lane & 3);
+    if (L1)
+        return {__ldca(tile + cq * 8 + rq), __ldca(tile + (cq + 1) * 8 + rq)};
     return {__ldcg(tile + cq * 8 + rq), __ldcg(tile + (cq + 1) * 8 + rq)};
 }
 
@@ -77,7 +82,7 @@ __device__ __forceinline__ double fac_elem(const Geo &g, const double *st, int r
 
 // y = M v (FULL: XT x XT tiles; else lower tiles T(i, j)); v: XP doubles in
 // shared memory; out[i] = row 8 i + rq, valid in every lane of the quad
-template <int XT, bool FULL>
+template <int XT, bool FULL, bool L1>
 __device__ __forceinline__ void matvec(const double *M, const double *v, double (&out)[XT], int lane) {
     const int cq = 2 * (lane & 3);
 #pragma unroll
@@ -87,7 +92,7 @@ __device__ __forceinline__ void matvec(const double *M, const double *v, double 
         for (int j = 0; j < XT; ++j) {
             if (!FULL && j > i)
                 continue;
-            const Frag f = ldw(M + (FULL ? fidx(XT, i, j) : T(i, j)) * kTileElems, lane);
+            const Frag f = ldw<L1>(M + (FULL ? fidx(XT, i, j) : T(i, j)) * kTileElems, lane);
             acc = fma(f.a, v[8 * j + cq], acc);
             acc = fma(f.b, v[8 * j + cq + 1], acc);
         }
@@ -97,7 +102,7 @@ __device__ __forceinline__ void matvec(const double *M, const double *v, double 
     }
 }
 // y = M' v; out[j][h] = entry 8 j + cq + h, valid in every lane with that cq
-template <int XT, bool FULL>
+template <int XT, bool FULL, bool L1>
 __device__ __forceinline__ void matvec_t(const double *M, const double *v, double (&out)[XT][2],
                                          int lane) {
     const int rq = lane >> 2;
@@ -108,7 +113,7 @@ __device__ __forceinline__ void matvec_t(const double *M, const double *v, doubl
         for (int i = 0; i < XT; ++i) {
             if (!FULL && j > i)
                 continue;
-            const Frag f = ldw(M + (FULL ? fidx(XT, i, j) : T(i, j)) * kTileElems, lane);
+            const Frag f = ldw<L1>(M + (FULL ? fidx(XT, i, j) : T(i, j)) * kTileElems, lane);
             const double vi = v[8 * i + rq];
             a0 = fma(f.a, vi, a0);
             a1 = fma(f.b, vi, a1);
@@ -155,7 +160,7 @@ __device__ __forceinline__ void matvec_r(const Frag (&M)[N], const double *v, do
     }
 }
 // y = M v with M upper triangular stored as tiles T(j, i) (memory)
-template <int XT>
+template <int XT, bool L1>
 __device__ __forceinline__ void matvec_upper(const double *M, const double *v, double (&out)[XT],
                                              int lane) {
     const int cq = 2 * (lane & 3);
@@ -164,7 +169,7 @@ __device__ __forceinline__ void matvec_upper(const double *M, const double *v, d
         double acc = 0.0;
 #pragma unroll
         for (int j = i; j < XT; ++j) {
-            const Frag f = ldw(M + T(j, i) * kTileElems, lane);
+            const Frag f = ldw<L1>(M + T(j, i) * kTileElems, lane);
             acc = fma(f.a, v[8 * j + cq], acc);
             acc = fma(f.b, v[8 * j + cq + 1], acc);
         }
@@ -258,6 +263,7 @@ template <int NX, int NW, int CL>
 __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_kernel(SchurArgs a) {
     using F = SF<NX>;
     constexpr int XT = F::XT, NL = F::NL, NF = F::NF, XP = F::XP;
+    constexpr bool L1 = CL == 1;
     constexpr long long TL = 64LL * NL, TF = 64LL * NF;
     extern __shared__ __align__(16) double sm[];
     const Geo &g = a.g;
@@ -401,7 +407,7 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                 scr[lane] = lane < NX ? __ldg(yv + lane) : 0.0;
             __syncwarp();
             double o[XT];
-            matvec_upper<XT>(ws + Lo.Tt + c * TL, scr, o, lane);
+            matvec_upper<XT, L1>(ws + Lo.Tt + c * TL, scr, o, lane);
 #pragma unroll
             for (int i = 0; i < XT; ++i)
                 if (q2 == 0)
@@ -441,11 +447,11 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
     // M_i of the level-l reduced system (see SFLayout)
     auto m_at = [&](int l, int i, int ti, int tj) -> Frag {
         if (l == 0)
-            return fadd(ldw(D + i * TL + T(ti, tj) * kTileElems, lane),
-                        ldw(Mb + ((i + 1) % P) * TL + T(ti, tj) * kTileElems, lane));
-        Frag f = ldw(D + (i << l) * TL + T(ti, tj) * kTileElems, lane);
+            return fadd(ldw<L1>(D + i * TL + T(ti, tj) * kTileElems, lane),
+                        ldw<L1>(Mb + ((i + 1) % P) * TL + T(ti, tj) * kTileElems, lane));
+        Frag f = ldw<L1>(D + (i << l) * TL + T(ti, tj) * kTileElems, lane);
         if (i > 0)
-            f = fsub(f, ldw(D + ((i << l) - (1 << (l - 1))) * TL + T(ti, tj) * kTileElems, lane));
+            f = fsub(f, ldw<L1>(D + ((i << l) - (1 << (l - 1))) * TL + T(ti, tj) * kTileElems, lane));
         return f;
     };
     const int Tb = Lo.T, Lc = Lo.crl; // PCR tail blocks, CR levels before it
@@ -502,8 +508,8 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                     Frag kp[XT], kk[XT];
 #pragma unroll
                     for (int t = 0; t < XT; ++t) {
-                        kp[t] = ldw_t(Kp + fidx(XT, t, i) * kTileElems, lane); // (K_{k-1}')(i, t)
-                        kk[t] = has_y ? ldw(Kk + fidx(XT, i, t) * kTileElems, lane) : Frag{0.0, 0.0};
+                        kp[t] = ldw_t<L1>(Kp + fidx(XT, t, i) * kTileElems, lane); // (K_{k-1}')(i, t)
+                        kk[t] = has_y ? ldw<L1>(Kk + fidx(XT, i, t) * kTileElems, lane) : Frag{0.0, 0.0};
                     }
 #pragma unroll
                     for (int j = 0; j < XT; ++j) {
@@ -583,9 +589,9 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
 #pragma unroll
                     for (int j = 0; j <= i; ++j)
                         Lt[T(i, j)] = Lo.levels == 0
-                                          ? fadd(ldw(D + T(i, j) * kTileElems, lane),
-                                                 ldw(Mb + T(i, j) * kTileElems, lane))
-                                          : ldw(D + T(i, j) * kTileElems, lane);
+                                          ? fadd(ldw<L1>(D + T(i, j) * kTileElems, lane),
+                                                 ldw<L1>(Mb + T(i, j) * kTileElems, lane))
+                                          : ldw<L1>(D + T(i, j) * kTileElems, lane);
                 const double dfloor = 1e-14 * tiles::diag_absmax<XT>(Lt, NX, lane);
                 int pf = -1;
                 Frag Li[NL];
@@ -608,7 +614,7 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                         if (q2 == 0)
                             xs[8 * i + rq] = o[i];
                     __syncwarp();
-                    matvec_t<XT, false>(ws + Lo.Lb, xs, o2, lane);
+                    matvec_t<XT, false, L1>(ws + Lo.Lb, xs, o2, lane);
                     __syncwarp();
 #pragma unroll
                     for (int j = 0; j < XT; ++j)
@@ -629,7 +635,7 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
             // (PCRFactor::resolve) runs inside the levels.
             auto pm = [&](int pl, int k, int ti, int tj) -> Frag {
                 return pl == 0 ? m_at(Lc, k, ti, tj)
-                               : ldw(ws + Lo.PM + ((pl - 1) & 1) * Tb * TL + k * TL + T(ti, tj) * kTileElems,
+                               : ldw<L1>(ws + Lo.PM + ((pl - 1) & 1) * Tb * TL + k * TL + T(ti, tj) * kTileElems,
                                      lane);
             };
             auto pk = [&](int pl, int k) -> const double * {
@@ -672,7 +678,7 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                         __syncwarp();
                         if (fin) {
                             double o2[XT][2];
-                            matvec_t<XT, false>(Lio, xk, o2, lane);
+                            matvec_t<XT, false, L1>(Lio, xk, o2, lane);
                             __syncwarp();
 #pragma unroll
                             for (int j = 0; j < XT; ++j)
@@ -694,8 +700,8 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                         Frag kp[XT], kk[XT];
 #pragma unroll
                         for (int t = 0; t < XT; ++t) {
-                            kp[t] = Kp ? ldw_t(Kp + fidx(XT, t, i) * kTileElems, lane) : Frag{0.0, 0.0};
-                            kk[t] = ldw(Kk + fidx(XT, i, t) * kTileElems, lane);
+                            kp[t] = Kp ? ldw_t<L1>(Kp + fidx(XT, t, i) * kTileElems, lane) : Frag{0.0, 0.0};
+                            kk[t] = ldw<L1>(Kk + fidx(XT, i, t) * kTileElems, lane);
                         }
 #pragma unroll
                         for (int j = 0; j < XT; ++j) {
@@ -728,14 +734,14 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
 #pragma unroll
                             for (int t = 0; t < XT; ++t) {
                                 if (j <= i && lo)
-                                    tile_gemm_nt(yy, ldw(Yl + fidx(XT, i, t) * kTileElems, lane),
-                                                 ldw(Yl + fidx(XT, j, t) * kTileElems, lane));
+                                    tile_gemm_nt(yy, ldw<L1>(Yl + fidx(XT, i, t) * kTileElems, lane),
+                                                 ldw<L1>(Yl + fidx(XT, j, t) * kTileElems, lane));
                                 if (hi) {
-                                    const Frag ui = ldw(Uh + fidx(XT, i, t) * kTileElems, lane);
+                                    const Frag ui = ldw<L1>(Uh + fidx(XT, i, t) * kTileElems, lane);
                                     if (j <= i)
-                                        tile_gemm_nt(uu, ui, ldw(Uh + fidx(XT, j, t) * kTileElems, lane));
-                                    tile_gemm_nt_sub(yu, ldw(Yh + fidx(XT, i, t) * kTileElems, lane),
-                                                     ldw(Uh + fidx(XT, j, t) * kTileElems, lane));
+                                        tile_gemm_nt(uu, ui, ldw<L1>(Uh + fidx(XT, j, t) * kTileElems, lane));
+                                    tile_gemm_nt_sub(yu, ldw<L1>(Yh + fidx(XT, i, t) * kTileElems, lane),
+                                                     ldw<L1>(Uh + fidx(XT, j, t) * kTileElems, lane));
                                 }
                             }
                             if (j <= i)
@@ -745,9 +751,9 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                     if (fwd_fused) { // x_k -= Y_{k-st} bt_{k-st} + U_{k+st} bt_{k+st}
                         double o1[XT], o2[XT];
                         if (lo)
-                            matvec<XT, true>(Yl, bt + (size_t)(k - st) * XP, o1, lane);
+                            matvec<XT, true, L1>(Yl, bt + (size_t)(k - st) * XP, o1, lane);
                         if (hi)
-                            matvec<XT, true>(Uh, bt + (size_t)(k + st) * XP, o2, lane);
+                            matvec<XT, true, L1>(Uh, bt + (size_t)(k + st) * XP, o2, lane);
                         double *xk = xs + (size_t)(k << Lc) * XP;
                         __syncwarp();
 #pragma unroll
@@ -774,7 +780,7 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                 for (int mm = vwarp; mm < half; mm += VNW) { // x_k <- L^{-1} x_k
                     double *xk = xs + (size_t)(2 * mm + 1) * stride * XP;
                     double o[XT];
-                    matvec<XT, false>(ws + Lo.Li + (o0 + mm) * TL, xk, o, lane);
+                    matvec<XT, false, L1>(ws + Lo.Li + (o0 + mm) * TL, xk, o, lane);
                     __syncwarp();
 #pragma unroll
                     for (int i = 0; i < XT; ++i)
@@ -785,10 +791,10 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                 for (int mm = vwarp; mm < half; mm += VNW) { // x_e -= U x_k + Y_prev x_k'
                     double *xe = xs + (size_t)2 * mm * stride * XP;
                     double o[XT], o2[XT];
-                    matvec<XT, true>(ws + Lo.U + (o0 + mm) * TF, xs + (size_t)(2 * mm + 1) * stride * XP,
+                    matvec<XT, true, L1>(ws + Lo.U + (o0 + mm) * TF, xs + (size_t)(2 * mm + 1) * stride * XP,
                                      o, lane);
                     if (mm > 0)
-                        matvec<XT, true>(ws + Lo.Y + (o0 + mm - 1) * TF,
+                        matvec<XT, true, L1>(ws + Lo.Y + (o0 + mm - 1) * TF,
                                          xs + (size_t)(2 * mm - 1) * stride * XP, o2, lane);
                     __syncwarp();
 #pragma unroll
@@ -806,7 +812,7 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                         double *xk = xs + (size_t)(k << Lc) * XP;
                         const double *Lio = ws + Lo.PLi + (size_t)(pl * Tb + k) * TL;
                         double o[XT];
-                        matvec<XT, false>(Lio, xk, o, lane);
+                        matvec<XT, false, L1>(Lio, xk, o, lane);
                         double *dst = fin ? xk : bt + (size_t)k * XP;
                         __syncwarp();
 #pragma unroll
@@ -816,7 +822,7 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                         __syncwarp();
                         if (fin) { // x_k <- L^{-T} L^{-1} x_k
                             double o2[XT][2];
-                            matvec_t<XT, false>(Lio, xk, o2, lane);
+                            matvec_t<XT, false, L1>(Lio, xk, o2, lane);
                             __syncwarp();
 #pragma unroll
                             for (int j = 0; j < XT; ++j)
@@ -834,10 +840,10 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                         const bool lo = k >= st, hi = k + st < Tb;
                         double o1[XT], o2[XT];
                         if (lo)
-                            matvec<XT, true>(ws + Lo.PY + (size_t)(pl * Tb + k - st) * TF,
+                            matvec<XT, true, L1>(ws + Lo.PY + (size_t)(pl * Tb + k - st) * TF,
                                              bt + (size_t)(k - st) * XP, o1, lane);
                         if (hi)
-                            matvec<XT, true>(ws + Lo.PU + (size_t)(pl * Tb + k + st) * TF,
+                            matvec<XT, true, L1>(ws + Lo.PU + (size_t)(pl * Tb + k + st) * TF,
                                              bt + (size_t)(k + st) * XP, o2, lane);
                         double *xk = xs + (size_t)(k << Lc) * XP;
                         __syncwarp();
@@ -851,14 +857,14 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                 }
             } else if (vwarp == 0) { // base: x_0 <- L_b^{-T} L_b^{-1} x_0
                 double o[XT], o2[XT][2];
-                matvec<XT, false>(ws + Lo.Lb, xs, o, lane);
+                matvec<XT, false, L1>(ws + Lo.Lb, xs, o, lane);
                 __syncwarp();
 #pragma unroll
                 for (int i = 0; i < XT; ++i)
                     if (q2 == 0)
                         xs[8 * i + rq] = o[i];
                 __syncwarp();
-                matvec_t<XT, false>(ws + Lo.Lb, xs, o2, lane);
+                matvec_t<XT, false, L1>(ws + Lo.Lb, xs, o2, lane);
                 __syncwarp();
 #pragma unroll
                 for (int j = 0; j < XT; ++j)
@@ -878,10 +884,10 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                 double *xo = xs + (size_t)(2 * mm + 1) * stride * XP;
                 double t1[XT][2], t2[XT][2], t3[XT][2];
                 const bool has_y = 2 * mm + 2 < sl;
-                matvec_t<XT, true>(ws + Lo.U + (o0 + mm) * TF, xs + (size_t)2 * mm * stride * XP, t1,
+                matvec_t<XT, true, L1>(ws + Lo.U + (o0 + mm) * TF, xs + (size_t)2 * mm * stride * XP, t1,
                                    lane);
                 if (has_y)
-                    matvec_t<XT, true>(ws + Lo.Y + (o0 + mm) * TF,
+                    matvec_t<XT, true, L1>(ws + Lo.Y + (o0 + mm) * TF,
                                        xs + (size_t)((2 * mm + 2) * stride % P) * XP, t2, lane);
                 __syncwarp();
 #pragma unroll
@@ -891,7 +897,7 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                         xo[8 * j + cq + 1] -= has_y ? t1[j][1] + t2[j][1] : t1[j][1];
                     }
                 __syncwarp();
-                matvec_t<XT, false>(ws + Lo.Li + (o0 + mm) * TL, xo, t3, lane); // L^{-T} xo
+                matvec_t<XT, false, L1>(ws + Lo.Li + (o0 + mm) * TL, xo, t3, lane); // L^{-T} xo
                 __syncwarp();
 #pragma unroll
                 for (int j = 0; j < XT; ++j)
