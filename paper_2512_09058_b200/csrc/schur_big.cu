@@ -74,6 +74,36 @@ __device__ __forceinline__ void blk_axpy_lower(double *C, const double *A, const
     }
 }
 
+// C = A over all XT x XT tiles (shared -> global stream-out of a block)
+template <int XT, int NW>
+__device__ __forceinline__ void blk_copy(double *C, const double *A, int warp, int lane) {
+    for (int t = warp; t < XT * XT; t += NW)
+        st_frag(C + t * kTileElems, lane, ld_frag(A + t * kTileElems, lane));
+}
+// the lower tiles of A, zero upper tiles
+template <int XT, int NW>
+__device__ __forceinline__ void blk_copy_lower(double *C, const double *A, int warp, int lane) {
+    for (int t = warp; t < XT * XT; t += NW)
+        st_frag(C + t * kTileElems, lane, t % XT <= t / XT ? ld_frag(A + t * kTileElems, lane) : Frag{0.0, 0.0});
+}
+
+// shared-memory layout (doubles): per-warp scratch, the solve vectors (the
+// CR contributions cu / cy alias bwd_neg, dead once the rhs is assembled)
+// and two 64 x 64 working blocks: the pivot block (factored in place) and
+// L^{-1} of each elimination (T of each column in phase 1), the operands
+// the block ops read most, stay in shared memory; L^{-1} / T are streamed
+// out to the persistent factor. Two CTAs of 8 warps per SM (measured:
+// 2.57 -> 2.44 ms at config 3; four shared blocks at one 16- or 8-warp CTA
+// per SM: 3.29 / 3.88 ms -- two instances per SM hide each other's barriers)
+template <int NX, int NW> struct SBSmem {
+    static constexpr int XT = NX / 8, BLK = XT * XT * kTileElems;
+    __host__ __device__ static size_t vec(int P) {
+        const size_t bn = (size_t)P * NX > (size_t)(P / 2 + 1) * NX * 2 ? (size_t)P * NX : (size_t)(P / 2 + 1) * NX * 2;
+        return (size_t)NW * kTileElems + (size_t)P * NX + bn + 2 * NX;
+    }
+    __host__ __device__ static size_t total(int P) { return vec(P) + 2 * (size_t)BLK; }
+};
+
 template <int NX, int NW>
 __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
     constexpr int XT = NX / 8, NF = XT * XT;
@@ -88,12 +118,15 @@ __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
     double *ws = a.schur + (size_t)b * Lo.total;
     double *Tt = ws + Lo.Tt, *D = ws + Lo.D, *Mb = ws + Lo.Mb, *K = ws + Lo.K, *S1 = ws + Lo.S1,
            *S2 = ws + Lo.S2;
+    using SB = SBSmem<NX, NW>;
     double *scr = sm;                       // NW x 64
     double *xs = scr + NW * kTileElems;     // P x NX
-    double *bns = xs + (size_t)P * NX;      // P x NX
-    double *cu = bns + (size_t)P * NX;      // P/2 x NX
+    double *bns = xs + (size_t)P * NX;      // P x NX (then cu / cy)
+    double *cu = bns;                       // P/2 x NX
     double *cy = cu + (size_t)(P / 2 + 1) * NX;
-    double *v1 = cy + (size_t)(P / 2 + 1) * NX, *v2 = v1 + NX; // NX each
+    double *v1 = sm + SB::vec(P) - 2 * NX, *v2 = v1 + NX; // NX each
+    double *B0 = sm + SB::vec(P), *B1 = B0 + SB::BLK;
+    (void)S1;
     const bool fwd_fused = a.do_factor && a.do_solve;
     int fail = -1, fail_l = 0, fail_k = 0;
 
@@ -107,33 +140,35 @@ __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
         const int xt0 = nu / 8;
         double *Tc = Tt + c * TF;
         if (a.do_factor) {
-            // L_Q -> S1 (lower), LA -> S2 (full), -Mfwd -> D[c] (lower)
+            // L_Q -> B0 (lower), LA -> B1 (full), -Mfwd -> D[c] (lower)
             const double *tr = a.trail + chain * g.NTT * kTileElems;
+            double *LAb = S2, *Tb = B1; // LA (global scratch), T (shared)
             for (int t = warp; t < NF; t += NW) {
                 const int i = t / XT, j = t % XT;
-                st_frag(S2 + t * kTileElems, lane, ld_frag_g(ftile(CT + i, xt0 + j), lane));
+                st_frag(LAb + t * kTileElems, lane, ld_frag_g(ftile(CT + i, xt0 + j), lane));
                 if (j <= i) {
-                    st_frag(S1 + t * kTileElems, lane, ld_frag_g(ftile(xt0 + i, xt0 + j), lane));
+                    st_frag(B0 + t * kTileElems, lane, ld_frag_g(ftile(xt0 + i, xt0 + j), lane));
                     Frag m = ld_frag_g(tr + tri_index(i, j) * kTileElems, lane);
                     st_frag(D + c * TF + t * kTileElems, lane, Frag{-m.a, -m.b});
                 }
             }
             __syncthreads();
-            ctat::cta_trtri<XT, NW>(S1, Tc, scr, warp, lane); // Tt = L_Q^{-1}
+            ctat::cta_trtri<XT, NW>(B0, Tb, scr, warp, lane); // Tt = L_Q^{-1} (shared)
             // Mbwd = T T' (T(i,k) = Tt(k,i)', upper) ; K[c-1] = -LA T'
-            ctat::cta_gemm<XT, NW, true, true, ctat::kGeMaxIJ, true>(Mb + c * TF, nullptr, 1.0, Tc, Tc, warp, lane);
+            ctat::cta_gemm<XT, NW, true, true, ctat::kGeMaxIJ, true>(Mb + c * TF, nullptr, 1.0, Tb, Tb, warp, lane);
             double *Kc = K + (size_t)((c + P - 1) % P) * TF;
             if (c > 0)
-                ctat::cta_gemm<XT, NW, false, true, ctat::kGeJ, false>(Kc, nullptr, -1.0, S2, Tc, warp, lane);
+                ctat::cta_gemm<XT, NW, false, true, ctat::kGeJ, false>(Kc, nullptr, -1.0, LAb, Tb, warp, lane);
             else
                 blk_zero<XT, NW>(Kc, warp, lane);
+            blk_copy_lower<XT, NW>(Tc, Tb, warp, lane); // persistent T (kkt::solve), upper tiles zero
         }
         if (a.do_solve) { // bwd_neg_c = T x'_{n-1} = Tt' x'
             const double *yv = a.y + (chain * n + (n - 1)) * g.nux + nu;
             for (int k = tid; k < NX; k += 32 * NW)
                 v1[k] = __ldg(yv + k);
             __syncthreads();
-            ctat::cta_matvec<XT, NW, true, true>(Tc, v1, bns + c * NX, 1.0, false, warp, lane);
+            ctat::cta_matvec<XT, NW, true, true>(a.do_factor ? B1 : Tc, v1, bns + c * NX, 1.0, false, warp, lane);
         }
         __syncthreads();
     }
@@ -174,14 +209,14 @@ __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
             for (int mm = 0; mm < half; ++mm) {
                 const int k = 2 * mm + 1;
                 const bool has_y = k < s - 1, last = mm == half - 1;
-                double *Li = ws + Lo.Li + (out0 + mm) * TF, *U = ws + Lo.U + (out0 + mm) * TF;
-                double *Y = ws + Lo.Y + (out0 + mm) * TF;
+                double *Lig = ws + Lo.Li + (out0 + mm) * TF, *Ug = ws + Lo.U + (out0 + mm) * TF;
+                double *Yg = ws + Lo.Y + (out0 + mm) * TF;
+                double *Li = B1, *U = Ug, *Y = Yg; // L^{-1} in shared memory
                 const double *Kp = K + (size_t)((k - 1) << l) * TF, *Kk = K + (size_t)(k << l) * TF;
-                assemble(S1, k);
-                assemble(S2, 2 * mm); // the even block, used after the products
+                assemble(B0, k);
                 __syncthreads();
                 int f = -1;
-                ctat::cta_potrf_inv<XT, NW>(S1, Li, scr, NX, warp, lane, tid, f);
+                ctat::cta_potrf_inv<XT, NW>(B0, Li, scr, NX, warp, lane, tid, f);
                 if (warp == 0 && f >= 0 && fail < 0) {
                     fail = f;
                     fail_l = l;
@@ -194,6 +229,8 @@ __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
                 else
                     blk_zero<XT, NW>(Y, warp, lane);
                 __syncthreads();
+                blk_copy<XT, NW>(Lig, Li, warp, lane); // persistent CR factor
+                assemble(B0, 2 * mm); // the even block (B0's L is dead)
                 if (fwd_fused) { // x_k <- Li x_k ; contributions U x_k, Y x_k
                     double *xk = xs + (size_t)(k << l) * NX;
                     ctat::cta_matvec<XT, NW, false, true>(Li, xk, v1, 1.0, false, warp, lane);
@@ -205,7 +242,8 @@ __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
                     ctat::cta_matvec<XT, NW, false, false>(Y, xk, cy + mm * NX, 1.0, false, warp, lane);
                 }
                 // M' = M_2mm - U U' -> D[2mm << l]; CY = Y Y' -> D[k << l]; K' = -Y U' -> K[2mm << l]
-                ctat::cta_gemm<XT, NW, false, false, ctat::kAll, true>(D + (size_t)((2 * mm) << l) * TF, S2, -1.0,
+                __syncthreads();
+                ctat::cta_gemm<XT, NW, false, false, ctat::kAll, true>(D + (size_t)((2 * mm) << l) * TF, B0, -1.0,
                                                                       U, U, warp, lane);
                 ctat::cta_gemm<XT, NW, false, false, ctat::kAll, true>(D + (size_t)(k << l) * TF, nullptr, 1.0, Y,
                                                                       Y, warp, lane);
@@ -229,12 +267,14 @@ __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
         }
         // cr_factor_base
         if (Lo.levels == 0)
-            blk_axpy_lower<XT, NW>(S1, D, Mb, 1.0, warp, lane);
+            blk_axpy_lower<XT, NW>(B0, D, Mb, 1.0, warp, lane);
         else
-            blk_axpy_lower<XT, NW>(S1, D, nullptr, 0.0, warp, lane);
+            blk_axpy_lower<XT, NW>(B0, D, nullptr, 0.0, warp, lane);
         __syncthreads();
         int f = -1;
-        ctat::cta_potrf_inv<XT, NW>(S1, ws + Lo.Lb, scr, NX, warp, lane, tid, f);
+        ctat::cta_potrf_inv<XT, NW>(B0, B1, scr, NX, warp, lane, tid, f);
+        __syncthreads();
+        blk_copy<XT, NW>(ws + Lo.Lb, B1, warp, lane);
         if (warp == 0 && f >= 0 && fail < 0) {
             fail = f;
             fail_l = Lo.levels;
@@ -315,12 +355,13 @@ template <int NX> bool launch_sb(const Geo &g, cudaStream_t st, const SchurArgs 
     if (g.nx != NX)
         return false;
     constexpr int NW = 8;
-    const size_t smem = ((size_t)NW * kTileElems + (size_t)g.P * NX * 2 + (size_t)(g.P / 2 + 1) * NX * 2 +
-                         2 * NX) * sizeof(double);
-    if (smem > 200 * 1024)
+    const size_t smem = SBSmem<NX, NW>::total(g.P) * sizeof(double);
+    if (smem > 227 * 1024)
         return false;
     static DeviceOnce once;
-    once_per_device(once, [&] { return cudaFuncSetAttribute(schur_big_kernel<NX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
+    once_per_device(once, [&] {
+        return cudaFuncSetAttribute(schur_big_kernel<NX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    });
     launch_pdl(schur_big_kernel<NX, NW>, dim3(g.batch), dim3(32 * NW), smem, st, 1, sa);
     return true;
 }
