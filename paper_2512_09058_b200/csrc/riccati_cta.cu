@@ -666,12 +666,6 @@ template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStre
         double load[kMaxW][kMaxCT] = {};
         int nown[kMaxW] = {};
         const double kUpd = 2 * 16.0, kFac = 1400.0; // cycles: one tile update, one diagonal factorization
-#ifndef CYQ_CTA_KINT
-#define CYQ_CTA_KINT 0.0
-#endif
-        // the look-ahead factorization shares the FP64 pipe of its SM
-        // sub-partition with the other warps there: their DMMAs delay it
-        const double kInt = CYQ_CTA_KINT;
         auto cost = [&]() {
             double t = 0;
             for (int kb = 0; kb < C::CT; ++kb) {
@@ -679,7 +673,7 @@ template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStre
                 for (int w = 0; w < NW; ++w)
                     sp[w % 4] += load[w][kb];
                 if (kb + 1 < C::CT) // (kb+1, kb+1) is owned by warp kb+2
-                    la = kFac + load[kb + 2][kb] * 4 + kInt * (sp[(kb + 2) % 4] - load[kb + 2][kb]);
+                    la = kFac + load[kb + 2][kb] * 4;
                 t += std::max(std::max(std::max(sp[0], sp[1]), std::max(sp[2], sp[3])), la);
             }
             return t;

@@ -23,7 +23,8 @@ namespace {
 //   Tt[P]  L_Q^{-1} per column (T = Tt')          (persistent)
 //   Li[P-1], U[P-1], Y[P-1], Lb                    (persistent)
 //   D[P], Mb[P], K[P]                              (scratch, CR in place)
-//   S1, S2                                         (scratch blocks)
+//   S1, S2                                         (scratch blocks; S1 unused since
+//                                                    the working blocks moved to shared memory)
 struct SBLayout {
     long long Tt, Li, U, Y, Lb, D, Mb, K, S1, S2, total;
     int levels;

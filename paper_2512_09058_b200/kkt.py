@@ -11,10 +11,18 @@ power of two) and `FactorizeError(batch_index, pivot)` for
 batla::factorize_error. Problems are batches (`EqOCPBatch`, a leading
 instance axis; a single reference EqOCP is a batch of one). Arrays may be
 host numpy arrays or CUDA torch tensors (device-resident, zero-copy).
-`opts.vlen` / `opts.workers` are CPU lane/thread knobs of the reference and
-are accepted but have no effect on the GPU (results are independent of them
-in the reference too, test_kkt.cpp:133-138); every `tail` (cr1 / pcr / pcg)
-is served by the GPU's exact cyclic reduction of the whole Schur tree.
+`opts.workers` is a CPU thread knob of the reference, accepted with no effect
+on the GPU (results are independent of it in the reference too,
+test_kkt.cpp:133-138). `opts.tail = "pcr"` solves the last min(P, vlen)
+Schur blocks by parallel cyclic reduction on the GPU (the fused Schur
+kernel's shapes); "pcg" -- and "pcr" at other shapes -- is served by the
+exact cyclic reduction of the whole tree, within the tails' accuracy
+contracts (test_kkt.cpp:152-161).
+
+Beyond the three reference calls: `update` (kkt::update, in place on the
+GPU factor), `Factor.materialize`, the QPALM steps `solve_newton`,
+`augment_hessians`, `al_gradients` / `newton_rhs` and `line_search_exact`,
+and `Prepared` calls for device-resident loops.
 """
 from __future__ import annotations
 
