@@ -368,6 +368,21 @@ int dump_phases(cyq_ctx *ctx, const Geo &g, const long long *ph, const long long
         fprintf(stderr, "phase s=%d init+WW %lld chol %lld store %lld mw %lld V %lld\n", s,
                 h[s * 8 + 1] - h[s * 8 + 0], h[s * 8 + 2] - h[s * 8 + 1], h[s * 8 + 3] - h[s * 8 + 2],
                 h[s * 8 + 4] - h[s * 8 + 3], (s + 1 < g.n ? h[(s + 1) * 8] : h[g.n * 8]) - h[s * 8 + 4]);
+#ifdef CYQ_TRACE
+    if (g.nx == 64) { // riccati_cta column-loop trace: per (kb, warp) event clocks relative to the step start
+        const int NW = 16, CT = 12;
+        std::vector<long long> t(CT * NW * 8);
+        CU(cudaMemcpy(t.data(), ph + 4096, t.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+        long long t0 = t[0];
+        for (int kb = 0; kb < CT; ++kb)
+            for (int w = 0; w < NW; ++w) {
+                const long long *e = &t[(kb * NW + w) * 8];
+                fprintf(stderr, "trace kb=%d w=%d start %lld A %lld bar1 %lld pick %lld trail %lld bar2 %lld fac %lld\n", kb, w,
+                        e[0] - t0, e[1] - e[0], e[2] - e[1], e[3] - e[2], e[4] - e[3], e[5] - e[4],
+                        e[6] ? e[6] - e[2] : 0);
+            }
+    }
+#endif
     if (q[31] > 1 && q[31] < 31) {
         fprintf(stderr, "schur phases (instance 0):");
         for (long long k = 1; k < q[31]; ++k)
@@ -405,6 +420,7 @@ int launch_pipeline(cyq_ctx *ctx, const Geo &g, const ProbView &p, const FactorW
     if (o.phase_prof) {
         if (!ctx->phase)
             CU(cudaMalloc(&ctx->phase, 8 * 4096 * sizeof(long long)));
+        CU(cudaMemsetAsync(ctx->phase, 0, 8 * 4096 * sizeof(long long), ctx->stream));
         ra.phase = ctx->phase;
     }
     {

@@ -38,6 +38,7 @@
 #include "riccati_common.cuh"
 
 #include <algorithm>
+#include <vector>
 #include <type_traits>
 #include <cstdlib>
 
@@ -47,13 +48,19 @@ using namespace cyqb::ric;
 
 namespace {
 
-// per-warp tile lists (host-built, launch_c): c_list[w][k] = (ti << 8 | tj),
-// tile columns non-increasing in k; c_cnt[w][kb + 1] = number of my tiles
-// with tile column > kb (the update prefix at block column kb), c_cnt[w][0]
-// = all my tiles
-constexpr int kMaxW = 16, kMaxL = 32, kMaxCT = 31;
-__constant__ unsigned short c_list[kMaxW * kMaxL];
-__constant__ unsigned char c_cnt[kMaxW * (kMaxCT + 1)];
+// per-warp tile lists (host-built, launch_c): tile k of warp w is (ti, tj),
+// tile columns non-increasing in k; count kb + 1 = number of the warp's tiles
+// with tile column > kb (the update prefix at block column kb), count 0 =
+// all its tiles.
+// The kernel keeps both PACKED IN REGISTERS for the whole launch (c_lpk: three
+// tiles per word, 5 bits each for ti and tj; c_cpk: sixteen 4-bit counts):
+// an indexed constant load costs ~100 cycles, and the unrolled list walks
+// issued one per tile -- predicated-off ones included -- on the critical
+// path of every block column (the pick-up walk alone took ~1400 cycles of
+// each ~3500-cycle column step).
+constexpr int kMaxW = 16, kMaxL = 15, kMaxCT = 15, kLW = 5;
+__constant__ unsigned c_lpk[kMaxW * kLW];
+__constant__ unsigned long long c_cpk[kMaxW];
 
 template <int NU, int NX, int NW> struct CS {
     static_assert(NU % 8 == 0 && NX % 8 == 0, "tile-aligned shapes only");
@@ -63,7 +70,8 @@ template <int NU, int NX, int NW> struct CS {
     static constexpr int TT = CT + BT;
     static constexpr int NT = TT * (TT + 1) / 2;
     static constexpr int NL = NT - CT;            // list tiles (all but pivot diagonals)
-    static_assert(NW >= CT + 1 && NW <= kMaxW && CT <= kMaxCT, "one warp per pivot diagonal tile");
+    static_assert(NW % 4 == 0 && 3 * (NW / 4) >= CT && NW <= kMaxW && CT <= kMaxCT,
+                  "one bulk warp (warp % 4 != 0) per pivot diagonal tile");
     static constexpr int TOP = 8 * CT, RHS = TOP + NX, RT = RHS / 8, RR = RHS % 8;
     static constexpr int XT0 = NU / 8, NXC = NX / 8; // x columns: tiles XT0 .. CT-1
     static constexpr int NPT = CT * (CT + 1) / 2 + BT * CT;
@@ -77,7 +85,7 @@ template <int NU, int NX, int NW> struct CS {
     // (compile-time loop starts: no predicated-off DMMAs)
     static constexpr int NPURE = (RT - CT) * (RT - CT + 1) / 2;
     static constexpr int NPS = NPURE / NW;
-    static_assert(MAXL <= kMaxL, "list table size");
+    static_assert(MAXL <= kMaxL && TT <= 32, "packed list: 15 tiles of 5 + 5 bits, 4-bit counts");
     // [B A] and L_Q row strides, padded by 8 doubles: the V = BA' L_Q
     // operand loads (4 rows x 8 columns per warp) then need the minimum two
     // shared-memory wavefronts instead of four
@@ -94,8 +102,10 @@ template <int NU, int NX, int NW> struct CS {
     static constexpr int O_RU0 = O_MW + NX;                        // NU
     static constexpr int O_RED = O_RU0 + NU;                       // 32 (pivot floor)
     static constexpr int O_SCR = O_RED + 32;                       // 64 (transpose)
-    static constexpr int O_MB = O_SCR + kTileElems;                // 1 mbarrier ([B A] staging)
-    static constexpr int SMEM = O_MB + 2;
+    static constexpr int O_DG = O_SCR + kTileElems;                // CT pivot diagonal tiles (hand-off)
+    static constexpr int O_MB = O_DG + CT * kTileElems;            // 1 mbarrier ([B A] staging)
+    static constexpr int O_LMB = O_MB + 2;                         // CT mbarriers (L_kk^{-1} published)
+    static constexpr int SMEM = O_LMB + CT + (CT & 1);
     __host__ __device__ static constexpr int T(int i, int j) { return i * (i + 1) / 2 + j; }
     // stored-factor tile index of panel tile (i, j), j < CT
     __host__ __device__ static constexpr int PI(int i, int j) {
@@ -271,20 +281,40 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
     const bool implicit_rhs = (a.p.ru == nullptr);
     const double sgn = implicit_rhs ? -1.0 : 1.0;
     int fail_piv = -1, fail_stage = 0;
-    // warp w = 1..CT owns the pivot diagonal tile (w-1, w-1)
-    const int dkb = warp - 1;
+    // Warp 0 is the PIVOT WARP: it factors every pivot diagonal tile. Its SM
+    // sub-partition (warps 0, 4, 8, ...) holds only tiles of the first block
+    // columns (host plan), so after the first steps no DMMA of another warp
+    // queues ahead of the pivot chain's FP64 instructions. The bulk warps
+    // (warp % 4 != 0) each keep one pivot diagonal tile (dkb, dkb) up to date
+    // in `dg` and hand it over through shared memory two steps before its turn
+    const int dkb = (warp & 3) ? (warp >> 2) * 3 + (warp & 3) - 1 : -1;
     const bool diag_owner = dkb >= 0 && dkb < CT;
     // my list tiles (ti, tj) from constant memory (warp-uniform loads, no
     // index registers)
-    const int mycnt = c_cnt[warp * (kMaxCT + 1)];
-#define LTI(k) ((int)(c_list[warp * kMaxL + (k)] >> 8))
-#define LTJ(k) ((int)(c_list[warp * kMaxL + (k)] & 255))
+    // opk[k] = byte offsets of the (ti, tj) slots in a column buffer, ti in
+    // the low half (compile-time k everywhere: plain registers)
+    unsigned opk[MAXL];
+#pragma unroll
+    for (int k = 0; k < MAXL; ++k) {
+        const unsigned e = (c_lpk[warp * kLW + k / 3] >> (10 * (k % 3))) & 1023u;
+        opk[k] = ((e & 31u) << 9) | ((e >> 5) << 25);
+    }
+    const unsigned long long cpk = c_cpk[warp];
+    const int mycnt = (int)(cpk & 15u);
+#define LTI(k) ((int)((opk[k] >> 9) & 31u))
+#define LTJ(k) ((int)(opk[k] >> 25))
+#define CNT(kb) ((int)((cpk >> (4 * (kb))) & 15u))
     for (int i = tid; i < C::SMEM; i += NTH)
         sm[i] = 0.0;
     unsigned long long *bamb = reinterpret_cast<unsigned long long *>(sm + C::O_MB);
+    unsigned long long *lmb = reinterpret_cast<unsigned long long *>(sm + C::O_LMB);
+    double *dgs = sm + C::O_DG;
     int baph = 0; // completed [B A] stagings (mbarrier phases)
+    __syncthreads();
     if (tid == 0) {
         mb_init(bamb, 1);
+        for (int d = 0; d < CT; ++d)
+            mb_init(lmb + d, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -367,8 +397,37 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         st_frag(linvb + (kb & 1) * kTileElems, lane, Frag{tscr[cq * 8 + rq], tscr[(cq + 1) * 8 + rq]});
         __syncwarp();
     };
+    // pivot warp: diagonal tile d from its hand-off slot (updates of block
+    // columns < d-1 applied by its owner), the last update (column d-1) here,
+    // factor, publish L_dd^{-1} (mbarrier lmb[d]), L_dd to the stored factor
+    // and to the x-space L_Q
+    auto pivot_step = [&](int d, double dfloor, int s) {
+        dg = ld_frag(dgs + d * kTileElems, lane);
+        if (d > 0) {
+            const Frag li = ld_frag(colb + (((d - 1) & 1) * TT + d) * kTileElems, lane);
+            tile_gemm_nt_sub(dg, li, li);
+        }
+#ifndef CYQ_X_NOFAC
+        factor_diag(d, dfloor, s);
+#endif
+        mb_signal(lmb + d, lane);
+        st_frag(a.fac + (((size_t)chain * n + s) * C::NPT + C::PI(d, d)) * kTileElems, lane, dg);
+        if (d >= C::XT0) {
+            const int r = 8 * d + rq - NU, c0 = 8 * d + cq - NU;
+            LQ[r * C::LQS + c0] = dg.a;
+            LQ[r * C::LQS + c0 + 1] = dg.b;
+        }
+    };
 
     long long *ph = (a.phase && chain == 0 && tid == 0) ? a.phase : nullptr;
+#ifdef CYQ_TRACE
+    // per-warp event clocks of the column loop at stage CYQ_TRACE (chain 0):
+    // a.phase[4096 + ((kb * NW + warp) * 8 + e)]
+    long long *trc = (a.phase && chain == 0 && lane == 0) ? a.phase + 4096 : nullptr;
+#define TRC(e) do { if (trc && s == CYQ_TRACE) trc[(kb * NW + warp) * 8 + (e)] = clock64(); } while (0)
+#else
+#define TRC(e) do { } while (0)
+#endif
     for (int s = 0; s < n; ++s) {
         if (ph) ph[s * 8 + 0] = clock64();
         const int j = g.stage_of(c, s), xi = g.x_index_of(c, s);
@@ -434,93 +493,107 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
             if (lane == 0)
                 atomicMax(red, (unsigned long long)__double_as_longlong(v));
         }
-        // raw column-0 tiles -> column buffer 0 (the last list positions)
-#pragma unroll
-        for (int k = 0; k < MAXL; ++k) {
-            if (k >= mycnt)
-                break;
-            if (LTJ(k) == 0)
-                st_frag(colb + LTI(k) * kTileElems, lane, acc[k]);
-        }
-        __syncthreads(); // W and BA_0 reads done, pivot floor, column 0 published
+        // pivot diagonal tiles 0 and 1 go to the pivot warp now (tile d > 1
+        // two steps before its turn, below)
+        if (diag_owner && dkb <= 1)
+            st_frag(dgs + dkb * kTileElems, lane, dg);
+        __syncthreads(); // W and BA_0 reads done, pivot floor, diagonal tiles 0 / 1 handed over
         if (s == 0 && n > 1)
             stage_BA_cta<NU, NX, NW, TMA>(g, a.p, b, g.stage_of(c, 1), sm, tid, bamb);
         const double dfloor = 1e-14 * __longlong_as_double((long long)red[0]);
-        if (dkb == 0)
-            factor_diag(0, dfloor, s);
-        __syncthreads(); // linv[0]
+        if (warp == 0)
+            pivot_step(0, dfloor, s);
 
         // ---- blocked Cholesky with look-ahead ----------------------------
+        // Per block column kb, ONE CTA barrier: every warp solves its own
+        // (complete) column-kb tiles in registers against the published
+        // L_kk^{-1} (X <- X L_kk^{-T}, two DMMAs; the wait is on the mbarrier
+        // the pivot warp arrives at) and writes them to column buffer kb & 1;
+        // barrier; then the pivot warp updates and factors (kb+1, kb+1) while
+        // the bulk warps apply column kb to their tiles. Buffer kb & 1 is
+        // rewritten at step kb + 2, after the barrier of step kb + 1.
 #pragma unroll 1
         for (int kb = 0; kb < CT; ++kb) {
             const int par = kb & 1;
-            double *col = colb + par * TT * kTileElems, *nxt = colb + (par ^ 1) * TT * kTileElems;
-            // (A) solve the column-kb tiles in place: X <- X (L_kk^{-1})'
-            {
+            double *col = colb + par * TT * kTileElems;
+            TRC(0);
+            const int cnt = CNT(kb + 1);
+            const int hi = CNT(kb);
+            const unsigned colS = smem_u32(col) + 16 * lane;
+            auto lds = [](unsigned a) {
+                Frag f;
+                asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(f.a), "=d"(f.b) : "r"(a) : "memory");
+                return f;
+            };
+            auto sts = [](unsigned a, const Frag &f) {
+                asm volatile("st.shared.v2.f64 [%0], {%1,%2};" ::"r"(a), "d"(f.a), "d"(f.b) : "memory");
+            };
+            // (A) my column-kb tiles: list positions [cnt, hi). Switch-entered
+            // straight-line code here and below: a walk over the unrolled
+            // list costs issue slots for every slot it skips
+            if (hi > cnt) {
+                mb_wait(lmb + kb, s & 1);
                 const Frag linv = ld_frag(linvb + par * kTileElems, lane);
-                for (int ti = kb + 1 + warp; ti < TT; ti += NW) {
-                    const Frag x = ld_frag(col + ti * kTileElems, lane);
-                    Frag r{0.0, 0.0};
-                    tile_gemm_nt(r, x, linv);
-                    st_frag(col + ti * kTileElems, lane, r);
+#define SOLVE_CASE(K)                                                                                  \
+    case K:                                                                                            \
+        if constexpr (K < MAXL) {                                                                      \
+            if (K >= hi)                                                                               \
+                break;                                                                                 \
+            constexpr int T = K < MAXL ? K : 0;                                                        \
+            Frag r{0.0, 0.0};                                                                          \
+            tile_gemm_nt(r, acc[T], linv);                                                             \
+            acc[T] = r;                                                                                \
+            sts(colS + (opk[T] & 0xffffu), r);                                                         \
+        }
+                switch (cnt) {
+                    SOLVE_CASE(0) SOLVE_CASE(1) SOLVE_CASE(2) SOLVE_CASE(3) SOLVE_CASE(4) SOLVE_CASE(5)
+                    SOLVE_CASE(6) SOLVE_CASE(7) SOLVE_CASE(8) SOLVE_CASE(9) SOLVE_CASE(10) SOLVE_CASE(11)
+                    SOLVE_CASE(12) SOLVE_CASE(13) SOLVE_CASE(14)
+                default: break;
                 }
+#undef SOLVE_CASE
             }
+            TRC(1);
             __syncthreads(); // column kb solved
-            // (B) look-ahead: the owner of (kb+1, kb+1) updates and factors it
-            // (its list holds few tiles right of column kb: the host plan)
-            if (dkb == kb + 1 && kb + 1 < CT) {
-                const Frag li = ld_frag(col + (kb + 1) * kTileElems, lane);
-                tile_gemm_nt_sub(dg, li, li);
-                factor_diag(kb + 1, dfloor, s);
+            TRC(2);
+            // (B) look-ahead by the pivot warp; the diagonal-tile owners apply
+            // column kb, the owner of (kb+2, kb+2) hands it over
+            if (warp == 0) {
+                if (kb + 1 < CT)
+                    pivot_step(kb + 1, dfloor, s);
+                TRC(6);
             } else if (diag_owner && dkb > kb + 1) {
                 const Frag li = ld_frag(col + dkb * kTileElems, lane);
                 tile_gemm_nt_sub(dg, li, li);
+                if (dkb == kb + 2)
+                    st_frag(dgs + dkb * kTileElems, lane, dg);
             }
-            // my solved column-kb tiles back into registers: list positions
-            // [cnt, hi) (right after the update prefix)
-            const int cnt = c_cnt[warp * (kMaxCT + 1) + kb + 1];
-            const int hi = c_cnt[warp * (kMaxCT + 1) + kb];
-#pragma unroll
-            for (int k = 0; k < MAXL; ++k) {
-                if (k >= hi)
-                    break;
-                if (k >= cnt)
-                    acc[k] = ld_frag(col + LTI(k) * kTileElems, lane);
-            }
-            // trailing update of my prefix: C(ti, tj) -= L(ti, kb) L(tj, kb)';
-            // completed column-(kb+1) tiles are published for step kb+1. The
-            // next tile's operands are loaded one iteration ahead (a read of
-            // a valid column slot even past the prefix)
-            auto trail = [&](auto K0C) {
-                constexpr int K0 = decltype(K0C)::value;
-                if (cnt <= K0)
-                    return;
-                int tj = LTJ(K0);
-                Frag li = ld_frag(col + LTI(K0) * kTileElems, lane), lj = ld_frag(col + tj * kTileElems, lane);
-#pragma unroll
-                for (int k = K0; k < MAXL; ++k) {
-                    if (k >= cnt)
-                        break;
-                    Frag nli{0.0, 0.0}, nlj{0.0, 0.0};
-                    int ntj = 0;
-                    if (k + 1 < MAXL) {
-                        ntj = LTJ(k + 1);
-                        nli = ld_frag(col + LTI(k + 1) * kTileElems, lane);
-                        nlj = ld_frag(col + ntj * kTileElems, lane);
-                    }
-                    tile_gemm_nt_sub(acc[k], li, lj);
-                    if (tj == kb + 1)
-                        st_frag(nxt + LTI(k) * kTileElems, lane, acc[k]);
-                    li = nli;
-                    lj = nlj;
-                    tj = ntj;
+            TRC(3);
+            // trailing update of my prefix: C(ti, tj) -= L(ti, kb) L(tj, kb)',
+            // tiles cnt-1 .. 0 (.. NPS when the ALQ ALQ' terms cancel on the
+            // pure tiles)
+#ifndef CYQ_X_NOTRAIL
+            {
+                const bool skip = kb >= C::XT0 && s + 1 < n;
+#define UPD_CASE(K)                                                                                    \
+    case K:                                                                                            \
+        if constexpr (K <= MAXL && K >= 1) {                                                           \
+            if (K == C::NPS && skip)                                                                   \
+                break;                                                                                 \
+            constexpr int T = (K >= 1 && K <= MAXL) ? K - 1 : 0;                                       \
+            const Frag li = lds(colS + (opk[T] & 0xffffu)), lj = lds(colS + (opk[T] >> 16));           \
+            tile_gemm_nt_sub(acc[T], li, lj);                                                          \
+        }
+                switch ((skip && cnt <= C::NPS) ? 0 : cnt) {
+                    UPD_CASE(15) UPD_CASE(14) UPD_CASE(13) UPD_CASE(12) UPD_CASE(11) UPD_CASE(10) UPD_CASE(9)
+                    UPD_CASE(8) UPD_CASE(7) UPD_CASE(6) UPD_CASE(5) UPD_CASE(4) UPD_CASE(3) UPD_CASE(2)
+                    UPD_CASE(1)
+                default: break;
                 }
-            };
-            if (kb >= C::XT0 && s + 1 < n)
-                trail(std::integral_constant<int, C::NPS>{}); // ALQ ALQ' cancels on pure tiles
-            else
-                trail(std::integral_constant<int, 0>{});
-            __syncthreads(); // column kb consumed, column kb+1 / linv published
+#undef UPD_CASE
+            }
+#endif
+            TRC(4);
         }
         if (tid == 0)
             red[0] = 0ull;
@@ -547,8 +620,6 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                     }
                 }
             }
-            if (diag_owner)
-                st_frag(dst + C::PI(dkb, dkb) * kTileElems, lane, dg);
         }
         if (ph) ph[s * 8 + 3] = clock64();
 
@@ -568,11 +639,6 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                 // ALQ rows (coupling rows, x columns) -> W tile rows >= CT
                 if (ti >= CT && tj >= C::XT0 && tj < CT)
                     st_frag(Wsm + (ti * C::NXC + (tj - C::XT0)) * kTileElems, lane, acc[k]);
-            }
-            if (diag_owner && dkb >= C::XT0) {
-                const int r = 8 * dkb + rq - NU, c0 = 8 * dkb + cq - NU;
-                LQ[r * C::LQS + c0] = dg.a;
-                LQ[r * C::LQS + c0 + 1] = dg.b;
             }
             wait_BA(bamb, baph); // BA_{s+1}, f_{s+1}
             __syncthreads();
@@ -642,6 +708,8 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         atomicMin(a.fail + b, my_fail);
 #undef LTI
 #undef LTJ
+#undef CNT
+#undef TRC
 }
 
 namespace {
@@ -656,55 +724,94 @@ template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStre
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e0 != cudaSuccess)
             return e0;
-        // tile plan: every list tile (all but the pivot diagonals) goes,
-        // in tile-column-descending order, to the warp that minimises the
-        // modelled Cholesky time sum_kb max(DMMA issue per SM sub-partition,
-        // look-ahead warp's factorization + its own updates): the owner of
-        // (kb+1, kb+1) is then left with few tiles right of column kb
-        unsigned short h[kMaxW * kMaxL] = {};
+        // tile plan. The skip-mode pure tiles go first (NPS per warp at slots
+        // 0 .. NPS-1; they take trailing updates only from the u columns, kb <
+        // XT0). The warps of the pivot warp's SM sub-partition (w % 4 == 0)
+        // then fill up with the tiles of the first block columns -- column 0
+        // (never updated) first, the pivot warp itself taking only those -- so
+        // that sub-partition issues no DMMA after the first steps and the
+        // pivot chain's FP64 instructions are not queued behind any. Every
+        // other tile goes, in tile-column-descending order, to the bulk warp
+        // that minimises the modelled time sum_kb max(DMMA issue per bulk
+        // sub-partition). Lists stay in tile-column-descending order.
+        constexpr int kPL = 32; // plan-time list stride
+        unsigned short h[kMaxW * kPL] = {};
         unsigned char cnt[kMaxW * (kMaxCT + 1)] = {};
         double load[kMaxW][kMaxCT] = {};
         int nown[kMaxW] = {};
-        const double kUpd = 2 * 16.0, kFac = 1400.0; // cycles: one tile update, one diagonal factorization
+        const double kUpd = 2 * 16.0; // cycles: one tile update
+        auto quiet = [&](int w) { return w % 4 == 0; };
         auto cost = [&]() {
             double t = 0;
             for (int kb = 0; kb < C::CT; ++kb) {
-                double sp[4] = {}, la = 0;
+                double sp[4] = {};
                 for (int w = 0; w < NW; ++w)
                     sp[w % 4] += load[w][kb];
-                if (kb + 1 < C::CT) // (kb+1, kb+1) is owned by warp kb+2
-                    la = kFac + load[kb + 2][kb] * 4;
-                t += std::max(std::max(std::max(sp[0], sp[1]), std::max(sp[2], sp[3])), la);
+                t += std::max(std::max(sp[1], sp[2]), sp[3]);
             }
             return t;
         };
-        // skip-mode pure tiles first: NPS per warp at slots 0 .. NPS-1 (they
-        // take trailing updates only from the u columns, kb < XT0)
-        auto is_pure = [&](int ti, int tj) { return ti >= C::CT && tj >= C::CT && ti < C::RT && tj < C::RT; };
-        bool skip_mode[64][64] = {};
+        bool placed[64][64] = {};
+        auto give = [&](int w, int ti, int tj, int upd_cols) {
+            for (int kb = 0; kb < upd_cols; ++kb)
+                load[w][kb] += kUpd;
+            h[w * kPL + nown[w]++] = (unsigned short)((ti << 8) | tj);
+            placed[ti][tj] = true;
+        };
         {
             int w = 0;
             for (int tj = C::RT - 1; tj >= C::CT && C::NPS > 0; --tj)
                 for (int ti = C::RT - 1; ti >= tj; --ti) {
                     if (w >= NW * C::NPS)
                         break;
-                    const int ww = w % NW;
-                    h[ww * kMaxL + nown[ww]++] = (unsigned short)((ti << 8) | tj);
-                    for (int kb = 0; kb < C::XT0; ++kb)
-                        load[ww][kb] += kUpd;
-                    skip_mode[ti][tj] = true;
+                    give(w % NW, ti, tj, C::XT0);
                     ++w;
                 }
         }
-        (void)is_pure;
+        {
+            // quiet sub-partition: the pivot warp fills up with column-0
+            // tiles, the others take block columns 0, 1, 2, ... round-robin
+            // until their slots are full
+            std::vector<int> quiet_part[kMaxW];
+            int room[kMaxW] = {};
+            for (int w = 0; w < NW; w += 4)
+                room[w] = C::MAXL - nown[w];
+            int w = 4 % NW;
+            for (int tj = 0; tj < C::CT; ++tj)
+                for (int ti = tj + 1; ti < C::TT; ++ti) {
+                    int q = -1;
+                    if (tj == 0 && room[0] > 0)
+                        q = 0;
+                    else
+                        for (int t = 0; t < NW / 4 && q < 0; ++t, w = (w + 4) % NW)
+                            if (w != 0 && room[w] > 0)
+                                q = w;
+                    if (q < 0)
+                        continue;
+                    if (q != 0)
+                        w = (q + 4) % NW;
+                    quiet_part[q].push_back((ti << 8) | tj);
+                    placed[ti][tj] = true;
+                    --room[q];
+                }
+            // column-descending order inside each list
+            for (int q = 0; q < NW; q += 4) {
+                std::stable_sort(quiet_part[q].begin(), quiet_part[q].end(),
+                                 [](int x, int y) { return (x & 255) > (y & 255); });
+                for (int e : quiet_part[q]) {
+                    placed[e >> 8][e & 255] = false;
+                    give(q, e >> 8, e & 255, std::min(e & 255, C::CT));
+                }
+            }
+        }
         for (int tj = C::TT - 1; tj >= 0; --tj)
             for (int ti = C::TT - 1; ti >= tj; --ti) {
-                if ((ti == tj && tj < C::CT) || skip_mode[ti][tj])
+                if ((ti == tj && tj < C::CT) || placed[ti][tj])
                     continue;
                 int best = -1;
                 double bc = 0;
                 for (int w = 0; w < NW; ++w) {
-                    if (nown[w] >= C::MAXL)
+                    if (quiet(w) || nown[w] >= C::MAXL)
                         continue;
                     for (int kb = 0; kb < std::min(tj, C::CT); ++kb)
                         load[w][kb] += kUpd;
@@ -714,21 +821,64 @@ template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStre
                     if (best < 0 || cw < bc)
                         best = w, bc = cw;
                 }
-                for (int kb = 0; kb < std::min(tj, C::CT); ++kb)
-                    load[best][kb] += kUpd;
-                h[best * kMaxL + nown[best]++] = (unsigned short)((ti << 8) | tj);
+                if (best < 0) { // bulk warps full: a quiet warp (not the pivot warp) takes it
+                    for (int w = 4; w < NW && best < 0; w += 4)
+                        if (nown[w] < C::MAXL)
+                            best = w;
+                    if (best < 0)
+                        best = 0;
+                    // keep its list in column-descending order: insert before lower columns
+                    int pos = nown[best];
+                    while (pos > C::NPS && (h[best * kPL + pos - 1] & 255) < tj) {
+                        h[best * kPL + pos] = h[best * kPL + pos - 1];
+                        --pos;
+                    }
+                    h[best * kPL + pos] = (unsigned short)((ti << 8) | tj);
+                    ++nown[best];
+                    placed[ti][tj] = true;
+                    for (int kb = 0; kb < std::min(tj, C::CT); ++kb)
+                        load[best][kb] += kUpd;
+                    continue;
+                }
+                give(best, ti, tj, std::min(tj, C::CT));
             }
+        // the plan must place every list tile once, within MAXL slots per
+        // warp, tile columns non-increasing from slot NPS on
+        {
+            int seen = 0;
+            for (int w = 0; w < NW; ++w) {
+                if (nown[w] > C::MAXL)
+                    return cudaErrorInvalidValue;
+                for (int k = 0; k < nown[w]; ++k) {
+                    ++seen;
+                    if (k > C::NPS && (h[w * kPL + k] & 255) > (h[w * kPL + k - 1] & 255))
+                        return cudaErrorInvalidValue;
+                }
+            }
+            if (seen != C::NL)
+                return cudaErrorInvalidValue;
+        }
         for (int w = 0; w < NW; ++w) {
             cnt[w * (kMaxCT + 1)] = (unsigned char)nown[w];
             for (int kb = 0; kb < C::CT; ++kb) {
                 int m = 0;
                 for (int k = 0; k < nown[w]; ++k)
-                    m += (h[w * kMaxL + k] & 255) > kb;
+                    m += (h[w * kPL + k] & 255) > kb;
                 cnt[w * (kMaxCT + 1) + kb + 1] = (unsigned char)m;
             }
         }
-        const cudaError_t e1 = cudaMemcpyToSymbol(c_list, h, sizeof h);
-        return e1 != cudaSuccess ? e1 : cudaMemcpyToSymbol(c_cnt, cnt, sizeof cnt);
+        unsigned lpk[kMaxW * kLW] = {};
+        unsigned long long cpk[kMaxW] = {};
+        for (int w = 0; w < NW; ++w) {
+            for (int k = 0; k < nown[w]; ++k) {
+                const unsigned ti = h[w * kPL + k] >> 8, tj = h[w * kPL + k] & 255;
+                lpk[w * kLW + k / 3] |= (ti | (tj << 5)) << (10 * (k % 3));
+            }
+            for (int kb = 0; kb < 16; ++kb) // counts past CT repeat the last one (nothing to publish)
+                cpk[w] |= (unsigned long long)cnt[w * (kMaxCT + 1) + std::min(kb, C::CT)] << (4 * kb);
+        }
+        const cudaError_t e1 = cudaMemcpyToSymbol(c_lpk, lpk, sizeof lpk);
+        return e1 != cudaSuccess ? e1 : cudaMemcpyToSymbol(c_cpk, cpk, sizeof cpk);
     });
     riccati_cta_kernel<NU, NX, NW, TMA><<<ra.grid_chains(), 32 * NW, smem, st>>>(ra);
     return true;

@@ -17,7 +17,14 @@ dev = EqOCPBatch.__new__(EqOCPBatch)
 for k in OCP_FIELDS:
     setattr(dev, k, torch.from_numpy(getattr(p, k)).cuda())
 ctx = kkt.Context(0)
-kkt.solve_problem(dev, kkt.FactorOptions(P=c.P), ctx=ctx)
+def run():
+    try:
+        kkt.solve_problem(dev, kkt.FactorOptions(P=c.P), ctx=ctx)
+    except kkt.FactorizeError as e:  # elimination builds (tools/variant_build.sh) break the numbers
+        print("ignored:", e)
+
+
+run()
 with ctx.options(phase_prof=1):
-    kkt.solve_problem(dev, kkt.FactorOptions(P=c.P), ctx=ctx)
+    run()
 torch.cuda.synchronize()
