@@ -378,9 +378,16 @@ int dump_phases(cyq_ctx *ctx, const Geo &g, const long long *ph, const long long
             for (int w = 0; w < NW; ++w) {
                 const long long *e = &t[(kb * NW + w) * 8];
                 fprintf(stderr, "trace kb=%d w=%d start %lld A %lld bar1 %lld pick %lld trail %lld bar2 %lld fac %lld\n", kb, w,
-                        e[0] - t0, e[1] - e[0], e[2] - e[1], e[3] - e[2], e[4] - e[3], e[5] - e[4],
-                        e[6] ? e[6] - e[2] : 0);
+                        e[0] - t0, e[1] - e[0], e[2] - e[1], e[3] - e[2], e[4] - e[3], e[5] ? e[5] - e[0] : 0,
+                        e[7] ? e[7] - e[0] : 0);
             }
+        std::vector<long long> pt(CT * 8);
+        CU(cudaMemcpy(pt.data(), ph + 6144, pt.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+        for (int d = 0; d < CT; ++d) {
+            const long long *e = &pt[d * 8];
+            fprintf(stderr, "pivot d=%d start %lld load+update %lld pivots0-3 %lld pivots4-7 %lld publish %lld signal %lld\n",
+                    d, e[0] - t0, e[1] - e[0], e[2] - e[1], e[3] - e[2], e[4] - e[3], e[5] - e[4]);
+        }
     }
 #endif
     if (q[31] > 1 && q[31] < 31) {

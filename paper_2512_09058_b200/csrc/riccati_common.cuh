@@ -91,6 +91,23 @@ __device__ __forceinline__ void mb_wait(unsigned long long *mb, int par) {
 }
 #endif
 
+// ---- shared-memory flags: a one-writer hand-off that is usually already
+// there when its readers look (an mbarrier try_wait costs ~200 cycles even
+// on a completed phase, an acquire load ~30). The writer's warp stores its
+// data, then one lane releases the flag; readers spin on the expected value.
+__device__ __forceinline__ void flag_set(unsigned *f, unsigned v, int lane) {
+    __syncwarp();
+    if (lane == 0)
+        asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(f)), "r"(v) : "memory");
+    __syncwarp();
+}
+__device__ __forceinline__ void flag_wait(const unsigned *f, unsigned v) {
+    unsigned r;
+    do {
+        asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(r) : "r"(smem_u32(f)) : "memory");
+    } while (r != v);
+}
+
 // async copy of cnt doubles (16-byte granules when both ends are aligned),
 // or an identity / zero fill when src == nullptr
 template <int CNT, int DIAG, int NTHR = 32>

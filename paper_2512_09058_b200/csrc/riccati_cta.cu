@@ -69,13 +69,15 @@ template <int NU, int NX, int NW> struct CS {
     static constexpr int BT = (NX + 1 + 7) / 8;   // coupling + rhs tile rows
     static constexpr int TT = CT + BT;
     static constexpr int NT = TT * (TT + 1) / 2;
-    static constexpr int NL = NT - CT;            // list tiles (all but pivot diagonals)
+    // list tiles: all but the pivot diagonal tiles (d, d) and the tiles left
+    // of them (d, d-1), which the pivot warp takes over (kernel comment)
+    static constexpr int NL = NT - CT - (CT - 1);
     static_assert(NW % 4 == 0 && 3 * (NW / 4) >= CT && NW <= kMaxW && CT <= kMaxCT,
                   "one bulk warp (warp % 4 != 0) per pivot diagonal tile");
     static constexpr int TOP = 8 * CT, RHS = TOP + NX, RT = RHS / 8, RR = RHS % 8;
     static constexpr int XT0 = NU / 8, NXC = NX / 8; // x columns: tiles XT0 .. CT-1
     static constexpr int NPT = CT * (CT + 1) / 2 + BT * CT;
-    static constexpr int MAXL = (NL + NW - 1) / NW;  // tiles per warp (the host plan meets it)
+    static constexpr int MAXL = (NL + NW - 2) / (NW - 1); // tiles per warp; the pivot warp holds none
     // "pure" coupling tiles (rows and columns all coupling rows: tile rows
     // CT .. RT-1, tile row RT holds the rhs row): their ALQ_s ALQ_s' terms
     // cancel between stage s's trailing update and stage s+1's W W' (only
@@ -92,8 +94,8 @@ template <int NU, int NX, int NW> struct CS {
     static constexpr int PW = NUX + 8, LQS = NX + 8;
     // shared memory (doubles)
     static constexpr int O_W = 0;                                  // TT x NXC tiles
-    static constexpr int O_COL = O_W + TT * NXC * kTileElems;      // 2 x TT tiles
-    static constexpr int O_LINV = O_COL + 2 * TT * kTileElems;     // 2 tiles (by kb parity)
+    static constexpr int O_COL = O_W + TT * NXC * kTileElems;      // 3 x TT tiles (by kb % 3)
+    static constexpr int O_LINV = O_COL + 3 * TT * kTileElems;     // 2 tiles (by kb parity)
     static constexpr int O_BA = O_LINV + 2 * kTileElems;           // NX x PW
     static constexpr int O_LQ = O_BA + NX * PW;                    // NX x LQS (x-space L_Q)
     static constexpr int O_F = O_LQ + NX * LQS;                    // NX
@@ -104,8 +106,9 @@ template <int NU, int NX, int NW> struct CS {
     static constexpr int O_SCR = O_RED + 32;                       // 64 (transpose)
     static constexpr int O_DG = O_SCR + kTileElems;                // CT pivot diagonal tiles (hand-off)
     static constexpr int O_MB = O_DG + CT * kTileElems;            // 1 mbarrier ([B A] staging)
-    static constexpr int O_LMB = O_MB + 2;                         // CT mbarriers (L_kk^{-1} published)
-    static constexpr int SMEM = O_LMB + CT + (CT & 1);
+    static constexpr int O_LMB = O_MB + 2;                         // CT flags (L_kk^{-1} published), 32-bit
+    static constexpr int O_HMB = O_LMB + (CT + 1) / 2;             // CT flags (tiles handed to the pivot warp)
+    static constexpr int SMEM = O_HMB + (CT + 1) / 2 + 1;
     __host__ __device__ static constexpr int T(int i, int j) { return i * (i + 1) / 2 + j; }
     // stored-factor tile index of panel tile (i, j), j < CT
     __host__ __device__ static constexpr int PI(int i, int j) {
@@ -276,30 +279,43 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
     double *Wsm = sm + C::O_W, *colb = sm + C::O_COL, *linvb = sm + C::O_LINV, *BA = sm + C::O_BA;
     double *LQ = sm + C::O_LQ, *fb = sm + C::O_F, *yx = sm + C::O_YX, *mw = sm + C::O_MW;
     double *ru0 = sm + C::O_RU0;
-    unsigned long long *red = reinterpret_cast<unsigned long long *>(sm + C::O_RED);
     double *tscr = sm + C::O_SCR;
     const bool implicit_rhs = (a.p.ru == nullptr);
     const double sgn = implicit_rhs ? -1.0 : 1.0;
     int fail_piv = -1, fail_stage = 0;
-    // Warp 0 is the PIVOT WARP: it factors every pivot diagonal tile. Its SM
+    // Warp 0 is the PIVOT WARP: it holds no list tile and runs the serial
+    // chain of the blocked Cholesky by itself -- solve (d, d-1) against
+    // L_{d-1}^{-1}, apply it to (d, d), factor (d, d), publish L_dd^{-1} --
+    // without waiting at the CTA barriers (it only arrives). Its SM
     // sub-partition (warps 0, 4, 8, ...) holds only tiles of the first block
     // columns (host plan), so after the first steps no DMMA of another warp
-    // queues ahead of the pivot chain's FP64 instructions. The bulk warps
-    // (warp % 4 != 0) each keep one pivot diagonal tile (dkb, dkb) up to date
-    // in `dg` and hand it over through shared memory two steps before its turn
+    // queues ahead of the chain's FP64 instructions. The bulk warps (warp % 4
+    // != 0) each keep one pivot diagonal tile (dkb, dkb) in `dg` and the tile
+    // left of it (dkb, dkb-1) in `sd` up to date and hand both over through
+    // shared memory (mbarrier hmb[dkb]) once column dkb-2 has been applied
     const int dkb = (warp & 3) ? (warp >> 2) * 3 + (warp & 3) - 1 : -1;
     const bool diag_owner = dkb >= 0 && dkb < CT;
     // my list tiles (ti, tj) from constant memory (warp-uniform loads, no
     // index registers)
     // opk[k] = byte offsets of the (ti, tj) slots in a column buffer, ti in
     // the low half (compile-time k everywhere: plain registers)
+    // (the words pass through an empty asm so that the compiler keeps them in
+    // registers: it otherwise re-reads the constant bank, ~100+ cycles per
+    // indexed load, at the top of every block-column step)
+    unsigned lpk[kLW];
+#pragma unroll
+    for (int i = 0; i < kLW; ++i) {
+        lpk[i] = c_lpk[warp * kLW + i];
+        asm volatile("" : "+r"(lpk[i]));
+    }
     unsigned opk[MAXL];
 #pragma unroll
     for (int k = 0; k < MAXL; ++k) {
-        const unsigned e = (c_lpk[warp * kLW + k / 3] >> (10 * (k % 3))) & 1023u;
+        const unsigned e = (lpk[k / 3] >> (10 * (k % 3))) & 1023u;
         opk[k] = ((e & 31u) << 9) | ((e >> 5) << 25);
     }
-    const unsigned long long cpk = c_cpk[warp];
+    unsigned long long cpk = c_cpk[warp];
+    asm volatile("" : "+l"(cpk));
     const int mycnt = (int)(cpk & 15u);
 #define LTI(k) ((int)((opk[k] >> 9) & 31u))
 #define LTJ(k) ((int)(opk[k] >> 25))
@@ -307,14 +323,14 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
     for (int i = tid; i < C::SMEM; i += NTH)
         sm[i] = 0.0;
     unsigned long long *bamb = reinterpret_cast<unsigned long long *>(sm + C::O_MB);
-    unsigned long long *lmb = reinterpret_cast<unsigned long long *>(sm + C::O_LMB);
+    // hand-off flags (value s + 1 at stage s; zero-filled above)
+    unsigned *lmb = reinterpret_cast<unsigned *>(sm + C::O_LMB);
+    unsigned *hmb = reinterpret_cast<unsigned *>(sm + C::O_HMB);
     double *dgs = sm + C::O_DG;
     int baph = 0; // completed [B A] stagings (mbarrier phases)
     __syncthreads();
     if (tid == 0) {
         mb_init(bamb, 1);
-        for (int d = 0; d < CT; ++d)
-            mb_init(lmb + d, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -338,7 +354,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
 #pragma unroll
     for (int k = 0; k < MAXL; ++k)
         acc[k] = Frag{0.0, 0.0};
-    Frag dg{0.0, 0.0};
+    Frag dg{0.0, 0.0}, sd{0.0, 0.0};
 
     // the owner factors its diagonal tile dg (L_kk, upper zeroed) and
     // publishes L_kk^{-1} -> linv[kb & 1] (identity tile carried through the
@@ -347,6 +363,13 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
     // early (d = (k+1, k+1), u = (k+1, k) before this step's update):
     // pv' = d - (u iv)^2, the owner lane's exact fma -- no shuffle on the
     // rsqrt -> mul -> fma pivot chain (as riccati_warp.cu; bit-identical)
+#ifdef CYQ_TRACE
+    // pivot-warp event clocks: a.phase[6144 + d * 8 + e] (stage CYQ_TRACE, chain 0)
+    long long *ptrc = (a.phase && chain == 0 && tid == 0) ? a.phase + 6144 : nullptr;
+#define PTRC(d, e) do { if (ptrc && s == CYQ_TRACE) ptrc[(d) * 8 + (e)] = clock64(); } while (0)
+#else
+#define PTRC(d, e) do { } while (0)
+#endif
     auto factor_diag = [&](int kb, double dfloor, int s) {
         Frag idt{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0};
         double pvn = 0.0;
@@ -381,6 +404,8 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                 dg.a = (q2 == src) ? nv : dg.a;
             dg.a = fma(-lrk, lc0, dg.a);
             dg.b = fma(-lrk, lc1, dg.b);
+            if (kk == 3)
+                PTRC(kb, 2);
             const double vq = (kk & 1) ? idt.b : idt.a;
             const double xrq = __shfl_sync(0xffffffffu, vq, 4 * rq + src) * iv;
             if (kk & 1)
@@ -392,26 +417,57 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         }
         if (cq > rq) dg.a = 0.0;
         if (cq + 1 > rq) dg.b = 0.0;
+        PTRC(kb, 3);
         st_frag(tscr, lane, idt); // L^{-1} = (L^{-T})'
         __syncwarp();
         st_frag(linvb + (kb & 1) * kTileElems, lane, Frag{tscr[cq * 8 + rq], tscr[(cq + 1) * 8 + rq]});
         __syncwarp();
     };
-    // pivot warp: diagonal tile d from its hand-off slot (updates of block
-    // columns < d-1 applied by its owner), the last update (column d-1) here,
-    // factor, publish L_dd^{-1} (mbarrier lmb[d]), L_dd to the stored factor
-    // and to the x-space L_Q
+    // The CTA barrier of block column kb (named barrier 1): the bulk warps
+    // wait, the pivot warp only arrives
+    // (ids 1 + kb % 2: its arrival for step kb follows the completion of
+    // step kb-2's barrier -- the hand-over it waited for -- not of step kb-1's)
+    auto bar_wait = [](int kb) { asm volatile("bar.sync %0, %1;" ::"r"(1 + (kb & 1)), "n"(NTH) : "memory"); };
+    auto bar_arrive = [](int kb) {
+        __threadfence_block();
+        asm volatile("bar.arrive %0, %1;" ::"r"(1 + (kb & 1)), "n"(NTH) : "memory");
+    };
+    // pivot warp, block column d: the tiles (d, d-1) and (d, d) arrive from
+    // their owner (hmb[d]; updates of the block columns < d-1 applied);
+    // L(d, d-1) = X L_{d-1}^{-T} goes to column buffer (d-1) % 3 (every warp's
+    // operand at step d-1) before the pivot warp's arrival at that step's
+    // barrier, to the stored factor and to the x-space L_Q; then (d, d) -= L
+    // L', factor, publish L_dd^{-1} (lmb[d]), store L_dd
     auto pivot_step = [&](int d, double dfloor, int s) {
+        PTRC(d, 0);
+        double *fdst = a.fac + ((size_t)chain * n + s) * C::NPT * kTileElems;
+        if (d > 0)
+            flag_wait(hmb + d, s + 1);
         dg = ld_frag(dgs + d * kTileElems, lane);
         if (d > 0) {
-            const Frag li = ld_frag(colb + (((d - 1) & 1) * TT + d) * kTileElems, lane);
+            double *slot = colb + (((d - 1) % 3) * TT + d) * kTileElems;
+            const Frag x = ld_frag(slot, lane);
+            const Frag linv = ld_frag(linvb + ((d - 1) & 1) * kTileElems, lane);
+            Frag li{0.0, 0.0};
+            tile_gemm_nt(li, x, linv);
+            st_frag(slot, lane, li);
+            bar_arrive(d - 1);
             tile_gemm_nt_sub(dg, li, li);
+            st_frag(fdst + C::PI(d, d - 1) * kTileElems, lane, li);
+            if (d - 1 >= C::XT0) {
+                const int r = 8 * d + rq - NU, c0 = 8 * (d - 1) + cq - NU;
+                LQ[r * C::LQS + c0] = li.a;
+                LQ[r * C::LQS + c0 + 1] = li.b;
+            }
         }
+        PTRC(d, 1);
 #ifndef CYQ_X_NOFAC
         factor_diag(d, dfloor, s);
 #endif
-        mb_signal(lmb + d, lane);
-        st_frag(a.fac + (((size_t)chain * n + s) * C::NPT + C::PI(d, d)) * kTileElems, lane, dg);
+        PTRC(d, 4);
+        flag_set(lmb + d, s + 1, lane);
+        PTRC(d, 5);
+        st_frag(fdst + C::PI(d, d) * kTileElems, lane, dg);
         if (d >= C::XT0) {
             const int r = 8 * d + rq - NU, c0 = 8 * d + cq - NU;
             LQ[r * C::LQS + c0] = dg.a;
@@ -419,7 +475,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         }
     };
 
-    long long *ph = (a.phase && chain == 0 && tid == 0) ? a.phase : nullptr;
+    long long *ph = (a.phase && chain == 0 && tid == 32) ? a.phase : nullptr; // a bulk warp's view
 #ifdef CYQ_TRACE
     // per-warp event clocks of the column loop at stage CYQ_TRACE (chain 0):
     // a.phase[4096 + ((kb * NW + warp) * 8 + e)]
@@ -439,7 +495,64 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         const double *qg = qin ? (a.p.qx ? a.p.qx : a.p.q) + ((size_t)b * (N + 1) + xi) * NX : nullptr;
         const double *ru0p = (implicit_rhs && j0) ? ru0 : nullptr;
         const bool aligned = ((reinterpret_cast<uintptr_t>(a.p.R) | reinterpret_cast<uintptr_t>(a.p.Q)) & 15) == 0;
-        // ---- init (H_s from global, coupling rows BA_0 at s = 0, rhs row) ---
+        // ---- init (H_s from global, coupling rows BA_0 at s = 0, rhs row) and
+        // += W W' (s > 0). The pivot warp prepares every pivot diagonal tile
+        // (two at a time: the 16 DMMAs of a tile are one dependent chain) in
+        // the hand-off slots dgs[] and takes the pivot floor max |diag|
+        // (kernels.cpp:21-29) from them; a bulk warp first prepares the tile
+        // left of its diagonal tile (the owner of (1, 0) hands it over at
+        // once), then its list tiles.
+        double dfloor = 0.0;
+        if (warp == 0) {
+            double vmax = 0.0;
+#pragma unroll 1
+            for (int d = 0; d < CT; d += 2) {
+                const int d1 = d + 1 < CT ? d + 1 : d;
+                Frag t0 = init_tile<NU, NX, NW>(d, d, rq, cq, s, sgn, Rg, Sg, Qg, rg, qg, ru0p, BA, aligned);
+                Frag t1 = init_tile<NU, NX, NW>(d1, d1, rq, cq, s, sgn, Rg, Sg, Qg, rg, qg, ru0p, BA, aligned);
+                if (s > 0) {
+#pragma unroll
+                    for (int kt = 0; kt < C::NXC; ++kt) {
+                        const Frag w0 = ld_frag(Wsm + (d * C::NXC + kt) * kTileElems, lane);
+                        const Frag w1 = ld_frag(Wsm + (d1 * C::NXC + kt) * kTileElems, lane);
+                        dmma(t0, w0.a, w0.a);
+                        dmma(t1, w1.a, w1.a);
+                        dmma(t0, w0.b, w0.b);
+                        dmma(t1, w1.b, w1.b);
+                    }
+                }
+                const double v0 = (rq & 1) ? t0.b : t0.a, v1 = (rq & 1) ? t1.b : t1.a;
+                vmax = fmax(vmax, ((lane & 3) == rq / 2) ? fmax(fabs(v0), fabs(v1)) : 0.0);
+                st_frag(dgs + d * kTileElems, lane, t0);
+                st_frag(dgs + d1 * kTileElems, lane, t1);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+                vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+            dfloor = 1e-14 * vmax;
+        }
+        // the tiles the pivot warp takes over go through shared memory: (dkb,
+        // dkb-1) into its slot of column buffer (dkb-1) % 3, (dkb, dkb) back
+        // into dgs[]
+        auto hand_over = [&]() {
+            if (dkb >= 2)
+                st_frag(dgs + dkb * kTileElems, lane, dg);
+            st_frag(colb + (((dkb - 1) % 3) * TT + dkb) * kTileElems, lane, sd);
+            flag_set(hmb + dkb, s + 1, lane);
+        };
+        if (diag_owner && dkb > 0) {
+            sd = init_tile<NU, NX, NW>(dkb, dkb - 1, rq, cq, s, sgn, Rg, Sg, Qg, rg, qg, ru0p, BA, aligned);
+            if (s > 0) {
+#pragma unroll
+                for (int kt = 0; kt < C::NXC; ++kt) {
+                    const Frag wi = ld_frag(Wsm + (dkb * C::NXC + kt) * kTileElems, lane);
+                    const Frag wj = ld_frag(Wsm + ((dkb - 1) * C::NXC + kt) * kTileElems, lane);
+                    tile_gemm_nt(sd, wi, wj);
+                }
+            }
+            if (dkb == 1)
+                hand_over(); // block column 0 updates nothing of (1, 0)
+        }
 #pragma unroll
         for (int k = 0; k < MAXL; ++k) {
             if (k >= mycnt)
@@ -448,9 +561,6 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
             if (tj < CT)
                 acc[k] = init_tile<NU, NX, NW>(ti, tj, rq, cq, s, sgn, Rg, Sg, Qg, rg, qg, ru0p, BA, aligned);
         }
-        if (diag_owner)
-            dg = init_tile<NU, NX, NW>(dkb, dkb, rq, cq, s, sgn, Rg, Sg, Qg, rg, qg, ru0p, BA, aligned);
-        // ---- += W W' (s > 0) --------------------------------------------
         if (s > 0) {
 #pragma unroll
             for (int k = C::NPS; k < MAXL; ++k) { // skip-mode pure tiles: no W W'
@@ -462,13 +572,6 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                     const Frag wi = ld_frag(Wsm + (ti * C::NXC + kt) * kTileElems, lane);
                     const Frag wj = ld_frag(Wsm + (tj * C::NXC + kt) * kTileElems, lane);
                     tile_gemm_nt(acc[k], wi, wj);
-                }
-            }
-            if (diag_owner) {
-#pragma unroll
-                for (int kt = 0; kt < C::NXC; ++kt) {
-                    const Frag wi = ld_frag(Wsm + (dkb * C::NXC + kt) * kTileElems, lane);
-                    tile_gemm_nt(dg, wi, wi);
                 }
             }
         }
@@ -483,40 +586,43 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                 pf_lines(a.p.Q + ((size_t)b * (N + 1) + x1) * NX * NX, NX * NX * 8, tid, NTH);
         }
         if (ph) ph[s * 8 + 1] = clock64();
-        // ---- pivot floor: max |diag| (kernels.cpp:21-29) ---------------------
-        if (diag_owner) {
-            double v = (rq & 1) ? dg.b : dg.a;
-            v = ((lane & 3) == rq / 2) ? fabs(v) : 0.0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
-                v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-            if (lane == 0)
-                atomicMax(red, (unsigned long long)__double_as_longlong(v));
-        }
-        // pivot diagonal tiles 0 and 1 go to the pivot warp now (tile d > 1
-        // two steps before its turn, below)
-        if (diag_owner && dkb <= 1)
-            st_frag(dgs + dkb * kTileElems, lane, dg);
-        __syncthreads(); // W and BA_0 reads done, pivot floor, diagonal tiles 0 / 1 handed over
+        // W and BA_0 reads done, dgs[] written. The pivot warp only arrives
+        // (s > 0) and starts on block column 0 while the others finish W W'
+        if (warp == 0 && s > 0) {
+            __threadfence_block();
+            asm volatile("bar.arrive 3, %0;" ::"n"(NTH) : "memory");
+        } else
+            asm volatile("bar.sync 3, %0;" ::"n"(NTH) : "memory");
         if (s == 0 && n > 1)
             stage_BA_cta<NU, NX, NW, TMA>(g, a.p, b, g.stage_of(c, 1), sm, tid, bamb);
-        const double dfloor = 1e-14 * __longlong_as_double((long long)red[0]);
         if (warp == 0)
             pivot_step(0, dfloor, s);
+        else if (diag_owner && dkb >= 2)
+            dg = ld_frag(dgs + dkb * kTileElems, lane);
 
-        // ---- blocked Cholesky with look-ahead ----------------------------
-        // Per block column kb, ONE CTA barrier: every warp solves its own
-        // (complete) column-kb tiles in registers against the published
-        // L_kk^{-1} (X <- X L_kk^{-T}, two DMMAs; the wait is on the mbarrier
-        // the pivot warp arrives at) and writes them to column buffer kb & 1;
-        // barrier; then the pivot warp updates and factors (kb+1, kb+1) while
-        // the bulk warps apply column kb to their tiles. Buffer kb & 1 is
-        // rewritten at step kb + 2, after the barrier of step kb + 1.
+        // ---- blocked Cholesky, the pivot chain decoupled --------------------
+        // Per block column kb a bulk warp waits for L_kk^{-1} (lmb[kb]),
+        // solves its own (complete) column-kb tiles in registers (X <- X
+        // L_kk^{-T}, two DMMAs) into column buffer kb % 3, passes the step's
+        // barrier, brings its (dkb, dkb) / (dkb, dkb-1) up to date (handing
+        // them over at kb = dkb - 2) and applies column kb to its list prefix.
+        // The pivot warp meanwhile runs pivot_step(kb + 1). Buffer kb % 3 is
+        // next written at step kb + 3: by the owners' hand-over during the
+        // trailing updates of step kb + 1, i.e. after the barrier of step kb +
+        // 1, which every warp reaches with its reads of step kb done.
 #pragma unroll 1
         for (int kb = 0; kb < CT; ++kb) {
             const int par = kb & 1;
-            double *col = colb + par * TT * kTileElems;
+            double *col = colb + (kb % 3) * TT * kTileElems;
             TRC(0);
+            if (warp == 0) {
+                if (kb + 1 < CT)
+                    pivot_step(kb + 1, dfloor, s);
+                else
+                    bar_arrive(kb);
+                TRC(6);
+                continue;
+            }
             const int cnt = CNT(kb + 1);
             const int hi = CNT(kb);
             const unsigned colS = smem_u32(col) + 16 * lane;
@@ -532,41 +638,74 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
             // straight-line code here and below: a walk over the unrolled
             // list costs issue slots for every slot it skips
             if (hi > cnt) {
-                mb_wait(lmb + kb, s & 1);
+                flag_wait(lmb + kb, s + 1);
+                TRC(5);
                 const Frag linv = ld_frag(linvb + par * kTileElems, lane);
-#define SOLVE_CASE(K)                                                                                  \
-    case K:                                                                                            \
-        if constexpr (K < MAXL) {                                                                      \
-            if (K >= hi)                                                                               \
-                break;                                                                                 \
-            constexpr int T = K < MAXL ? K : 0;                                                        \
-            Frag r{0.0, 0.0};                                                                          \
-            tile_gemm_nt(r, acc[T], linv);                                                             \
-            acc[T] = r;                                                                                \
-            sts(colS + (opk[T] & 0xffffu), r);                                                         \
-        }
-                switch (cnt) {
-                    SOLVE_CASE(0) SOLVE_CASE(1) SOLVE_CASE(2) SOLVE_CASE(3) SOLVE_CASE(4) SOLVE_CASE(5)
-                    SOLVE_CASE(6) SOLVE_CASE(7) SOLVE_CASE(8) SOLVE_CASE(9) SOLVE_CASE(10) SOLVE_CASE(11)
-                    SOLVE_CASE(12) SOLVE_CASE(13) SOLVE_CASE(14)
-                default: break;
+                TRC(7);
+                // entered at slot cnt through a compare tree (a switch becomes
+                // a jump table: one more indexed constant load per step)
+#define SOLVE_AT(K)                                                                                    \
+    SV_##K : if constexpr (K < MAXL) {                                                                 \
+        if (K >= hi)                                                                                   \
+            goto SV_END;                                                                               \
+        constexpr int T = K < MAXL ? K : 0;                                                            \
+        Frag r{0.0, 0.0};                                                                              \
+        tile_gemm_nt(r, acc[T], linv);                                                                 \
+        acc[T] = r;                                                                                    \
+        sts(colS + (opk[T] & 0xffffu), r);                                                             \
+    }
+                if (cnt < 8) {
+                    if (cnt < 4) {
+                        if (cnt < 2) {
+                            if (cnt == 0)
+                                goto SV_0;
+                            goto SV_1;
+                        }
+                        if (cnt == 2)
+                            goto SV_2;
+                        goto SV_3;
+                    }
+                    if (cnt < 6) {
+                        if (cnt == 4)
+                            goto SV_4;
+                        goto SV_5;
+                    }
+                    if (cnt == 6)
+                        goto SV_6;
+                    goto SV_7;
                 }
-#undef SOLVE_CASE
+                if (cnt < 12) {
+                    if (cnt < 10) {
+                        if (cnt == 8)
+                            goto SV_8;
+                        goto SV_9;
+                    }
+                    if (cnt == 10)
+                        goto SV_10;
+                    goto SV_11;
+                }
+                if (cnt < 13)
+                    goto SV_12;
+                if (cnt < 14)
+                    goto SV_13;
+                goto SV_14;
+                SOLVE_AT(0) SOLVE_AT(1) SOLVE_AT(2) SOLVE_AT(3) SOLVE_AT(4) SOLVE_AT(5) SOLVE_AT(6) SOLVE_AT(7)
+                SOLVE_AT(8) SOLVE_AT(9) SOLVE_AT(10) SOLVE_AT(11) SOLVE_AT(12) SOLVE_AT(13) SOLVE_AT(14)
+            SV_END:;
+#undef SOLVE_AT
             }
             TRC(1);
-            __syncthreads(); // column kb solved
+            bar_wait(kb); // column kb solved (the pivot warp's tile (kb+1, kb) included)
             TRC(2);
-            // (B) look-ahead by the pivot warp; the diagonal-tile owners apply
-            // column kb, the owner of (kb+2, kb+2) hands it over
-            if (warp == 0) {
-                if (kb + 1 < CT)
-                    pivot_step(kb + 1, dfloor, s);
-                TRC(6);
-            } else if (diag_owner && dkb > kb + 1) {
+            // (B) the diagonal-tile owners apply column kb to (dkb, dkb) and
+            // (dkb, dkb-1); the owner of block column kb+2's hands them over
+            if (diag_owner && dkb > kb + 1) {
                 const Frag li = ld_frag(col + dkb * kTileElems, lane);
+                const Frag lj = ld_frag(col + (dkb - 1) * kTileElems, lane);
                 tile_gemm_nt_sub(dg, li, li);
+                tile_gemm_nt_sub(sd, li, lj);
                 if (dkb == kb + 2)
-                    st_frag(dgs + dkb * kTileElems, lane, dg);
+                    hand_over();
             }
             TRC(3);
             // trailing update of my prefix: C(ti, tj) -= L(ti, kb) L(tj, kb)',
@@ -595,8 +734,6 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
 #endif
             TRC(4);
         }
-        if (tid == 0)
-            red[0] = 0ull;
         if (ph) ph[s * 8 + 2] = clock64();
 
         // ---- store the factor tiles and y_s' ---------------------------------
@@ -710,6 +847,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
 #undef LTJ
 #undef CNT
 #undef TRC
+#undef PTRC
 }
 
 namespace {
@@ -759,12 +897,12 @@ template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStre
             placed[ti][tj] = true;
         };
         {
-            int w = 0;
+            int w = 0; // the pivot warp (0) holds no tile
             for (int tj = C::RT - 1; tj >= C::CT && C::NPS > 0; --tj)
                 for (int ti = C::RT - 1; ti >= tj; --ti) {
-                    if (w >= NW * C::NPS)
+                    if (w >= (NW - 1) * C::NPS)
                         break;
-                    give(w % NW, ti, tj, C::XT0);
+                    give(1 + w % (NW - 1), ti, tj, C::XT0);
                     ++w;
                 }
         }
@@ -774,11 +912,11 @@ template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStre
             // until their slots are full
             std::vector<int> quiet_part[kMaxW];
             int room[kMaxW] = {};
-            for (int w = 0; w < NW; w += 4)
+            for (int w = 4; w < NW; w += 4)
                 room[w] = C::MAXL - nown[w];
             int w = 4 % NW;
             for (int tj = 0; tj < C::CT; ++tj)
-                for (int ti = tj + 1; ti < C::TT; ++ti) {
+                for (int ti = tj + 2; ti < C::TT; ++ti) { // (tj+1, tj) is the pivot warp's
                     int q = -1;
                     if (tj == 0 && room[0] > 0)
                         q = 0;
@@ -806,7 +944,7 @@ template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStre
         }
         for (int tj = C::TT - 1; tj >= 0; --tj)
             for (int ti = C::TT - 1; ti >= tj; --ti) {
-                if ((ti == tj && tj < C::CT) || placed[ti][tj])
+                if ((ti == tj && tj < C::CT) || (ti == tj + 1 && ti < C::CT) || placed[ti][tj])
                     continue;
                 int best = -1;
                 double bc = 0;
@@ -826,7 +964,7 @@ template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStre
                         if (nown[w] < C::MAXL)
                             best = w;
                     if (best < 0)
-                        best = 0;
+                        return cudaErrorInvalidValue;
                     // keep its list in column-descending order: insert before lower columns
                     int pos = nown[best];
                     while (pos > C::NPS && (h[best * kPL + pos - 1] & 255) < tj) {
