@@ -365,9 +365,11 @@ int dump_phases(cyq_ctx *ctx, const Geo &g, const long long *ph, const long long
     CU(cudaMemcpyAsync(q.data(), sph, 32 * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     for (int s = 0; s < g.n; ++s)
-        fprintf(stderr, "phase s=%d init+WW %lld chol %lld store %lld mw %lld V %lld\n", s,
+        fprintf(stderr, "phase s=%d init+WW %lld chol %lld store %lld mw %lld V %lld (wl %lld tiles %lld wait %lld rest %lld)\n", s,
                 h[s * 8 + 1] - h[s * 8 + 0], h[s * 8 + 2] - h[s * 8 + 1], h[s * 8 + 3] - h[s * 8 + 2],
-                h[s * 8 + 4] - h[s * 8 + 3], (s + 1 < g.n ? h[(s + 1) * 8] : h[g.n * 8]) - h[s * 8 + 4]);
+                h[s * 8 + 4] - h[s * 8 + 3], (s + 1 < g.n ? h[(s + 1) * 8] : h[g.n * 8]) - h[s * 8 + 4],
+                h[s * 8 + 5] - h[s * 8 + 4], h[s * 8 + 6] - h[s * 8 + 5], h[s * 8 + 7] - h[s * 8 + 6],
+                (s + 1 < g.n ? h[(s + 1) * 8] : h[g.n * 8]) - h[s * 8 + 7]);
 #ifdef CYQ_TRACE
     if (g.nx == 64) { // riccati_cta column-loop trace: per (kb, warp) event clocks relative to the step start
         const int NW = 16, CT = 12;

@@ -265,6 +265,21 @@ __device__ __forceinline__ Frag init_tile(int ti, int tj, int rq, int cq, int s,
 
 } // namespace
 
+// Kernel layout: after the common set-up the CTA splits for good into the
+// PIVOT WARP (warp 0) and the BULK WARPS (1 .. NW-1), two code paths with their
+// own registers (the pivot path holds no panel tile, the bulk path none of the
+// factorization's temporaries) that meet at named barriers:
+//   1 + kb % 2  block column kb (bulk warps wait, the pivot warp only arrives)
+//   3           stage top (W and BA_0 read, dgs[] written)
+//   4           the CTA-wide phases after the column loop
+// Warp 0 holds no list tile and runs the serial chain of the blocked Cholesky
+// by itself -- solve (d, d-1) against L_{d-1}^{-1}, apply it to (d, d), factor
+// (d, d), publish L_dd^{-1}. Its SM sub-partition (warps 0, 4, 8, ...) holds
+// only tiles of the first block columns (host plan), so after the first steps
+// no DMMA of another warp queues ahead of the chain's FP64 instructions. The
+// bulk warps with warp % 4 != 0 each keep one pivot diagonal tile (dkb, dkb) in
+// `dg` and the tile left of it (dkb, dkb-1) in `sd` up to date and hand both
+// over through shared memory (flag hmb[dkb]) once column dkb-2 is applied.
 template <int NU, int NX, int NW, bool TMA>
 __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) {
     using C = CS<NU, NX, NW>;
@@ -282,44 +297,6 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
     double *tscr = sm + C::O_SCR;
     const bool implicit_rhs = (a.p.ru == nullptr);
     const double sgn = implicit_rhs ? -1.0 : 1.0;
-    int fail_piv = -1, fail_stage = 0;
-    // Warp 0 is the PIVOT WARP: it holds no list tile and runs the serial
-    // chain of the blocked Cholesky by itself -- solve (d, d-1) against
-    // L_{d-1}^{-1}, apply it to (d, d), factor (d, d), publish L_dd^{-1} --
-    // without waiting at the CTA barriers (it only arrives). Its SM
-    // sub-partition (warps 0, 4, 8, ...) holds only tiles of the first block
-    // columns (host plan), so after the first steps no DMMA of another warp
-    // queues ahead of the chain's FP64 instructions. The bulk warps (warp % 4
-    // != 0) each keep one pivot diagonal tile (dkb, dkb) in `dg` and the tile
-    // left of it (dkb, dkb-1) in `sd` up to date and hand both over through
-    // shared memory (mbarrier hmb[dkb]) once column dkb-2 has been applied
-    const int dkb = (warp & 3) ? (warp >> 2) * 3 + (warp & 3) - 1 : -1;
-    const bool diag_owner = dkb >= 0 && dkb < CT;
-    // my list tiles (ti, tj) from constant memory (warp-uniform loads, no
-    // index registers)
-    // opk[k] = byte offsets of the (ti, tj) slots in a column buffer, ti in
-    // the low half (compile-time k everywhere: plain registers)
-    // (the words pass through an empty asm so that the compiler keeps them in
-    // registers: it otherwise re-reads the constant bank, ~100+ cycles per
-    // indexed load, at the top of every block-column step)
-    unsigned lpk[kLW];
-#pragma unroll
-    for (int i = 0; i < kLW; ++i) {
-        lpk[i] = c_lpk[warp * kLW + i];
-        asm volatile("" : "+r"(lpk[i]));
-    }
-    unsigned opk[MAXL];
-#pragma unroll
-    for (int k = 0; k < MAXL; ++k) {
-        const unsigned e = (lpk[k / 3] >> (10 * (k % 3))) & 1023u;
-        opk[k] = ((e & 31u) << 9) | ((e >> 5) << 25);
-    }
-    unsigned long long cpk = c_cpk[warp];
-    asm volatile("" : "+l"(cpk));
-    const int mycnt = (int)(cpk & 15u);
-#define LTI(k) ((int)((opk[k] >> 9) & 31u))
-#define LTJ(k) ((int)(opk[k] >> 25))
-#define CNT(kb) ((int)((cpk >> (4 * (kb))) & 15u))
     for (int i = tid; i < C::SMEM; i += NTH)
         sm[i] = 0.0;
     unsigned long long *bamb = reinterpret_cast<unsigned long long *>(sm + C::O_MB);
@@ -327,7 +304,6 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
     unsigned *lmb = reinterpret_cast<unsigned *>(sm + C::O_LMB);
     unsigned *hmb = reinterpret_cast<unsigned *>(sm + C::O_HMB);
     double *dgs = sm + C::O_DG;
-    int baph = 0; // completed [B A] stagings (mbarrier phases)
     __syncthreads();
     if (tid == 0) {
         mb_init(bamb, 1);
@@ -336,6 +312,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
     __syncthreads();
     // prologue: BA_0, S_0 x_init (ru[0] term)
     {
+        int ph0 = 0;
         const int j0 = g.stage_of(c, 0);
         stage_BA_cta<NU, NX, NW, TMA>(g, a.p, b, j0, sm, tid, bamb);
         if (implicit_rhs && c == 0)
@@ -346,170 +323,249 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                           __ldg(a.p.x_init + (size_t)b * NX + k);
                 ru0[i] = s0;
             }
-        wait_BA(bamb, baph);
+        wait_BA(bamb, ph0);
     }
     __syncthreads();
 
-    Frag acc[MAXL];
+    // ---- pieces shared by the two paths ---------------------------------------
+    struct StageIn {
+        const double *Rg, *Sg, *Qg, *rg, *qg, *ru0p;
+        bool aligned;
+    };
+    auto stage_in = [&](int s) {
+        const int j = g.stage_of(c, s), xi = g.x_index_of(c, s);
+        const bool j0 = j == 0, in = j < N, qin = xi <= N;
+        StageIn r;
+        r.Rg = in ? a.p.R + ((size_t)b * N + j) * NU * NU : nullptr;
+        r.Sg = (in && !j0) ? a.p.S + ((size_t)b * N + j) * NU * NX : nullptr;
+        r.Qg = qin ? a.p.Q + ((size_t)b * (N + 1) + xi) * NX * NX : nullptr;
+        r.rg = in ? (a.p.ru ? a.p.ru : a.p.r) + ((size_t)b * N + j) * NU : nullptr;
+        r.qg = qin ? (a.p.qx ? a.p.qx : a.p.q) + ((size_t)b * (N + 1) + xi) * NX : nullptr;
+        r.ru0p = (implicit_rhs && j0) ? ru0 : nullptr;
+        r.aligned = ((reinterpret_cast<uintptr_t>(a.p.R) | reinterpret_cast<uintptr_t>(a.p.Q)) & 15) == 0;
+        return r;
+    };
+    auto tile0 = [&](int ti, int tj, int s, const StageIn &in) {
+        return init_tile<NU, NX, NW>(ti, tj, rq, cq, s, sgn, in.Rg, in.Sg, in.Qg, in.rg, in.qg, in.ru0p, BA,
+                                     in.aligned);
+    };
+    // prefetch H_{s+1} into L2
+    auto prefetch_next = [&](int s) {
+        if (s + 1 < n) {
+            const int j1 = g.stage_of(c, s + 1), x1 = g.x_index_of(c, s + 1);
+            if (j1 < N) {
+                pf_lines(a.p.R + ((size_t)b * N + j1) * NU * NU, NU * NU * 8, tid, NTH);
+                pf_lines(a.p.S + ((size_t)b * N + j1) * NU * NX, NU * NX * 8, tid, NTH);
+            }
+            if (x1 <= N)
+                pf_lines(a.p.Q + ((size_t)b * (N + 1) + x1) * NX * NX, NX * NX * 8, tid, NTH);
+        }
+    };
+    auto bar_wait = [](int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NTH) : "memory"); };
+    auto bar_arrive = [](int id) {
+        __threadfence_block();
+        asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(NTH) : "memory");
+    };
+    // W of stage s+1 once the factor tiles of stage s are out (every warp):
+    // -wl_new = L_Q' (sgn f) + x' (kkt_solve.cpp:85-90; 8 lanes per entry,
+    // split k, shuffle-reduced), V = BA_{s+1}' L_Q -> W tile rows 0..CT-1
+    // (DMMA, one tile per warp pass, two accumulators to halve the dependent
+    // DMMA chain), the rhs row of W, [B A] of stage s+2 on its way
+    auto next_W = [&](int s, int &baph, long long *ph) {
+        wait_BA(bamb, baph); // BA_{s+1}, f_{s+1}
+        bar_wait(4);
+        if (ph) ph[s * 8 + 4] = clock64();
+        for (int t0 = 4 * warp; t0 < NX; t0 += 4 * NW) {
+            const int t = t0 + (lane >> 3), part = lane & 7;
+            double q = 0.0;
+            if (t < NX)
+                for (int k = t + part; k < NX; k += 8)
+                    q += LQ[k * C::LQS + t] * (sgn * fb[k]);
+            q += __shfl_xor_sync(0xffffffffu, q, 1);
+            q += __shfl_xor_sync(0xffffffffu, q, 2);
+            q += __shfl_xor_sync(0xffffffffu, q, 4);
+            if (t < NX && part == 0) {
+                q += yx[t];
+                mw[t] = q;
+                a.wl[((size_t)chain * n + s) * NX + t] = -q;
+            }
+        }
+        if (ph) ph[s * 8 + 5] = clock64();
+        // V tiles in pairs (ti, kt = P) + (ti, kt = NXC-1-P): L_Q is lower
+        // triangular, so a pair is NXC + 1 k-tiles of work whatever P is, and
+        // both tiles share the BA' operands. P is a compile-time case: every
+        // operand is one 8-byte load at an immediate offset from two base
+        // registers, four accumulator chains per pair.
+        {
+            constexpr int NP = (C::NXC + 1) / 2, NITEM = CT * NP;
+            const double *pa0 = BA + (lane & 3) * C::PW + rq, *pb0 = LQ + (lane & 3) * C::LQS + rq;
+            auto item = [&](auto PC, int ti) {
+                constexpr int P = decltype(PC)::value, Q = C::NXC - 1 - P;
+                const double *pa = pa0 + 8 * ti;
+                Frag fa0{0.0, 0.0}, fa1{0.0, 0.0}, fb0{0.0, 0.0}, fb1{0.0, 0.0};
 #pragma unroll
-    for (int k = 0; k < MAXL; ++k)
-        acc[k] = Frag{0.0, 0.0};
-    Frag dg{0.0, 0.0}, sd{0.0, 0.0};
+                for (int ks = 2 * P; ks < NX / 4; ++ks) {
+                    const double av = pa[4 * ks * C::PW];
+                    dmma((ks & 1) ? fa1 : fa0, av, pb0[4 * ks * C::LQS + 8 * P]);
+                    if (Q != P && ks >= 2 * Q)
+                        dmma((ks & 1) ? fb1 : fb0, av, pb0[4 * ks * C::LQS + 8 * Q]);
+                }
+                st_frag(Wsm + (ti * C::NXC + P) * kTileElems, lane, Frag{fa0.a + fa1.a, fa0.b + fa1.b});
+                if (Q != P)
+                    st_frag(Wsm + (ti * C::NXC + Q) * kTileElems, lane, Frag{fb0.a + fb1.a, fb0.b + fb1.b});
+            };
+            for (int v = warp; v < NITEM; v += NW) {
+                const int ti = v % CT;
+                switch (v / CT) {
+                case 0: item(std::integral_constant<int, 0>{}, ti); break;
+                case 1: if constexpr (NP > 1) item(std::integral_constant<int, (NP > 1 ? 1 : 0)>{}, ti); break;
+                case 2: if constexpr (NP > 2) item(std::integral_constant<int, (NP > 2 ? 2 : 0)>{}, ti); break;
+                case 3: if constexpr (NP > 3) item(std::integral_constant<int, (NP > 3 ? 3 : 0)>{}, ti); break;
+                default: break;
+                }
+            }
+            static_assert(NP <= 4, "V pair cases");
+        }
+        if (ph) ph[s * 8 + 6] = clock64();
+        bar_wait(4); // mw ready, V written, BA / LQ reads done
+        if (ph) ph[s * 8 + 7] = clock64();
+        // rhs row of W: -wl in row RHS of tile row RT (other rows of that
+        // tile row: coupling rows, stored by their owners)
+        for (int t = tid; t < NX; t += NTH)
+            Wsm[(C::RT * C::NXC + t / 8) * kTileElems + C::RR * 8 + t % 8] = mw[t];
+        if (s + 2 < n)
+            stage_BA_cta<NU, NX, NW, TMA>(g, a.p, b, g.stage_of(c, s + 2), sm, tid, bamb);
+        bar_wait(4);
+    };
 
-    // the owner factors its diagonal tile dg (L_kk, upper zeroed) and
-    // publishes L_kk^{-1} -> linv[kb & 1] (identity tile carried through the
-    // pivot steps gives L^{-T}; transposed through shared memory)
-    // The next pivot is computed in every lane from values shuffled one step
-    // early (d = (k+1, k+1), u = (k+1, k) before this step's update):
-    // pv' = d - (u iv)^2, the owner lane's exact fma -- no shuffle on the
-    // rsqrt -> mul -> fma pivot chain (as riccati_warp.cu; bit-identical)
+    if (warp == 0) {
+        // =====================================================================
+        // PIVOT WARP
+        // =====================================================================
+        int baph = 1; // completed [B A] stagings (mbarrier phases)
+        int fail_piv = -1, fail_stage = 0;
+        Frag dg{0.0, 0.0};
 #ifdef CYQ_TRACE
-    // pivot-warp event clocks: a.phase[6144 + d * 8 + e] (stage CYQ_TRACE, chain 0)
-    long long *ptrc = (a.phase && chain == 0 && tid == 0) ? a.phase + 6144 : nullptr;
+        // pivot-warp event clocks: a.phase[6144 + d * 8 + e] (stage CYQ_TRACE, chain 0)
+        long long *ptrc = (a.phase && chain == 0 && tid == 0) ? a.phase + 6144 : nullptr;
 #define PTRC(d, e) do { if (ptrc && s == CYQ_TRACE) ptrc[(d) * 8 + (e)] = clock64(); } while (0)
 #else
 #define PTRC(d, e) do { } while (0)
 #endif
-    auto factor_diag = [&](int kb, double dfloor, int s) {
-        Frag idt{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0};
-        double pvn = 0.0;
+        // Factors the diagonal tile dg (L_kk, upper zeroed) and publishes
+        // L_kk^{-1} -> linv[kb & 1] (identity tile carried through the pivot
+        // steps gives L^{-T}; transposed through shared memory). The next
+        // pivot is computed in every lane from values shuffled one step early
+        // (d = (k+1, k+1), u = (k+1, k) before this step's update): pv' = d -
+        // (u iv)^2, the owner lane's exact fma -- no shuffle on the rsqrt ->
+        // mul -> fma pivot chain (as riccati_warp.cu)
+        auto factor_diag = [&](int kb, double dfloor, int s) {
+            Frag idt{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0};
+            double pvn = 0.0;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            const int src = kk / 2;
-            const double vk = (kk & 1) ? dg.b : dg.a;
-            const double pv = kk == 0 ? __shfl_sync(0xffffffffu, vk, 4 * kk + src) : pvn;
-            const double urk = __shfl_sync(0xffffffffu, vk, 4 * rq + src);
-            const double uc0 = __shfl_sync(0xffffffffu, vk, 4 * cq + src);
-            const double uc1 = __shfl_sync(0xffffffffu, vk, 4 * (cq + 1) + src);
-            double dn = 0.0, un = 0.0;
-            if (kk + 1 < 8) {
-                dn = __shfl_sync(0xffffffffu, ((kk + 1) & 1) ? dg.b : dg.a, 4 * (kk + 1) + (kk + 1) / 2);
-                un = __shfl_sync(0xffffffffu, vk, 4 * (kk + 1) + src);
+            for (int kk = 0; kk < 8; ++kk) {
+                const int src = kk / 2;
+                const double vk = (kk & 1) ? dg.b : dg.a;
+                const double pv = kk == 0 ? __shfl_sync(0xffffffffu, vk, 4 * kk + src) : pvn;
+                const double urk = __shfl_sync(0xffffffffu, vk, 4 * rq + src);
+                const double uc0 = __shfl_sync(0xffffffffu, vk, 4 * cq + src);
+                const double uc1 = __shfl_sync(0xffffffffu, vk, 4 * (cq + 1) + src);
+                double dn = 0.0, un = 0.0;
+                if (kk + 1 < 8) {
+                    dn = __shfl_sync(0xffffffffu, ((kk + 1) & 1) ? dg.b : dg.a, 4 * (kk + 1) + (kk + 1) / 2);
+                    un = __shfl_sync(0xffffffffu, vk, 4 * (kk + 1) + src);
+                }
+                const bool first = !(pv > dfloor && isfinite(pv)) && fail_piv < 0;
+                fail_piv = first ? 8 * kb + kk : fail_piv;
+                fail_stage = first ? s : fail_stage;
+                const double iv = rsqrt_nr(pv);
+                if (kk + 1 < 8) {
+                    const double l = un * iv;
+                    pvn = fma(-l, l, dn);
+                }
+                const double lc0 = (cq > kk) ? uc0 * iv : 0.0;
+                const double lc1 = (cq + 1 > kk) ? uc1 * iv : 0.0;
+                const double lrk = urk * iv;
+                const double nv = (rq == kk) ? pv * iv : lrk;
+                if (kk & 1)
+                    dg.b = (q2 == src) ? nv : dg.b;
+                else
+                    dg.a = (q2 == src) ? nv : dg.a;
+                dg.a = fma(-lrk, lc0, dg.a);
+                dg.b = fma(-lrk, lc1, dg.b);
+                if (kk == 3)
+                    PTRC(kb, 2);
+                const double vq = (kk & 1) ? idt.b : idt.a;
+                const double xrq = __shfl_sync(0xffffffffu, vq, 4 * rq + src) * iv;
+                if (kk & 1)
+                    idt.b = (q2 == src) ? xrq : idt.b;
+                else
+                    idt.a = (q2 == src) ? xrq : idt.a;
+                idt.a -= xrq * lc0;
+                idt.b -= xrq * lc1;
             }
-            const bool first = !(pv > dfloor && isfinite(pv)) && fail_piv < 0;
-            fail_piv = first ? 8 * kb + kk : fail_piv;
-            fail_stage = first ? s : fail_stage;
-            const double iv = rsqrt_nr(pv);
-            if (kk + 1 < 8) {
-                const double l = un * iv;
-                pvn = fma(-l, l, dn);
+            if (cq > rq) dg.a = 0.0;
+            if (cq + 1 > rq) dg.b = 0.0;
+            PTRC(kb, 3);
+            st_frag(tscr, lane, idt); // L^{-1} = (L^{-T})'
+            __syncwarp();
+            st_frag(linvb + (kb & 1) * kTileElems, lane, Frag{tscr[cq * 8 + rq], tscr[(cq + 1) * 8 + rq]});
+            __syncwarp();
+        };
+        // Block column d: the tiles (d, d-1) and (d, d) arrive from their
+        // owner (hmb[d]; updates of the block columns < d-1 applied); L(d, d-1)
+        // = X L_{d-1}^{-T} goes to column buffer (d-1) % 3 (every warp's
+        // operand at step d-1) before the arrival at that step's barrier (ids
+        // 1 + kb % 2: the arrival for step kb follows the completion of step
+        // kb-2's barrier -- the hand-over waited for -- not of step kb-1's), to
+        // the stored factor and to the x-space L_Q; then (d, d) -= L L',
+        // factor, publish L_dd^{-1} (lmb[d]), store L_dd
+        auto pivot_step = [&](int d, double dfloor, int s) {
+            PTRC(d, 0);
+            double *fdst = a.fac + ((size_t)chain * n + s) * C::NPT * kTileElems;
+            if (d > 0)
+                flag_wait(hmb + d, s + 1);
+            dg = ld_frag(dgs + d * kTileElems, lane);
+            if (d > 0) {
+                double *slot = colb + (((d - 1) % 3) * TT + d) * kTileElems;
+                const Frag x = ld_frag(slot, lane);
+                const Frag linv = ld_frag(linvb + ((d - 1) & 1) * kTileElems, lane);
+                Frag li{0.0, 0.0};
+                tile_gemm_nt(li, x, linv);
+                st_frag(slot, lane, li);
+                bar_arrive(1 + ((d - 1) & 1));
+                tile_gemm_nt_sub(dg, li, li);
+                st_frag(fdst + C::PI(d, d - 1) * kTileElems, lane, li);
+                if (d - 1 >= C::XT0) {
+                    const int r = 8 * d + rq - NU, c0 = 8 * (d - 1) + cq - NU;
+                    LQ[r * C::LQS + c0] = li.a;
+                    LQ[r * C::LQS + c0 + 1] = li.b;
+                }
             }
-            const double lc0 = (cq > kk) ? uc0 * iv : 0.0;
-            const double lc1 = (cq + 1 > kk) ? uc1 * iv : 0.0;
-            const double lrk = urk * iv;
-            const double nv = (rq == kk) ? pv * iv : lrk;
-            if (kk & 1)
-                dg.b = (q2 == src) ? nv : dg.b;
-            else
-                dg.a = (q2 == src) ? nv : dg.a;
-            dg.a = fma(-lrk, lc0, dg.a);
-            dg.b = fma(-lrk, lc1, dg.b);
-            if (kk == 3)
-                PTRC(kb, 2);
-            const double vq = (kk & 1) ? idt.b : idt.a;
-            const double xrq = __shfl_sync(0xffffffffu, vq, 4 * rq + src) * iv;
-            if (kk & 1)
-                idt.b = (q2 == src) ? xrq : idt.b;
-            else
-                idt.a = (q2 == src) ? xrq : idt.a;
-            idt.a -= xrq * lc0;
-            idt.b -= xrq * lc1;
-        }
-        if (cq > rq) dg.a = 0.0;
-        if (cq + 1 > rq) dg.b = 0.0;
-        PTRC(kb, 3);
-        st_frag(tscr, lane, idt); // L^{-1} = (L^{-T})'
-        __syncwarp();
-        st_frag(linvb + (kb & 1) * kTileElems, lane, Frag{tscr[cq * 8 + rq], tscr[(cq + 1) * 8 + rq]});
-        __syncwarp();
-    };
-    // The CTA barrier of block column kb (named barrier 1): the bulk warps
-    // wait, the pivot warp only arrives
-    // (ids 1 + kb % 2: its arrival for step kb follows the completion of
-    // step kb-2's barrier -- the hand-over it waited for -- not of step kb-1's)
-    auto bar_wait = [](int kb) { asm volatile("bar.sync %0, %1;" ::"r"(1 + (kb & 1)), "n"(NTH) : "memory"); };
-    auto bar_arrive = [](int kb) {
-        __threadfence_block();
-        asm volatile("bar.arrive %0, %1;" ::"r"(1 + (kb & 1)), "n"(NTH) : "memory");
-    };
-    // pivot warp, block column d: the tiles (d, d-1) and (d, d) arrive from
-    // their owner (hmb[d]; updates of the block columns < d-1 applied);
-    // L(d, d-1) = X L_{d-1}^{-T} goes to column buffer (d-1) % 3 (every warp's
-    // operand at step d-1) before the pivot warp's arrival at that step's
-    // barrier, to the stored factor and to the x-space L_Q; then (d, d) -= L
-    // L', factor, publish L_dd^{-1} (lmb[d]), store L_dd
-    auto pivot_step = [&](int d, double dfloor, int s) {
-        PTRC(d, 0);
-        double *fdst = a.fac + ((size_t)chain * n + s) * C::NPT * kTileElems;
-        if (d > 0)
-            flag_wait(hmb + d, s + 1);
-        dg = ld_frag(dgs + d * kTileElems, lane);
-        if (d > 0) {
-            double *slot = colb + (((d - 1) % 3) * TT + d) * kTileElems;
-            const Frag x = ld_frag(slot, lane);
-            const Frag linv = ld_frag(linvb + ((d - 1) & 1) * kTileElems, lane);
-            Frag li{0.0, 0.0};
-            tile_gemm_nt(li, x, linv);
-            st_frag(slot, lane, li);
-            bar_arrive(d - 1);
-            tile_gemm_nt_sub(dg, li, li);
-            st_frag(fdst + C::PI(d, d - 1) * kTileElems, lane, li);
-            if (d - 1 >= C::XT0) {
-                const int r = 8 * d + rq - NU, c0 = 8 * (d - 1) + cq - NU;
-                LQ[r * C::LQS + c0] = li.a;
-                LQ[r * C::LQS + c0 + 1] = li.b;
-            }
-        }
-        PTRC(d, 1);
+            PTRC(d, 1);
 #ifndef CYQ_X_NOFAC
-        factor_diag(d, dfloor, s);
+            factor_diag(d, dfloor, s);
 #endif
-        PTRC(d, 4);
-        flag_set(lmb + d, s + 1, lane);
-        PTRC(d, 5);
-        st_frag(fdst + C::PI(d, d) * kTileElems, lane, dg);
-        if (d >= C::XT0) {
-            const int r = 8 * d + rq - NU, c0 = 8 * d + cq - NU;
-            LQ[r * C::LQS + c0] = dg.a;
-            LQ[r * C::LQS + c0 + 1] = dg.b;
-        }
-    };
-
-    long long *ph = (a.phase && chain == 0 && tid == 32) ? a.phase : nullptr; // a bulk warp's view
-#ifdef CYQ_TRACE
-    // per-warp event clocks of the column loop at stage CYQ_TRACE (chain 0):
-    // a.phase[4096 + ((kb * NW + warp) * 8 + e)]
-    long long *trc = (a.phase && chain == 0 && lane == 0) ? a.phase + 4096 : nullptr;
-#define TRC(e) do { if (trc && s == CYQ_TRACE) trc[(kb * NW + warp) * 8 + (e)] = clock64(); } while (0)
-#else
-#define TRC(e) do { } while (0)
-#endif
-    for (int s = 0; s < n; ++s) {
-        if (ph) ph[s * 8 + 0] = clock64();
-        const int j = g.stage_of(c, s), xi = g.x_index_of(c, s);
-        const bool j0 = j == 0, in = j < N, qin = xi <= N;
-        const double *Rg = in ? a.p.R + ((size_t)b * N + j) * NU * NU : nullptr;
-        const double *Sg = (in && !j0) ? a.p.S + ((size_t)b * N + j) * NU * NX : nullptr;
-        const double *Qg = qin ? a.p.Q + ((size_t)b * (N + 1) + xi) * NX * NX : nullptr;
-        const double *rg = in ? (a.p.ru ? a.p.ru : a.p.r) + ((size_t)b * N + j) * NU : nullptr;
-        const double *qg = qin ? (a.p.qx ? a.p.qx : a.p.q) + ((size_t)b * (N + 1) + xi) * NX : nullptr;
-        const double *ru0p = (implicit_rhs && j0) ? ru0 : nullptr;
-        const bool aligned = ((reinterpret_cast<uintptr_t>(a.p.R) | reinterpret_cast<uintptr_t>(a.p.Q)) & 15) == 0;
-        // ---- init (H_s from global, coupling rows BA_0 at s = 0, rhs row) and
-        // += W W' (s > 0). The pivot warp prepares every pivot diagonal tile
-        // (two at a time: the 16 DMMAs of a tile are one dependent chain) in
-        // the hand-off slots dgs[] and takes the pivot floor max |diag|
-        // (kernels.cpp:21-29) from them; a bulk warp first prepares the tile
-        // left of its diagonal tile (the owner of (1, 0) hands it over at
-        // once), then its list tiles.
-        double dfloor = 0.0;
-        if (warp == 0) {
+            PTRC(d, 4);
+            flag_set(lmb + d, s + 1, lane);
+            PTRC(d, 5);
+            st_frag(fdst + C::PI(d, d) * kTileElems, lane, dg);
+            if (d >= C::XT0) {
+                const int r = 8 * d + rq - NU, c0 = 8 * d + cq - NU;
+                LQ[r * C::LQS + c0] = dg.a;
+                LQ[r * C::LQS + c0 + 1] = dg.b;
+            }
+        };
+        for (int s = 0; s < n; ++s) {
+            const StageIn in = stage_in(s);
+            // every pivot diagonal tile H_s + W W' (two at a time: the 16 DMMAs
+            // of a tile are one dependent chain) -> dgs[]; the pivot floor
+            // 1e-14 max |diag| (kernels.cpp:21-29)
             double vmax = 0.0;
 #pragma unroll 1
             for (int d = 0; d < CT; d += 2) {
                 const int d1 = d + 1 < CT ? d + 1 : d;
-                Frag t0 = init_tile<NU, NX, NW>(d, d, rq, cq, s, sgn, Rg, Sg, Qg, rg, qg, ru0p, BA, aligned);
-                Frag t1 = init_tile<NU, NX, NW>(d1, d1, rq, cq, s, sgn, Rg, Sg, Qg, rg, qg, ru0p, BA, aligned);
+                Frag t0 = tile0(d, d, s, in), t1 = tile0(d1, d1, s, in);
                 if (s > 0) {
 #pragma unroll
                     for (int kt = 0; kt < C::NXC; ++kt) {
@@ -529,11 +585,86 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1)
                 vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
-            dfloor = 1e-14 * vmax;
+            const double dfloor = 1e-14 * vmax;
+            prefetch_next(s);
+            // stage top: only an arrival for s > 0 (block column 0 starts while
+            // the bulk warps finish W W'); at s = 0 the [B A] copy below
+            // overwrites BA_0, still being read
+            if (s > 0)
+                bar_arrive(3);
+            else
+                bar_wait(3);
+            if (s == 0 && n > 1)
+                stage_BA_cta<NU, NX, NW, TMA>(g, a.p, b, g.stage_of(c, 1), sm, tid, bamb);
+#pragma unroll 1
+            for (int d = 0; d < CT; ++d)
+                pivot_step(d, dfloor, s);
+            bar_arrive(1 + ((CT - 1) & 1)); // barrier of the last block column
+            if (s + 1 < n)
+                next_W(s, baph, nullptr);
         }
-        // the tiles the pivot warp takes over go through shared memory: (dkb,
-        // dkb-1) into its slot of column buffer (dkb-1) % 3, (dkb, dkb) back
-        // into dgs[]
+        unsigned long long my_fail = fail_piv >= 0 ? fail_key(kKindRiccati, c, fail_stage, fail_piv) : ~0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            my_fail = min(my_fail, __shfl_xor_sync(0xffffffffu, my_fail, o));
+        if (lane == 0 && my_fail != ~0ull)
+            atomicMin(a.fail + b, my_fail);
+#undef PTRC
+        return;
+    }
+
+    // =========================================================================
+    // BULK WARPS
+    // =========================================================================
+    int baph = 1;
+    const int dkb = (warp & 3) ? (warp >> 2) * 3 + (warp & 3) - 1 : -1;
+    const bool diag_owner = dkb >= 0 && dkb < CT;
+    // my list tiles: opk[k] = byte offsets of the (ti, tj) slots in a column
+    // buffer, ti in the low half (compile-time k everywhere: plain registers).
+    // The packed words pass through an empty asm so that the compiler keeps
+    // them in registers: it otherwise re-reads the constant bank, ~100+
+    // cycles per indexed load, at the top of every block-column step
+    unsigned lpk[kLW];
+#pragma unroll
+    for (int i = 0; i < kLW; ++i) {
+        lpk[i] = c_lpk[warp * kLW + i];
+        asm volatile("" : "+r"(lpk[i]));
+    }
+    unsigned opk[MAXL];
+#pragma unroll
+    for (int k = 0; k < MAXL; ++k) {
+        const unsigned e = (lpk[k / 3] >> (10 * (k % 3))) & 1023u;
+        opk[k] = ((e & 31u) << 9) | ((e >> 5) << 25);
+    }
+    unsigned long long cpk = c_cpk[warp];
+    asm volatile("" : "+l"(cpk));
+    const int mycnt = (int)(cpk & 15u);
+#define LTI(k) ((int)((opk[k] >> 9) & 31u))
+#define LTJ(k) ((int)(opk[k] >> 25))
+#define CNT(kb) ((int)((cpk >> (4 * (kb))) & 15u))
+    Frag acc[MAXL];
+#pragma unroll
+    for (int k = 0; k < MAXL; ++k)
+        acc[k] = Frag{0.0, 0.0};
+    Frag dg{0.0, 0.0}, sd{0.0, 0.0};
+    long long *ph = (a.phase && chain == 0 && tid == 32) ? a.phase : nullptr; // a bulk warp's view
+#ifdef CYQ_TRACE
+    // per-warp event clocks of the column loop at stage CYQ_TRACE (chain 0):
+    // a.phase[4096 + ((kb * NW + warp) * 8 + e)]
+    long long *trc = (a.phase && chain == 0 && lane == 0) ? a.phase + 4096 : nullptr;
+#define TRC(e) do { if (trc && s == CYQ_TRACE) trc[(kb * NW + warp) * 8 + (e)] = clock64(); } while (0)
+#else
+#define TRC(e) do { } while (0)
+#endif
+    for (int s = 0; s < n; ++s) {
+        if (ph) ph[s * 8 + 0] = clock64();
+        const StageIn in = stage_in(s);
+        // ---- init (H_s from global, coupling rows BA_0 at s = 0, rhs row) and
+        // += W W' (s > 0): first the tile left of my diagonal tile (the owner
+        // of (1, 0) hands it over at once: block column 0 updates nothing of
+        // it), then my list tiles. The tiles the pivot warp takes over go
+        // through shared memory: (dkb, dkb-1) into its slot of column buffer
+        // (dkb-1) % 3, (dkb, dkb) back into dgs[]
         auto hand_over = [&]() {
             if (dkb >= 2)
                 st_frag(dgs + dkb * kTileElems, lane, dg);
@@ -541,7 +672,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
             flag_set(hmb + dkb, s + 1, lane);
         };
         if (diag_owner && dkb > 0) {
-            sd = init_tile<NU, NX, NW>(dkb, dkb - 1, rq, cq, s, sgn, Rg, Sg, Qg, rg, qg, ru0p, BA, aligned);
+            sd = tile0(dkb, dkb - 1, s, in);
             if (s > 0) {
 #pragma unroll
                 for (int kt = 0; kt < C::NXC; ++kt) {
@@ -551,7 +682,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                 }
             }
             if (dkb == 1)
-                hand_over(); // block column 0 updates nothing of (1, 0)
+                hand_over();
         }
 #pragma unroll
         for (int k = 0; k < MAXL; ++k) {
@@ -559,7 +690,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                 break;
             const int ti = LTI(k), tj = LTJ(k);
             if (tj < CT)
-                acc[k] = init_tile<NU, NX, NW>(ti, tj, rq, cq, s, sgn, Rg, Sg, Qg, rg, qg, ru0p, BA, aligned);
+                acc[k] = tile0(ti, tj, s, in);
         }
         if (s > 0) {
 #pragma unroll
@@ -575,29 +706,12 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                 }
             }
         }
-        // prefetch H_{s+1} into L2; BA_1 at s = 0 (BA_0 has been read)
-        if (s + 1 < n) {
-            const int j1 = g.stage_of(c, s + 1), x1 = g.x_index_of(c, s + 1);
-            if (j1 < N) {
-                pf_lines(a.p.R + ((size_t)b * N + j1) * NU * NU, NU * NU * 8, tid, NTH);
-                pf_lines(a.p.S + ((size_t)b * N + j1) * NU * NX, NU * NX * 8, tid, NTH);
-            }
-            if (x1 <= N)
-                pf_lines(a.p.Q + ((size_t)b * (N + 1) + x1) * NX * NX, NX * NX * 8, tid, NTH);
-        }
+        prefetch_next(s);
         if (ph) ph[s * 8 + 1] = clock64();
-        // W and BA_0 reads done, dgs[] written. The pivot warp only arrives
-        // (s > 0) and starts on block column 0 while the others finish W W'
-        if (warp == 0 && s > 0) {
-            __threadfence_block();
-            asm volatile("bar.arrive 3, %0;" ::"n"(NTH) : "memory");
-        } else
-            asm volatile("bar.sync 3, %0;" ::"n"(NTH) : "memory");
+        bar_wait(3); // W and BA_0 reads done, dgs[] written
         if (s == 0 && n > 1)
             stage_BA_cta<NU, NX, NW, TMA>(g, a.p, b, g.stage_of(c, 1), sm, tid, bamb);
-        if (warp == 0)
-            pivot_step(0, dfloor, s);
-        else if (diag_owner && dkb >= 2)
+        if (diag_owner && dkb >= 2)
             dg = ld_frag(dgs + dkb * kTileElems, lane);
 
         // ---- blocked Cholesky, the pivot chain decoupled --------------------
@@ -606,25 +720,23 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         // L_kk^{-T}, two DMMAs) into column buffer kb % 3, passes the step's
         // barrier, brings its (dkb, dkb) / (dkb, dkb-1) up to date (handing
         // them over at kb = dkb - 2) and applies column kb to its list prefix.
-        // The pivot warp meanwhile runs pivot_step(kb + 1). Buffer kb % 3 is
+        // The pivot warp meanwhile runs block column kb + 1. Buffer kb % 3 is
         // next written at step kb + 3: by the owners' hand-over during the
         // trailing updates of step kb + 1, i.e. after the barrier of step kb +
         // 1, which every warp reaches with its reads of step kb done.
+        // (per-step values carried along instead of recomputed: the chain of
+        // dependent integer instructions at the loop top was ~150 cycles)
+        unsigned long long cw = cpk;
+        int cb = 0;
 #pragma unroll 1
         for (int kb = 0; kb < CT; ++kb) {
             const int par = kb & 1;
-            double *col = colb + (kb % 3) * TT * kTileElems;
+            double *col = colb + cb * TT * kTileElems;
+            cb = cb == 2 ? 0 : cb + 1;
             TRC(0);
-            if (warp == 0) {
-                if (kb + 1 < CT)
-                    pivot_step(kb + 1, dfloor, s);
-                else
-                    bar_arrive(kb);
-                TRC(6);
-                continue;
-            }
-            const int cnt = CNT(kb + 1);
-            const int hi = CNT(kb);
+            const int hi = (int)((unsigned)cw & 15u);
+            cw >>= 4;
+            const int cnt = (int)((unsigned)cw & 15u);
             const unsigned colS = smem_u32(col) + 16 * lane;
             auto lds = [](unsigned a) {
                 Frag f;
@@ -634,16 +746,15 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
             auto sts = [](unsigned a, const Frag &f) {
                 asm volatile("st.shared.v2.f64 [%0], {%1,%2};" ::"r"(a), "d"(f.a), "d"(f.b) : "memory");
             };
-            // (A) my column-kb tiles: list positions [cnt, hi). Switch-entered
-            // straight-line code here and below: a walk over the unrolled
-            // list costs issue slots for every slot it skips
+            // (A) my column-kb tiles: list positions [cnt, hi), straight-line
+            // code entered at slot cnt through a compare tree (a walk over
+            // the unrolled list costs issue slots for every slot it skips, a
+            // switch becomes a jump table: an indexed constant load per step)
             if (hi > cnt) {
                 flag_wait(lmb + kb, s + 1);
                 TRC(5);
                 const Frag linv = ld_frag(linvb + par * kTileElems, lane);
                 TRC(7);
-                // entered at slot cnt through a compare tree (a switch becomes
-                // a jump table: one more indexed constant load per step)
 #define SOLVE_AT(K)                                                                                    \
     SV_##K : if constexpr (K < MAXL) {                                                                 \
         if (K >= hi)                                                                                   \
@@ -695,7 +806,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
 #undef SOLVE_AT
             }
             TRC(1);
-            bar_wait(kb); // column kb solved (the pivot warp's tile (kb+1, kb) included)
+            bar_wait(1 + par); // column kb solved (the pivot warp's tile (kb+1, kb) included)
             TRC(2);
             // (B) the diagonal-tile owners apply column kb to (dkb, dkb) and
             // (dkb, dkb-1); the owner of block column kb+2's hands them over
@@ -761,8 +872,9 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         if (ph) ph[s * 8 + 3] = clock64();
 
         if (s + 1 < n) {
-            // ---- W for stage s+1 -------------------------------------------
-            // L_Q (x block of the pivot tiles) -> LQ (x-space, row-major)
+            // ---- W for stage s+1: L_Q (x block of the pivot tiles) -> LQ
+            // (x-space, row-major; the pivot warp's tiles are there), ALQ rows
+            // (coupling rows, x columns) -> W tile rows >= CT
 #pragma unroll
             for (int k = 0; k < MAXL; ++k) {
                 if (k >= mycnt)
@@ -773,55 +885,10 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                     LQ[r * C::LQS + c0] = acc[k].a;
                     LQ[r * C::LQS + c0 + 1] = acc[k].b;
                 }
-                // ALQ rows (coupling rows, x columns) -> W tile rows >= CT
                 if (ti >= CT && tj >= C::XT0 && tj < CT)
                     st_frag(Wsm + (ti * C::NXC + (tj - C::XT0)) * kTileElems, lane, acc[k]);
             }
-            wait_BA(bamb, baph); // BA_{s+1}, f_{s+1}
-            __syncthreads();
-            if (ph) ph[s * 8 + 4] = clock64();
-            // -wl_new = L_Q' (sgn f) + x'   (kkt_solve.cpp:85-90): 8 lanes per
-            // entry (split k, shuffle-reduced), spread over all warps
-            for (int t0 = 4 * warp; t0 < NX; t0 += 4 * NW) {
-                const int t = t0 + (lane >> 3), part = lane & 7;
-                double q = 0.0;
-                if (t < NX)
-                    for (int k = t + part; k < NX; k += 8)
-                        q += LQ[k * C::LQS + t] * (sgn * fb[k]);
-                q += __shfl_xor_sync(0xffffffffu, q, 1);
-                q += __shfl_xor_sync(0xffffffffu, q, 2);
-                q += __shfl_xor_sync(0xffffffffu, q, 4);
-                if (t < NX && part == 0) {
-                    q += yx[t];
-                    mw[t] = q;
-                    a.wl[((size_t)chain * n + s) * NX + t] = -q;
-                }
-            }
-            // V = BA_{s+1}' L_Q -> W tile rows 0..CT-1 (DMMA, one tile per warp
-            // pass, two accumulators to halve the dependent DMMA chain)
-            for (int v = warp; v < CT * C::NXC; v += NW) {
-                const int ti = v / C::NXC, kt = v % C::NXC;
-                Frag f0{0.0, 0.0}, f1{0.0, 0.0};
-                int ks = 2 * kt; // L_Q upper part is zero
-                for (; ks + 1 < NX / 4; ks += 2) {
-                    const int K0 = 4 * ks + (lane & 3), K1 = K0 + 4;
-                    dmma(f0, BA[K0 * C::PW + 8 * ti + rq], LQ[K0 * C::LQS + 8 * kt + rq]);
-                    dmma(f1, BA[K1 * C::PW + 8 * ti + rq], LQ[K1 * C::LQS + 8 * kt + rq]);
-                }
-                if (ks < NX / 4) {
-                    const int K0 = 4 * ks + (lane & 3);
-                    dmma(f0, BA[K0 * C::PW + 8 * ti + rq], LQ[K0 * C::LQS + 8 * kt + rq]);
-                }
-                st_frag(Wsm + (ti * C::NXC + kt) * kTileElems, lane, Frag{f0.a + f1.a, f0.b + f1.b});
-            }
-            __syncthreads(); // mw ready, V written, BA / LQ reads done
-            // rhs row of W: -wl in row RHS of tile row RT (other rows of
-            // that tile row: coupling rows, already stored above)
-            for (int t = tid; t < NX; t += NTH)
-                Wsm[(C::RT * C::NXC + t / 8) * kTileElems + C::RR * 8 + t % 8] = mw[t];
-            if (s + 2 < n)
-                stage_BA_cta<NU, NX, NW, TMA>(g, a.p, b, g.stage_of(c, s + 2), sm, tid, bamb);
-            __syncthreads();
+            next_W(s, baph, ph);
         }
     }
 
@@ -836,18 +903,10 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
             st_frag(a.trail + ((size_t)chain * g.NTT + C::T(ti - CT, tj - CT)) * kTileElems, lane,
                     acc[k]);
     }
-    unsigned long long my_fail =
-        fail_piv >= 0 ? fail_key(kKindRiccati, c, fail_stage, fail_piv) : ~0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-        my_fail = min(my_fail, __shfl_xor_sync(0xffffffffu, my_fail, o));
-    if (lane == 0 && my_fail != ~0ull)
-        atomicMin(a.fail + b, my_fail);
 #undef LTI
 #undef LTJ
 #undef CNT
 #undef TRC
-#undef PTRC
 }
 
 namespace {
