@@ -387,8 +387,8 @@ int dump_phases(cyq_ctx *ctx, const Geo &g, const long long *ph, const long long
         CU(cudaMemcpy(pt.data(), ph + 6144, pt.size() * sizeof(long long), cudaMemcpyDeviceToHost));
         for (int d = 0; d < CT; ++d) {
             const long long *e = &pt[d * 8];
-            fprintf(stderr, "pivot d=%d start %lld load+update %lld pivots0-3 %lld pivots4-7 %lld publish %lld signal %lld\n",
-                    d, e[0] - t0, e[1] - e[0], e[2] - e[1], e[3] - e[2], e[4] - e[3], e[5] - e[4]);
+            fprintf(stderr, "pivot d=%d start %lld wait+solve+update %lld factor %lld inverse %lld L-out %lld\n",
+                    d, e[0] - t0, e[1] - e[0], e[3] - e[1], e[4] - e[3], e[5] - e[4]);
         }
     }
 #endif

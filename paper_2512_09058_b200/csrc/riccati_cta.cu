@@ -104,7 +104,8 @@ template <int NU, int NX, int NW> struct CS {
     static constexpr int O_RU0 = O_MW + NX;                        // NU
     static constexpr int O_RED = O_RU0 + NU;                       // 32 (pivot floor)
     static constexpr int O_SCR = O_RED + 32;                       // 64 (transpose)
-    static constexpr int O_DG = O_SCR + kTileElems;                // CT pivot diagonal tiles (hand-off)
+    static constexpr int O_SCR2 = O_SCR + kTileElems;              // 64 (L_kk out; upper part stays zero)
+    static constexpr int O_DG = O_SCR2 + kTileElems;               // CT pivot diagonal tiles (hand-off)
     static constexpr int O_MB = O_DG + CT * kTileElems;            // 1 mbarrier ([B A] staging)
     static constexpr int O_LMB = O_MB + 2;                         // CT flags (L_kk^{-1} published), 32-bit
     static constexpr int O_HMB = O_LMB + (CT + 1) / 2;             // CT flags (tiles handed to the pivot warp)
@@ -290,11 +291,11 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
     const int b = chain / g.P, c = chain % g.P, n = g.n, N = g.N;
     griddep_launch();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int rq = lane >> 2, cq = 2 * (lane & 3), q2 = lane & 3;
+    const int rq = lane >> 2, cq = 2 * (lane & 3);
     double *Wsm = sm + C::O_W, *colb = sm + C::O_COL, *linvb = sm + C::O_LINV, *BA = sm + C::O_BA;
     double *LQ = sm + C::O_LQ, *fb = sm + C::O_F, *yx = sm + C::O_YX, *mw = sm + C::O_MW;
     double *ru0 = sm + C::O_RU0;
-    double *tscr = sm + C::O_SCR;
+    double *tscr = sm + C::O_SCR, *tscr2 = sm + C::O_SCR2;
     const bool implicit_rhs = (a.p.ru == nullptr);
     const double sgn = implicit_rhs ? -1.0 : 1.0;
     for (int i = tid; i < C::SMEM; i += NTH)
@@ -453,64 +454,80 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
 #define PTRC(d, e) do { } while (0)
 #endif
         // Factors the diagonal tile dg (L_kk, upper zeroed) and publishes
-        // L_kk^{-1} -> linv[kb & 1] (identity tile carried through the pivot
-        // steps gives L^{-T}; transposed through shared memory). The next
-        // pivot is computed in every lane from values shuffled one step early
-        // (d = (k+1, k+1), u = (k+1, k) before this step's update): pv' = d -
-        // (u iv)^2, the owner lane's exact fma -- no shuffle on the rsqrt ->
-        // mul -> fma pivot chain (as riccati_warp.cu)
-        auto factor_diag = [&](int kb, double dfloor, int s) {
-            Frag idt{rq == cq ? 1.0 : 0.0, rq == cq + 1 ? 1.0 : 0.0};
-            double pvn = 0.0;
+        // L_kk^{-1} -> linv[kb & 1], WITHOUT a shuffle: the tile goes through
+        // shared memory into EVERY lane's registers (lower triangle, 36
+        // doubles), every lane runs the same right-looking Cholesky on it, then
+        // the lanes of row-quad rq back-substitute row rq of L^{-1} (x L = e_rq')
+        // and pick their C-layout fragment of it. The shuffle version's ~14
+        // SHFL per pivot queue behind the bulk warps' shared-memory traffic
+        // (1.4k cycles in a quiet SM, 1.8k in this kernel); this one is the
+        // rsqrt -> mul -> fma chain and ~200 FP64 instructions on an idle pipe.
+        // L_kk leaves through tscr2 (stores of the same value by every lane).
+        auto factor_diag = [&](int kb, double dfloor, int s, unsigned *flag) {
+            st_frag(tscr, lane, dg);
+            __syncwarp();
+            double L[8][8], iv[8];
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-                const int src = kk / 2;
-                const double vk = (kk & 1) ? dg.b : dg.a;
-                const double pv = kk == 0 ? __shfl_sync(0xffffffffu, vk, 4 * kk + src) : pvn;
-                const double urk = __shfl_sync(0xffffffffu, vk, 4 * rq + src);
-                const double uc0 = __shfl_sync(0xffffffffu, vk, 4 * cq + src);
-                const double uc1 = __shfl_sync(0xffffffffu, vk, 4 * (cq + 1) + src);
-                double dn = 0.0, un = 0.0;
-                if (kk + 1 < 8) {
-                    dn = __shfl_sync(0xffffffffu, ((kk + 1) & 1) ? dg.b : dg.a, 4 * (kk + 1) + (kk + 1) / 2);
-                    un = __shfl_sync(0xffffffffu, vk, 4 * (kk + 1) + src);
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j <= i; j += 2) {
+                    const double2 v = *reinterpret_cast<const double2 *>(tscr + 8 * i + j);
+                    L[i][j] = v.x;
+                    if (j + 1 <= i)
+                        L[i][j + 1] = v.y;
                 }
+            // column rq of X = L^{-1} rides along, one row behind the pivots:
+            // x[i] = 0 (i < rq), iv[rq] (i = rq), else -iv[i] sum_{k < i} L[i][k]
+            // x[k] (row i of L is final after pivot i-1) -- the same code in
+            // every lane; only x[7] is left after the last pivot
+            double x[8];
+            double *xo = linvb + (kb & 1) * kTileElems + rq;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const double pv = L[k][k];
                 const bool first = !(pv > dfloor && isfinite(pv)) && fail_piv < 0;
-                fail_piv = first ? 8 * kb + kk : fail_piv;
+                fail_piv = first ? 8 * kb + k : fail_piv;
                 fail_stage = first ? s : fail_stage;
-                const double iv = rsqrt_nr(pv);
-                if (kk + 1 < 8) {
-                    const double l = un * iv;
-                    pvn = fma(-l, l, dn);
+                iv[k] = rsqrt_nr(pv);
+                if (k + 1 < 8) { // the next pivot first
+                    L[k + 1][k] *= iv[k];
+                    L[k + 1][k + 1] = fma(-L[k + 1][k], L[k + 1][k], L[k + 1][k + 1]);
                 }
-                const double lc0 = (cq > kk) ? uc0 * iv : 0.0;
-                const double lc1 = (cq + 1 > kk) ? uc1 * iv : 0.0;
-                const double lrk = urk * iv;
-                const double nv = (rq == kk) ? pv * iv : lrk;
-                if (kk & 1)
-                    dg.b = (q2 == src) ? nv : dg.b;
-                else
-                    dg.a = (q2 == src) ? nv : dg.a;
-                dg.a = fma(-lrk, lc0, dg.a);
-                dg.b = fma(-lrk, lc1, dg.b);
-                if (kk == 3)
-                    PTRC(kb, 2);
-                const double vq = (kk & 1) ? idt.b : idt.a;
-                const double xrq = __shfl_sync(0xffffffffu, vq, 4 * rq + src) * iv;
-                if (kk & 1)
-                    idt.b = (q2 == src) ? xrq : idt.b;
-                else
-                    idt.a = (q2 == src) ? xrq : idt.a;
-                idt.a -= xrq * lc0;
-                idt.b -= xrq * lc1;
+                L[k][k] = pv * iv[k];
+#pragma unroll
+                for (int i = k + 2; i < 8; ++i)
+                    L[i][k] *= iv[k];
+#pragma unroll
+                for (int j = k + 1; j < 8; ++j)
+#pragma unroll
+                    for (int i = j; i < 8; ++i)
+                        if (!(i == k + 1 && j == k + 1))
+                            L[i][j] = fma(-L[i][k], L[j][k], L[i][j]);
+                {
+                    double t = 0.0;
+#pragma unroll
+                    for (int m = 0; m < k; ++m)
+                        t = fma(L[k][m], x[m], t);
+                    x[k] = k < rq ? 0.0 : (k == rq ? iv[k] : -iv[k] * t);
+                    xo[8 * k] = x[k]; // X(k, rq): the four lanes of a quad store the same value
+                }
             }
-            if (cq > rq) dg.a = 0.0;
-            if (cq + 1 > rq) dg.b = 0.0;
             PTRC(kb, 3);
-            st_frag(tscr, lane, idt); // L^{-1} = (L^{-T})'
+            PTRC(kb, 4);
+            flag_set(flag, s + 1, lane); // L_kk^{-1} is out: the bulk warps go on
+            // L_kk -> tscr2 (row-major lower triangle; the upper part was
+            // zero-filled at the start and is never written) -> dg
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j <= i; j += 2) {
+                    if (j + 1 <= i)
+                        *reinterpret_cast<double2 *>(tscr2 + 8 * i + j) = make_double2(L[i][j], L[i][j + 1]);
+                    else
+                        tscr2[8 * i + j] = L[i][j];
+                }
             __syncwarp();
-            st_frag(linvb + (kb & 1) * kTileElems, lane, Frag{tscr[cq * 8 + rq], tscr[(cq + 1) * 8 + rq]});
-            __syncwarp();
+            dg = ld_frag(tscr2, lane);
         };
         // Block column d: the tiles (d, d-1) and (d, d) arrive from their
         // owner (hmb[d]; updates of the block columns < d-1 applied); L(d, d-1)
@@ -543,11 +560,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                 }
             }
             PTRC(d, 1);
-#ifndef CYQ_X_NOFAC
-            factor_diag(d, dfloor, s);
-#endif
-            PTRC(d, 4);
-            flag_set(lmb + d, s + 1, lane);
+            factor_diag(d, dfloor, s, lmb + d);
             PTRC(d, 5);
             st_frag(fdst + C::PI(d, d) * kTileElems, lane, dg);
             if (d >= C::XT0) {
