@@ -155,7 +155,7 @@ def ncu_traffic(cfg_idx, batch):
     committed `ncu --set full` summary of the same workload
     (profiles/ncu_r0X_panel_cfgK.json, tools/ncu_summary.py), newest round
     first; None if no capture of this exact batch exists."""
-    for name in (f"ncu_r02_panel_cfg{cfg_idx}", f"ncu_r01_panel_cfg{cfg_idx}"):
+    for name in (f"ncu_r02b_panel_cfg{cfg_idx}", f"ncu_r02_panel_cfg{cfg_idx}", f"ncu_r01_panel_cfg{cfg_idx}"):
         path = os.path.join(ROOT, "profiles", name + ".json")
         if not os.path.exists(path):
             continue

@@ -6,33 +6,37 @@
 //   kkt_factor.cpp:163-185  Mfwd = sum LB LB' + LA LA' (trailing block)
 //   kkt_solve.cpp:72-134    forward substitution + coupling rows (rhs row)
 //
-// Execution model (one CTA of NW warps per partition column):
+// Execution model (one CTA of NW warps per partition column; the kernel
+// comment has the details):
 //  * the extended panel (TT x TT lower tiles, 231 at config 3) lives in the
-//    warps' registers for the stage. Warp kb+1 (kb < CT) owns the pivot
-//    diagonal tile (kb, kb) in a dedicated register tile; every other tile is
-//    on a per-warp LIST ordered by tile column descending, planned on the
-//    host (launch_c: a greedy over a cycle model, so that the look-ahead
-//    warp of each block column holds few tiles right of it). At block column
-//    kb the tiles a warp must update (tj > kb) are a PREFIX of its list and
-//    the update loop leaves through a warp-uniform branch: no predicated-off
-//    DMMA is ever issued (they occupy the DMMA pipe like real ones; the
-//    previous triangular-order ownership issued 58% of its DMMAs
-//    predicated off);
-//  * blocked right-looking Cholesky with look-ahead, per block column kb:
-//    (A) the raw column-kb tiles, published in shared memory by their owners
-//        at the end of the previous step, are solved in place there
-//        (X <- X L_kk^{-T} = X (L_kk^{-1})', two DMMAs) by any warp -- a
-//        runtime loop over the column, no register-array indexing;
-//    (B) the owner of (kb+1, kb+1) applies column kb to it and factors it
-//        (identity tile carried through the pivot steps -> L^{-1} for free),
-//        while every warp takes its solved column-kb tiles back into
-//        registers, applies C -= L_i L_j' to its list prefix and publishes
-//        its (now complete) column-(kb+1) tiles into the other buffer;
-//    two __syncthreads per block column;
+//    registers of the BULK WARPS (1 .. NW-1) for the stage: every tile but the
+//    pivot diagonal tiles (d, d) and the tiles left of them (d, d-1) is on a
+//    per-warp LIST ordered by tile column descending, planned on the host
+//    (launch_c) and kept packed in registers. At block column kb the tiles a
+//    warp must update (tj > kb) are a PREFIX of its list, its own column-kb
+//    tiles the slots right behind it: straight-line code entered at the right
+//    slot, no predicated-off DMMA (they occupy the DMMA pipe like real ones),
+//    no walk over the list, no indexed constant load (~100+ cycles each);
+//  * blocked right-looking Cholesky with the serial chain DECOUPLED: the
+//    PIVOT WARP (warp 0, on an SM sub-partition whose other warps hold only
+//    tiles of the first block columns) solves (d, d-1) against L_{d-1}^{-1},
+//    applies it to (d, d), factors (d, d) without a shuffle (the tile
+//    replicated in every lane's registers) and publishes L_dd^{-1}; it only
+//    arrives at the step barriers. A bulk warp, per block column: waits for
+//    L_kk^{-1} (a release/acquire flag), solves its own column-kb tiles in
+//    registers (X <- X L_kk^{-T}, two DMMAs) into column buffer kb % 3, one
+//    CTA barrier, keeps its (d, d) / (d, d-1) up to date (handing them to the
+//    pivot warp two steps before their turn) and applies column kb to its
+//    list prefix (C -= L_i L_j', operands from the column buffer);
 //  * shared memory holds W = [V; ALQ; -wl] (the next stage's W W' operand),
 //    [B A] of the next stage (cp.async, one stage ahead), L_Q in x-space
-//    (the B operand of V = BA' L_Q) and the column buffers; H_s is read
-//    straight from global memory (L2-prefetched one stage ahead).
+//    (the B operand of V = BA' L_Q), three column buffers and the hand-off
+//    slots; H_s is read straight from global memory (L2-prefetched one stage
+//    ahead).
+// Round-2 history at config 3 (256 x N=512): 32.4 ms (two barriers per block
+// column, look-ahead by rotating owners, lists in constant memory) -> 25.4 ms;
+// tools/trail_bench.cu and the CYQ_TRACE build (tools/phase_run.py) are the
+// measurements behind each step.
 #include "kkt_common.cuh"
 #include "kernels.h"
 #include "riccati_common.cuh"
