@@ -65,6 +65,7 @@ namespace {
 constexpr int kMaxW = 16, kMaxL = 15, kMaxCT = 15, kLW = 5;
 __constant__ unsigned c_lpk[kMaxW * kLW];
 __constant__ unsigned long long c_cpk[kMaxW];
+__constant__ unsigned c_ppk[kMaxW * 4]; // stored-factor tile index PI(ti, tj) of every list tile, a byte each
 
 template <int NU, int NX, int NW> struct CS {
     static_assert(NU % 8 == 0 && NX % 8 == 0, "tile-aligned shapes only");
@@ -655,6 +656,13 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
     }
     unsigned long long cpk = c_cpk[warp];
     asm volatile("" : "+l"(cpk));
+    unsigned ppk[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        ppk[i] = c_ppk[warp * 4 + i];
+        asm volatile("" : "+r"(ppk[i]));
+    }
+#define PIK(k) ((ppk[(k) / 4] >> (8 * ((k) % 4))) & 255u)
     const int mycnt = (int)(cpk & 15u);
 #define LTI(k) ((int)((opk[k] >> 9) & 31u))
 #define LTJ(k) ((int)(opk[k] >> 25))
@@ -768,6 +776,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
             // the unrolled list costs issue slots for every slot it skips, a
             // switch becomes a jump table: an indexed constant load per step)
             if (hi > cnt) {
+                double *fdst = a.fac + ((size_t)chain * n + s) * C::NPT * kTileElems;
                 flag_wait(lmb + kb, s + 1);
                 TRC(5);
                 const Frag linv = ld_frag(linvb + par * kTileElems, lane);
@@ -781,6 +790,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         tile_gemm_nt(r, acc[T], linv);                                                                 \
         acc[T] = r;                                                                                    \
         sts(colS + (opk[T] & 0xffffu), r);                                                             \
+        st_frag(fdst + PIK(T) * kTileElems, lane, r);                                                  \
     }
                 if (cnt < 8) {
                     if (cnt < 4) {
@@ -864,24 +874,20 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         }
         if (ph) ph[s * 8 + 2] = clock64();
 
-        // ---- store the factor tiles and y_s' ---------------------------------
+        // ---- y_s' (the factor tiles went out as they were solved) -------------
         {
-            double *dst = a.fac + ((size_t)chain * n + s) * C::NPT * kTileElems;
 #pragma unroll
             for (int k = 0; k < MAXL; ++k) {
                 if (k >= mycnt)
                     break;
                 const int ti = LTI(k), tj = LTJ(k);
-                if (tj < CT) {
-                    st_frag(dst + C::PI(ti, tj) * kTileElems, lane, acc[k]);
-                    if (ti == C::RT && rq == C::RR) {
-                        double *yv = a.y + ((size_t)chain * n + s) * C::NUX;
-                        yv[8 * tj + cq] = acc[k].a;
-                        yv[8 * tj + cq + 1] = acc[k].b;
-                        if (tj >= C::XT0) {
-                            yx[8 * tj + cq - NU] = acc[k].a;
-                            yx[8 * tj + cq + 1 - NU] = acc[k].b;
-                        }
+                if (tj < CT && ti == C::RT && rq == C::RR) {
+                    double *yv = a.y + ((size_t)chain * n + s) * C::NUX;
+                    yv[8 * tj + cq] = acc[k].a;
+                    yv[8 * tj + cq + 1] = acc[k].b;
+                    if (tj >= C::XT0) {
+                        yx[8 * tj + cq - NU] = acc[k].a;
+                        yx[8 * tj + cq + 1 - NU] = acc[k].b;
                     }
                 }
             }
@@ -923,6 +929,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
 #undef LTI
 #undef LTJ
 #undef CNT
+#undef PIK
 #undef TRC
 }
 
@@ -1091,7 +1098,17 @@ template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStre
             for (int kb = 0; kb < 16; ++kb) // counts past CT repeat the last one (nothing to publish)
                 cpk[w] |= (unsigned long long)cnt[w * (kMaxCT + 1) + std::min(kb, C::CT)] << (4 * kb);
         }
-        const cudaError_t e1 = cudaMemcpyToSymbol(c_lpk, lpk, sizeof lpk);
+        unsigned ppk[kMaxW * 4] = {};
+        static_assert(C::NPT <= 256 && kMaxL <= 16, "stored-tile indices packed as bytes");
+        for (int w = 0; w < NW; ++w)
+            for (int k = 0; k < nown[w]; ++k) {
+                const int ti = h[w * kPL + k] >> 8, tj = h[w * kPL + k] & 255;
+                if (tj < C::CT)
+                    ppk[w * 4 + k / 4] |= (unsigned)C::PI(ti, tj) << (8 * (k % 4));
+            }
+        cudaError_t e1 = cudaMemcpyToSymbol(c_lpk, lpk, sizeof lpk);
+        if (e1 == cudaSuccess)
+            e1 = cudaMemcpyToSymbol(c_ppk, ppk, sizeof ppk);
         return e1 != cudaSuccess ? e1 : cudaMemcpyToSymbol(c_cpk, cpk, sizeof cpk);
     });
     riccati_cta_kernel<NU, NX, NW, TMA><<<ra.grid_chains(), 32 * NW, smem, st>>>(ra);

@@ -131,6 +131,9 @@ __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
     const bool fwd_fused = a.do_factor && a.do_solve;
     int fail = -1, fail_l = 0, fail_k = 0;
 
+    long long *ph = (a.phase && b == 0 && threadIdx.x == 0) ? a.phase : nullptr;
+    int php = 0;
+    if (ph) ph[php++] = clock64();
     // ---- phase 1: per column T, Mbwd, K, Mfwd, bwd_neg ------------------
     for (int c = 0; c < P; ++c) {
         const size_t chain = (size_t)b * P + c;
@@ -174,6 +177,7 @@ __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
         __syncthreads();
     }
 
+    if (ph) ph[php++] = clock64();
     // ---- Schur rhs b_i = fd[n i] - fwd_i + bwd_neg_{(i+1) % P} ------------
     if (a.do_solve) {
         ProbAcc pa{a.p, g, b};
@@ -194,9 +198,11 @@ __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
         __syncthreads();
     }
 
+    if (ph) ph[php++] = clock64();
     // ---- CR levels (in place in D / K, as schur_fused.cu) -----------------
     if (a.do_factor) {
         for (int l = 0, s = P; l < Lo.levels; ++l, s >>= 1) {
+            if (ph && l > 0) ph[php++] = clock64();
             const int half = s / 2, hcy = l > 0 ? 1 << (l - 1) : 0;
             const long long out0 = P - (P >> l);
             auto assemble = [&](double *dst, int i) { // level-l diagonal block i -> dst
@@ -315,6 +321,7 @@ __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
                 }
             }
         }
+        if (ph) ph[php++] = clock64();
         // base: x_0 <- Lb^{-T} Lb^{-1} x_0
         ctat::cta_matvec<XT, NW, false, true>(ws + Lo.Lb, xs, v1, 1.0, false, warp, lane);
         __syncthreads();
@@ -348,6 +355,10 @@ __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
                 a.lam_out[((size_t)b * g.N + n * i) * NX + k] = lam;
         }
     }
+    if (ph) {
+        ph[php++] = clock64();
+        ph[31] = php;
+    }
     if (warp == 0 && lane == 0 && fail >= 0)
         atomicMin(a.fail + b, fail_key(kKindCR, fail_l, fail_k, fail));
 }
@@ -355,7 +366,10 @@ __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
 template <int NX> bool launch_sb(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
     if (g.nx != NX)
         return false;
-    constexpr int NW = 8;
+#ifndef CYQ_SB_NW
+#define CYQ_SB_NW 8
+#endif
+    constexpr int NW = CYQ_SB_NW;
     const size_t smem = SBSmem<NX, NW>::total(g.P) * sizeof(double);
     if (smem > 227 * 1024)
         return false;
