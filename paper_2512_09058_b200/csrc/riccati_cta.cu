@@ -383,10 +383,18 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         if (ph) ph[s * 8 + 4] = clock64();
         for (int t0 = 4 * warp; t0 < NX; t0 += 4 * NW) {
             const int t = t0 + (lane >> 3), part = lane & 7;
-            double q = 0.0;
-            if (t < NX)
-                for (int k = t + part; k < NX; k += 8)
-                    q += LQ[k * C::LQS + t] * (sgn * fb[k]);
+            double q = 0.0, q1 = 0.0;
+            if (t < NX) {
+#pragma unroll
+                for (int i = 0; i < NX / 8; i += 2) { // L_Q is lower triangular: rows k >= t
+                    const int k0 = t + part + 8 * i, k1 = k0 + 8;
+                    if (k0 < NX)
+                        q = fma(LQ[k0 * C::LQS + t], fb[k0], q);
+                    if (k1 < NX)
+                        q1 = fma(LQ[k1 * C::LQS + t], fb[k1], q1);
+                }
+                q = sgn * (q + q1);
+            }
             q += __shfl_xor_sync(0xffffffffu, q, 1);
             q += __shfl_xor_sync(0xffffffffu, q, 2);
             q += __shfl_xor_sync(0xffffffffu, q, 4);
@@ -775,6 +783,29 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
             // code entered at slot cnt through a compare tree (a walk over
             // the unrolled list costs issue slots for every slot it skips, a
             // switch becomes a jump table: an indexed constant load per step)
+            // a solved tile of the x columns also feeds stage s+1: L_Q (x block of
+            // the pivot tiles) -> LQ (x-space, row-major), ALQ rows (coupling rows)
+            // -> W tile rows >= CT (both next read after this stage's block columns)
+            auto fill_next = [&](unsigned o, const Frag &r) {
+                const int ti = (int)((o >> 9) & 31u), tj = (int)(o >> 25);
+                if (ti == C::RT && rq == C::RR) { // the rhs row: y_s'
+                    double *yv = a.y + ((size_t)chain * n + s) * C::NUX;
+                    yv[8 * tj + cq] = r.a;
+                    yv[8 * tj + cq + 1] = r.b;
+                    if (tj >= C::XT0) {
+                        yx[8 * tj + cq - NU] = r.a;
+                        yx[8 * tj + cq + 1 - NU] = r.b;
+                    }
+                }
+                if (s + 1 < n && tj >= C::XT0) {
+                    if (ti < CT) {
+                        const int rr = 8 * ti + rq - NU, c0 = 8 * tj + cq - NU;
+                        LQ[rr * C::LQS + c0] = r.a;
+                        LQ[rr * C::LQS + c0 + 1] = r.b;
+                    } else
+                        st_frag(Wsm + (ti * C::NXC + (tj - C::XT0)) * kTileElems, lane, r);
+                }
+            };
             if (hi > cnt) {
                 double *fdst = a.fac + ((size_t)chain * n + s) * C::NPT * kTileElems;
                 flag_wait(lmb + kb, s + 1);
@@ -791,6 +822,7 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         acc[T] = r;                                                                                    \
         sts(colS + (opk[T] & 0xffffu), r);                                                             \
         st_frag(fdst + PIK(T) * kTileElems, lane, r);                                                  \
+        fill_next(opk[T], r);                                                                          \
     }
                 if (cnt < 8) {
                     if (cnt < 4) {
@@ -874,43 +906,12 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         }
         if (ph) ph[s * 8 + 2] = clock64();
 
-        // ---- y_s' (the factor tiles went out as they were solved) -------------
-        {
-#pragma unroll
-            for (int k = 0; k < MAXL; ++k) {
-                if (k >= mycnt)
-                    break;
-                const int ti = LTI(k), tj = LTJ(k);
-                if (tj < CT && ti == C::RT && rq == C::RR) {
-                    double *yv = a.y + ((size_t)chain * n + s) * C::NUX;
-                    yv[8 * tj + cq] = acc[k].a;
-                    yv[8 * tj + cq + 1] = acc[k].b;
-                    if (tj >= C::XT0) {
-                        yx[8 * tj + cq - NU] = acc[k].a;
-                        yx[8 * tj + cq + 1 - NU] = acc[k].b;
-                    }
-                }
-            }
-        }
+        // (the factor tiles, y_s' and the x-column tiles stage s+1 needs went out as
+        // they were solved)
         if (ph) ph[s * 8 + 3] = clock64();
 
         if (s + 1 < n) {
-            // ---- W for stage s+1: L_Q (x block of the pivot tiles) -> LQ
-            // (x-space, row-major; the pivot warp's tiles are there), ALQ rows
-            // (coupling rows, x columns) -> W tile rows >= CT
-#pragma unroll
-            for (int k = 0; k < MAXL; ++k) {
-                if (k >= mycnt)
-                    break;
-                const int ti = LTI(k), tj = LTJ(k);
-                if (ti >= C::XT0 && ti < CT && tj >= C::XT0) {
-                    const int r = 8 * ti + rq - NU, c0 = 8 * tj + cq - NU;
-                    LQ[r * C::LQS + c0] = acc[k].a;
-                    LQ[r * C::LQS + c0 + 1] = acc[k].b;
-                }
-                if (ti >= CT && tj >= C::XT0 && tj < CT)
-                    st_frag(Wsm + (ti * C::NXC + (tj - C::XT0)) * kTileElems, lane, acc[k]);
-            }
+            // ---- W for stage s+1 (L_Q and the ALQ rows went out as they were solved)
             next_W(s, baph, ph);
         }
     }
