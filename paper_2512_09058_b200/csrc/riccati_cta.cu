@@ -788,15 +788,6 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
             // -> W tile rows >= CT (both next read after this stage's block columns)
             auto fill_next = [&](unsigned o, const Frag &r) {
                 const int ti = (int)((o >> 9) & 31u), tj = (int)(o >> 25);
-                if (ti == C::RT && rq == C::RR) { // the rhs row: y_s'
-                    double *yv = a.y + ((size_t)chain * n + s) * C::NUX;
-                    yv[8 * tj + cq] = r.a;
-                    yv[8 * tj + cq + 1] = r.b;
-                    if (tj >= C::XT0) {
-                        yx[8 * tj + cq - NU] = r.a;
-                        yx[8 * tj + cq + 1 - NU] = r.b;
-                    }
-                }
                 if (s + 1 < n && tj >= C::XT0) {
                     if (ti < CT) {
                         const int rr = 8 * ti + rq - NU, c0 = 8 * tj + cq - NU;
@@ -906,8 +897,25 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
         }
         if (ph) ph[s * 8 + 2] = clock64();
 
-        // (the factor tiles, y_s' and the x-column tiles stage s+1 needs went out as
-        // they were solved)
+        // ---- y_s' (the factor tiles and the x-column tiles stage s+1 needs went
+        // out as they were solved)
+        {
+#pragma unroll
+            for (int k = 0; k < MAXL; ++k) {
+                if (k >= mycnt)
+                    break;
+                const int ti = LTI(k), tj = LTJ(k);
+                if (tj < CT && ti == C::RT && rq == C::RR) {
+                    double *yv = a.y + ((size_t)chain * n + s) * C::NUX;
+                    yv[8 * tj + cq] = acc[k].a;
+                    yv[8 * tj + cq + 1] = acc[k].b;
+                    if (tj >= C::XT0) {
+                        yx[8 * tj + cq - NU] = acc[k].a;
+                        yx[8 * tj + cq + 1 - NU] = acc[k].b;
+                    }
+                }
+            }
+        }
         if (ph) ph[s * 8 + 3] = clock64();
 
         if (s + 1 < n) {
