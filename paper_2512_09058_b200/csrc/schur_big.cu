@@ -366,8 +366,12 @@ __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
 template <int NX> bool launch_sb(const Geo &g, cudaStream_t st, const SchurArgs &sa) {
     if (g.nx != NX)
         return false;
+    // 16 warps per instance CTA (two CTAs per SM, 64 registers): the block
+    // operations are chains of dependent DMMAs per tile, so more warps per
+    // block shorten every step (config 3: 8 / 12 / 16 warps 2.44 / 2.31 /
+    // 2.27 ms)
 #ifndef CYQ_SB_NW
-#define CYQ_SB_NW 8
+#define CYQ_SB_NW 16
 #endif
     constexpr int NW = CYQ_SB_NW;
     const size_t smem = SBSmem<NX, NW>::total(g.P) * sizeof(double);
