@@ -34,7 +34,7 @@
 //    slots; H_s is read straight from global memory (L2-prefetched one stage
 //    ahead).
 // Round-2 history at config 3 (256 x N=512): 32.4 ms (two barriers per block
-// column, look-ahead by rotating owners, lists in constant memory) -> 25.4 ms;
+// column, look-ahead by rotating owners, lists in constant memory) -> 24.5 ms;
 // tools/trail_bench.cu and the CYQ_TRACE build (tools/phase_run.py) are the
 // measurements behind each step.
 #include "kkt_common.cuh"
