@@ -872,7 +872,6 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
             // trailing update of my prefix: C(ti, tj) -= L(ti, kb) L(tj, kb)',
             // tiles cnt-1 .. 0 (.. NPS when the ALQ ALQ' terms cancel on the
             // pure tiles)
-#ifndef CYQ_X_NOTRAIL
             {
                 const bool skip = kb >= C::XT0 && s + 1 < n;
 #define UPD_CASE(K)                                                                                    \
@@ -892,7 +891,6 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
                 }
 #undef UPD_CASE
             }
-#endif
             TRC(4);
         }
         if (ph) ph[s * 8 + 2] = clock64();
