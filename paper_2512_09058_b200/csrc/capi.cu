@@ -856,7 +856,9 @@ int cyq_solve_problem_batch(cyq_ctx *ctx, const cyq_dims *dims, const cyq_ocp_ba
     const ProbView dp = carve_prob(base, g);
     const size_t B = g.batch, N = g.N, nx = g.nx, nu = g.nu;
     const SolView svall{base + pd, base + pd + B * N * nu, base + pd + B * N * nu + B * (N + 1) * nx};
-    const int nch = B >= 256 ? 8 : (B >= 32 ? 4 : 1);
+    // (more, smaller chunks for multi-GB problems: the copies are the bound and
+    // the last chunk's kernels are the only part they do not hide)
+    const int nch = B >= 256 ? (pd * sizeof(double) > (4ull << 30) ? 16 : 8) : (B >= 32 ? 4 : 1);
     const int per = (int)((B + nch - 1) / nch);
     Geo gc = g;
     gc.batch = per;
