@@ -52,7 +52,7 @@ LIVE_DMMA_KERNELS = [
     "schur_fused_kernelILi16ELi4ELi1",             # config 4 Schur/CR
     "schur_fused_kernelILi12ELi16ELi8",            # config 2 Schur/CR (8-CTA cluster)
     "schur_fused_kernelILi10ELi16ELi1",            # config 0 Schur/CR
-    "schur_big_kernelILi64ELi8",                   # config 3 Schur/CR
+    "schur_big_kernelILi64ELi16",                  # config 3 Schur/CR
     "riccati_panel_kernel_t",                      # generic panel (other shapes)
 ]
 
