@@ -92,9 +92,10 @@ __device__ __forceinline__ void mb_wait(unsigned long long *mb, int par) {
 #endif
 
 // ---- shared-memory flags: a one-writer hand-off that is usually already
-// there when its readers look (an mbarrier try_wait costs ~200 cycles even
-// on a completed phase, an acquire load ~30). The writer's warp stores its
-// data, then one lane releases the flag; readers spin on the expected value.
+// there when its readers look. The writer's warp stores its data, then one
+// lane releases the flag; readers spin on the expected value (an acquire
+// load per look). Measured neutral against mbarrier try_wait on the config-3
+// panel; kept because the value (stage + 1) needs no phase bookkeeping.
 __device__ __forceinline__ void flag_set(unsigned *f, unsigned v, int lane) {
     __syncwarp();
     if (lane == 0)
