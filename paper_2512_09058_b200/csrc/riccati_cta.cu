@@ -941,32 +941,30 @@ __global__ void __launch_bounds__(32 * NW, 1) riccati_cta_kernel(RiccatiArgs a) 
 }
 
 namespace {
-template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
-    if (g.nu != NU || g.nx != NX)
-        return false;
-    using C = CS<NU, NX, NW>;
-    const size_t smem = (size_t)C::SMEM * sizeof(double);
-    static DeviceOnce once;
-    once_per_device(once, [&]() -> cudaError_t {
-        const cudaError_t e0 = cudaFuncSetAttribute(riccati_cta_kernel<NU, NX, NW, TMA>,
-                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e0 != cudaSuccess)
-            return e0;
+constexpr int kPL = 32; // plan-time list stride
+
+// Host tile plan of the CTA panel: h[w * kPL + k] = (ti << 8 | tj) of warp
+// w's list slot k, nown[w] its tile count, cnt[w * (kMaxCT + 1) + kb] the
+// number of its tiles with tile column >= kb ... see the comment inside.
+// Returns false if the plan does not place every list tile once within MAXL
+// slots per warp in tile-column-descending order (tests/test_cta_plan.py
+// checks the rest through cyqb_debug_cta_plan).
+template <class C, int NW> bool plan_tiles(unsigned short *h, unsigned char *cnt, int *nown) {
+    std::fill(h, h + kMaxW * kPL, (unsigned short)0);
+    std::fill(cnt, cnt + kMaxW * (kMaxCT + 1), (unsigned char)0);
+    std::fill(nown, nown + kMaxW, 0);
+    {
         // tile plan. The skip-mode pure tiles go first (NPS per warp at slots
         // 0 .. NPS-1; they take trailing updates only from the u columns, kb <
-        // XT0). The warps of the pivot warp's SM sub-partition (w % 4 == 0)
-        // then fill up with the tiles of the first block columns -- column 0
-        // (never updated) first, the pivot warp itself taking only those -- so
-        // that sub-partition issues no DMMA after the first steps and the
-        // pivot chain's FP64 instructions are not queued behind any. Every
+        // XT0); the pivot warp (0) holds no tile. The other warps of its SM
+        // sub-partition (w % 4 == 0) then fill up with the tiles of the first
+        // block columns -- column 0 (never updated) first -- so that
+        // sub-partition issues no DMMA after the first steps and the pivot
+        // chain's FP64 instructions are not queued behind any. Every
         // other tile goes, in tile-column-descending order, to the bulk warp
         // that minimises the modelled time sum_kb max(DMMA issue per bulk
         // sub-partition). Lists stay in tile-column-descending order.
-        constexpr int kPL = 32; // plan-time list stride
-        unsigned short h[kMaxW * kPL] = {};
-        unsigned char cnt[kMaxW * (kMaxCT + 1)] = {};
         double load[kMaxW][kMaxCT] = {};
-        int nown[kMaxW] = {};
         const double kUpd = 2 * 16.0; // cycles: one tile update
         auto quiet = [&](int w) { return w % 4 == 0; };
         auto cost = [&]() {
@@ -1054,7 +1052,7 @@ template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStre
                         if (nown[w] < C::MAXL)
                             best = w;
                     if (best < 0)
-                        return cudaErrorInvalidValue;
+                        return false;
                     // keep its list in column-descending order: insert before lower columns
                     int pos = nown[best];
                     while (pos > C::NPS && (h[best * kPL + pos - 1] & 255) < tj) {
@@ -1076,15 +1074,15 @@ template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStre
             int seen = 0;
             for (int w = 0; w < NW; ++w) {
                 if (nown[w] > C::MAXL)
-                    return cudaErrorInvalidValue;
+                    return false;
                 for (int k = 0; k < nown[w]; ++k) {
                     ++seen;
                     if (k > C::NPS && (h[w * kPL + k] & 255) > (h[w * kPL + k - 1] & 255))
-                        return cudaErrorInvalidValue;
+                        return false;
                 }
             }
             if (seen != C::NL)
-                return cudaErrorInvalidValue;
+                return false;
         }
         for (int w = 0; w < NW; ++w) {
             cnt[w * (kMaxCT + 1)] = (unsigned char)nown[w];
@@ -1095,6 +1093,26 @@ template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStre
                 cnt[w * (kMaxCT + 1) + kb + 1] = (unsigned char)m;
             }
         }
+    }
+    return true;
+}
+
+template <int NU, int NX, int NW, bool TMA> bool launch_c(const Geo &g, cudaStream_t st, const RiccatiArgs &ra) {
+    if (g.nu != NU || g.nx != NX)
+        return false;
+    using C = CS<NU, NX, NW>;
+    const size_t smem = (size_t)C::SMEM * sizeof(double);
+    static DeviceOnce once;
+    once_per_device(once, [&]() -> cudaError_t {
+        const cudaError_t e0 = cudaFuncSetAttribute(riccati_cta_kernel<NU, NX, NW, TMA>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e0 != cudaSuccess)
+            return e0;
+        unsigned short h[kMaxW * kPL];
+        unsigned char cnt[kMaxW * (kMaxCT + 1)];
+        int nown[kMaxW];
+        if (!plan_tiles<C, NW>(h, cnt, nown))
+            return cudaErrorInvalidValue;
         unsigned lpk[kMaxW * kLW] = {};
         unsigned long long cpk[kMaxW] = {};
         for (int w = 0; w < NW; ++w) {
@@ -1132,3 +1150,12 @@ bool launch_riccati_cta(const Geo &g, cudaStream_t st, const RiccatiArgs &ra, bo
 }
 
 } // namespace cyqb
+
+// Not part of the C ABI (include/cyqlone_b200.h): the config-3 tile plan for
+// tests/test_cta_plan.py -- lists[16 * 32] = (ti << 8 | tj), counts[16 * 16],
+// nown[16], dims[6] = {TT, CT, RT, MAXL, NPS, NW}. Returns 0 if the plan is valid.
+extern "C" int cyqb_debug_cta_plan(unsigned short *lists, unsigned char *counts, int *nown, int *dims) {
+    using C = cyqb::CS<32, 64, 16>;
+    dims[0] = C::TT, dims[1] = C::CT, dims[2] = C::RT, dims[3] = C::MAXL, dims[4] = C::NPS, dims[5] = 16;
+    return cyqb::plan_tiles<C, 16>(lists, counts, nown) ? 0 : 1;
+}
