@@ -29,6 +29,9 @@ SHAPES = [
     (21, 16, 8, 16, 2), (40, 17, 7, 8, 1), (12, 24, 8, 4, 1), (10, 33, 5, 2, 1),
     (64, 5, 10, 64, 1), (50, 12, 4, 32, 2), (16, 40, 24, 4, 1), (8, 72, 8, 2, 1),
     (20, 64, 32, 4, 1),
+    # the CTA panel (nx = 64, nu = 32): one stage per chain, N < P (padding
+    # chains), N not a multiple of P, a single chain, two stages
+    (4, 64, 32, 4, 2), (3, 64, 32, 4, 1), (13, 64, 32, 4, 2), (6, 64, 32, 1, 1), (8, 64, 32, 4, 3),
 ]
 
 
