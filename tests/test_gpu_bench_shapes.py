@@ -168,3 +168,21 @@ def test_config3_tma_staging_variant_matches_oracle(oracle):
     base = kkt.solve_problem(p, kkt.FactorOptions(P=32))
     for k in ("u", "x", "lam"):
         assert np.array_equal(getattr(sol, k), getattr(base, k))
+
+
+def test_config3_pivot_failure_reported_by_the_pivot_warp():
+    # the CTA panel's pivot warp owns every pivot check: an indefinite R at one
+    # stage of one instance is reported for that instance, chain and stage only
+    p = synth.generate(3, seed=31, batch=3, N=64)
+    P, n = 4, 16                # 16 stages per chain
+    j = 37                      # Partition::stage_of: stage n c - s -> chain 3, position 11
+    c, spos = -(-j // n), n * -(-j // n) - j
+    p.R[1, j] = -5.0 * np.eye(p.nu)
+    sol, rc, st = kkt.solve_problem(p, kkt.FactorOptions(P=P), raise_on_error=False)
+    assert rc == 2
+    assert [s.code != 0 for s in st] == [False, True, False]
+    assert (st[1].column_or_level, st[1].stage) == (c, spos) == (3, 11) and 0 <= st[1].pivot < p.nu
+    good = p.subset([0, 2])
+    ref = kkt.solve_problem(good, kkt.FactorOptions(P=P))
+    got = sol.__class__(sol.u[[0, 2]], sol.x[[0, 2]], sol.lam[[0, 2]])
+    assert rel_error(got, ref).max() < 1e-13
