@@ -104,6 +104,19 @@ __device__ __forceinline__ void flag_set(unsigned *f, unsigned v, int lane) {
 }
 // (every lane spins: with one lane polling and a __syncwarp the config-3 panel
 // measured +0.9 ms, a nanosleep back-off between the looks was neutral)
+#ifdef CYQ_MB_WATCHDOG // debug builds: a hand-off that never comes reports and traps
+__device__ __forceinline__ void flag_wait(const unsigned *f, unsigned v) {
+    unsigned r = ~v;
+    for (long long it = 0; r != v; ++it) {
+        asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(r) : "r"(smem_u32(f)) : "memory");
+        if (r != v && it == (1LL << 24) && (threadIdx.x & 31) == 0 && blockIdx.x < 2) {
+            printf("flag_wait stuck: block %d warp %d flag smem+%u = %u, expected %u\n", blockIdx.x,
+                   threadIdx.x >> 5, smem_u32(f), r, v);
+            __trap();
+        }
+    }
+}
+#else
 __device__ __forceinline__ void flag_wait(const unsigned *f, unsigned v) {
     // (first look outside the loop: the rotated do-while form of the same
     // wait measured +0.35 ms on the config-3 panel)
@@ -113,6 +126,7 @@ __device__ __forceinline__ void flag_wait(const unsigned *f, unsigned v) {
         asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(r) : "r"(smem_u32(f)) : "memory");
     }
 }
+#endif
 
 // async copy of cnt doubles (16-byte granules when both ends are aligned),
 // or an identity / zero fill when src == nullptr
