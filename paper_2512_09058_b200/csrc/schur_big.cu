@@ -165,7 +165,8 @@ __global__ void __launch_bounds__(32 * NW, 2) schur_big_kernel(SchurArgs a) {
                 ctat::cta_gemm<XT, NW, false, true, ctat::kGeJ, false>(Kc, nullptr, -1.0, LAb, Tb, warp, lane);
             else
                 blk_zero<XT, NW>(Kc, warp, lane);
-            blk_copy_lower<XT, NW>(Tc, Tb, warp, lane); // persistent T (kkt::solve), upper tiles zero
+            if (!a.do_solve) // persistent T: read again only by kkt::solve on a kept factor
+                blk_copy_lower<XT, NW>(Tc, Tb, warp, lane); // (upper tiles zero)
         }
         if (a.do_solve) { // bwd_neg_c = T x'_{n-1} = Tt' x'
             const double *yv = a.y + (chain * n + (n - 1)) * g.nux + nu;

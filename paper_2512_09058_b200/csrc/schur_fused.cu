@@ -347,12 +347,16 @@ __global__ void __launch_bounds__(32 * NW, NW <= 4 ? 16 / NW : 1) schur_fused_ke
                 tiles::diag_inverses<XT, NL>(Lq, Zd, Ld, lane, scr);
                 tiles::blocked_inverse<XT, NL>(Lq, Zd, Ld, Li, X);
             }
-            double *Tc = ws + Lo.Tt + c * TL;
+            // persistent T: read again only by kkt::solve on a kept factor --
+            // a factor + solve call works on transient scratch
+            if (!a.do_solve) {
+                double *Tc = ws + Lo.Tt + c * TL;
 #pragma unroll
-            for (int i = 0; i < XT; ++i)
+                for (int i = 0; i < XT; ++i)
 #pragma unroll
-                for (int j = i; j < XT; ++j)
-                    st_frag(Tc + T(j, i) * kTileElems, lane, X[i * XT + j]);
+                    for (int j = i; j < XT; ++j)
+                        st_frag(Tc + T(j, i) * kTileElems, lane, X[i * XT + j]);
+            }
             // Mbwd = T T' (kkt_factor.cpp:174), lower tiles
             double *Mbc = Mb + c * TL;
 #pragma unroll
